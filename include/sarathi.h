@@ -1,0 +1,251 @@
+/*
+ * sarathi.h — C ABI of libsarathi.so, the B200-native (sm_100a) hot path of SARATHI
+ * (Agrawal et al., arXiv 2308.16369): the decode-maximal hybrid-batch transformer forward pass.
+ *
+ * Citations: P:Lnnn = /root/reference/PAPER.md line nnn (section in parentheses).
+ *
+ * The problem the library solves (§4.3 "Decode-Maximal Batching"): one iteration runs
+ * ONE prefill chunk (§4.2 "Chunked-prefills") together with up to B-1 single-token decodes of
+ * other requests, fusing all linear operations over the p + d tokens into one matmul
+ * each while attention runs separately per token kind.  KV caches are pre-allocated per
+ * request for its maximum length and updated in place (§4.5).
+ *
+ * Conventions
+ *  - Every function returning int returns SARATHI_OK (0) or a negative SARATHI_E* code; the
+ *    thread-local message of the last failure is returned by sarathi_last_error().
+ *  - On any error raised before device work is enqueued, library state is unchanged.
+ *  - Host arrays passed in are owned by the caller and read synchronously during the call.
+ *  - Device work is enqueued on the stream given in sarathi_dist.stream (NULL = legacy default
+ *    stream); outputs are valid after the caller synchronises that stream.
+ *  - One model handle serves one host thread (no internal locking).  One handle per GPU/process.
+ *  - Under tensor parallelism (world > 1, Megatron column/row sharding, §2.3) every rank
+ *    makes identical calls in the same order; integer metadata (schedules, block tables, slot
+ *    mappings) is computed identically on every rank.
+ */
+#ifndef SARATHI_H_
+#define SARATHI_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------------------------ */
+#define SARATHI_OK 0
+#define SARATHI_EINVAL (-1)       /* bad argument / configuration (e.g. heads % world != 0, T > cap) */
+#define SARATHI_ENOKV (-2)        /* KV block reservation does not fit (admission failure)        */
+#define SARATHI_EUNKNOWN_REQ (-3) /* request id not allocated                                      */
+#define SARATHI_EDUP (-4)         /* request twice in one batch (incl. as prefill and decode)      */
+#define SARATHI_EPOS (-5)         /* start_pos / position != the request's cached length           */
+#define SARATHI_EOVERFLOW (-6)    /* would exceed the request's reserved max_tokens                */
+#define SARATHI_ECUDA (-7)        /* CUDA runtime error (device state may be undefined)            */
+#define SARATHI_ENCCL (-8)        /* NCCL error                                                    */
+#define SARATHI_ESTATE (-9)       /* call out of order (e.g. run before alloc_kv)                  */
+
+/* ---- model --------------------------------------------------------------------------------- */
+typedef struct sarathi_model sarathi_model;
+
+#define SARATHI_FFN_SWIGLU 0 /* gate, up, down (LLaMA)                                   */
+#define SARATHI_FFN_GELU 1   /* ffn_ln1 + GELU-tanh + ffn_ln2 (Table, GPT-3) */
+
+/* Logical (unsharded) decoder-only transformer, P:L193-203 (§2.1) with readings O-1..O-8. */
+typedef struct {
+  int32_t n_layers;   /* L                                                    */
+  int32_t hidden;     /* H (embedding size)                           */
+  int32_t n_heads;    /* query heads                                          */
+  int32_t n_kv_heads; /* key/value heads (== n_heads for MHA; GQA otherwise)  */
+  int32_t head_dim;   /* 64 or 128                                            */
+  int32_t ffn_hidden; /* H2 ("second hidden dimension")               */
+  int32_t vocab;      /* V                                                    */
+  int32_t ffn_kind;   /* SARATHI_FFN_*                                        */
+  float rms_eps;      /* RMSNorm epsilon (1e-5)                               */
+  float rope_base;    /* RoPE base (10000)                                    */
+  int32_t max_seq_len;          /* positions < max_seq_len (RoPE table size)  */
+  int32_t max_tokens_per_batch; /* cap on T = p + d (workspace sizing)        */
+} sarathi_model_config;
+
+/* Process / device placement.  world == 1: no NCCL.  world > 1: nccl_unique_id points to the
+ * 128-byte ncclUniqueId produced by sarathi_nccl_unique_id() on rank 0 and broadcast by the
+ * caller (e.g. over a torch.distributed process group). */
+typedef struct {
+  int32_t rank;
+  int32_t world;
+  int32_t device;             /* CUDA device ordinal used by this handle               */
+  const void* nccl_unique_id; /* 128 bytes, or NULL when world == 1                    */
+  void* stream;               /* cudaStream_t all device work is enqueued on            */
+} sarathi_dist;
+
+/* Writes a fresh ncclUniqueId (128 bytes) to out.  Host only.  ENCCL if NCCL is unavailable. */
+int sarathi_nccl_unique_id(void* out128);
+
+/* Creates the model on dist->device and generates this rank's weight shards ON DEVICE from the
+ * counter-based generator spec (synth/__init__.py header; seed = weight_seed).  Weights are
+ * packed in kernel layout: per layer QKV [(nq+2nkv)/t*hd, H], gate||up interleaved in 64-row
+ * blocks [2*H2/t, H], O [H, nq*hd/t], down [H, H2/t]; embedding and final norm replicated; LM
+ * head vocab-parallel [ceil(V/t), H].  Ownership: the library owns all device memory.
+ * Errors: EINVAL (bad config / divisibility by world), ECUDA (allocation), ENCCL. */
+int sarathi_init_model(const sarathi_model_config* cfg, const sarathi_dist* dist, uint64_t weight_seed,
+                       sarathi_model** out);
+
+void sarathi_destroy(sarathi_model* m);
+
+/* Allocates the paged KV pools: per layer K and V, bf16 [num_blocks][n_kv/t][block_size][hd].
+ * block_size: multiple of 16 in [16, 256].  Call once, after init, before any request.
+ * Errors: EINVAL, ESTATE (already allocated), ECUDA (out of memory). */
+int sarathi_alloc_kv(sarathi_model* m, int64_t num_blocks, int32_t block_size);
+
+/* Bytes of KV cache one token occupies on this rank over all layers, m_kv (reading O-18). */
+int sarathi_kv_bytes_per_token(const sarathi_model* m, int64_t* out);
+
+/* Max batch B = floor((M_G - M_S) / (L * m_kv)) (§4.3) where M_G - M_S is the device
+ * memory currently free minus reserve_bytes and L = tokens_per_request.  Host + cudaMemGetInfo. */
+int sarathi_max_batch(const sarathi_model* m, int32_t tokens_per_request, int64_t reserve_bytes, int32_t* B_out);
+
+/* Reserves ceil(max_tokens / block_size) KV blocks for req_id, lowest-free-block-first
+ * (reading O-17), i.e. the paper's up-front pre-allocation.  cached length := 0.
+ * Errors: EINVAL (max_tokens < 1 or > max_seq_len, or id in use), ENOKV, ESTATE. */
+int sarathi_request_alloc(sarathi_model* m, int64_t req_id, int32_t max_tokens);
+/* Releases the request's blocks.  EUNKNOWN_REQ. */
+int sarathi_request_free(sarathi_model* m, int64_t req_id);
+/* Current cached length (tokens whose K,V are in the cache).  EUNKNOWN_REQ. */
+int sarathi_request_cached_len(const sarathi_model* m, int64_t req_id, int32_t* len_out);
+
+/* One prefill chunk: token_ids[n_tokens] (host) at positions start_pos .. start_pos+n_tokens-1.
+ * start_pos must equal the request's cached length (chunk j of §4.2). */
+typedef struct {
+  int64_t req_id;
+  int32_t start_pos;
+  int32_t n_tokens;
+  const int32_t* token_ids;
+} sarathi_prefill_chunk;
+
+/* d single-token decodes of other requests (host arrays of length n).  positions[i] must equal
+ * the cached length of req_ids[i]; each request at most once per batch. */
+typedef struct {
+  int32_t n;
+  const int64_t* req_ids;
+  const int32_t* token_ids;
+  const int32_t* positions;
+} sarathi_decode_set;
+
+#define SARATHI_RETURN_ALL_ROWS 1 /* logits for all T rows (chunk rows then decodes) instead of R */
+#define SARATHI_DUMP_LAYERS 2     /* keep every layer's residual for sarathi_debug_hidden        */
+#define SARATHI_LOGITS_HOST 4     /* `logits` is pinned/pageable HOST memory: copy D2H + sync    */
+#define SARATHI_NO_LOGITS 8       /* skip final norm + LM head (e.g. non-final prefill chunks)   */
+
+/* Runs one hybrid batch (§4.3): token matrix = [chunk tokens (p) ; decode tokens (d)], T = p + d,
+ * 1 <= T <= max_tokens_per_batch.  prefill may be NULL (decode-only batch, the paper's baseline
+ * P:L26) and decodes may be NULL or n == 0 (prefill-only batch).
+ * logits: fp32 [R][V] (device memory unless SARATHI_LOGITS_HOST), R = d + (prefill ? 1 : 0),
+ *   row 0 = the chunk's LAST token, then decodes in decode-set order (reading O-11);
+ *   with SARATHI_RETURN_ALL_ROWS, R = T rows in token-matrix order.
+ * Effects: K,V of all T tokens appended in place; cached lengths advance by p (chunk) and 1
+ *   (each decode).  Under TP the full [R][V] logits are produced on every rank.
+ * Errors (state unchanged): EINVAL, EUNKNOWN_REQ, EDUP, EPOS, EOVERFLOW, ESTATE; ECUDA/ENCCL
+ *   after enqueue (state undefined). */
+int sarathi_run_hybrid_batch(sarathi_model* m, const sarathi_prefill_chunk* prefill, const sarathi_decode_set* decodes,
+                             float* logits, int32_t flags);
+
+/* Rolls a request back to new_len cached tokens (new_len <= current cached length); its later KV
+ * slots are overwritten by subsequent appends.  Used to replay one fixed batch composition in
+ * benchmarks.  EUNKNOWN_REQ, EINVAL. */
+int sarathi_request_truncate(sarathi_model* m, int64_t req_id, int32_t new_len);
+
+/* Bytes the last sarathi_run_hybrid_batch moved host->device (batch metadata: token ids, positions,
+ * slots, block tables) and device->host (logits, only with SARATHI_LOGITS_HOST). */
+int sarathi_last_io_bytes(const sarathi_model* m, int64_t* h2d, int64_t* d2h);
+
+/* Per-op CUDA-event timers (SURVEY §5 tracing).  When enabled, every kernel group of
+ * run_hybrid_batch is bracketed by events on the model stream; sarathi_op_times synchronises the
+ * stream and returns the accumulated milliseconds and launch counts per op id since the last
+ * reset (reset = 1 clears them after reading).  Op ids: SARATHI_OP_*. */
+#define SARATHI_OP_EMBED 0
+#define SARATHI_OP_RMSNORM 1
+#define SARATHI_OP_GEMM_QKV 2
+#define SARATHI_OP_PREFILL_ATTN 3
+#define SARATHI_OP_DECODE_ATTN 4
+#define SARATHI_OP_GEMM_O 5
+#define SARATHI_OP_GEMM_GATE_UP 6
+#define SARATHI_OP_GEMM_DOWN 7
+#define SARATHI_OP_LM_HEAD 8
+#define SARATHI_OP_ALLREDUCE 9
+#define SARATHI_OP_OTHER 10
+#define SARATHI_NUM_OPS 11
+int sarathi_set_profiling(sarathi_model* m, int32_t enable);
+int sarathi_op_times(sarathi_model* m, double* ms_out, int64_t* counts_out, int32_t n, int32_t reset);
+
+/* ---- debug / parity hooks (host outputs, synchronise the stream) ------------------------ */
+/* slot mapping of the last batch: out[T] with slot = table[pos / bs] * bs + pos % bs. */
+int sarathi_debug_slot_mapping(const sarathi_model* m, int32_t* out, int32_t cap, int32_t* T_out);
+/* block table of a request: out[n]. */
+int sarathi_debug_block_table(const sarathi_model* m, int64_t req_id, int32_t* out, int32_t cap, int32_t* n_out);
+/* residual stream h (fp32 [T][H]) after `layer` (0-based) of the last batch run with
+ * SARATHI_DUMP_LAYERS; layer == -1 gives the embedding output (input of layer 0). */
+int sarathi_debug_hidden(const sarathi_model* m, int32_t layer, float* host_out);
+/* K and V (bf16 bits, [n][n_kv/t][hd] each) of positions pos0..pos0+n-1 of a request, layer l. */
+int sarathi_debug_kv(const sarathi_model* m, int32_t layer, int64_t req_id, int32_t pos0, int32_t n,
+                     uint16_t* host_k, uint16_t* host_v);
+/* Copies `count` bf16 values (bits) of a packed weight tensor, starting at element `offset`.
+ * tensor: 0 qkv, 1 o, 2 gate||up, 3 down, 4 g1, 5 g2 (per layer); 16 emb, 17 final gain, 18 lm head. */
+int sarathi_debug_weight(const sarathi_model* m, int32_t layer, int32_t tensor, int64_t offset, int64_t count,
+                         uint16_t* host_out);
+/* Number of kernels this library launched since the handle was created (gpu_launches). */
+int sarathi_launch_count(const sarathi_model* m, int64_t* out);
+
+const char* sarathi_last_error(void);
+
+/* ---- host-side scheduler (decode-maximal batching, §4.3) — no CUDA --------------------- */
+/* Policy (reading O-16): FCFS admission by (arrival, id) while fewer than B requests run and the
+ * full (P+D)-token KV reservation fits in the sched's own block allocator (lowest-free-first,
+ * same algorithm as the model's); batch = <= 1 chunk of min(C_eff, P - done) from the oldest
+ * running request with prefill left (C_eff = C, or C-(B-1) with tile_adjust) + every
+ * decode-phase request in admission order, at most B-1 with a chunk and B without.
+ * SARATHI_POLICY_ORCA_BEST: C_eff = the full remaining prompt.
+ * SARATHI_POLICY_REQUEST_LEVEL: cohorts; prompts as prefill-only batches, then decode-only. */
+#define SARATHI_POLICY_SARATHI 0
+#define SARATHI_POLICY_ORCA_BEST 1
+#define SARATHI_POLICY_REQUEST_LEVEL 2
+
+typedef struct sarathi_sched sarathi_sched;
+
+typedef struct {
+  int32_t iteration;
+  int64_t prefill_req; /* -1 if no chunk */
+  int32_t prefill_start;
+  int32_t prefill_len;
+  int32_t n_decodes;
+  int32_t n_admitted; /* requests admitted while forming this plan (call request_alloc for them) */
+} sarathi_plan;
+
+int sarathi_sched_create(int32_t B, int32_t C, int32_t policy, int32_t tile_adjust, int64_t num_blocks,
+                         int32_t block_size, sarathi_sched** out);
+void sarathi_sched_destroy(sarathi_sched* s);
+/* P >= 1, D >= 0.  EINVAL on duplicate id. */
+int sarathi_sched_submit(sarathi_sched* s, int64_t req_id, int32_t P, int32_t D, int32_t arrival_iter);
+/* Forms the next plan.  Returns 1 with a plan, 0 if idle (nothing eligible this iteration; call
+ * sarathi_sched_idle_step), <0 on error.  dec_req[cap], dec_pos[cap], admitted[cap] receive the
+ * decode items and newly admitted ids; EINVAL if cap is too small. */
+int sarathi_sched_next(sarathi_sched* s, sarathi_plan* plan, int64_t* dec_req, int32_t* dec_pos, int64_t* admitted,
+                       int32_t cap);
+/* Marks the last plan as executed; finished[cap] receives requests that completed (free their KV). */
+int sarathi_sched_complete(sarathi_sched* s, int64_t* finished, int32_t cap, int32_t* n_finished);
+int sarathi_sched_idle_step(sarathi_sched* s);
+int sarathi_sched_done(const sarathi_sched* s, int32_t* done);
+int sarathi_sched_block_table(const sarathi_sched* s, int64_t req_id, int32_t* out, int32_t cap, int32_t* n_out);
+
+/* ---- kernel-level entry points (device pointers, caller's stream) for parity tests ------ */
+/* out = X · Wᵀ on tcgen05: W bf16 [M][K] (K-major), X bf16 [N][K]; mode 0: out bf16 [N][M],
+ * 1: out fp32 [N][M], 2: out fp32 += (residual add), 3: SiLU(gate)·up with gate/up interleaved in
+ * 64-row blocks of W -> out bf16 [N][M/2], 4: GELU-tanh -> bf16.  K % 64 == 0, N >= 1.
+ * force_splits > 0 forces the split-K factor (else heuristic). */
+int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t N, int32_t K, int32_t mode,
+                    int32_t force_splits, void* stream);
+/* out[r] = bf16(RMSNorm(h[r]) * g), h fp32 [R][H], g bf16 [H]. */
+int sarathi_op_rmsnorm(const float* h, const void* g, void* out, int32_t R, int32_t H, float eps, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SARATHI_H_ */

@@ -1,0 +1,378 @@
+// extern "C" boundary (include/sarathi.h): argument checks, status codes, thread-local errors.
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/sarathi.h"
+#include "model.hpp"
+
+struct sarathi_model {
+  sarathi::Model m;
+};
+struct sarathi_sched {
+  sarathi::Scheduler* s = nullptr;
+  sarathi::PlanOut last;
+};
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int from(const sarathi::Status& s) {
+  if (s.code != SARATHI_OK) g_err = s.msg;
+  return s.code;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sarathi_last_error(void) { return g_err.c_str(); }
+
+int sarathi_nccl_unique_id(void* out128) {
+  if (!out128) return fail(SARATHI_EINVAL, "nccl_unique_id: NULL");
+  std::string err;
+  const int r = sarathi::nccl_unique_id(out128, &err);
+  if (r != SARATHI_OK) return fail(r, err);
+  return SARATHI_OK;
+}
+
+int sarathi_init_model(const sarathi_model_config* cfg, const sarathi_dist* dist, uint64_t weight_seed,
+                       sarathi_model** out) {
+  if (!cfg || !dist || !out) return fail(SARATHI_EINVAL, "init_model: NULL argument");
+  auto* h = new (std::nothrow) sarathi_model();
+  if (!h) return fail(SARATHI_EINVAL, "init_model: out of host memory");
+  const sarathi::Status s = h->m.init(*cfg, *dist, weight_seed);
+  if (s.code != SARATHI_OK) {
+    h->m.destroy();
+    delete h;
+    return from(s);
+  }
+  *out = h;
+  return SARATHI_OK;
+}
+
+void sarathi_destroy(sarathi_model* m) {
+  if (!m) return;
+  m->m.destroy();
+  delete m;
+}
+
+int sarathi_alloc_kv(sarathi_model* m, int64_t num_blocks, int32_t block_size) {
+  if (!m) return fail(SARATHI_EINVAL, "alloc_kv: NULL model");
+  return from(m->m.alloc_kv(num_blocks, block_size));
+}
+
+int sarathi_kv_bytes_per_token(const sarathi_model* m, int64_t* out) {
+  if (!m || !out) return fail(SARATHI_EINVAL, "kv_bytes_per_token: NULL");
+  *out = 2ll * m->m.cfg.n_layers * m->m.nkv_l * m->m.cfg.head_dim * 2;
+  return SARATHI_OK;
+}
+
+int sarathi_max_batch(const sarathi_model* m, int32_t tokens_per_request, int64_t reserve_bytes, int32_t* B_out) {
+  if (!m || !B_out || tokens_per_request < 1) return fail(SARATHI_EINVAL, "max_batch: bad argument");
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return fail(SARATHI_ECUDA, "cudaMemGetInfo failed");
+  const double num = static_cast<double>(fr) - static_cast<double>(reserve_bytes);
+  const double mkv = 2.0 * m->m.cfg.n_layers * m->m.nkv_l * m->m.cfg.head_dim * 2;
+  *B_out = num <= 0 ? 0 : static_cast<int32_t>(num / (tokens_per_request * mkv));
+  return SARATHI_OK;
+}
+
+int sarathi_request_alloc(sarathi_model* m, int64_t req_id, int32_t max_tokens) {
+  if (!m) return fail(SARATHI_EINVAL, "request_alloc: NULL model");
+  auto& M = m->m;
+  if (!M.kv_ready) return fail(SARATHI_ESTATE, "request_alloc: alloc_kv not called");
+  if (max_tokens < 1 || max_tokens > M.cfg.max_seq_len) return fail(SARATHI_EINVAL, "request_alloc: max_tokens out of range");
+  if (M.alloc.has(req_id)) return fail(SARATHI_EINVAL, "request_alloc: id already allocated");
+  if (!M.alloc.alloc(req_id, max_tokens)) return fail(SARATHI_ENOKV, "request_alloc: not enough free KV blocks");
+  M.cached[req_id] = 0;
+  return SARATHI_OK;
+}
+
+int sarathi_request_free(sarathi_model* m, int64_t req_id) {
+  if (!m) return fail(SARATHI_EINVAL, "request_free: NULL model");
+  if (!m->m.alloc.has(req_id)) return fail(SARATHI_EUNKNOWN_REQ, "request_free: unknown request");
+  m->m.alloc.free(req_id);
+  m->m.cached.erase(req_id);
+  return SARATHI_OK;
+}
+
+int sarathi_request_cached_len(const sarathi_model* m, int64_t req_id, int32_t* len_out) {
+  if (!m || !len_out) return fail(SARATHI_EINVAL, "request_cached_len: NULL");
+  auto it = m->m.cached.find(req_id);
+  if (it == m->m.cached.end()) return fail(SARATHI_EUNKNOWN_REQ, "request_cached_len: unknown request");
+  *len_out = it->second;
+  return SARATHI_OK;
+}
+
+int sarathi_request_truncate(sarathi_model* m, int64_t req_id, int32_t new_len) {
+  if (!m) return fail(SARATHI_EINVAL, "request_truncate: NULL model");
+  auto it = m->m.cached.find(req_id);
+  if (it == m->m.cached.end()) return fail(SARATHI_EUNKNOWN_REQ, "request_truncate: unknown request");
+  if (new_len < 0 || new_len > it->second) return fail(SARATHI_EINVAL, "request_truncate: new_len > cached length");
+  it->second = new_len;
+  return SARATHI_OK;
+}
+
+int sarathi_last_io_bytes(const sarathi_model* m, int64_t* h2d, int64_t* d2h) {
+  if (!m || !h2d || !d2h) return fail(SARATHI_EINVAL, "last_io_bytes: NULL");
+  *h2d = m->m.last_h2d;
+  *d2h = m->m.last_d2h;
+  return SARATHI_OK;
+}
+
+int sarathi_set_profiling(sarathi_model* m, int32_t enable) {
+  if (!m) return fail(SARATHI_EINVAL, "set_profiling: NULL");
+  m->m.profiling = enable != 0;
+  return SARATHI_OK;
+}
+
+int sarathi_op_times(sarathi_model* m, double* ms_out, int64_t* counts_out, int32_t n, int32_t reset) {
+  if (!m || !ms_out || !counts_out || n < SARATHI_NUM_OPS) return fail(SARATHI_EINVAL, "op_times: bad argument");
+  const sarathi::Status s = m->m.collect_op_times();
+  if (s.code != SARATHI_OK) return from(s);
+  for (int i = 0; i < SARATHI_NUM_OPS; ++i) {
+    ms_out[i] = m->m.op_ms[i];
+    counts_out[i] = m->m.op_count[i];
+    if (reset) {
+      m->m.op_ms[i] = 0;
+      m->m.op_count[i] = 0;
+    }
+  }
+  return SARATHI_OK;
+}
+
+int sarathi_run_hybrid_batch(sarathi_model* m, const sarathi_prefill_chunk* prefill, const sarathi_decode_set* decodes,
+                             float* logits, int32_t flags) {
+  if (!m) return fail(SARATHI_EINVAL, "run_hybrid_batch: NULL model");
+  return from(m->m.run(prefill, decodes, logits, flags));
+}
+
+int sarathi_debug_slot_mapping(const sarathi_model* m, int32_t* out, int32_t cap, int32_t* T_out) {
+  if (!m || !T_out) return fail(SARATHI_EINVAL, "debug_slot_mapping: NULL");
+  const auto& s = m->m.last_slots;
+  *T_out = static_cast<int32_t>(s.size());
+  if (out) {
+    if (cap < static_cast<int32_t>(s.size())) return fail(SARATHI_EINVAL, "debug_slot_mapping: cap too small");
+    std::memcpy(out, s.data(), s.size() * sizeof(int32_t));
+  }
+  return SARATHI_OK;
+}
+
+int sarathi_debug_block_table(const sarathi_model* m, int64_t req_id, int32_t* out, int32_t cap, int32_t* n_out) {
+  if (!m || !n_out) return fail(SARATHI_EINVAL, "debug_block_table: NULL");
+  if (!m->m.alloc.has(req_id)) return fail(SARATHI_EUNKNOWN_REQ, "debug_block_table: unknown request");
+  const auto& t = m->m.alloc.table(req_id);
+  *n_out = static_cast<int32_t>(t.size());
+  if (out) {
+    if (cap < static_cast<int32_t>(t.size())) return fail(SARATHI_EINVAL, "debug_block_table: cap too small");
+    std::memcpy(out, t.data(), t.size() * sizeof(int32_t));
+  }
+  return SARATHI_OK;
+}
+
+int sarathi_debug_hidden(const sarathi_model* m, int32_t layer, float* host_out) {
+  if (!m || !host_out) return fail(SARATHI_EINVAL, "debug_hidden: NULL");
+  const auto& M = m->m;
+  if (!M.last_dumped || !M.dump) return fail(SARATHI_ESTATE, "debug_hidden: last batch not run with DUMP_LAYERS");
+  if (layer < -1 || layer >= M.cfg.n_layers) return fail(SARATHI_EINVAL, "debug_hidden: layer out of range");
+  cudaStreamSynchronize(M.stream);
+  const size_t n = static_cast<size_t>(M.last_T) * M.cfg.hidden;
+  if (cudaMemcpy(host_out, M.dump + static_cast<size_t>(layer + 1) * M.Tmax * M.cfg.hidden, n * 4,
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(SARATHI_ECUDA, "debug_hidden: copy failed");
+  return SARATHI_OK;
+}
+
+int sarathi_debug_kv(const sarathi_model* m, int32_t layer, int64_t req_id, int32_t pos0, int32_t n, uint16_t* host_k,
+                     uint16_t* host_v) {
+  if (!m || !host_k || !host_v) return fail(SARATHI_EINVAL, "debug_kv: NULL");
+  const auto& M = m->m;
+  if (!M.kv_ready || layer < 0 || layer >= M.cfg.n_layers) return fail(SARATHI_EINVAL, "debug_kv: bad layer/state");
+  if (!M.alloc.has(req_id)) return fail(SARATHI_EUNKNOWN_REQ, "debug_kv: unknown request");
+  if (pos0 < 0 || n < 0 || pos0 + n > M.alloc.reserved(req_id)) return fail(SARATHI_EINVAL, "debug_kv: range");
+  cudaStreamSynchronize(M.stream);
+  const int hd = M.cfg.head_dim, bs = M.block_size;
+  for (int i = 0; i < n; ++i) {
+    const int64_t sl = M.alloc.slot(req_id, pos0 + i);
+    for (int hh = 0; hh < M.nkv_l; ++hh) {
+      const size_t row = (static_cast<size_t>(sl / bs) * M.nkv_l + hh) * bs + sl % bs;
+      const size_t dst = (static_cast<size_t>(i) * M.nkv_l + hh) * hd;
+      if (cudaMemcpy(host_k + dst, M.kpool[layer] + row * hd, hd * 2, cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(host_v + dst, M.vpool[layer] + row * hd, hd * 2, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return fail(SARATHI_ECUDA, "debug_kv: copy failed");
+    }
+  }
+  return SARATHI_OK;
+}
+
+int sarathi_debug_weight(const sarathi_model* m, int32_t layer, int32_t tensor, int64_t offset, int64_t count,
+                         uint16_t* host_out) {
+  if (!m || !host_out || offset < 0 || count < 0) return fail(SARATHI_EINVAL, "debug_weight: bad argument");
+  const auto& M = m->m;
+  const __nv_bfloat16* src = nullptr;
+  size_t total = 0;
+  const size_t H = M.cfg.hidden;
+  if (tensor < 16) {
+    if (layer < 0 || layer >= M.cfg.n_layers) return fail(SARATHI_EINVAL, "debug_weight: layer");
+    const auto& w = M.layers[layer];
+    switch (tensor) {
+      case 0: src = w.qkv; total = static_cast<size_t>(M.qkv_rows) * H; break;
+      case 1: src = w.o; total = H * M.q_dim_l; break;
+      case 2: src = w.gu; total = static_cast<size_t>(M.gu_rows) * H; break;
+      case 3: src = w.down; total = H * M.h2_l; break;
+      case 4: src = w.g1; total = H; break;
+      case 5: src = w.g2; total = H; break;
+      default: return fail(SARATHI_EINVAL, "debug_weight: tensor");
+    }
+  } else {
+    switch (tensor) {
+      case 16: src = M.emb; total = static_cast<size_t>(M.cfg.vocab) * H; break;
+      case 17: src = M.gf; total = H; break;
+      case 18: src = M.lm; total = static_cast<size_t>(M.vocab_l) * H; break;
+      default: return fail(SARATHI_EINVAL, "debug_weight: tensor");
+    }
+  }
+  if (static_cast<size_t>(offset + count) > total) return fail(SARATHI_EINVAL, "debug_weight: range");
+  cudaStreamSynchronize(M.stream);
+  if (cudaMemcpy(host_out, src + offset, count * 2, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(SARATHI_ECUDA, "debug_weight: copy failed");
+  return SARATHI_OK;
+}
+
+int sarathi_launch_count(const sarathi_model* m, int64_t* out) {
+  if (!m || !out) return fail(SARATHI_EINVAL, "launch_count: NULL");
+  *out = m->m.launches;
+  return SARATHI_OK;
+}
+
+// ---- scheduler ----
+int sarathi_sched_create(int32_t B, int32_t C, int32_t policy, int32_t tile_adjust, int64_t num_blocks,
+                         int32_t block_size, sarathi_sched** out) {
+  if (!out || B < 1 || C < 1 || policy < 0 || policy > 2 || num_blocks < 0 || block_size < 1)
+    return fail(SARATHI_EINVAL, "sched_create: bad argument");
+  if (tile_adjust && C <= B - 1) return fail(SARATHI_EINVAL, "sched_create: tile-adjusted chunk C-(B-1) must be >= 1");
+  auto* s = new (std::nothrow) sarathi_sched();
+  if (!s) return fail(SARATHI_EINVAL, "sched_create: out of memory");
+  s->s = new sarathi::Scheduler(B, C, policy, tile_adjust != 0, num_blocks, block_size);
+  *out = s;
+  return SARATHI_OK;
+}
+
+void sarathi_sched_destroy(sarathi_sched* s) {
+  if (!s) return;
+  delete s->s;
+  delete s;
+}
+
+int sarathi_sched_submit(sarathi_sched* s, int64_t req_id, int32_t P, int32_t D, int32_t arrival_iter) {
+  if (!s) return fail(SARATHI_EINVAL, "sched_submit: NULL");
+  std::string err;
+  if (!s->s->submit(req_id, P, D, arrival_iter, &err)) return fail(SARATHI_EINVAL, err);
+  return SARATHI_OK;
+}
+
+int sarathi_sched_next(sarathi_sched* s, sarathi_plan* plan, int64_t* dec_req, int32_t* dec_pos, int64_t* admitted,
+                       int32_t cap) {
+  if (!s || !plan) return fail(SARATHI_EINVAL, "sched_next: NULL");
+  sarathi::PlanOut p;
+  const bool have = s->s->next(&p);
+  if (static_cast<int32_t>(p.decodes.size()) > cap || static_cast<int32_t>(p.admitted.size()) > cap)
+    return fail(SARATHI_EINVAL, "sched_next: cap too small");
+  plan->iteration = p.iteration;
+  plan->prefill_req = p.prefill_req;
+  plan->prefill_start = p.prefill_start;
+  plan->prefill_len = p.prefill_len;
+  plan->n_decodes = static_cast<int32_t>(p.decodes.size());
+  plan->n_admitted = static_cast<int32_t>(p.admitted.size());
+  for (size_t i = 0; i < p.decodes.size(); ++i) {
+    if (dec_req) dec_req[i] = p.decodes[i].first;
+    if (dec_pos) dec_pos[i] = p.decodes[i].second;
+  }
+  for (size_t i = 0; i < p.admitted.size(); ++i)
+    if (admitted) admitted[i] = p.admitted[i];
+  return have ? 1 : 0;
+}
+
+int sarathi_sched_complete(sarathi_sched* s, int64_t* finished, int32_t cap, int32_t* n_finished) {
+  if (!s || !n_finished) return fail(SARATHI_EINVAL, "sched_complete: NULL");
+  const auto fin = s->s->complete();
+  if (static_cast<int32_t>(fin.size()) > cap && finished) return fail(SARATHI_EINVAL, "sched_complete: cap too small");
+  *n_finished = static_cast<int32_t>(fin.size());
+  for (size_t i = 0; i < fin.size(); ++i)
+    if (finished) finished[i] = fin[i];
+  return SARATHI_OK;
+}
+
+int sarathi_sched_idle_step(sarathi_sched* s) {
+  if (!s) return fail(SARATHI_EINVAL, "sched_idle_step: NULL");
+  s->s->idle_step();
+  return SARATHI_OK;
+}
+
+int sarathi_sched_done(const sarathi_sched* s, int32_t* done) {
+  if (!s || !done) return fail(SARATHI_EINVAL, "sched_done: NULL");
+  *done = s->s->done() ? 1 : 0;
+  return SARATHI_OK;
+}
+
+int sarathi_sched_block_table(const sarathi_sched* s, int64_t req_id, int32_t* out, int32_t cap, int32_t* n_out) {
+  if (!s || !n_out) return fail(SARATHI_EINVAL, "sched_block_table: NULL");
+  const auto& a = s->s->allocator();
+  if (!a.has(req_id)) return fail(SARATHI_EUNKNOWN_REQ, "sched_block_table: unknown request");
+  const auto& t = a.table(req_id);
+  *n_out = static_cast<int32_t>(t.size());
+  if (out) {
+    if (cap < static_cast<int32_t>(t.size())) return fail(SARATHI_EINVAL, "sched_block_table: cap");
+    std::memcpy(out, t.data(), t.size() * sizeof(int32_t));
+  }
+  return SARATHI_OK;
+}
+
+// ---- kernel-level ops ----
+int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t N, int32_t K, int32_t mode,
+                    int32_t force_splits, void* stream) {
+  using namespace sarathi;
+  if (!W || !X || !out || M < 1 || N < 1 || K < 64 || K % 64 || mode < 0 || mode > 4)
+    return fail(SARATHI_EINVAL, "op_gemm: bad argument (K % 64 == 0, mode 0..4)");
+  if (mode == EPI_SILU_MUL && M % 128) return fail(SARATHI_EINVAL, "op_gemm: SiLU mode needs M % 128 == 0");
+  static float* ws = nullptr;
+  static int* ctr = nullptr;
+  static size_t ws_floats = static_cast<size_t>(32) << 20;
+  if (!ws) {
+    if (cudaMalloc(&ws, ws_floats * 4) != cudaSuccess || cudaMalloc(&ctr, (1 << 16) * 4) != cudaSuccess ||
+        cudaMemset(ctr, 0, (1 << 16) * 4) != cudaSuccess)
+      return fail(SARATHI_ECUDA, "op_gemm: workspace allocation failed");
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  GemmPlan pl = plan_gemm(M, N, K, sms, ws_floats, force_splits);
+  if (force_splits > 0 && pl.splits != force_splits) return fail(SARATHI_EINVAL, "op_gemm: split factor not realisable");
+  CUtensorMap mw, mx;
+  if (!make_tmap_bf16(&mw, W, M, K, K, 128) || !make_tmap_bf16(&mx, X, N, K, K, pl.bn))
+    return fail(SARATHI_ECUDA, "op_gemm: tensor map encode failed");
+  EpiParams ep;
+  ep.mode = mode;
+  ep.out = out;
+  ep.ldo = mode == EPI_SILU_MUL ? M / 2 : M;
+  ep.ws = ws;
+  ep.counters = ctr;
+  const cudaError_t e = launch_gemm(mw, mx, pl, ep, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(SARATHI_ECUDA, std::string("op_gemm: ") + cudaGetErrorString(e));
+  return SARATHI_OK;
+}
+
+int sarathi_op_rmsnorm(const float* h, const void* g, void* out, int32_t R, int32_t H, float eps, void* stream) {
+  if (!h || !g || !out || R < 0 || H < 4 || H % 4) return fail(SARATHI_EINVAL, "op_rmsnorm: bad argument");
+  const cudaError_t e = sarathi::launch_rmsnorm(const_cast<float*>(h), nullptr, static_cast<const __nv_bfloat16*>(g),
+                                                static_cast<__nv_bfloat16*>(out), nullptr, R, H, eps,
+                                                static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(SARATHI_ECUDA, std::string("op_rmsnorm: ") + cudaGetErrorString(e));
+  return SARATHI_OK;
+}
+
+}  // extern "C"

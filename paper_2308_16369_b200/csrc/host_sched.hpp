@@ -1,0 +1,86 @@
+// Host-side KV block allocator and decode-maximal batching scheduler (pure C++, no CUDA).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <set>
+#include <string>
+#include <vector>
+
+namespace sarathi {
+
+// Paged KV block allocator: a request reserves ceil(max_tokens / bs) blocks up front (the paper
+// pre-allocates KV per maximum sequence length, §4.5), lowest-free-block-first
+// (reading O-17) so the tables are deterministic and identical on every TP rank.
+class BlockAllocator {
+ public:
+  BlockAllocator() = default;
+  BlockAllocator(int64_t num_blocks, int32_t block_size);
+  int64_t num_blocks() const { return num_blocks_; }
+  int32_t block_size() const { return block_size_; }
+  int64_t blocks_for(int64_t max_tokens) const { return (max_tokens + block_size_ - 1) / block_size_; }
+  bool can_alloc(int64_t max_tokens) const { return blocks_for(max_tokens) <= static_cast<int64_t>(free_.size()); }
+  bool has(int64_t req) const { return tables_.count(req) != 0; }
+  // returns false if it does not fit
+  bool alloc(int64_t req, int32_t max_tokens);
+  void free(int64_t req);
+  const std::vector<int32_t>& table(int64_t req) const { return tables_.at(req); }
+  int32_t reserved(int64_t req) const { return reserved_.at(req); }
+  int64_t free_blocks() const { return static_cast<int64_t>(free_.size()); }
+  // slot = table[pos / bs] * bs + pos % bs
+  int64_t slot(int64_t req, int32_t pos) const {
+    const auto& t = tables_.at(req);
+    return static_cast<int64_t>(t[pos / block_size_]) * block_size_ + pos % block_size_;
+  }
+
+ private:
+  int64_t num_blocks_ = 0;
+  int32_t block_size_ = 1;
+  std::set<int32_t> free_;
+  std::map<int64_t, std::vector<int32_t>> tables_;
+  std::map<int64_t, int32_t> reserved_;
+};
+
+struct PlanOut {
+  int32_t iteration = 0;
+  int64_t prefill_req = -1;
+  int32_t prefill_start = 0, prefill_len = 0;
+  std::vector<std::pair<int64_t, int32_t>> decodes;  // (req, position)
+  std::vector<int64_t> admitted;
+};
+
+// Decode-maximal batching (§4.3) with the paper's comparison policies
+// (request-level baseline P:L26, Orca best case P:L104).  Mirrors the policy statement in
+// include/sarathi.h; the Python twin in oracle/sched.py is an independent implementation.
+class Scheduler {
+ public:
+  enum Policy { SARATHI = 0, ORCA_BEST = 1, REQUEST_LEVEL = 2 };
+  Scheduler(int32_t B, int32_t C, int32_t policy, bool tile_adjust, int64_t num_blocks, int32_t block_size);
+  bool submit(int64_t req, int32_t P, int32_t D, int32_t arrival, std::string* err);
+  // true if a plan was formed
+  bool next(PlanOut* out);
+  std::vector<int64_t> complete();
+  void idle_step() { ++iteration_; }
+  bool done() const;
+  const BlockAllocator& allocator() const { return alloc_; }
+
+ private:
+  struct Req {
+    int64_t id;
+    int32_t P, D, arrival;
+    int32_t prefill_done = 0, decode_done = 0;
+    bool admitted = false, finished = false;
+    int64_t admit_seq = -1;
+  };
+  std::vector<Req*> running();
+  int32_t B_, C_, policy_;
+  bool tile_adjust_;
+  BlockAllocator alloc_;
+  std::map<int64_t, Req> reqs_;
+  int32_t iteration_ = 0;
+  int64_t admit_counter_ = 0;
+  bool have_plan_ = false;
+  PlanOut last_;
+};
+
+}  // namespace sarathi

@@ -1,0 +1,72 @@
+// Host-visible declarations of the non-GEMM kernels.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace sarathi {
+
+struct DecodeAttnArgs {
+  const __nv_bfloat16* q = nullptr;  // [T][q_ld]; decode j reads row q_row0 + j
+  int q_ld = 0;
+  int q_row0 = 0;
+  const void* kcache = nullptr;  // bf16 [num_blocks][n_kv_local][block_size][head_dim]
+  const void* vcache = nullptr;
+  const int* block_tables = nullptr;  // [d][max_blocks]
+  const int* ctx = nullptr;           // [d] keys to attend (= position + 1)
+  int max_blocks = 0;
+  int d = 0;
+  int n_q_local = 0, n_kv_local = 0, head_dim = 128, block_size = 64;
+  float scale = 0.f;
+  int splits = 1, blocks_per_split = 1, stages = 2;
+  float* part_o = nullptr;    // [d][n_q_local][splits][head_dim]
+  float* part_lse = nullptr;  // [d][n_q_local][splits]
+  __nv_bfloat16* out = nullptr;  // [T][out_ld]; row q_row0 + j
+  int out_ld = 0;
+};
+
+struct PrefillAttnArgs {
+  const __nv_bfloat16* q = nullptr;  // [T][q_ld], chunk rows q_row0 .. q_row0+p-1
+  int q_ld = 0;
+  int q_row0 = 0;
+  const void* kcache = nullptr;
+  const void* vcache = nullptr;
+  const int* block_table = nullptr;  // [max_blocks] of the prefill request
+  int start = 0;  // s: tokens cached before the chunk
+  int p = 0;      // chunk tokens
+  int n_q_local = 0, n_kv_local = 0, head_dim = 128, block_size = 64;
+  float scale = 0.f;
+  __nv_bfloat16* out = nullptr;
+  int out_ld = 0;
+};
+
+size_t decode_smem_bytes(int head_dim, int block_size, int stages, int G);
+cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
+cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t st);
+
+// h[t][:] = float(E[tok[t]][:])
+cudaError_t launch_embedding(const int* tok, const __nv_bfloat16* E, float* h, int T, int H, cudaStream_t st);
+
+// out[r][:] = bf16(RMSNorm(h[row(r)]) * g); row(r) = rows ? rows[r] : r.
+// If add != nullptr (TP all-reduced partial, bf16): h[row] += add[row] first and h is updated.
+cudaError_t launch_rmsnorm(float* h, const __nv_bfloat16* add, const __nv_bfloat16* g, __nv_bfloat16* out,
+                           const int* rows, int R, int H, float eps, cudaStream_t st);
+
+// h[t][:] += add[t][:] (bf16 -> fp32), no norm (last layer under TP before the final norm)
+cudaError_t launch_residual_add(float* h, const __nv_bfloat16* add, int T, int H, cudaStream_t st);
+
+// logits[r][rank*Vl + c] = gathered[rank][r][c]  (vocab-parallel all-gather layout -> [R][V])
+cudaError_t launch_vocab_permute(const float* gathered, float* logits, int world, int R, int Vl, int V,
+                                 cudaStream_t st);
+
+// Device weight generator (same counter-based spec as synth/__init__.py, independent code).
+// dst[r][c] = bf16_rne( f32(2*u24 - (2^24-1)) * scale[r] ), u24 = splitmix64(seed ^ (tau[r] << 40 | base[r] + c)) >> 40
+cudaError_t launch_weightgen(__nv_bfloat16* dst, int rows, int cols, const int* tau, const float* scale,
+                             const long long* base, unsigned long long seed, cudaStream_t st);
+// dst[i] = bf16_rne( 1.0f + f32(v) * f32(0.1/2^24) )  over flat indices [base, base+n)
+cudaError_t launch_gaingen(__nv_bfloat16* dst, int n, int tau, long long base, unsigned long long seed,
+                           cudaStream_t st);
+
+}  // namespace sarathi

@@ -1,0 +1,695 @@
+// Engine behind the C ABI: model init (device-side weight generation), paged KV pools, and the
+// per-iteration kernel sequence of one decode-maximal hybrid batch (§4.3).
+//
+// Per layer l (PAPER.md L193-203 block; TP per L249 §2.3):
+//   a  = RMSNorm(h; g1)                           [rmsnorm kernel; + pending TP all-reduce]
+//   q,K,V = a Wqkv^T, RoPE, KV append at slot[t]  [tcgen05 GEMM, EPI_QKV_ROPE]
+//   o[0:p]  = prefill attention (chunk rows)      [prefill_attention]
+//   o[p:T]  = decode attention (decode rows)      [decode_attention (+combine)]
+//   h += o Wo^T                                   [GEMM EPI_ADD_F32 | TP: bf16 partial + ncclAllReduce]
+//   b  = RMSNorm(h; g2)
+//   f  = SiLU(b Wg^T) * (b Wu^T)                  [GEMM EPI_SILU_MUL | GELU: EPI_GELU]
+//   h += f Wd^T                                   [GEMM EPI_ADD_F32 | TP: bf16 partial + ncclAllReduce]
+// then logits = RMSNorm(h[rows]; g_f) Wlm^T for the R requested rows (vocab-parallel under TP).
+#include "model.hpp"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <set>
+
+namespace sarathi {
+
+namespace {
+
+// ---- NCCL, resolved at run time (only needed for world > 1) ----
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclAllGather) allGather = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+};
+
+NcclApi* nccl_api(std::string* err) {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+      api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+      api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(h, "ncclAllReduce"));
+      api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(h, "ncclAllGather"));
+      api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+      api.errStr = reinterpret_cast<decltype(api.errStr)>(dlsym(h, "ncclGetErrorString"));
+      api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.allGather && api.commDestroy;
+    }
+  }
+  if (!api.ok) {
+    if (err) *err = "NCCL unavailable (dlopen libnccl.so.2 failed; import torch first)";
+    return nullptr;
+  }
+  return &api;
+}
+
+// Counter-based generator constants (synth/__init__.py spec).
+constexpr int kWQ = 0, kWK = 1, kWV = 2, kWO = 3, kWG = 4, kWU = 5, kWD = 6, kG1 = 7, kG2 = 8;
+constexpr int kEmbTau = 1 << 20, kGfTau = (1 << 20) + 1, kWlmTau = (1 << 20) + 2;
+
+float weight_scale(double sigma) { return static_cast<float>(std::sqrt(3.0) * sigma / 16777216.0); }
+
+}  // namespace
+
+int nccl_unique_id(void* out128, std::string* err) {
+  NcclApi* api = nccl_api(err);
+  if (!api) return SARATHI_ENCCL;
+  ncclUniqueId id;
+  if (api->getUniqueId(&id) != ncclSuccess) {
+    if (err) *err = "ncclGetUniqueId failed";
+    return SARATHI_ENCCL;
+  }
+  std::memcpy(out128, &id, sizeof(id));
+  return SARATHI_OK;
+}
+
+Status Model::check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return Status::ok();
+  return Status::err(SARATHI_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename T>
+Status Model::dalloc(T** p, size_t count) {
+  void* ptr = nullptr;
+  cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess) return Status::err(SARATHI_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  allocations.push_back(ptr);
+  *p = static_cast<T*>(ptr);
+  return Status::ok();
+}
+
+#define SRET(x)                  \
+  do {                           \
+    Status _s = (x);             \
+    if (_s.code != SARATHI_OK) return _s; \
+  } while (0)
+
+Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_t seed_) {
+  cfg = c;
+  rank = d.rank;
+  world = d.world;
+  device = d.device;
+  stream = static_cast<cudaStream_t>(d.stream);
+  seed = seed_;
+  const int H = c.hidden, hd = c.head_dim;
+  if (c.n_layers < 1 || H < 64 || H % 64 || (hd != 64 && hd != 128) || c.n_heads < 1 || c.n_kv_heads < 1 ||
+      c.n_heads % c.n_kv_heads || c.vocab < 1 || c.max_seq_len < 1 || c.max_tokens_per_batch < 1 ||
+      c.max_tokens_per_batch > 8192 || (c.ffn_kind != SARATHI_FFN_SWIGLU && c.ffn_kind != SARATHI_FFN_GELU))
+    return Status::err(SARATHI_EINVAL, "init_model: invalid model configuration");
+  if (world < 1 || rank < 0 || rank >= world)
+    return Status::err(SARATHI_EINVAL, "init_model: invalid rank/world");
+  if (c.n_heads % world || c.n_kv_heads % world || c.ffn_hidden % (64 * world) || c.vocab % world)
+    return Status::err(SARATHI_EINVAL,
+                       "init_model: n_heads, n_kv_heads, vocab must divide by world and ffn_hidden by 64*world");
+  const int G = c.n_heads / c.n_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return Status::err(SARATHI_EINVAL, "init_model: GQA group must be 1/2/4/8");
+  nq_l = c.n_heads / world;
+  nkv_l = c.n_kv_heads / world;
+  q_dim_l = nq_l * hd;
+  kv_dim_l = nkv_l * hd;
+  qkv_rows = q_dim_l + 2 * kv_dim_l;
+  h2_l = c.ffn_hidden / world;
+  gu_rows = c.ffn_kind == SARATHI_FFN_SWIGLU ? 2 * h2_l : h2_l;
+  vocab_l = c.vocab / world;
+  if (q_dim_l % 64) return Status::err(SARATHI_EINVAL, "init_model: local q dim must be a multiple of 64");
+  if (qkv_rows % 128 && hd == 128) return Status::err(SARATHI_EINVAL, "init_model: qkv rows not tile aligned");
+  SRET(check(cudaSetDevice(device), "cudaSetDevice"));
+  cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device);
+
+  if (world > 1) {
+    std::string err;
+    NcclApi* api = nccl_api(&err);
+    if (!api) return Status::err(SARATHI_ENCCL, err);
+    if (!d.nccl_unique_id) return Status::err(SARATHI_EINVAL, "init_model: nccl_unique_id required for world > 1");
+    ncclUniqueId id;
+    std::memcpy(&id, d.nccl_unique_id, sizeof(id));
+    ncclComm_t comm;
+    ncclResult_t r = api->commInitRank(&comm, world, id, rank);
+    if (r != ncclSuccess)
+      return Status::err(SARATHI_ENCCL, std::string("ncclCommInitRank: ") + (api->errStr ? api->errStr(r) : "?"));
+    nccl = comm;
+  }
+
+  // ---- weights, generated on device shard by shard ----
+  const int L = c.n_layers;
+  const double s_in = 1.0 / std::sqrt(static_cast<double>(H));
+  const double depth = 1.0 / std::sqrt(2.0 * L);
+  const double s_o = depth / std::sqrt(static_cast<double>(c.n_heads) * hd);
+  const double s_d = depth / std::sqrt(static_cast<double>(c.ffn_hidden));
+  std::vector<int> tau;
+  std::vector<float> scl;
+  std::vector<long long> base;
+  int* d_tau = nullptr;
+  float* d_scl = nullptr;
+  long long* d_base = nullptr;
+  const int max_rows = std::max({qkv_rows, gu_rows, H, vocab_l, c.vocab});
+  SRET(dalloc(&d_tau, max_rows));
+  SRET(dalloc(&d_scl, max_rows));
+  SRET(dalloc(&d_base, max_rows));
+  auto gen = [&](__nv_bfloat16* dst, int rows, int cols) -> Status {
+    SRET(check(cudaMemcpyAsync(d_tau, tau.data(), rows * sizeof(int), cudaMemcpyHostToDevice, stream), "H2D"));
+    SRET(check(cudaMemcpyAsync(d_scl, scl.data(), rows * sizeof(float), cudaMemcpyHostToDevice, stream), "H2D"));
+    SRET(check(cudaMemcpyAsync(d_base, base.data(), rows * sizeof(long long), cudaMemcpyHostToDevice, stream), "H2D"));
+    SRET(check(launch_weightgen(dst, rows, cols, d_tau, d_scl, d_base, seed, stream), "weightgen"));
+    ++launches;
+    return check(cudaStreamSynchronize(stream), "weightgen sync");  // host vectors are reused
+  };
+  auto fill = [&](int rows) {
+    tau.assign(rows, 0);
+    scl.assign(rows, 0.f);
+    base.assign(rows, 0);
+  };
+  layers.resize(L);
+  for (int l = 0; l < L; ++l) {
+    LayerWeights& w = layers[l];
+    SRET(dalloc(&w.qkv, static_cast<size_t>(qkv_rows) * H));
+    SRET(dalloc(&w.o, static_cast<size_t>(H) * q_dim_l));
+    SRET(dalloc(&w.gu, static_cast<size_t>(gu_rows) * H));
+    SRET(dalloc(&w.down, static_cast<size_t>(H) * h2_l));
+    SRET(dalloc(&w.g1, H));
+    SRET(dalloc(&w.g2, H));
+    // QKV: [q_r ; k_r ; v_r], column-parallel (rank's heads of the logical Wq, Wk, Wv)
+    fill(qkv_rows);
+    for (int r = 0; r < qkv_rows; ++r) {
+      long long lrow;
+      int kind;
+      if (r < q_dim_l) {
+        kind = kWQ;
+        lrow = static_cast<long long>(rank) * q_dim_l + r;
+      } else if (r < q_dim_l + kv_dim_l) {
+        kind = kWK;
+        lrow = static_cast<long long>(rank) * kv_dim_l + (r - q_dim_l);
+      } else {
+        kind = kWV;
+        lrow = static_cast<long long>(rank) * kv_dim_l + (r - q_dim_l - kv_dim_l);
+      }
+      tau[r] = 16 * l + kind;
+      scl[r] = weight_scale(s_in);
+      base[r] = lrow * H;
+    }
+    SRET(gen(w.qkv, qkv_rows, H));
+    // O: row-parallel [H][q_dim_l] = columns rank*q_dim_l.. of the logical [H][nq*hd]
+    fill(H);
+    for (int r = 0; r < H; ++r) {
+      tau[r] = 16 * l + kWO;
+      scl[r] = weight_scale(s_o);
+      base[r] = static_cast<long long>(r) * c.n_heads * hd + static_cast<long long>(rank) * q_dim_l;
+    }
+    SRET(gen(w.o, H, q_dim_l));
+    // gate||up interleaved in 64-row blocks (SwiGLU) or W1 (GELU)
+    fill(gu_rows);
+    for (int r = 0; r < gu_rows; ++r) {
+      int kind = kWG;
+      long long fl = r;
+      if (c.ffn_kind == SARATHI_FFN_SWIGLU) {
+        const int blk = r / 128, w2 = r % 128;
+        kind = w2 < 64 ? kWG : kWU;
+        fl = static_cast<long long>(blk) * 64 + (w2 % 64);
+      }
+      tau[r] = 16 * l + kind;
+      scl[r] = weight_scale(s_in);
+      base[r] = (static_cast<long long>(rank) * h2_l + fl) * H;
+    }
+    SRET(gen(w.gu, gu_rows, H));
+    // down: row-parallel [H][h2_l]
+    fill(H);
+    for (int r = 0; r < H; ++r) {
+      tau[r] = 16 * l + kWD;
+      scl[r] = weight_scale(s_d);
+      base[r] = static_cast<long long>(r) * c.ffn_hidden + static_cast<long long>(rank) * h2_l;
+    }
+    SRET(gen(w.down, H, h2_l));
+    SRET(check(launch_gaingen(w.g1, H, 16 * l + kG1, 0, seed, stream), "gaingen"));
+    SRET(check(launch_gaingen(w.g2, H, 16 * l + kG2, 0, seed, stream), "gaingen"));
+    launches += 2;
+    if (!make_tmap_bf16(&w.m_qkv, w.qkv, qkv_rows, H, H, 128) || !make_tmap_bf16(&w.m_o, w.o, H, q_dim_l, q_dim_l, 128) ||
+        !make_tmap_bf16(&w.m_gu, w.gu, gu_rows, H, H, 128) || !make_tmap_bf16(&w.m_down, w.down, H, h2_l, h2_l, 128))
+      return Status::err(SARATHI_ECUDA, "cuTensorMapEncodeTiled failed for a weight");
+  }
+  // embedding (replicated), final gain, LM head (vocab-parallel)
+  SRET(dalloc(&emb, static_cast<size_t>(c.vocab) * H));
+  fill(c.vocab);
+  for (int r = 0; r < c.vocab; ++r) {
+    tau[r] = kEmbTau;
+    scl[r] = weight_scale(1.0);
+    base[r] = static_cast<long long>(r) * H;
+  }
+  SRET(gen(emb, c.vocab, H));
+  SRET(dalloc(&gf, H));
+  SRET(check(launch_gaingen(gf, H, kGfTau, 0, seed, stream), "gaingen"));
+  ++launches;
+  SRET(dalloc(&lm, static_cast<size_t>(vocab_l) * H));
+  fill(vocab_l);
+  for (int r = 0; r < vocab_l; ++r) {
+    tau[r] = kWlmTau;
+    scl[r] = weight_scale(s_in);
+    base[r] = (static_cast<long long>(rank) * vocab_l + r) * H;
+  }
+  SRET(gen(lm, vocab_l, H));
+  if (!make_tmap_bf16(&m_lm, lm, vocab_l, H, H, 128)) return Status::err(SARATHI_ECUDA, "tensor map (lm head)");
+
+  // RoPE tables (fp64 on host -> fp32), reading O-7
+  {
+    const int half = hd / 2;
+    std::vector<float> cs(static_cast<size_t>(c.max_seq_len) * half), sn(cs.size());
+    for (int p = 0; p < c.max_seq_len; ++p)
+      for (int i = 0; i < half; ++i) {
+        const double inv = std::pow(static_cast<double>(c.rope_base), -(2.0 * i) / hd);
+        const double ang = p * inv;
+        cs[static_cast<size_t>(p) * half + i] = static_cast<float>(std::cos(ang));
+        sn[static_cast<size_t>(p) * half + i] = static_cast<float>(std::sin(ang));
+      }
+    SRET(dalloc(&rope_cos, cs.size()));
+    SRET(dalloc(&rope_sin, sn.size()));
+    SRET(check(cudaMemcpy(rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice), "H2D rope"));
+    SRET(check(cudaMemcpy(rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice), "H2D rope"));
+  }
+
+  // activations / workspaces
+  Tmax = c.max_tokens_per_batch;
+  SRET(dalloc(&h, static_cast<size_t>(Tmax) * H));
+  SRET(dalloc(&a, static_cast<size_t>(Tmax) * H));
+  SRET(dalloc(&q, static_cast<size_t>(Tmax) * q_dim_l));
+  SRET(dalloc(&o, static_cast<size_t>(Tmax) * q_dim_l));
+  SRET(dalloc(&f, static_cast<size_t>(Tmax) * h2_l));
+  SRET(dalloc(&ar, static_cast<size_t>(Tmax) * H));
+  SRET(dalloc(&af, static_cast<size_t>(Tmax) * H));
+  SRET(dalloc(&logits_dev, static_cast<size_t>(Tmax) * c.vocab));
+  if (world > 1) {
+    SRET(dalloc(&logits_local, static_cast<size_t>(Tmax) * vocab_l));
+    SRET(dalloc(&logits_gather, static_cast<size_t>(world) * Tmax * vocab_l));
+  }
+  gemm_ws_floats = static_cast<size_t>(48) << 20;
+  SRET(dalloc(&gemm_ws, gemm_ws_floats));
+  SRET(dalloc(&gemm_counters, 1 << 16));
+  SRET(check(cudaMemset(gemm_counters, 0, (1 << 16) * sizeof(int)), "memset"));
+  part_cap = static_cast<size_t>(32) << 20;
+  SRET(dalloc(&part_o, part_cap));
+  SRET(dalloc(&part_lse, part_cap / 64 + 1024));
+  SRET(check(cudaStreamSynchronize(stream), "init sync"));
+  return Status::ok();
+}
+
+Status Model::alloc_kv(int64_t nb, int32_t bs) {
+  if (kv_ready) return Status::err(SARATHI_ESTATE, "alloc_kv: already allocated");
+  if (nb < 1 || nb > (1ll << 31) - 1 || bs < 16 || bs > 256 || bs % 16)
+    return Status::err(SARATHI_EINVAL, "alloc_kv: num_blocks >= 1, block_size multiple of 16 in [16, 256]");
+  const size_t per = static_cast<size_t>(nb) * nkv_l * bs * cfg.head_dim;
+  kpool.resize(cfg.n_layers);
+  vpool.resize(cfg.n_layers);
+  for (int l = 0; l < cfg.n_layers; ++l) {
+    SRET(dalloc(&kpool[l], per));
+    SRET(dalloc(&vpool[l], per));
+  }
+  num_blocks = nb;
+  block_size = bs;
+  max_blocks_per_req = (cfg.max_seq_len + bs - 1) / bs;
+  alloc = BlockAllocator(nb, bs);
+  meta_ints = static_cast<size_t>(5) * Tmax + static_cast<size_t>(Tmax + 1) * max_blocks_per_req;
+  SRET(dalloc(&meta_dev, meta_ints));
+  for (int i = 0; i < 2; ++i) {
+    void* hp = nullptr;
+    SRET(check(cudaMallocHost(&hp, meta_ints * sizeof(int)), "cudaMallocHost"));
+    meta_host_buf[i] = static_cast<int*>(hp);
+    SRET(check(cudaEventCreateWithFlags(&meta_ev[i], cudaEventDisableTiming), "cudaEventCreate"));
+  }
+  kv_ready = true;
+  return Status::ok();
+}
+
+Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, int N, const EpiParams& ep_in) {
+  auto pk = std::make_tuple(M, N, K);
+  auto it = plans.find(pk);
+  if (it == plans.end()) it = plans.emplace(pk, plan_gemm(M, N, K, num_sms, gemm_ws_floats)).first;
+  const GemmPlan& pl = it->second;
+  auto xk = std::make_tuple(X, N, K, pl.bn);
+  auto xi = xmaps.find(xk);
+  if (xi == xmaps.end()) {
+    CUtensorMap m;
+    if (!make_tmap_bf16(&m, X, N, K, ldx, pl.bn)) return Status::err(SARATHI_ECUDA, "tensor map (activation)");
+    xi = xmaps.emplace(xk, m).first;
+  }
+  EpiParams ep = ep_in;
+  ep.ws = gemm_ws;
+  ep.counters = gemm_counters;
+  ++launches;
+  return check(launch_gemm(mw, xi->second, pl, ep, stream), "gemm launch");
+}
+
+cudaEvent_t Model::op_begin() {
+  if (!profiling) return nullptr;
+  if (ev_used + 2 > ev_pool.size()) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool.push_back(e);
+    }
+  }
+  cudaEvent_t b = ev_pool[ev_used++];
+  cudaEventRecord(b, stream);
+  return b;
+}
+
+void Model::op_end(int op, cudaEvent_t b) {
+  if (!b) return;
+  cudaEvent_t e = ev_pool[ev_used++];
+  cudaEventRecord(e, stream);
+  pending_ops.emplace_back(op, b, e);
+}
+
+Status Model::collect_op_times() {
+  SRET(check(cudaStreamSynchronize(stream), "op timers sync"));
+  for (auto& t : pending_ops) {
+    float ms = 0.f;
+    SRET(check(cudaEventElapsedTime(&ms, std::get<1>(t), std::get<2>(t)), "cudaEventElapsedTime"));
+    op_ms[std::get<0>(t)] += ms;
+    op_count[std::get<0>(t)] += 1;
+  }
+  pending_ops.clear();
+  ev_used = 0;
+  return Status::ok();
+}
+
+Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* dec, float* logits, int32_t flags) {
+  if (!kv_ready) return Status::err(SARATHI_ESTATE, "run_hybrid_batch: alloc_kv not called");
+  const int p = pre ? pre->n_tokens : 0;
+  const int d = dec ? dec->n : 0;
+  const int T = p + d;
+  if (p < 0 || d < 0 || (pre && p == 0)) return Status::err(SARATHI_EINVAL, "run_hybrid_batch: empty chunk / negative count");
+  if (T < 1 || T > Tmax) return Status::err(SARATHI_EINVAL, "run_hybrid_batch: T must be in [1, max_tokens_per_batch]");
+  if (!logits && !(flags & SARATHI_NO_LOGITS)) return Status::err(SARATHI_EINVAL, "run_hybrid_batch: logits is NULL");
+  // ---- validation (state unchanged on error) ----
+  std::set<int64_t> seen;
+  if (pre) {
+    if (!pre->token_ids) return Status::err(SARATHI_EINVAL, "prefill token_ids NULL");
+    if (!alloc.has(pre->req_id)) return Status::err(SARATHI_EUNKNOWN_REQ, "prefill request not allocated");
+    if (pre->start_pos != cached.at(pre->req_id)) return Status::err(SARATHI_EPOS, "prefill start_pos != cached length");
+    if (pre->start_pos + p > alloc.reserved(pre->req_id))
+      return Status::err(SARATHI_EOVERFLOW, "prefill chunk exceeds the request's reservation");
+    seen.insert(pre->req_id);
+  }
+  if (d > 0 && (!dec->req_ids || !dec->token_ids || !dec->positions))
+    return Status::err(SARATHI_EINVAL, "decode arrays NULL");
+  for (int j = 0; j < d; ++j) {
+    const int64_t r = dec->req_ids[j];
+    if (!alloc.has(r)) return Status::err(SARATHI_EUNKNOWN_REQ, "decode request not allocated");
+    if (seen.count(r)) return Status::err(SARATHI_EDUP, "request appears twice in the batch");
+    seen.insert(r);
+    if (dec->positions[j] != cached.at(r) || dec->positions[j] < 1)
+      return Status::err(SARATHI_EPOS, "decode position != cached length (or no prefix)");
+    if (dec->positions[j] + 1 > alloc.reserved(r)) return Status::err(SARATHI_EOVERFLOW, "decode exceeds reservation");
+  }
+  for (int i = 0; i < p; ++i)
+    if (pre->token_ids[i] < 0 || pre->token_ids[i] >= cfg.vocab) return Status::err(SARATHI_EINVAL, "token id out of range");
+  for (int j = 0; j < d; ++j)
+    if (dec->token_ids[j] < 0 || dec->token_ids[j] >= cfg.vocab) return Status::err(SARATHI_EINVAL, "token id out of range");
+  if (pre && pre->start_pos + p > cfg.max_seq_len) return Status::err(SARATHI_EINVAL, "position >= max_seq_len");
+  for (int j = 0; j < d; ++j)
+    if (dec->positions[j] >= cfg.max_seq_len) return Status::err(SARATHI_EINVAL, "position >= max_seq_len");
+
+  if (profiling && ev_used > 16384) SRET(collect_op_times());
+  const bool all_rows = flags & SARATHI_RETURN_ALL_ROWS;
+  const bool want_logits = !(flags & SARATHI_NO_LOGITS);
+  const int R = all_rows ? T : d + (p > 0 ? 1 : 0);
+  // ---- metadata (host, pinned) -> one H2D copy ----
+  const size_t off_tok = 0, off_pos = Tmax, off_slot = 2 * static_cast<size_t>(Tmax), off_rows = 3 * static_cast<size_t>(Tmax),
+               off_ctx = 4 * static_cast<size_t>(Tmax), off_ptab = 5 * static_cast<size_t>(Tmax),
+               off_dtab = off_ptab + max_blocks_per_req;
+  meta_flip ^= 1;
+  int* mh = meta_host_buf[meta_flip];
+  SRET(check(cudaEventSynchronize(meta_ev[meta_flip]), "metadata buffer reuse"));  // its last H2D finished
+  last_slots.assign(T, 0);
+  for (int i = 0; i < p; ++i) {
+    const int pos = pre->start_pos + i;
+    mh[off_tok + i] = pre->token_ids[i];
+    mh[off_pos + i] = pos;
+    mh[off_slot + i] = static_cast<int>(alloc.slot(pre->req_id, pos));
+  }
+  if (pre) {
+    const auto& t = alloc.table(pre->req_id);
+    for (int b = 0; b < max_blocks_per_req; ++b) mh[off_ptab + b] = b < static_cast<int>(t.size()) ? t[b] : 0;
+  }
+  for (int j = 0; j < d; ++j) {
+    const int pos = dec->positions[j];
+    mh[off_tok + p + j] = dec->token_ids[j];
+    mh[off_pos + p + j] = pos;
+    mh[off_slot + p + j] = static_cast<int>(alloc.slot(dec->req_ids[j], pos));
+    mh[off_ctx + j] = pos + 1;
+    const auto& t = alloc.table(dec->req_ids[j]);
+    for (int b = 0; b < max_blocks_per_req; ++b)
+      mh[off_dtab + static_cast<size_t>(j) * max_blocks_per_req + b] = b < static_cast<int>(t.size()) ? t[b] : 0;
+  }
+  for (int r = 0; r < R; ++r) mh[off_rows + r] = all_rows ? r : (p > 0 ? (r == 0 ? p - 1 : p + r - 1) : r);
+  for (int i = 0; i < T; ++i) last_slots[i] = mh[off_slot + i];
+  const size_t copy_ints = off_dtab + static_cast<size_t>(d) * max_blocks_per_req;
+  SRET(check(cudaMemcpyAsync(meta_dev, mh, copy_ints * sizeof(int), cudaMemcpyHostToDevice, stream), "H2D metadata"));
+  last_h2d = static_cast<int64_t>(copy_ints * sizeof(int));
+  last_d2h = 0;
+  SRET(check(cudaEventRecord(meta_ev[meta_flip], stream), "event record"));
+  const int* d_tok = meta_dev + off_tok;
+  const int* d_pos = meta_dev + off_pos;
+  const int* d_slot = meta_dev + off_slot;
+  const int* d_rows = meta_dev + off_rows;
+  const int* d_ctx = meta_dev + off_ctx;
+  const int* d_ptab = meta_dev + off_ptab;
+  const int* d_dtab = meta_dev + off_dtab;
+
+  const int H = cfg.hidden, hd = cfg.head_dim;
+  const bool dump_layers = flags & SARATHI_DUMP_LAYERS;
+  if (dump_layers && !dump) SRET(dalloc(&dump, static_cast<size_t>(cfg.n_layers + 1) * Tmax * H));
+  auto dump_h = [&](int idx) -> Status {
+    if (!dump_layers) return Status::ok();
+    return check(cudaMemcpyAsync(dump + static_cast<size_t>(idx) * Tmax * H, h, static_cast<size_t>(T) * H * 4,
+                                 cudaMemcpyDeviceToDevice, stream),
+                 "dump");
+  };
+  NcclApi* api = world > 1 ? nccl_api(nullptr) : nullptr;
+  auto allreduce = [&]() -> Status {
+    ncclResult_t r = api->allReduce(ar, ar, static_cast<size_t>(T) * H, ncclBfloat16, ncclSum,
+                                    static_cast<ncclComm_t>(nccl), stream);
+    if (r != ncclSuccess) return Status::err(SARATHI_ENCCL, "ncclAllReduce failed");
+    return Status::ok();
+  };
+
+  cudaEvent_t ob = op_begin();
+  SRET(check(launch_embedding(d_tok, emb, h, T, H, stream), "embedding"));
+  op_end(SARATHI_OP_EMBED, ob);
+  ++launches;
+  SRET(dump_h(0));
+  const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
+  bool pending_ar = false;  // TP: down-proj partial in `ar` not yet added to h
+  for (int l = 0; l < cfg.n_layers; ++l) {
+    LayerWeights& w = layers[l];
+    ob = op_begin();
+    SRET(check(launch_rmsnorm(h, pending_ar ? ar : nullptr, w.g1, a, nullptr, T, H, cfg.rms_eps, stream), "rmsnorm1"));
+    op_end(SARATHI_OP_RMSNORM, ob);
+    ++launches;
+    pending_ar = false;
+    if (l > 0) SRET(dump_h(l));  // h after layer l-1 (TP: once the all-reduce has been added)
+    EpiParams e;
+    e.mode = EPI_QKV_ROPE;
+    e.out = q;
+    e.ldo = q_dim_l;
+    e.pos = d_pos;
+    e.slot = d_slot;
+    e.rope_cos = rope_cos;
+    e.rope_sin = rope_sin;
+    e.kcache = kpool[l];
+    e.vcache = vpool[l];
+    e.head_dim = hd;
+    e.n_q_local = nq_l;
+    e.n_kv_local = nkv_l;
+    e.block_size = block_size;
+    ob = op_begin();
+    SRET(gemm(w.m_qkv, qkv_rows, H, a, H, T, e));
+    op_end(SARATHI_OP_GEMM_QKV, ob);
+    if (p > 0) {
+      PrefillAttnArgs pa;
+      pa.q = q;
+      pa.q_ld = q_dim_l;
+      pa.q_row0 = 0;
+      pa.kcache = kpool[l];
+      pa.vcache = vpool[l];
+      pa.block_table = d_ptab;
+      pa.start = pre->start_pos;
+      pa.p = p;
+      pa.n_q_local = nq_l;
+      pa.n_kv_local = nkv_l;
+      pa.head_dim = hd;
+      pa.block_size = block_size;
+      pa.scale = scale;
+      pa.out = o;
+      pa.out_ld = q_dim_l;
+      ob = op_begin();
+      SRET(check(launch_prefill_attention(pa, stream), "prefill attention"));
+      op_end(SARATHI_OP_PREFILL_ATTN, ob);
+      ++launches;
+    }
+    if (d > 0) {
+      DecodeAttnArgs da;
+      da.q = q;
+      da.q_ld = q_dim_l;
+      da.q_row0 = p;
+      da.kcache = kpool[l];
+      da.vcache = vpool[l];
+      da.block_tables = d_dtab;
+      da.ctx = d_ctx;
+      da.max_blocks = max_blocks_per_req;
+      da.d = d;
+      da.n_q_local = nq_l;
+      da.n_kv_local = nkv_l;
+      da.head_dim = hd;
+      da.block_size = block_size;
+      da.scale = scale;
+      int max_nblk = 0;
+      for (int j = 0; j < d; ++j) max_nblk = std::max(max_nblk, (dec->positions[j] + 1 + block_size - 1) / block_size);
+      const int base_ctas = d * nkv_l;
+      int splits = 1;
+      const int target = 2 * num_sms;
+      if (base_ctas < target) splits = std::min(max_nblk, (target + base_ctas - 1) / base_ctas);
+      const size_t per_split = static_cast<size_t>(d) * nq_l * hd;
+      splits = static_cast<int>(std::max<size_t>(1, std::min<size_t>(splits, part_cap / per_split)));
+      da.blocks_per_split = (max_nblk + splits - 1) / splits;
+      da.splits = (max_nblk + da.blocks_per_split - 1) / da.blocks_per_split;
+      da.stages = 3;
+      da.part_o = part_o;
+      da.part_lse = part_lse;
+      da.out = o;
+      da.out_ld = q_dim_l;
+      ob = op_begin();
+      SRET(check(launch_decode_attention(da, stream), "decode attention"));
+      op_end(SARATHI_OP_DECODE_ATTN, ob);
+      launches += da.splits > 1 ? 2 : 1;
+    }
+    // O-projection (postproj) + residual / TP all-reduce
+    EpiParams eo;
+    if (world == 1) {
+      eo.mode = EPI_ADD_F32;
+      eo.out = h;
+      eo.ldo = H;
+    } else {
+      eo.mode = EPI_STORE_BF16;
+      eo.out = ar;
+      eo.ldo = H;
+    }
+    ob = op_begin();
+    SRET(gemm(w.m_o, H, q_dim_l, o, q_dim_l, T, eo));
+    op_end(SARATHI_OP_GEMM_O, ob);
+    if (world > 1) {
+      ob = op_begin();
+      SRET(allreduce());
+      op_end(SARATHI_OP_ALLREDUCE, ob);
+    }
+    ob = op_begin();
+    SRET(check(launch_rmsnorm(h, world > 1 ? ar : nullptr, w.g2, a, nullptr, T, H, cfg.rms_eps, stream), "rmsnorm2"));
+    op_end(SARATHI_OP_RMSNORM, ob);
+    ++launches;
+    // FFN
+    EpiParams ef;
+    ef.mode = cfg.ffn_kind == SARATHI_FFN_SWIGLU ? EPI_SILU_MUL : EPI_GELU;
+    ef.out = f;
+    ef.ldo = h2_l;
+    ob = op_begin();
+    SRET(gemm(w.m_gu, gu_rows, H, a, H, T, ef));
+    op_end(SARATHI_OP_GEMM_GATE_UP, ob);
+    EpiParams ed;
+    if (world == 1) {
+      ed.mode = EPI_ADD_F32;
+      ed.out = h;
+      ed.ldo = H;
+    } else {
+      ed.mode = EPI_STORE_BF16;
+      ed.out = ar;
+      ed.ldo = H;
+    }
+    ob = op_begin();
+    SRET(gemm(w.m_down, H, h2_l, f, h2_l, T, ed));
+    op_end(SARATHI_OP_GEMM_DOWN, ob);
+    if (world > 1) {
+      ob = op_begin();
+      SRET(allreduce());
+      op_end(SARATHI_OP_ALLREDUCE, ob);
+      pending_ar = true;
+    }
+  }
+  if (pending_ar && (dump_layers || !want_logits || all_rows)) {
+    SRET(check(launch_residual_add(h, ar, T, H, stream), "residual add"));
+    ++launches;
+    pending_ar = false;
+  }
+  SRET(dump_h(cfg.n_layers));
+  if (want_logits) {
+    ob = op_begin();
+    // final norm on the R logit rows (adds the pending TP partial for exactly those rows)
+    SRET(check(launch_rmsnorm(h, pending_ar ? ar : nullptr, gf, af, d_rows, R, H, cfg.rms_eps, stream), "final norm"));
+    ++launches;
+    const bool host_out = flags & SARATHI_LOGITS_HOST;
+    float* target = host_out ? logits_dev : logits;
+    EpiParams el;
+    el.mode = EPI_STORE_F32;
+    if (world == 1) {
+      el.out = target;
+      el.ldo = cfg.vocab;
+      SRET(gemm(m_lm, vocab_l, H, af, H, R, el));
+    } else {
+      el.out = logits_local;
+      el.ldo = vocab_l;
+      SRET(gemm(m_lm, vocab_l, H, af, H, R, el));
+      ncclResult_t r = api->allGather(logits_local, logits_gather, static_cast<size_t>(R) * vocab_l, ncclFloat32,
+                                      static_cast<ncclComm_t>(nccl), stream);
+      if (r != ncclSuccess) return Status::err(SARATHI_ENCCL, "ncclAllGather failed");
+      SRET(check(launch_vocab_permute(logits_gather, target, world, R, vocab_l, cfg.vocab, stream), "permute"));
+      ++launches;
+    }
+    op_end(SARATHI_OP_LM_HEAD, ob);
+    if (host_out) {
+      last_d2h = static_cast<int64_t>(R) * cfg.vocab * 4;
+      SRET(check(cudaMemcpyAsync(logits, logits_dev, static_cast<size_t>(R) * cfg.vocab * 4, cudaMemcpyDeviceToHost, stream),
+                 "D2H logits"));
+      SRET(check(cudaStreamSynchronize(stream), "sync logits"));
+    }
+  }
+  SRET(check(cudaGetLastError(), "launch"));
+  // ---- state advance (a12) ----
+  if (pre) cached[pre->req_id] += p;
+  for (int j = 0; j < d; ++j) cached[dec->req_ids[j]] += 1;
+  last_T = T;
+  last_dumped = dump_layers;
+  return Status::ok();
+}
+
+void Model::destroy() {
+  if (stream) cudaStreamSynchronize(stream);
+  if (nccl) {
+    NcclApi* api = nccl_api(nullptr);
+    if (api) api->commDestroy(static_cast<ncclComm_t>(nccl));
+    nccl = nullptr;
+  }
+  for (void* p : allocations) cudaFree(p);
+  allocations.clear();
+  for (int i = 0; i < 2; ++i) {
+    if (meta_host_buf[i]) cudaFreeHost(meta_host_buf[i]);
+    if (meta_ev[i]) cudaEventDestroy(meta_ev[i]);
+    meta_host_buf[i] = nullptr;
+    meta_ev[i] = nullptr;
+  }
+}
+
+}  // namespace sarathi

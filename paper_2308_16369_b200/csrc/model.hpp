@@ -1,0 +1,123 @@
+// Internal model state behind the sarathi_model handle.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/sarathi.h"
+#include "gemm.cuh"
+#include "host_sched.hpp"
+#include "kernels.cuh"
+
+namespace sarathi {
+
+struct Status {
+  int code = SARATHI_OK;
+  std::string msg;
+  static Status ok() { return Status(); }
+  static Status err(int c, std::string m) {
+    Status s;
+    s.code = c;
+    s.msg = std::move(m);
+    return s;
+  }
+};
+
+struct LayerWeights {
+  __nv_bfloat16* qkv = nullptr;   // [(nq_l + 2 nkv_l) hd][H]
+  __nv_bfloat16* o = nullptr;     // [H][nq_l hd]
+  __nv_bfloat16* gu = nullptr;    // [2 H2_l][H] gate/up interleaved in 64-row blocks (SwiGLU) | [H2_l][H] (GELU)
+  __nv_bfloat16* down = nullptr;  // [H][H2_l]
+  __nv_bfloat16* g1 = nullptr;    // [H]
+  __nv_bfloat16* g2 = nullptr;    // [H]
+  CUtensorMap m_qkv, m_o, m_gu, m_down;
+};
+
+struct Model {
+  sarathi_model_config cfg{};
+  int rank = 0, world = 1, device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  uint64_t seed = 0;
+  // sharded sizes
+  int nq_l = 0, nkv_l = 0, q_dim_l = 0, kv_dim_l = 0, qkv_rows = 0, h2_l = 0, gu_rows = 0, vocab_l = 0;
+  // weights
+  __nv_bfloat16* emb = nullptr;  // [V][H]
+  __nv_bfloat16* gf = nullptr;   // [H]
+  __nv_bfloat16* lm = nullptr;   // [vocab_l][H]
+  CUtensorMap m_lm;
+  std::vector<LayerWeights> layers;
+  std::vector<void*> allocations;
+  // rope tables [max_seq_len][hd/2]
+  float* rope_cos = nullptr;
+  float* rope_sin = nullptr;
+  // KV cache
+  bool kv_ready = false;
+  int64_t num_blocks = 0;
+  int block_size = 0;
+  int max_blocks_per_req = 0;
+  std::vector<__nv_bfloat16*> kpool, vpool;
+  BlockAllocator alloc;
+  std::map<int64_t, int32_t> cached;
+  // activations / workspaces (Tmax rows)
+  int Tmax = 0;
+  float* h = nullptr;
+  __nv_bfloat16 *a = nullptr, *q = nullptr, *o = nullptr, *f = nullptr, *ar = nullptr, *af = nullptr;
+  float* logits_dev = nullptr;     // [Tmax][V]   (host-output / TP staging)
+  float* logits_local = nullptr;   // [Tmax][vocab_l]
+  float* logits_gather = nullptr;  // [world][Tmax][vocab_l]
+  float* gemm_ws = nullptr;
+  size_t gemm_ws_floats = 0;
+  int* gemm_counters = nullptr;
+  float* part_o = nullptr;
+  float* part_lse = nullptr;
+  size_t part_cap = 0;  // floats in part_o
+  int* meta_dev = nullptr;
+  int* meta_host_buf[2] = {nullptr, nullptr};  // pinned, double-buffered
+  cudaEvent_t meta_ev[2] = {nullptr, nullptr};
+  int meta_flip = 0;
+  size_t meta_ints = 0;
+  float* dump = nullptr;     // [(L+1)][Tmax][H]
+  int last_T = 0;
+  bool last_dumped = false;
+  std::vector<int32_t> last_slots;
+  // caches
+  std::map<std::tuple<int, int, int>, GemmPlan> plans;
+  std::map<std::tuple<const void*, int, int, int>, CUtensorMap> xmaps;
+  // NCCL
+  void* nccl = nullptr;
+  int64_t launches = 0;
+  // I/O accounting and per-op timers
+  int64_t last_h2d = 0, last_d2h = 0;
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending_ops;
+  double op_ms[SARATHI_NUM_OPS] = {0};
+  int64_t op_count[SARATHI_NUM_OPS] = {0};
+  cudaEvent_t op_begin();
+  void op_end(int op, cudaEvent_t b);
+  Status collect_op_times();
+
+  Status init(const sarathi_model_config& c, const sarathi_dist& d, uint64_t seed);
+  Status alloc_kv(int64_t num_blocks, int32_t block_size);
+  Status run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* dec, float* logits, int32_t flags);
+  void destroy();
+
+  // helpers
+  Status gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, int N, const EpiParams& ep);
+  Status check(cudaError_t e, const char* what);
+  template <typename T>
+  Status dalloc(T** p, size_t count);
+};
+
+int nccl_unique_id(void* out128, std::string* err);
+
+}  // namespace sarathi

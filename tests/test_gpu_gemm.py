@@ -1,0 +1,105 @@
+"""GPU parity of the tcgen05 GEMM (through sarathi_op_gemm, the C ABI).
+
+Exactness first: small-integer operands are exact in bf16 and every partial sum is an integer
+< 2^24, so an fp32-accumulating GEMM must reproduce the integer product EXACTLY whatever the
+UMMA descriptor / swizzle / split-K path — a mis-encoded descriptor cannot hide.  Then random
+bf16 operands at the LLaMA-13B shapes against an fp64 matmul of the same bf16 values."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2308_16369_b200 import sarathi
+    return sarathi
+
+
+def _int_operands(M, N, K, seed):
+    g = torch.Generator().manual_seed(seed)
+    W = torch.randint(-3, 4, (M, K), generator=g).to(torch.bfloat16)
+    X = torch.randint(-3, 4, (N, K), generator=g).to(torch.bfloat16)
+    return W, X
+
+
+SHAPES = [
+    (128, 16, 64, 0), (128, 1, 64, 0), (256, 320, 5120, 1), (256, 320, 5120, 4), (384, 7, 128, 0),
+    (200, 37, 192, 0), (128, 600, 256, 0), (1280, 282, 8192, 0), (512, 257, 1024, 3), (640, 512, 640, 2),
+]
+
+
+@pytest.mark.parametrize("M,N,K,splits", SHAPES)
+def test_gemm_exact_integers_fp32_out(S, M, N, K, splits):
+    W, X = _int_operands(M, N, K, M + N + K)
+    ref = X.double() @ W.double().T
+    Wd, Xd = W.cuda(), X.cuda()
+    out = torch.full((N, M), float("nan"), device="cuda", dtype=torch.float32)
+    S.op_gemm(Wd.data_ptr(), Xd.data_ptr(), out.data_ptr(), M, N, K, S.EPI_STORE_F32, splits,
+              torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(out.double().cpu(), ref)
+
+
+@pytest.mark.parametrize("M,N,K,splits", [(256, 320, 5120, 0), (128, 33, 256, 2)])
+def test_gemm_exact_bf16_out_and_residual_add(S, M, N, K, splits):
+    W, X = _int_operands(M, N, K, 5)
+    ref = X.double() @ W.double().T
+    Wd, Xd = W.cuda(), X.cuda()
+    out = torch.empty((N, M), device="cuda", dtype=torch.bfloat16)
+    st = torch.cuda.current_stream().cuda_stream
+    S.op_gemm(Wd.data_ptr(), Xd.data_ptr(), out.data_ptr(), M, N, K, S.EPI_STORE_BF16, splits, st)
+    base = torch.arange(N * M, dtype=torch.float32).reshape(N, M).cuda()
+    acc = base.clone()
+    S.op_gemm(Wd.data_ptr(), Xd.data_ptr(), acc.data_ptr(), M, N, K, S.EPI_ADD_F32, splits, st)
+    torch.cuda.synchronize()
+    assert torch.equal(out.cpu(), ref.float().to(torch.bfloat16))
+    assert torch.equal(acc.double().cpu(), base.double().cpu() + ref)
+
+
+def test_gemm_silu_mul_interleaved(S):
+    M, N, K = 512, 40, 256   # 4 tiles: rows [128i, 128i+64) gate, [128i+64, 128i+128) up
+    g = torch.Generator().manual_seed(3)
+    W = (torch.randn(M, K, generator=g) / 16).to(torch.bfloat16)
+    X = torch.randn(N, K, generator=g).to(torch.bfloat16)
+    acc = (X.double() @ W.double().T).reshape(N, M // 128, 2, 64)
+    gate, up = acc[:, :, 0, :], acc[:, :, 1, :]
+    ref = (gate / (1 + torch.exp(-gate)) * up).reshape(N, M // 2)
+    out = torch.empty((N, M // 2), device="cuda", dtype=torch.bfloat16)
+    Wd, Xd = W.cuda(), X.cuda()   # keep the device tensors alive until the kernel ran
+    S.op_gemm(Wd.data_ptr(), Xd.data_ptr(), out.data_ptr(), M, N, K, S.EPI_SILU_MUL, 0,
+              torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    err = (out.double().cpu() - ref).abs().max() / ref.abs().max()
+    assert err < 1e-2
+
+
+def test_gemm_gelu(S):
+    M, N, K = 256, 24, 128
+    g = torch.Generator().manual_seed(4)
+    W = (torch.randn(M, K, generator=g) / 8).to(torch.bfloat16)
+    X = torch.randn(N, K, generator=g).to(torch.bfloat16)
+    ref = torch.nn.functional.gelu(X.double() @ W.double().T, approximate="tanh")
+    out = torch.empty((N, M), device="cuda", dtype=torch.bfloat16)
+    Wd, Xd = W.cuda(), X.cuda()
+    S.op_gemm(Wd.data_ptr(), Xd.data_ptr(), out.data_ptr(), M, N, K, S.EPI_GELU, 0,
+              torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert (out.double().cpu() - ref).abs().max() / ref.abs().max() < 1e-2
+
+
+@pytest.mark.parametrize("M,K", [(15360, 5120), (5120, 5120), (27648, 5120), (5120, 13824), (32000, 5120)])
+def test_gemm_llama13b_shapes_random(S, M, K):
+    N = 320
+    g = torch.Generator().manual_seed(M + K)
+    W = (torch.randn(M, K, generator=g) / K ** 0.5).to(torch.bfloat16)
+    X = torch.randn(N, K, generator=g).to(torch.bfloat16)
+    Wd, Xd = W.cuda(), X.cuda()
+    out = torch.empty((N, M), device="cuda", dtype=torch.float32)
+    S.op_gemm(Wd.data_ptr(), Xd.data_ptr(), out.data_ptr(), M, N, K, S.EPI_STORE_F32, 0,
+              torch.cuda.current_stream().cuda_stream)
+    ref = (Xd.double() @ Wd.double().T)
+    torch.cuda.synchronize()
+    err = ((out.double() - ref).abs().max() / ref.abs().max()).item()
+    assert err < 5e-5, err   # fp32 accumulation over K <= 13824 terms

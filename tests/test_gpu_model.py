@@ -1,0 +1,115 @@
+"""GPU end-to-end parity through the C ABI against the fp64 oracle (BASELINE.json config 1 and
+variants): logits of every row and the residual after every layer within 2e-2 relative error
+(north star); slot mappings, block tables and the schedule bit-exact; device-generated weights
+bit-exact to the synth spec."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import model as om
+from tests import gpu_harness as gh
+from tests.test_oracle_sched import CONFIG1_EXPECTED
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+CONFIG1 = [(1, 5, 12, 0), (2, 11, 12, 0), (3, 16, 12, 0), (0, 64, 4, 3)]
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2308_16369_b200 import sarathi
+    return sarathi
+
+
+def _check(steps, expected_plans=None):
+    if expected_plans is not None:
+        assert [s.plan for s in steps] == expected_plans
+    for s in steps:
+        assert np.array_equal(s.gpu_slots, s.ref_slots)
+    errs = gh.worst_errors(steps)
+    assert errs["logits"] <= TOL, errs
+    assert errs["hidden"] <= TOL, errs
+    return errs
+
+
+def test_config1_tiny_schedule(S):
+    steps = gh.run_schedule(S, synth.TINY, CONFIG1, B=4, C=16, num_blocks=32, block_size=16)
+    errs = _check(steps, CONFIG1_EXPECTED)
+    print("config1 worst errors", errs)
+
+
+def test_tiny_gqa_and_block64(S):
+    cfg = dataclasses.replace(synth.TINY, name="tiny-gqa", n_kv_heads=2, max_seq_len=256)
+    reqs = [(5, 70, 6, 0), (6, 3, 20, 0), (7, 130, 3, 2)]
+    steps = gh.run_schedule(S, cfg, reqs, B=3, C=32, num_blocks=16, block_size=64, weight_seed=3)
+    _check(steps)
+
+
+def test_tiny_gelu_ffn(S):
+    cfg = dataclasses.replace(synth.TINY, name="tiny-gelu", ffn_kind=synth.FFN_GELU, ffn_hidden=1024)
+    steps = gh.run_schedule(S, cfg, [(1, 20, 5, 0), (2, 9, 7, 0)], B=2, C=8, num_blocks=16, block_size=16,
+                            weight_seed=5)
+    _check(steps)
+
+
+def test_device_weights_bit_exact(S):
+    cfg = synth.TINY
+    m = S.Model(S.config_from(cfg, 16), seed=11)
+    H, hd = cfg.hidden, cfg.head_dim
+    for l in range(cfg.n_layers):
+        qkv = m.weight(l, 0, 0, (cfg.q_dim + 2 * cfg.kv_dim) * H).reshape(-1, H)
+        ref = np.concatenate([synth.layer_tensor_bits(cfg, 11, l, k) for k in (synth.WQ, synth.WK, synth.WV)])
+        assert np.array_equal(qkv, ref)
+        assert np.array_equal(m.weight(l, 1, 0, H * cfg.q_dim).reshape(H, -1), synth.layer_tensor_bits(cfg, 11, l, synth.WO))
+        gu = m.weight(l, 2, 0, 2 * cfg.ffn_hidden * H).reshape(-1, 128, H)
+        g = synth.layer_tensor_bits(cfg, 11, l, synth.WG).reshape(-1, 64, H)
+        u = synth.layer_tensor_bits(cfg, 11, l, synth.WU).reshape(-1, 64, H)
+        assert np.array_equal(gu[:, :64], g) and np.array_equal(gu[:, 64:], u)
+        assert np.array_equal(m.weight(l, 3, 0, H * cfg.ffn_hidden).reshape(H, -1), synth.layer_tensor_bits(cfg, 11, l, synth.WD))
+        assert np.array_equal(m.weight(l, 4, 0, H), synth.layer_tensor_bits(cfg, 11, l, synth.G1))
+        assert np.array_equal(m.weight(l, 5, 0, H), synth.layer_tensor_bits(cfg, 11, l, synth.G2))
+    assert np.array_equal(m.weight(0, 16, 0, cfg.vocab * H).reshape(cfg.vocab, H), synth.embedding_bits(cfg, 11))
+    assert np.array_equal(m.weight(0, 17, 0, H), synth.final_gain_bits(cfg, 11))
+    assert np.array_equal(m.weight(0, 18, 0, cfg.vocab * H).reshape(cfg.vocab, H), synth.lm_head_bits(cfg, 11))
+    m.close()
+
+
+def test_default_rows_and_errors_leave_state_unchanged(S):
+    cfg = synth.TINY
+    m = S.Model(S.config_from(cfg, 32), seed=0)
+    m.alloc_kv(10, 16)
+    m.request_alloc(1, 40)
+    m.request_alloc(2, 20)
+    toks1 = synth.tokens(7, 1, 0, 12, cfg.vocab)
+    toks2 = synth.tokens(7, 2, 0, 4, cfg.vocab)
+    full = np.zeros((12, cfg.vocab), np.float32)
+    R = m.run_hybrid_batch((1, 0, toks1), [], logits_host=full, flags=S.RETURN_ALL_ROWS)
+    assert R == 12 and m.cached_len(1) == 12
+    one = np.zeros((1, cfg.vocab), np.float32)
+    m.run_hybrid_batch((2, 0, toks2[:3]), [], logits_host=one)
+    assert m.cached_len(2) == 3
+    bad = [
+        (lambda: m.run_hybrid_batch((2, 0, toks2), [], logits_host=one), S.EPOS),
+        (lambda: m.run_hybrid_batch((2, 3, toks2[3:]), [(2, 5, 3)], logits_host=np.zeros((2, cfg.vocab), np.float32)), S.EDUP),
+        (lambda: m.run_hybrid_batch(None, [(9, 5, 3)], logits_host=one), S.EUNKNOWN_REQ),
+        (lambda: m.run_hybrid_batch(None, [(1, 5, 11)], logits_host=one), S.EPOS),
+        (lambda: m.run_hybrid_batch((2, 3, synth.tokens(7, 2, 3, 18, cfg.vocab)), [], logits_host=one), S.EOVERFLOW),
+        (lambda: m.request_alloc(3, 10 ** 6), S.EINVAL),
+        (lambda: m.request_alloc(3, 120), S.ENOKV),
+    ]
+    for fn, code in bad:
+        with pytest.raises(S.SarathiError) as e:
+            fn()
+        assert e.value.code == code, (code, str(e.value))
+    assert m.cached_len(1) == 12 and m.cached_len(2) == 3
+    # default R rows: row 0 = chunk's last token, then decodes in order
+    w = om.model_weights(cfg, 0)
+    out = np.zeros((2, cfg.vocab), np.float32)
+    m.run_hybrid_batch((2, 3, toks2[3:4]), [(1, int(synth.tokens(7, 1, 12, 1, cfg.vocab)[0]), 12)], logits_host=out)
+    ref2 = om.forward_full(w, toks2[:4]).logits[3]
+    ref1 = om.forward_full(w, np.concatenate([toks1, synth.tokens(7, 1, 12, 1, cfg.vocab)])).logits[12]
+    assert np.max(np.abs(out[0] - ref2)) / np.max(np.abs(ref2)) < TOL
+    assert np.max(np.abs(out[1] - ref1)) / np.max(np.abs(ref1)) < TOL
+    m.close()

@@ -1,0 +1,108 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol include/sarathi.h declares,
+rejects bad arguments, and its host scheduler / block allocator match the oracle's independent
+Python implementation bit-exactly (no GPU compute is called here)."""
+import os
+import random
+import re
+
+import pytest
+
+from oracle import sched as osch
+from tests.test_oracle_sched import CONFIG1_EXPECTED
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(__file__)), "include", "sarathi.h")
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2308_16369_b200 import build
+    build.build(verbose=False)
+    from paper_2308_16369_b200 import sarathi
+    return sarathi
+
+
+def test_library_exports_every_header_symbol(S):
+    text = open(HEADER).read()
+    declared = sorted(set(re.findall(r"\b(sarathi_[a-z_0-9]+)\s*\(", text)))
+    assert len(declared) >= 25
+    for name in declared:
+        assert hasattr(S.lib, name), name
+    assert sorted(S.EXPORTS) == declared
+
+
+def test_error_reporting_without_gpu(S):
+    with pytest.raises(S.SarathiError) as e:
+        S.Scheduler(0, 16, 10, 16)
+    assert e.value.code == S.EINVAL and "sched_create" in str(e.value)
+    with pytest.raises(S.SarathiError):
+        S.Scheduler(4, 3, 10, 16, tile_adjust=True)  # C-(B-1) = 0
+    s = S.Scheduler(4, 16, 10, 16)
+    s.submit(1, 5, 1)
+    with pytest.raises(S.SarathiError) as e:
+        s.submit(1, 5, 1)
+    assert e.value.code == S.EINVAL
+
+
+def _drain_cpp(S, B, C, nb, bs, reqs, policy=0, tile_adjust=False):
+    s = S.Scheduler(B, C, nb, bs, policy=policy, tile_adjust=tile_adjust)
+    for rid, P, D, arr in reqs:
+        s.submit(rid, P, D, arr)
+    plans, tables = [], {}
+    guard = 0
+    while not s.done():
+        guard += 1
+        assert guard < 100000
+        plan, admitted = s.next()
+        for rid in admitted:
+            tables[rid] = list(s.block_table(rid))
+        if plan is None:
+            s.idle_step()
+            continue
+        plans.append(plan)
+        s.complete()
+    return plans, tables
+
+
+def _drain_py(B, C, nb, bs, reqs, policy=osch.SARATHI, tile_adjust=False):
+    alloc = osch.BlockAllocator(nb, bs)
+    s = osch.Scheduler(B, C, alloc, policy=policy, tile_adjust=tile_adjust)
+    for rid, P, D, arr in reqs:
+        s.submit(rid, P, D, arr)
+    plans, tables = [], {}
+    while not s.done():
+        p = s.next_batch()
+        for rid, t in alloc.tables.items():
+            tables.setdefault(rid, list(t))
+        if p is None:
+            s.idle_step()
+            continue
+        plans.append((p.prefill, p.decodes))
+        s.complete(p)
+    return plans, tables
+
+
+def test_cpp_scheduler_config1_hand_trace(S):
+    reqs = [(1, 5, 12, 0), (2, 11, 12, 0), (3, 16, 12, 0), (0, 64, 4, 3)]
+    plans, tables = _drain_cpp(S, 4, 16, 32, 16, reqs)
+    assert plans == CONFIG1_EXPECTED
+    assert tables == {1: [0, 1], 2: [2, 3], 3: [4, 5], 0: [6, 7, 8, 9, 10]}
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("policy", [0, 1, 2])
+def test_cpp_scheduler_matches_python_twin(S, seed, policy):
+    rnd = random.Random(seed * 7 + policy)
+    B, C, bs = rnd.randint(1, 8), rnd.choice([4, 16, 64, 256]), rnd.choice([16, 64])
+    nb = rnd.randint(8, 200)
+    tile = policy == 0 and C > B - 1 and rnd.random() < 0.3
+    reqs = []
+    for rid in range(rnd.randint(1, 25)):
+        P, D = rnd.randint(1, 300), rnd.randint(0, 40)
+        if -(-(P + D) // bs) > nb:
+            continue
+        reqs.append((rid * 3 + 1, P, D, rnd.randint(0, 30)))
+    py_policy = [osch.SARATHI, osch.ORCA_BEST, osch.REQUEST_LEVEL][policy]
+    a = _drain_cpp(S, B, C, nb, bs, reqs, policy, tile)
+    b = _drain_py(B, C, nb, bs, reqs, py_policy, tile)
+    assert a[0] == b[0]
+    assert a[1] == b[1]

@@ -238,9 +238,19 @@ int sarathi_sched_block_table(const sarathi_sched* s, int64_t req_id, int32_t* o
 /* out = X · Wᵀ on tcgen05: W bf16 [M][K] (K-major), X bf16 [N][K]; mode 0: out bf16 [N][M],
  * 1: out fp32 [N][M], 2: out fp32 += (residual add), 3: SiLU(gate)·up with gate/up interleaved in
  * 64-row blocks of W -> out bf16 [N][M/2], 4: GELU-tanh -> bf16.  K % 64 == 0, N >= 1.
- * force_splits > 0 forces the split-K factor (else heuristic). */
+ * force_splits > 0 fixes the persistent stream-K grid size in CTA pairs (else one pair per 2 SMs).
+ * mode | SARATHI_GEMM_W_PACKED: W is already in the tile-major layout of sarathi_op_pack_weight
+ * (otherwise it is packed into a library-owned scratch buffer first, on the same stream). */
+#define SARATHI_GEMM_W_PACKED 0x100
 int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t N, int32_t K, int32_t mode,
                     int32_t force_splits, void* stream);
+/* Tile-major GEMM weight layout used by the library: out[ceil(rows/128)*128*cols] with element
+ * (r, c) of the row-major W[rows][cols] at
+ *     ((r/128)*(cols/64) + c/64)*8192 + (r%128)*64 + (((c%64)/8) ^ (r%8))*8 + c%8
+ * (padding rows zero).  Each [128 x 64] tile is 16 KB contiguous and already in the tcgen05 K-major
+ * SWIZZLE_128B shared-memory image, tiles ordered as a stream-K CTA consumes them, so one 1D bulk
+ * copy (one request) moves a tile HBM -> SMEM.  cols % 64 == 0. */
+int sarathi_op_pack_weight(const void* W, void* out, int32_t rows, int32_t cols, void* stream);
 /* out[r] = bf16(RMSNorm(h[r]) * g), h fp32 [R][H], g bf16 [H]. */
 int sarathi_op_rmsnorm(const float* h, const void* g, void* out, int32_t R, int32_t H, float eps, void* stream);
 

@@ -1,7 +1,10 @@
 // extern "C" boundary (include/sarathi.h): argument checks, status codes, thread-local errors.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "../../include/sarathi.h"
 #include "model.hpp"
@@ -214,32 +217,45 @@ int sarathi_debug_weight(const sarathi_model* m, int32_t layer, int32_t tensor, 
   if (!m || !host_out || offset < 0 || count < 0) return fail(SARATHI_EINVAL, "debug_weight: bad argument");
   const auto& M = m->m;
   const __nv_bfloat16* src = nullptr;
-  size_t total = 0;
-  const size_t H = M.cfg.hidden;
+  int rows = 0, cols = 0;
+  bool packed = true;  // GEMM weights live in the tile-major layout; report the logical [rows][cols] view
+  const int H = M.cfg.hidden;
   if (tensor < 16) {
     if (layer < 0 || layer >= M.cfg.n_layers) return fail(SARATHI_EINVAL, "debug_weight: layer");
     const auto& w = M.layers[layer];
     switch (tensor) {
-      case 0: src = w.qkv; total = static_cast<size_t>(M.qkv_rows) * H; break;
-      case 1: src = w.o; total = H * M.q_dim_l; break;
-      case 2: src = w.gu; total = static_cast<size_t>(M.gu_rows) * H; break;
-      case 3: src = w.down; total = H * M.h2_l; break;
-      case 4: src = w.g1; total = H; break;
-      case 5: src = w.g2; total = H; break;
+      case 0: src = w.qkv; rows = M.qkv_rows; cols = H; break;
+      case 1: src = w.o; rows = H; cols = M.q_dim_l; break;
+      case 2: src = w.gu; rows = M.gu_rows; cols = H; break;
+      case 3: src = w.down; rows = H; cols = M.h2_l; break;
+      case 4: src = w.g1; rows = 1; cols = H; packed = false; break;
+      case 5: src = w.g2; rows = 1; cols = H; packed = false; break;
       default: return fail(SARATHI_EINVAL, "debug_weight: tensor");
     }
   } else {
     switch (tensor) {
-      case 16: src = M.emb; total = static_cast<size_t>(M.cfg.vocab) * H; break;
-      case 17: src = M.gf; total = H; break;
-      case 18: src = M.lm; total = static_cast<size_t>(M.vocab_l) * H; break;
+      case 16: src = M.emb; rows = M.cfg.vocab; cols = H; packed = false; break;
+      case 17: src = M.gf; rows = 1; cols = H; packed = false; break;
+      case 18: src = M.lm; rows = M.vocab_l; cols = H; break;
       default: return fail(SARATHI_EINVAL, "debug_weight: tensor");
     }
   }
+  const size_t total = static_cast<size_t>(rows) * cols;
   if (static_cast<size_t>(offset + count) > total) return fail(SARATHI_EINVAL, "debug_weight: range");
   cudaStreamSynchronize(M.stream);
-  if (cudaMemcpy(host_out, src + offset, count * 2, cudaMemcpyDeviceToHost) != cudaSuccess)
+  if (!packed) {
+    if (cudaMemcpy(host_out, src + offset, count * 2, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail(SARATHI_ECUDA, "debug_weight: copy failed");
+    return SARATHI_OK;
+  }
+  const size_t padded = static_cast<size_t>((rows + 127) / 128) * 128 * cols;
+  std::vector<uint16_t> buf(padded);
+  if (cudaMemcpy(buf.data(), src, padded * 2, cudaMemcpyDeviceToHost) != cudaSuccess)
     return fail(SARATHI_ECUDA, "debug_weight: copy failed");
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t li = offset + i;
+    host_out[i] = buf[sarathi::packed_weight_index(static_cast<int>(li / cols), static_cast<int>(li % cols), cols)];
+  }
   return SARATHI_OK;
 }
 
@@ -336,6 +352,8 @@ int sarathi_sched_block_table(const sarathi_sched* s, int64_t req_id, int32_t* o
 int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t N, int32_t K, int32_t mode,
                     int32_t force_splits, void* stream) {
   using namespace sarathi;
+  const bool prepacked = (mode & SARATHI_GEMM_W_PACKED) != 0;
+  mode &= ~SARATHI_GEMM_W_PACKED;
   if (!W || !X || !out || M < 1 || N < 1 || K < 64 || K % 64 || mode < 0 || mode > 4)
     return fail(SARATHI_EINVAL, "op_gemm: bad argument (K % 64 == 0, mode 0..4)");
   if (mode == EPI_SILU_MUL && M % 128) return fail(SARATHI_EINVAL, "op_gemm: SiLU mode needs M % 128 == 0");
@@ -351,9 +369,22 @@ int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   GemmPlan pl = plan_gemm(M, N, K, sms, ws_floats, force_splits);
-  if (force_splits > 0 && pl.splits != force_splits) return fail(SARATHI_EINVAL, "op_gemm: split factor not realisable");
+  // pack W into the library's tile-major layout (the layout init_model generates weights in)
+  static __nv_bfloat16* wp = nullptr;
+  static size_t wp_elems = 0;
+  const size_t need = static_cast<size_t>((M + 127) / 128) * 128 * K;
+  if (need > wp_elems) {
+    if (wp) cudaFree(wp);
+    wp = nullptr;
+    if (cudaMalloc(&wp, need * 2) != cudaSuccess) return fail(SARATHI_ECUDA, "op_gemm: pack buffer allocation failed");
+    wp_elems = need;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!prepacked && (cudaMemsetAsync(wp, 0, need * 2, st) != cudaSuccess ||
+                     launch_pack_weight(static_cast<const __nv_bfloat16*>(W), wp, M, K, st) != cudaSuccess))
+    return fail(SARATHI_ECUDA, "op_gemm: weight packing failed");
   CUtensorMap mw, mx;
-  if (!make_tmap_bf16(&mw, W, M, K, K, 128) || !make_tmap_bf16(&mx, X, N, K, K, pl.bn))
+  if (!make_tmap_weight(&mw, prepacked ? W : wp, M, K) || !make_tmap_bf16(&mx, X, N, K, K, pl.box_rows))
     return fail(SARATHI_ECUDA, "op_gemm: tensor map encode failed");
   EpiParams ep;
   ep.mode = mode;
@@ -361,8 +392,42 @@ int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t 
   ep.ldo = mode == EPI_SILU_MUL ? M / 2 : M;
   ep.ws = ws;
   ep.counters = ctr;
-  const cudaError_t e = launch_gemm(mw, mx, pl, ep, static_cast<cudaStream_t>(stream));
+  if (const char* d = getenv("SARATHI_GEMM_DBG")) ep.dbg = atoi(d);
+  static unsigned long long* trace = nullptr;
+  const bool tracing = getenv("SARATHI_GEMM_TRACE") != nullptr;
+  if (tracing) {
+    if (!trace) cudaMalloc(&trace, 4096 * 8);
+    cudaMemsetAsync(trace, 0, 4096 * 8, st);
+    ep.trace = trace;
+  }
+  const cudaError_t e = launch_gemm(mw, mx, pl, ep, st);
+  if (tracing) {
+    unsigned long long h[4096];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+    const unsigned long long t0 = h[0];
+    fprintf(stderr, "gemm trace M=%d N=%d K=%d pairs=%d stages=%d units/pair~%lld\n", M, N, K, pl.ctas, pl.stages,
+            pl.units / pl.ctas);
+    for (int i = 0; i < 256 && h[i]; ++i)
+      fprintf(stderr, "u%3d issue0 %8.3f issue1 %8.3f full0 %8.3f full1(relay) %8.3f mma %8.3f us\n", i,
+              (h[i] - t0) * 1e-3, h[1024 + i] ? (h[1024 + i] - t0) * 1e-3 : -1.0,
+              h[2048 + i] ? (h[2048 + i] - t0) * 1e-3 : -1.0, h[1280 + i] ? (h[1280 + i] - t0) * 1e-3 : -1.0,
+              h[256 + i] ? (h[256 + i] - t0) * 1e-3 : -1.0);
+    for (int sgm = 0; sgm < 64 && h[512 + sgm]; ++sgm)
+      fprintf(stderr, "seg %d epilogue wake %8.3f us\n", sgm, (h[512 + sgm] - t0) * 1e-3);
+  }
   if (e != cudaSuccess) return fail(SARATHI_ECUDA, std::string("op_gemm: ") + cudaGetErrorString(e));
+  return SARATHI_OK;
+}
+
+int sarathi_op_pack_weight(const void* W, void* out, int32_t rows, int32_t cols, void* stream) {
+  if (!W || !out || rows < 1 || cols < 64 || cols % 64) return fail(SARATHI_EINVAL, "op_pack_weight: bad argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t n = static_cast<size_t>((rows + 127) / 128) * 128 * cols;
+  if (cudaMemsetAsync(out, 0, n * 2, st) != cudaSuccess ||
+      sarathi::launch_pack_weight(static_cast<const __nv_bfloat16*>(W), static_cast<__nv_bfloat16*>(out), rows, cols,
+                                  st) != cudaSuccess)
+    return fail(SARATHI_ECUDA, "op_pack_weight: launch failed");
   return SARATHI_OK;
 }
 

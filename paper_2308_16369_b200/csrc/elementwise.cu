@@ -122,9 +122,18 @@ __device__ __forceinline__ float odd_v(unsigned long long seed, unsigned long lo
   return static_cast<float>(v);  // |v| < 2^24: exact
 }
 
+// Tile-major, pre-swizzled GEMM weight layout: the [128 x 64] tile (m-tile, k-block) is 16 KB
+// contiguous, tiles ordered (m-tile, k-block) = the order a stream-K CTA consumes them, and inside
+// a tile row r's 16-byte chunk j sits at chunk j ^ (r % 8) — the UMMA K-major SWIZZLE_128B image,
+// so one 1D bulk copy lands a tile in shared memory ready for tcgen05.mma.
+__device__ __forceinline__ size_t packed_index(int r, int c, int cols) {
+  const int rr = r & 127, j = (c & 63) >> 3;
+  return ((static_cast<size_t>(r >> 7) * (cols >> 6) + (c >> 6)) << 13) + (rr << 6) + ((j ^ (rr & 7)) << 3) + (c & 7);
+}
+
 __global__ void weightgen_kernel(__nv_bfloat16* __restrict__ dst, int rows, int cols, const int* __restrict__ tau,
                                  const float* __restrict__ scale, const long long* __restrict__ base,
-                                 unsigned long long seed) {
+                                 unsigned long long seed, int packed) {
   const size_t total = static_cast<size_t>(rows) * cols;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -132,7 +141,17 @@ __global__ void weightgen_kernel(__nv_bfloat16* __restrict__ dst, int rows, int 
     const int c = static_cast<int>(i % cols);
     const float v = odd_v(seed, static_cast<unsigned long long>(tau[r]),
                           static_cast<unsigned long long>(base[r] + c));
-    dst[i] = __float2bfloat16_rn(__fmul_rn(v, scale[r]));
+    dst[packed ? packed_index(r, c, cols) : i] = __float2bfloat16_rn(__fmul_rn(v, scale[r]));
+  }
+}
+
+__global__ void pack_weight_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst, int rows,
+                                   int cols) {
+  const size_t total = static_cast<size_t>(rows) * cols;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / cols), c = static_cast<int>(i % cols);
+    dst[packed_index(r, c, cols)] = src[i];
   }
 }
 
@@ -182,9 +201,17 @@ cudaError_t launch_vocab_permute(const float* gathered, float* logits, int world
 }
 
 cudaError_t launch_weightgen(__nv_bfloat16* dst, int rows, int cols, const int* tau, const float* scale,
-                             const long long* base, unsigned long long seed, cudaStream_t st) {
+                             const long long* base, unsigned long long seed, int packed, cudaStream_t st) {
   if (rows == 0 || cols == 0) return cudaSuccess;
-  weightgen_kernel<<<148 * 16, 256, 0, st>>>(dst, rows, cols, tau, scale, base, seed);
+  if (packed && cols % 64) return cudaErrorInvalidValue;
+  weightgen_kernel<<<148 * 16, 256, 0, st>>>(dst, rows, cols, tau, scale, base, seed, packed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_weight(const __nv_bfloat16* src, __nv_bfloat16* dst, int rows, int cols, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  if (cols % 64) return cudaErrorInvalidValue;
+  pack_weight_kernel<<<148 * 16, 256, 0, st>>>(src, dst, rows, cols);
   return cudaGetLastError();
 }
 

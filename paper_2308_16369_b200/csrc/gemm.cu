@@ -3,16 +3,23 @@
 //
 // Decode-maximal batching fuses all p + d tokens of a hybrid batch into ONE matmul per linear so
 // every weight byte is fetched once for both kinds of token (§4.3).  With
-// T = p + d <= 512 tokens per batch, the natural sm_100a mapping is "swap-AB":
-//   D[m, t] = sum_k W[m, k] * X[t, k]       (UMMA M = 128 weight rows, N = bn tokens, K = 16/instr)
-// so each CTA streams a 128-row weight slab exactly once from HBM while the (small, L2-resident)
-// token matrix is re-read from L2.  Pipeline per CTA (192 threads, 1 CTA / SM):
+// T = p + d <= 512 tokens per batch the sm_100a mapping is "swap-AB":
+//     D[m, t] = sum_k W[m, k] * X[t, k]     UMMA M = 128 weight rows, N = all tokens (<= 256 per
+//                                           instruction, two instructions when T > 256), K = 16
+// so each weight byte is streamed from HBM exactly once while the small token matrix stays in L2.
+//
+// Persistent stream-K: grid = #SMs (1 CTA per SM); the (tile, k-block) iteration space is cut
+// into equal contiguous ranges, one per CTA, so every SM does the same amount of MMA work whatever
+// the number of 128-row tiles (QKV 120, O 40, gate/up 216, down 40, LM head 250 at LLaMA-13B).
+// A tile covered by several CTAs is reduced deterministically: each contributor writes an fp32
+// partial into its slot, the last to arrive (atomic counter) sums the slots in order and runs the
+// fused epilogue.  Warp roles (192 threads):
 //   warp 0      TMA producer: W tile [128 x 64] (evict_first) + X tile [bn x 64] (evict_last),
-//               128B swizzle, into an S-stage smem ring (full/empty mbarriers)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; tcgen05.commit frees stages
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> regs -> (split-K partial | smem tile) -> fused op
-// Split-K (grid.z) writes fp32 partials; the last-arriving CTA of a tile (atomic counter) reduces
-// them in split order (deterministic) and runs the epilogue.
+//               128B swizzle, S-stage smem ring (full/empty mbarriers), runs across segments
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; tcgen05.commit frees stages and
+//               signals the epilogue per segment; TMEM double-buffered when bn <= 256
+//   warps 2..5  epilogue straight from TMEM (tcgen05.ld 32x32b.x16): residual add, SiLU*up,
+//               GELU, RoPE + paged KV append, bf16/fp32 stores, or the stream-K partial
 #include "common.cuh"
 #include "gemm.cuh"
 
@@ -27,13 +34,21 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
-constexpr int kStilePitch = 132;             // fp32 staging row pitch (128 + 4 pad)
 constexpr int kThreads = 192;
+constexpr int kXPitch = 17;                  // xbuf [128][17] fp32 (partner exchange)
+constexpr int kWRowsPerTile = 32;            // packed W viewed as rows of 256 elements (512 B)
 
 struct KParams {
-  int M, N, KB, bn, m_tiles, n_tiles, splits, kb_per_split, stages;
+  int M, N, KB;
+  int bn, n_mma;          // tokens per tile; UMMAs per k-step (bn / n_mma tokens each, <= 256)
+  int pm_tiles, n_tiles;  // 256-row pair tiles, token tiles
+  long long units;        // total (pair tile, k-block) work units = pm_tiles * n_tiles * KB
+  int ctas;               // number of CTA PAIRS (grid = 2 * ctas)
+  int stages;
+  int nbuf;               // TMEM accumulator buffers (2 if bn <= 256)
+  int max_slots;          // partial slots per tile
   uint32_t tmem_cols;
-  uint32_t smem_main;  // bytes of ring / staging region
+  uint32_t ring_bytes;
 };
 
 SARATHI_DEVICE float silu_f(float x) { return x / (1.0f + __expf(-x)); }
@@ -42,250 +57,388 @@ SARATHI_DEVICE float gelu_tanh_f(float x) {
   return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
 }
 
+SARATHI_DEVICE long long unit_begin(int c, const KParams& p) {
+  return (static_cast<long long>(c) * p.units) / p.ctas;
+}
+// CTA owning work unit u under the balanced partition above.
+SARATHI_DEVICE int cta_of(long long u, const KParams& p) {
+  return static_cast<int>(((u + 1) * p.ctas - 1) / p.units);
+}
+
+// Epilogue for one 16-token chunk of a 128-row tile.  Thread r (0..127) holds acc row r, tokens c0..c0+15.
+SARATHI_DEVICE void epilogue_chunk(const KParams& p, const EpiParams& ep, float (&v)[16], int r, int mt, int nt,
+                                   int c0, int tvalid, float* xbuf, const int* s_pos, const int* s_slot) {
+  const int m = mt * kBM + r;
+  const long long t0 = static_cast<long long>(nt) * p.bn + c0;
+  const int nv = min(16, tvalid - c0);  // valid tokens in this chunk (>= 1)
+  switch (ep.mode) {
+    case EPI_STORE_BF16:
+    case EPI_GELU: {
+      if (m >= p.M) break;
+      __nv_bfloat16* out = static_cast<__nv_bfloat16*>(ep.out) + t0 * ep.ldo + m;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float x = ep.mode == EPI_GELU ? gelu_tanh_f(v[j]) : v[j];
+        if (j < nv) out[j * ep.ldo] = __float2bfloat16_rn(x);
+      }
+      break;
+    }
+    case EPI_STORE_F32: {
+      if (m >= p.M) break;
+      float* out = static_cast<float*>(ep.out) + t0 * ep.ldo + m;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < nv) out[j * ep.ldo] = v[j];
+      break;
+    }
+    case EPI_ADD_F32: {
+      if (m >= p.M) break;
+      float* out = static_cast<float*>(ep.out) + t0 * ep.ldo + m;
+      float o[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) o[j] = j < nv ? __ldcg(out + j * ep.ldo) : 0.f;  // 16 loads in flight
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < nv) out[j * ep.ldo] = o[j] + v[j];
+      break;
+    }
+    case EPI_SILU_MUL: {
+      // tile rows [0,64): gate features, [64,128): the matching up features (64-row interleave)
+      named_bar_sync(2, 128);  // xbuf free (previous chunk consumed)
+      if (r >= 64) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) xbuf[(r - 64) * kXPitch + j] = v[j];
+      }
+      named_bar_sync(2, 128);
+      if (r < 64) {
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(ep.out) + t0 * ep.ldo + mt * 64 + r;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float u = xbuf[r * kXPitch + j];
+          if (j < nv) out[j * ep.ldo] = __float2bfloat16_rn(silu_f(v[j]) * u);
+        }
+      }
+      break;
+    }
+    case EPI_QKV_ROPE: {
+      // rows are head-aligned (128 % head_dim == 0): rotate-half partner of row r is r ^ half.
+      const int hd = ep.head_dim, half = hd >> 1;
+      named_bar_sync(2, 128);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) xbuf[r * kXPitch + j] = v[j];
+      named_bar_sync(2, 128);
+      if (m >= p.M) break;
+      const int d = r % hd;   // dim within head
+      const int gh = m / hd;  // head index in [q heads | k heads | v heads]
+      const bool rope = gh < ep.n_q_local + ep.n_kv_local;
+      const bool isq = gh < ep.n_q_local;
+      const int partner = r ^ half;
+      const bool lowhalf = d < half;
+      const int dd = lowhalf ? d : d - half;
+      __nv_bfloat16* qout = static_cast<__nv_bfloat16*>(ep.out);
+      __nv_bfloat16* cache = static_cast<__nv_bfloat16*>(rope ? ep.kcache : ep.vcache);
+      const int kvh = isq ? 0 : (rope ? gh - ep.n_q_local : gh - ep.n_q_local - ep.n_kv_local);
+      float cs[16], sn[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {  // all table loads in flight before any store
+        cs[j] = 1.f;
+        sn[j] = 0.f;
+        if (rope && j < nv) {
+          const size_t ti = static_cast<size_t>(s_pos[c0 + j]) * half + dd;
+          cs[j] = __ldg(ep.rope_cos + ti);
+          sn[j] = __ldg(ep.rope_sin + ti);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j >= nv) continue;
+        const int t = c0 + j;
+        const float xp = xbuf[partner * kXPitch + j];
+        // x1 = low-half value, x2 = high-half value: y1 = x1 c - x2 s, y2 = x2 c + x1 s
+        const float y = lowhalf ? (v[j] * cs[j] - xp * sn[j]) : (v[j] * cs[j] + xp * sn[j]);
+        __nv_bfloat16* dst;
+        if (isq) {
+          dst = qout + (static_cast<long long>(nt) * p.bn + t) * ep.ldo + m;
+        } else {
+          const int sl = s_slot[t];
+          const size_t row =
+              (static_cast<size_t>(sl / ep.block_size) * ep.n_kv_local + kvh) * ep.block_size + sl % ep.block_size;
+          dst = cache + row * hd + d;
+        }
+        *dst = __float2bfloat16_rn(y);
+      }
+      break;
+    }
+    default:
+      break;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap mapW,
-                        const __grid_constant__ CUtensorMap mapX, const KParams p,
-                        const EpiParams ep) {
+    gemm_bf16_pair(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, const KParams p,
+                   const EpiParams ep) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t b_bytes = static_cast<uint32_t>(p.bn) * kBK * 2;
+  const uint32_t b_bytes = static_cast<uint32_t>(p.bn / 2) * kBK * 2;  // this CTA's half of the tokens
   const uint32_t stage_bytes = kABytes + b_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.smem_main);
-  uint64_t* empty = full + p.stages;
-  uint64_t* tfull = empty + p.stages;
-  uint32_t* holder = reinterpret_cast<uint32_t*>(tfull + 1);
+  float* xbuf = reinterpret_cast<float*>(smem + p.ring_bytes);         // [128][17]
+  int* s_pos = reinterpret_cast<int*>(xbuf + kBM * kXPitch);           // [bn]
+  int* s_slot = s_pos + p.bn;                                          // [bn]
+  uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_slot + p.bn) + 7) & ~uintptr_t(7));
+  uint64_t* full = bars;                // local: this CTA's W + X bytes landed
+  uint64_t* pfull = full + p.stages;    // leader only: the peer's stage landed (relayed)
+  uint64_t* empty = pfull + p.stages;
+  uint64_t* tfull = empty + p.stages;   // [2]
+  uint64_t* tempty = tfull + 2;         // [2] (leader's are the ones waited on)
+  uint32_t* holder = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ int s_last;
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
-  const int mt = blockIdx.x, nt = blockIdx.y, split = blockIdx.z;
-  const int kb0 = split * p.kb_per_split;
-  const int nk = min(p.kb_per_split, p.KB - kb0);
+  const uint32_t rank = cluster_ctarank();   // 0 = leader (issues the pair MMAs)
+  const int pair = blockIdx.x >> 1;
+  const long long u_begin = unit_begin(pair, p), u_end = unit_begin(pair + 1, p);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
+      mbar_init(&pfull[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapW);
     tma_prefetch_desc(&mapX);
   }
-  if (warp == 1) tmem_alloc(holder, p.tmem_cols);
+  if (warp == 1) tmem_alloc_pair(holder, p.tmem_cols);
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *holder;
+  const int ni = p.bn / p.n_mma;  // tokens per UMMA (multiple of 16, <= 256)
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
-    if (lane == 0) {
+    // ---------------- TMA producer (whole warp, warp-uniform; one elected lane issues) ----------------
+    {
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % p.stages;
-        const uint32_t ph = (i / p.stages) & 1;
+      // incremental (tile, k-block, stage, phase) counters: no integer division in the hot loop
+      const long long n = u_end - u_begin;
+      int tile = static_cast<int>(u_begin / p.KB), kb = static_cast<int>(u_begin % p.KB);
+      int pt = tile / p.n_tiles, nt = tile % p.n_tiles;
+      int s = 0;
+      uint32_t ph = 0;
+      int wrow = ((pt * 2 + static_cast<int>(rank)) * p.KB + kb) * kWRowsPerTile;  // row in the 512-B view
+      const uint32_t tx = 2 * (stage_bytes - ((ep.dbg & 1) ? b_bytes : 0) - ((ep.dbg & 2) ? kABytes : 0));
+      for (long long i = 0; i < n; ++i) {
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* a = smem + static_cast<size_t>(s) * stage_bytes;
         uint8_t* b = a + kABytes;
-        mbar_arrive_expect_tx(&full[s], stage_bytes);
-        const int kc = (kb0 + i) * kBK;
-        tma_load_2d(a, &mapW, &full[s], kc, mt * kBM, pol_w);
-        tma_load_2d(b, &mapX, &full[s], kc, nt * p.bn, pol_x);
+        // both CTAs' bytes are counted on the leader's full[s] (pair TMA)
+        if (rank == 0) mbar_arrive_expect_tx_warp(&full[s], tx);
+        // W tile: the contiguous 16 KB pre-swizzled tile as 32 rows x 512 B (unswizzled map)
+        if (!(ep.dbg & 2)) tma_load_2d_pair_warp(a, &mapW, &full[s], 0, wrow, pol_w);
+        if (!(ep.dbg & 1))
+          for (int j = 0; j < p.n_mma; ++j)
+            tma_load_2d_pair_warp(b + j * (ni / 2) * kBK * 2, &mapX, &full[s], kb * kBK,
+                                  nt * p.bn + j * ni + static_cast<int>(rank) * (ni / 2), pol_x);
+        if (ep.trace && blockIdx.x < 2 && i < 256 && lane == 0) ep.trace[blockIdx.x * 1024 + i] = globaltimer_ns();
+        if (++s == p.stages) {
+          s = 0;
+          ph ^= 1;
+        }
+        wrow += kWRowsPerTile;
+        if (++kb == p.KB) {  // next tile
+          kb = 0;
+          if (++nt == p.n_tiles) {
+            nt = 0;
+            ++pt;
+          }
+          wrow = (pt * 2 + static_cast<int>(rank)) * p.KB * kWRowsPerTile;
+        }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (lane 0 issues and commits) ----------------
-    const uint32_t idesc = make_idesc_bf16_f32(kBM, p.bn);
-    for (int i = 0; i < nk; ++i) {
-      const int s = i % p.stages;
-      const uint32_t ph = (i / p.stages) & 1;
-      mbar_wait(&full[s], ph);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t a = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
-        const uint32_t b = a + kABytes;
+    // ---------------- MMA issuer (leader, lane 0) / stage relay (peer) ----------------
+    if (rank == 0) {
+      const uint32_t idesc = make_idesc_bf16_f32(2 * kBM, ni);
+      int i = 0, seg = 0, s = 0;
+      uint32_t ph = 0;
+      long long u = u_begin;
+      int kb0 = static_cast<int>(u_begin % p.KB);
+      while (u < u_end) {
+        const int kb1 = static_cast<int>(min(static_cast<long long>(p.KB), kb0 + (u_end - u)));
+        const int buf = seg % p.nbuf;
+        const uint32_t use = seg / p.nbuf;
+        mbar_wait_cluster(&tempty[buf], (use & 1) ^ 1);  // both CTAs' epilogues drained it
+        tc_fence_after();
+        const uint32_t d0 = tmem + buf * 256;
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if (ep.trace && blockIdx.x == 0 && lane == 0 && i < 256) ep.trace[256 + i] = globaltimer_ns();
+          {
+            // warp-uniform issue (operands stay in uniform registers), one elected lane issues
+            const uint32_t a = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
+            const uint32_t b = a + kABytes;
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          umma_f16_ss(tmem, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc,
-                      (i | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
+              umma_f16_ss_pair_warp(d0, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc, acc);
+              if (p.n_mma == 2)
+                umma_f16_ss_pair_warp(d0 + ni, make_desc_k_sw128(a + k * 32),
+                                      make_desc_k_sw128(b + (ni / 2) * 128 + k * 32), idesc, acc);
+            }
+            umma_commit_pair_mc_warp(&empty[s], 0x3);
+            if (kb == kb1 - 1) umma_commit_pair_mc_warp(&tfull[buf], 0x3);
+          }
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
+          }
         }
-        umma_commit(&empty[s]);
-        if (i == nk - 1) umma_commit(tfull);
+        u += kb1 - kb0;
+        kb0 = 0;  // every later segment starts a new tile
+        ++seg;
       }
-      __syncwarp();
     }
   } else {
-    // ---------------- Epilogue (warps 2..5) ----------------
-    const int et = threadIdx.x - 64;             // 0..127
-    const uint32_t quarter = warp & 3;           // TMEM lane quarter this warp may access
-    const int r = static_cast<int>(quarter * 32 + lane);  // accumulator row (weight row in tile)
-    float* stile = reinterpret_cast<float*>(smem);        // [bn][kStilePitch] fp32, reuses ring
-    mbar_wait(tfull, 0);
-    tc_fence_after();
-    const uint32_t trow = tmem + ((quarter * 32u) << 16);
-
-    bool do_epilogue = true;
-    if (p.splits > 1) {
-      const size_t tile_elems = static_cast<size_t>(p.bn) * kBM;
-      float* wsp = ep.ws + (static_cast<size_t>(split * p.m_tiles + mt) * p.n_tiles + nt) * tile_elems;
-      for (int c0 = 0; c0 < p.bn; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld_32x32b_x16(trow + c0, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) __stcg(wsp + static_cast<size_t>(c0 + j) * kBM + r, __uint_as_float(v[j]));
-      }
-      __threadfence();
-      named_bar_sync(1, 128);
-      if (et == 0) {
-        int* ctr = ep.counters + mt * p.n_tiles + nt;
-        const int old = atomicAdd(ctr, 1);
-        s_last = (old == p.splits - 1);
-        if (s_last) *ctr = 0;  // re-arm for the next launch
-      }
-      named_bar_sync(1, 128);
-      do_epilogue = s_last != 0;
-      if (do_epilogue) {
-        __threadfence();
-        const float* base = ep.ws + (static_cast<size_t>(mt) * p.n_tiles + nt) * tile_elems;
-        const size_t split_stride = static_cast<size_t>(p.m_tiles) * p.n_tiles * tile_elems;
-        for (int c = 0; c < p.bn; ++c) {
-          float acc = 0.f;
-          for (int s = 0; s < p.splits; ++s)
-            acc += __ldcg(base + s * split_stride + static_cast<size_t>(c) * kBM + r);
-          stile[c * kStilePitch + r] = acc;
-        }
-      }
-    } else {
-      for (int c0 = 0; c0 < p.bn; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld_32x32b_x16(trow + c0, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) stile[(c0 + j) * kStilePitch + r] = __uint_as_float(v[j]);
-      }
-    }
-
-    if (do_epilogue) {
-      named_bar_sync(1, 128);
-      const int ew = et >> 5;
+    // ---------------- Epilogue (warps 2..5 of both CTAs) ----------------
+    const int et = threadIdx.x - 64;                        // 0..127
+    const uint32_t quarter = warp & 3;                      // TMEM lane quarter of this warp
+    const int r = static_cast<int>(quarter * 32 + lane);    // accumulator row within this CTA's half
+    const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+    int seg = 0;
+    long long u = u_begin;
+    const size_t tile_elems = static_cast<size_t>(p.bn) * kBM;
+    while (u < u_end) {
+      const int tile = static_cast<int>(u / p.KB);
+      const int kb0 = static_cast<int>(u % p.KB);
+      const int kb1 = static_cast<int>(min(static_cast<long long>(p.KB), kb0 + (u_end - u)));
+      const int pt = tile / p.n_tiles, nt = tile % p.n_tiles;
+      const int mt = pt * 2 + static_cast<int>(rank);       // this CTA's 128-row tile
+      const int buf = seg % p.nbuf;
+      const uint32_t use = seg / p.nbuf;
       const int tvalid = min(p.bn, p.N - nt * p.bn);
-      const int m0 = mt * kBM;
-      const int f = static_cast<int>(lane) * 4;
-      switch (ep.mode) {
-        case EPI_STORE_BF16:
-        case EPI_GELU: {
-          __nv_bfloat16* out = static_cast<__nv_bfloat16*>(ep.out);
-          const bool gelu = ep.mode == EPI_GELU;
-          for (int t = ew; t < tvalid; t += 4) {
-            const float4 v = *reinterpret_cast<const float4*>(stile + t * kStilePitch + f);
-            float x0 = v.x, x1 = v.y, x2 = v.z, x3 = v.w;
-            if (gelu) { x0 = gelu_tanh_f(x0); x1 = gelu_tanh_f(x1); x2 = gelu_tanh_f(x2); x3 = gelu_tanh_f(x3); }
-            __nv_bfloat16* dst = out + static_cast<long long>(nt * p.bn + t) * ep.ldo + m0 + f;
-            if (m0 + f + 3 < p.M) {
-              uint2 pk = make_uint2(pack_bf16x2(x0, x1), pack_bf16x2(x2, x3));
-              *reinterpret_cast<uint2*>(dst) = pk;
-            } else {
-              const float xs[4] = {x0, x1, x2, x3};
-              for (int j = 0; j < 4; ++j)
-                if (m0 + f + j < p.M) dst[j] = __float2bfloat16_rn(xs[j]);
-            }
-          }
-          break;
+      const bool whole = kb0 == 0 && kb1 == p.KB;
+      auto release_tmem = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + buf * 8);
+      };
+      if (ep.mode == EPI_QKV_ROPE) {  // stage per-token metadata for the fused KV append
+        named_bar_sync(2, 128);
+        for (int t = et; t < tvalid; t += 128) {
+          s_pos[t] = __ldg(ep.pos + nt * p.bn + t);
+          s_slot[t] = __ldg(ep.slot + nt * p.bn + t);
         }
-        case EPI_STORE_F32:
-        case EPI_ADD_F32: {
-          float* out = static_cast<float*>(ep.out);
-          const bool add = ep.mode == EPI_ADD_F32;
-          for (int t = ew; t < tvalid; t += 4) {
-            float4 v = *reinterpret_cast<const float4*>(stile + t * kStilePitch + f);
-            float* dst = out + static_cast<long long>(nt * p.bn + t) * ep.ldo + m0 + f;
-            if (m0 + f + 3 < p.M) {
-              if (add) {
-                const float4 o = *reinterpret_cast<const float4*>(dst);
-                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
-              }
-              *reinterpret_cast<float4*>(dst) = v;
-            } else {
-              const float xs[4] = {v.x, v.y, v.z, v.w};
-              for (int j = 0; j < 4; ++j)
-                if (m0 + f + j < p.M) dst[j] = add ? dst[j] + xs[j] : xs[j];
-            }
-          }
-          break;
-        }
-        case EPI_SILU_MUL: {
-          // rows [0,64) of the tile are gate features, [64,128) the matching up features.
-          __nv_bfloat16* out = static_cast<__nv_bfloat16*>(ep.out);
-          const int fo = static_cast<int>(lane) * 2;
-          for (int t = ew; t < tvalid; t += 4) {
-            const float* srow = stile + t * kStilePitch;
-            const float2 g = *reinterpret_cast<const float2*>(srow + fo);
-            const float2 u = *reinterpret_cast<const float2*>(srow + 64 + fo);
-            __nv_bfloat16* dst = out + static_cast<long long>(nt * p.bn + t) * ep.ldo + mt * 64 + fo;
-            *reinterpret_cast<uint32_t*>(dst) = pack_bf16x2(silu_f(g.x) * u.x, silu_f(g.y) * u.y);
-          }
-          break;
-        }
-        case EPI_QKV_ROPE: {
-          const int hd = ep.head_dim, half = hd >> 1;
-          __nv_bfloat16* qout = static_cast<__nv_bfloat16*>(ep.out);
-          __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(ep.kcache);
-          __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(ep.vcache);
-          const int pr = static_cast<int>(lane) * 2;   // first of this lane's two pairs
-          const int hh = pr / half, d = pr % half;     // head within tile, dim within half
-          const int f1 = hh * hd + d;
-          const int gm = m0 + f1;                      // global feature of x1
-          if (gm < p.M) {
-            const int gh = gm / hd;                    // global head index in [q | k | v]
-            for (int t = ew; t < tvalid; t += 4) {
-              const float* srow = stile + t * kStilePitch;
-              const int gt = nt * p.bn + t;
-              float2 x1 = *reinterpret_cast<const float2*>(srow + f1);
-              float2 x2 = *reinterpret_cast<const float2*>(srow + f1 + half);
-              if (gh < ep.n_q_local + ep.n_kv_local) {
-                const int ps = ep.pos[gt];
-                const float2 c = *reinterpret_cast<const float2*>(ep.rope_cos + static_cast<size_t>(ps) * half + d);
-                const float2 s = *reinterpret_cast<const float2*>(ep.rope_sin + static_cast<size_t>(ps) * half + d);
-                const float2 y1 = make_float2(x1.x * c.x - x2.x * s.x, x1.y * c.y - x2.y * s.y);
-                const float2 y2 = make_float2(x2.x * c.x + x1.x * s.x, x2.y * c.y + x1.y * s.y);
-                x1 = y1;
-                x2 = y2;
-              }
-              if (gh < ep.n_q_local) {
-                __nv_bfloat16* dst = qout + static_cast<long long>(gt) * ep.ldo + gh * hd + d;
-                *reinterpret_cast<uint32_t*>(dst) = pack_bf16x2(x1.x, x1.y);
-                *reinterpret_cast<uint32_t*>(dst + half) = pack_bf16x2(x2.x, x2.y);
-              } else {
-                const bool isk = gh < ep.n_q_local + ep.n_kv_local;
-                const int kvh = isk ? gh - ep.n_q_local : gh - ep.n_q_local - ep.n_kv_local;
-                const int sl = ep.slot[gt];
-                const size_t row = (static_cast<size_t>(sl / ep.block_size) * ep.n_kv_local + kvh) * ep.block_size +
-                                   sl % ep.block_size;
-                __nv_bfloat16* dst = (isk ? kc : vc) + row * hd + d;
-                *reinterpret_cast<uint32_t*>(dst) = pack_bf16x2(x1.x, x1.y);
-                *reinterpret_cast<uint32_t*>(dst + half) = pack_bf16x2(x2.x, x2.y);
-              }
-            }
-          }
-          break;
-        }
-        default:
-          break;
+        named_bar_sync(2, 128);
       }
+      if (lane == 0) mbar_wait(&tfull[buf], use & 1);
+      __syncwarp();
+      tc_fence_after();
+      if (ep.trace && blockIdx.x < 2 && et == 0 && seg < 64) ep.trace[blockIdx.x * 1024 + 512 + seg] = globaltimer_ns();
+      const uint32_t trow = tmem + buf * 256 + ((quarter * 32u) << 16);
+      const int nchunks = (tvalid + 15) / 16;
+      if (whole) {
+        for (int ch = 0; ch < nchunks; ++ch) {
+          uint32_t raw[16];
+          tmem_ld_32x32b_x16(trow + ch * 16, raw);
+          tmem_ld_wait();
+          if (ch == nchunks - 1) release_tmem();
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
+          epilogue_chunk(p, ep, v, r, mt, nt, ch * 16, tvalid, xbuf, s_pos, s_slot);
+        }
+      } else {
+        if (ep.mode == EPI_ADD_F32) {
+          // residual add: every contributor adds its partial straight into the fp32 residual
+          // (red.global.add; no partial buffer, no reduction pass)
+          const int m = mt * kBM + r;
+          for (int ch = 0; ch < nchunks; ++ch) {
+            uint32_t raw[16];
+            tmem_ld_32x32b_x16(trow + ch * 16, raw);
+            tmem_ld_wait();
+            if (ch == nchunks - 1) release_tmem();
+            if (m < p.M) {
+              float* out = static_cast<float*>(ep.out) + (static_cast<long long>(nt) * p.bn + ch * 16) * ep.ldo + m;
+              const int nv = min(16, tvalid - ch * 16);
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (j < nv) atomicAdd(out + j * ep.ldo, __uint_as_float(raw[j]));
+            }
+          }
+        } else {
+          // stream-K partial: slot = position of this pair among the tile's contributors; the last to
+          // arrive sums the slots in slot order (deterministic) and runs the fused epilogue
+          const int c_first = cta_of(static_cast<long long>(tile) * p.KB, p);
+          const int c_last = cta_of(static_cast<long long>(tile) * p.KB + p.KB - 1, p);
+          const int nslot = c_last - c_first + 1;
+          const int slot = pair - c_first;
+          const size_t tile128 = static_cast<size_t>(mt) * p.n_tiles + nt;
+          float* wsp = ep.ws + (tile128 * p.max_slots + slot) * tile_elems;
+          for (int ch = 0; ch < nchunks; ++ch) {
+            uint32_t raw[16];
+            tmem_ld_32x32b_x16(trow + ch * 16, raw);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) __stcg(wsp + static_cast<size_t>(ch * 16 + j) * kBM + r, __uint_as_float(raw[j]));
+          }
+          release_tmem();
+          __threadfence();
+          named_bar_sync(1, 128);
+          if (et == 0) {
+            int* ctr = ep.counters + tile128;
+            const int old = atomicAdd(ctr, 1);
+            s_last = (old == nslot - 1);
+            if (s_last) *ctr = 0;  // re-arm for the next launch
+          }
+          named_bar_sync(1, 128);
+          if (s_last) {
+            __threadfence();
+            const float* base = ep.ws + tile128 * p.max_slots * tile_elems;
+            for (int ch = 0; ch < nchunks; ++ch) {
+              float v[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = 0.f;
+              // all slots' loads of this chunk in flight before summing (slot order kept)
+              for (int s0 = 0; s0 < nslot; s0 += 4) {
+                float t[4][16];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float* src = base + (s0 + q) * tile_elems + static_cast<size_t>(ch * 16) * kBM + r;
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) t[q][j] = (s0 + q < nslot) ? __ldcg(src + j * kBM) : 0.f;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) v[j] += t[q][j];
+              }
+              epilogue_chunk(p, ep, v, r, mt, nt, ch * 16, tvalid, xbuf, s_pos, s_slot);
+            }
+          }
+        }
+      }
+      u += kb1 - kb0;
+      ++seg;
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, p.tmem_cols);
+    tmem_dealloc_pair(tmem, p.tmem_cols);
   }
 }
 
@@ -312,6 +465,8 @@ uint32_t pow2_cols(int n) {
   return c;
 }
 
+size_t extra_smem(int bn) { return kBM * kXPitch * 4 + 2 * static_cast<size_t>(bn) * 4 + 3 * 8 * 8 + 64 + 64; }
+
 }  // namespace
 
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
@@ -328,79 +483,104 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
   return r == CUDA_SUCCESS;
 }
 
-GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int force_splits) {
+GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int force_pairs) {
   GemmPlan pl;
   pl.M = M;
   pl.N = N;
   pl.K = K;
   const int KB = K / kBK;
-  pl.n_tiles = (N + 255) / 256;
+  pl.n_tiles = (N + 511) / 512;
   const int per = (N + pl.n_tiles - 1) / pl.n_tiles;
-  pl.bn = std::max(16, (per + 15) / 16 * 16);
-  pl.m_tiles = (M + kBM - 1) / kBM;
-  const size_t tile_elems = static_cast<size_t>(pl.bn) * kBM;
-
-  double best = 1e300;
-  int best_s = 1, best_kbps = KB;
-  const int smax = std::min(32, KB);
-  for (int s = 1; s <= smax; ++s) {
-    const int kbps = (KB + s - 1) / s;
-    const int s_eff = (KB + kbps - 1) / kbps;
-    if (s_eff != s) continue;
-    if (force_splits > 0 && s != force_splits) continue;
-    const size_t ws_need = s > 1 ? static_cast<size_t>(s) * pl.m_tiles * pl.n_tiles * tile_elems : 0;
-    if (ws_need > ws_cap_floats) continue;
-    const int ctas = pl.m_tiles * pl.n_tiles * s;
-    const int waves = (ctas + num_sms - 1) / num_sms;
-    const int active = std::min(ctas, num_sms);
-    // cycles per k-block per CTA: MMA (2*bn) vs this CTA's share of HBM weight streaming
-    const double t_kb = std::max(2.0 * pl.bn, kABytes * static_cast<double>(active) / 3400.0) + 64.0;
-    double est = waves * (kbps * t_kb + 1500.0);
-    if (s > 1) est += 800.0 + s * pl.bn * 4.0;  // partial write + last-CTA reduction
-    if (est < best * 0.98) {
-      best = est;
-      best_s = s;
-      best_kbps = kbps;
-    }
+  if (per <= 256) {
+    pl.n_mma = 1;
+    pl.bn = std::max(16, (per + 15) / 16 * 16);
+  } else {
+    pl.n_mma = 2;
+    pl.bn = (per + 31) / 32 * 32;
   }
-  pl.splits = best_s;
-  pl.kb_per_split = best_kbps;
-  pl.ws_floats = pl.splits > 1 ? static_cast<size_t>(pl.splits) * pl.m_tiles * pl.n_tiles * tile_elems : 0;
-  const size_t stage = kABytes + static_cast<size_t>(pl.bn) * kBK * 2;
-  const size_t budget = 224 * 1024;
-  int stages = static_cast<int>(std::min<size_t>(8, (budget - 2048) / stage));
-  stages = std::max(2, std::min(stages, std::max(2, pl.kb_per_split)));
-  pl.stages = stages;
-  const size_t main = std::max(stages * stage, static_cast<size_t>(pl.bn) * kStilePitch * 4);
-  pl.smem = main + 1024 + 256;
+  pl.box_rows = pl.bn / pl.n_mma / 2;  // each CTA of the pair holds half of every UMMA's tokens
+  pl.pm_tiles = (M + 2 * kBM - 1) / (2 * kBM);
+  pl.m_tiles = 2 * pl.pm_tiles;
+  const long long ptiles = static_cast<long long>(pl.pm_tiles) * pl.n_tiles;
+  pl.units = ptiles * KB;
+  // persistent grid: one CTA pair per 2 SMs, each pair with at least ~4 k-blocks of work
+  int pairs = static_cast<int>(std::min<long long>(num_sms / 2, std::max<long long>(1, pl.units / 4)));
+  if (force_pairs > 0) pairs = static_cast<int>(std::min<long long>(pl.units, force_pairs));
+  auto slots_for = [&](int g) {
+    const long long pc = pl.units / g;  // >= 1
+    const int s = pc >= KB ? 2 : static_cast<int>((KB + pc - 1) / pc) + 1;
+    return std::min(s, g);
+  };
+  int max_slots = slots_for(pairs);
+  const size_t tile_elems = static_cast<size_t>(pl.bn) * kBM;
+  const size_t tiles128 = static_cast<size_t>(pl.m_tiles) * pl.n_tiles;
+  while (pairs > 1 && tiles128 * max_slots * tile_elems > ws_cap_floats) {
+    pairs = std::max(1, pairs / 2);
+    max_slots = slots_for(pairs);
+  }
+  pl.ctas = pairs;
+  pl.max_slots = max_slots;
+  pl.splits = static_cast<int>((pl.units + pairs - 1) / pairs);  // units per pair (informational)
+  pl.kb_per_split = pl.splits;
+  pl.ws_floats = tiles128 * max_slots * tile_elems;
+  pl.nbuf = pl.bn <= 256 ? 2 : 1;
+  const size_t stage = kABytes + static_cast<size_t>(pl.bn / 2) * kBK * 2;
+  const size_t budget = 226 * 1024 - 1024 - extra_smem(pl.bn);
+  pl.stages = static_cast<int>(std::max<size_t>(2, std::min<size_t>(8, budget / stage)));
+  pl.smem = pl.stages * stage + extra_smem(pl.bn) + 1024;
   return pl;
 }
 
-cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const GemmPlan& pl,
-                        const EpiParams& ep, cudaStream_t stream) {
-  static size_t configured = 0;
-  if (pl.smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(std::max<size_t>(pl.smem, 200 * 1024)));
+bool make_tmap_weight(CUtensorMap* map, const void* w, int M, int K) {
+  PFN_encodeTiled_t enc = get_encode_fn();
+  if (!enc) return false;
+  const uint64_t rows = static_cast<uint64_t>((M + kBM - 1) / kBM) * (K / kBK) * kWRowsPerTile;
+  cuuint64_t dims[2] = {256, rows};
+  cuuint64_t strides[1] = {512};
+  cuuint32_t box[2] = {256, kWRowsPerTile};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const GemmPlan& pl, const EpiParams& ep,
+                        cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
     if (e != cudaSuccess) return e;
-    configured = std::max<size_t>(pl.smem, 200 * 1024);
+    configured = true;
   }
   KParams kp;
   kp.M = pl.M;
   kp.N = pl.N;
   kp.KB = pl.K / kBK;
   kp.bn = pl.bn;
-  kp.m_tiles = pl.m_tiles;
+  kp.n_mma = pl.n_mma;
+  kp.pm_tiles = pl.pm_tiles;
   kp.n_tiles = pl.n_tiles;
-  kp.splits = pl.splits;
-  kp.kb_per_split = pl.kb_per_split;
+  kp.units = pl.units;
+  kp.ctas = pl.ctas;
   kp.stages = pl.stages;
-  kp.tmem_cols = pow2_cols(pl.bn);
-  const size_t stage = kABytes + static_cast<size_t>(pl.bn) * kBK * 2;
-  kp.smem_main = static_cast<uint32_t>(std::max(pl.stages * stage, static_cast<size_t>(pl.bn) * kStilePitch * 4));
-  dim3 grid(pl.m_tiles, pl.n_tiles, pl.splits);
-  gemm_bf16_tc_kernel<<<grid, kThreads, pl.smem, stream>>>(mapW, mapX, kp, ep);
-  return cudaGetLastError();
+  kp.nbuf = pl.nbuf;
+  kp.max_slots = pl.max_slots;
+  kp.tmem_cols = pl.nbuf == 2 ? 512 : pow2_cols(pl.bn);
+  kp.ring_bytes = static_cast<uint32_t>(pl.stages * (kABytes + static_cast<size_t>(pl.bn / 2) * kBK * 2));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pl.ctas);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_bf16_pair, mapW, mapX, kp, ep);
 }
 
 }  // namespace sarathi

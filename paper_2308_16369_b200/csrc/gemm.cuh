@@ -35,26 +35,42 @@ struct EpiParams {
   // split-K workspace (fp32 partials) + per-tile arrival counters (kept zero between launches)
   float* ws = nullptr;
   int* counters = nullptr;
+  // debug: globaltimer stamps of the first CTA pair (producer issue / MMA full-wake / epilogue wake)
+  unsigned long long* trace = nullptr;
+  int dbg = 0;  // debug: bit0 skip X loads, bit1 skip W loads (timing experiments only; results invalid)
 };
 
 struct GemmPlan {
   int M = 0, N = 0, K = 0;
-  int bn = 0;          // tokens per CTA tile (multiple of 16, <= 256)
-  int m_tiles = 0, n_tiles = 0;
-  int splits = 1, kb_per_split = 0;
+  int bn = 0;          // tokens per tile (multiple of 16, <= 512)
+  int n_mma = 1;       // UMMAs per k-step (bn / n_mma <= 256 tokens each)
+  int box_rows = 0;    // X TMA box rows (per CTA of the pair: half of one UMMA's tokens)
+  int pm_tiles = 0;    // 256-row tiles (one per CTA pair)
+  int m_tiles = 0, n_tiles = 0;  // 128-row tiles (2 * pm_tiles), token tiles
+  long long units = 0; // (pair tile, k-block) work units
+  int ctas = 0;        // persistent grid size in CTA PAIRS
+  int max_slots = 1;   // stream-K partial slots per tile
+  int nbuf = 1;        // TMEM accumulator buffers
+  int splits = 1, kb_per_split = 0;  // units per CTA (informational)
   int stages = 0;
   size_t smem = 0;
-  size_t ws_floats = 0;  // workspace needed (splits > 1)
+  size_t ws_floats = 0;  // stream-K workspace needed
 };
 
-// Choose tile / split-K for C[N x M] = X[N x K] * W[M x K]^T on `num_sms` SMs.
-GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int force_splits = 0);
+// Persistent stream-K plan for C[N x M] = X[N x K] * W[M x K]^T on `num_sms` SMs (CTA pairs,
+// tcgen05 cta_group::2).  force_pairs > 0 fixes the grid (tests use it to exercise multi-pair
+// reductions of one tile).
+GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int force_pairs = 0);
 
 // 2D bf16 K-major tensor map with 128B swizzle: rows x cols(=K), box = box_rows x 64.
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                     uint64_t row_stride_elems, uint32_t box_rows);
 
-cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const GemmPlan& plan,
-                        const EpiParams& ep, cudaStream_t stream);
+// Tensor map over a tile-major, pre-swizzled weight (launch_pack_weight layout): each 16 KB tile
+// is read as 32 rows x 512 B (unswizzled box; the bytes are already the SW128 smem image).
+bool make_tmap_weight(CUtensorMap* map, const void* w, int M, int K);
+// mapW: make_tmap_weight map; mapX: activation [N][K] map (make_tmap_bf16, box rows plan.box_rows).
+cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const GemmPlan& plan, const EpiParams& ep,
+                        cudaStream_t stream);
 
 }  // namespace sarathi

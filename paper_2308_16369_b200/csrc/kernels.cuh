@@ -63,8 +63,17 @@ cudaError_t launch_vocab_permute(const float* gathered, float* logits, int world
 
 // Device weight generator (same counter-based spec as synth/__init__.py, independent code).
 // dst[r][c] = bf16_rne( f32(2*u24 - (2^24-1)) * scale[r] ), u24 = splitmix64(seed ^ (tau[r] << 40 | base[r] + c)) >> 40
+// packed != 0: write the tile-major GEMM layout (see packed_weight_index); dst must hold
+// ceil(rows/128)*128 rows (padding rows zeroed by the caller).
 cudaError_t launch_weightgen(__nv_bfloat16* dst, int rows, int cols, const int* tau, const float* scale,
-                             const long long* base, unsigned long long seed, cudaStream_t st);
+                             const long long* base, unsigned long long seed, int packed, cudaStream_t st);
+// Row-major [rows][cols] -> tile-major, SW128-pre-swizzled GEMM layout: element (r, c) at
+// ((r/128)*(cols/64) + c/64)*8192 + (r%128)*64 + (((c%64)/8) ^ (r%8))*8 + c%8.
+cudaError_t launch_pack_weight(const __nv_bfloat16* src, __nv_bfloat16* dst, int rows, int cols, cudaStream_t st);
+inline size_t packed_weight_index(int r, int c, int cols) {
+  const int rr = r & 127, j = (c & 63) >> 3;
+  return ((static_cast<size_t>(r >> 7) * (cols >> 6) + (c >> 6)) << 13) + (rr << 6) + ((j ^ (rr & 7)) << 3) + (c & 7);
+}
 // dst[i] = bf16_rne( 1.0f + f32(v) * f32(0.1/2^24) )  over flat indices [base, base+n)
 cudaError_t launch_gaingen(__nv_bfloat16* dst, int n, int tau, long long base, unsigned long long seed,
                            cudaStream_t st);

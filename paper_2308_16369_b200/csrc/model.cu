@@ -95,6 +95,13 @@ Status Model::dalloc(T** p, size_t count) {
   return Status::ok();
 }
 
+Status Model::dalloc_padded(__nv_bfloat16** p, int rows, int cols) {
+  const size_t n = static_cast<size_t>((rows + 127) / 128) * 128 * cols;
+  Status s = dalloc(p, n);
+  if (s.code != SARATHI_OK) return s;
+  return check(cudaMemsetAsync(*p, 0, n * 2, stream), "memset weight padding");
+}
+
 #define SRET(x)                  \
   do {                           \
     Status _s = (x);             \
@@ -163,11 +170,11 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   SRET(dalloc(&d_tau, max_rows));
   SRET(dalloc(&d_scl, max_rows));
   SRET(dalloc(&d_base, max_rows));
-  auto gen = [&](__nv_bfloat16* dst, int rows, int cols) -> Status {
+  auto gen = [&](__nv_bfloat16* dst, int rows, int cols, int packed) -> Status {
     SRET(check(cudaMemcpyAsync(d_tau, tau.data(), rows * sizeof(int), cudaMemcpyHostToDevice, stream), "H2D"));
     SRET(check(cudaMemcpyAsync(d_scl, scl.data(), rows * sizeof(float), cudaMemcpyHostToDevice, stream), "H2D"));
     SRET(check(cudaMemcpyAsync(d_base, base.data(), rows * sizeof(long long), cudaMemcpyHostToDevice, stream), "H2D"));
-    SRET(check(launch_weightgen(dst, rows, cols, d_tau, d_scl, d_base, seed, stream), "weightgen"));
+    SRET(check(launch_weightgen(dst, rows, cols, d_tau, d_scl, d_base, seed, packed, stream), "weightgen"));
     ++launches;
     return check(cudaStreamSynchronize(stream), "weightgen sync");  // host vectors are reused
   };
@@ -179,10 +186,11 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   layers.resize(L);
   for (int l = 0; l < L; ++l) {
     LayerWeights& w = layers[l];
-    SRET(dalloc(&w.qkv, static_cast<size_t>(qkv_rows) * H));
-    SRET(dalloc(&w.o, static_cast<size_t>(H) * q_dim_l));
-    SRET(dalloc(&w.gu, static_cast<size_t>(gu_rows) * H));
-    SRET(dalloc(&w.down, static_cast<size_t>(H) * h2_l));
+    // GEMM weights in the tile-major layout (rows padded to 128; padding zero)
+    SRET(dalloc_padded(&w.qkv, qkv_rows, H));
+    SRET(dalloc_padded(&w.o, H, q_dim_l));
+    SRET(dalloc_padded(&w.gu, gu_rows, H));
+    SRET(dalloc_padded(&w.down, H, h2_l));
     SRET(dalloc(&w.g1, H));
     SRET(dalloc(&w.g2, H));
     // QKV: [q_r ; k_r ; v_r], column-parallel (rank's heads of the logical Wq, Wk, Wv)
@@ -204,7 +212,7 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
       scl[r] = weight_scale(s_in);
       base[r] = lrow * H;
     }
-    SRET(gen(w.qkv, qkv_rows, H));
+    SRET(gen(w.qkv, qkv_rows, H, 1));
     // O: row-parallel [H][q_dim_l] = columns rank*q_dim_l.. of the logical [H][nq*hd]
     fill(H);
     for (int r = 0; r < H; ++r) {
@@ -212,7 +220,7 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
       scl[r] = weight_scale(s_o);
       base[r] = static_cast<long long>(r) * c.n_heads * hd + static_cast<long long>(rank) * q_dim_l;
     }
-    SRET(gen(w.o, H, q_dim_l));
+    SRET(gen(w.o, H, q_dim_l, 1));
     // gate||up interleaved in 64-row blocks (SwiGLU) or W1 (GELU)
     fill(gu_rows);
     for (int r = 0; r < gu_rows; ++r) {
@@ -227,7 +235,7 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
       scl[r] = weight_scale(s_in);
       base[r] = (static_cast<long long>(rank) * h2_l + fl) * H;
     }
-    SRET(gen(w.gu, gu_rows, H));
+    SRET(gen(w.gu, gu_rows, H, 1));
     // down: row-parallel [H][h2_l]
     fill(H);
     for (int r = 0; r < H; ++r) {
@@ -235,13 +243,13 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
       scl[r] = weight_scale(s_d);
       base[r] = static_cast<long long>(r) * c.ffn_hidden + static_cast<long long>(rank) * h2_l;
     }
-    SRET(gen(w.down, H, h2_l));
+    SRET(gen(w.down, H, h2_l, 1));
+    if (!make_tmap_weight(&w.m_qkv, w.qkv, qkv_rows, H) || !make_tmap_weight(&w.m_o, w.o, H, q_dim_l) ||
+        !make_tmap_weight(&w.m_gu, w.gu, gu_rows, H) || !make_tmap_weight(&w.m_down, w.down, H, h2_l))
+      return Status::err(SARATHI_ECUDA, "cuTensorMapEncodeTiled failed for a weight");
     SRET(check(launch_gaingen(w.g1, H, 16 * l + kG1, 0, seed, stream), "gaingen"));
     SRET(check(launch_gaingen(w.g2, H, 16 * l + kG2, 0, seed, stream), "gaingen"));
     launches += 2;
-    if (!make_tmap_bf16(&w.m_qkv, w.qkv, qkv_rows, H, H, 128) || !make_tmap_bf16(&w.m_o, w.o, H, q_dim_l, q_dim_l, 128) ||
-        !make_tmap_bf16(&w.m_gu, w.gu, gu_rows, H, H, 128) || !make_tmap_bf16(&w.m_down, w.down, H, h2_l, h2_l, 128))
-      return Status::err(SARATHI_ECUDA, "cuTensorMapEncodeTiled failed for a weight");
   }
   // embedding (replicated), final gain, LM head (vocab-parallel)
   SRET(dalloc(&emb, static_cast<size_t>(c.vocab) * H));
@@ -251,19 +259,19 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
     scl[r] = weight_scale(1.0);
     base[r] = static_cast<long long>(r) * H;
   }
-  SRET(gen(emb, c.vocab, H));
+  SRET(gen(emb, c.vocab, H, 0));
   SRET(dalloc(&gf, H));
   SRET(check(launch_gaingen(gf, H, kGfTau, 0, seed, stream), "gaingen"));
   ++launches;
-  SRET(dalloc(&lm, static_cast<size_t>(vocab_l) * H));
+  SRET(dalloc_padded(&lm, vocab_l, H));
   fill(vocab_l);
   for (int r = 0; r < vocab_l; ++r) {
     tau[r] = kWlmTau;
     scl[r] = weight_scale(s_in);
     base[r] = (static_cast<long long>(rank) * vocab_l + r) * H;
   }
-  SRET(gen(lm, vocab_l, H));
-  if (!make_tmap_bf16(&m_lm, lm, vocab_l, H, H, 128)) return Status::err(SARATHI_ECUDA, "tensor map (lm head)");
+  SRET(gen(lm, vocab_l, H, 1));
+  if (!make_tmap_weight(&m_lm, lm, vocab_l, H)) return Status::err(SARATHI_ECUDA, "tensor map (lm head)");
 
   // RoPE tables (fp64 on host -> fp32), reading O-7
   {
@@ -339,11 +347,11 @@ Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, 
   auto it = plans.find(pk);
   if (it == plans.end()) it = plans.emplace(pk, plan_gemm(M, N, K, num_sms, gemm_ws_floats)).first;
   const GemmPlan& pl = it->second;
-  auto xk = std::make_tuple(X, N, K, pl.bn);
+  auto xk = std::make_tuple(X, N, K, pl.box_rows);
   auto xi = xmaps.find(xk);
   if (xi == xmaps.end()) {
     CUtensorMap m;
-    if (!make_tmap_bf16(&m, X, N, K, ldx, pl.bn)) return Status::err(SARATHI_ECUDA, "tensor map (activation)");
+    if (!make_tmap_bf16(&m, X, N, K, ldx, pl.box_rows)) return Status::err(SARATHI_ECUDA, "tensor map (activation)");
     xi = xmaps.emplace(xk, m).first;
   }
   EpiParams ep = ep_in;

@@ -37,7 +37,7 @@ struct LayerWeights {
   __nv_bfloat16* down = nullptr;  // [H][H2_l]
   __nv_bfloat16* g1 = nullptr;    // [H]
   __nv_bfloat16* g2 = nullptr;    // [H]
-  CUtensorMap m_qkv, m_o, m_gu, m_down;
+  CUtensorMap m_qkv, m_o, m_gu, m_down;  // make_tmap_weight maps of the packed weights
 };
 
 struct Model {
@@ -116,6 +116,7 @@ struct Model {
   Status check(cudaError_t e, const char* what);
   template <typename T>
   Status dalloc(T** p, size_t count);
+  Status dalloc_padded(__nv_bfloat16** p, int rows, int cols);  // tile-major GEMM weight, rows -> x128
 };
 
 int nccl_unique_id(void* out128, std::string* err);

@@ -33,7 +33,9 @@ EXPORTS = [
     "sarathi_sched_submit", "sarathi_sched_next", "sarathi_sched_complete", "sarathi_sched_idle_step",
     "sarathi_sched_done", "sarathi_sched_block_table", "sarathi_op_gemm", "sarathi_op_rmsnorm",
     "sarathi_request_truncate", "sarathi_last_io_bytes", "sarathi_set_profiling", "sarathi_op_times",
+    "sarathi_op_pack_weight",
 ]
+GEMM_W_PACKED = 0x100
 OP_NAMES = ["embed", "rmsnorm", "gemm_qkv", "prefill_attn", "decode_attn", "gemm_o", "gemm_gate_up",
             "gemm_down", "lm_head", "allreduce", "other"]
 
@@ -105,6 +107,7 @@ def _load() -> C.CDLL:
         "sarathi_last_io_bytes": [VP, P(I64), P(I64)],
         "sarathi_set_profiling": [VP, I32],
         "sarathi_op_times": [VP, P(C.c_double), P(I64), I32, I32],
+        "sarathi_op_pack_weight": [VP, VP, I32, I32, VP],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -351,6 +354,11 @@ def op_gemm(W_ptr: int, X_ptr: int, out_ptr: int, M: int, N: int, K: int, mode: 
             stream: int = 0):
     _check(lib.sarathi_op_gemm(C.c_void_p(W_ptr), C.c_void_p(X_ptr), C.c_void_p(out_ptr), M, N, K, mode,
                                force_splits, C.c_void_p(stream) if stream else None))
+
+
+def op_pack_weight(W_ptr: int, out_ptr: int, rows: int, cols: int, stream: int = 0):
+    _check(lib.sarathi_op_pack_weight(C.c_void_p(W_ptr), C.c_void_p(out_ptr), rows, cols,
+                                      C.c_void_p(stream) if stream else None))
 
 
 def op_rmsnorm(h_ptr: int, g_ptr: int, out_ptr: int, R: int, H: int, eps: float, stream: int = 0):

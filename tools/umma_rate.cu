@@ -1,0 +1,135 @@
+// Microbenchmark: raw tcgen05.mma issue/execute rate (no memory traffic): kind::f16, bf16 in, fp32
+// accumulate, operands in shared memory (garbage), accumulator in TMEM.  1-CTA (M=128) and CTA-pair
+// (cta_group::2, M=256) for several N; commits every `per_commit` MMAs to an mbarrier and waits, like
+// a GEMM mainloop.  Used to size the GEMM.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2308_16369_b200/csrc -o tools/umma_rate tools/umma_rate.cu
+#include <cstdio>
+#include "common.cuh"
+
+using namespace sarathi;
+
+template <int PAIR, int WARP>
+__global__ void __launch_bounds__(128, 1) umma_loop(int N, int iters, int per_commit, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t holder;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    if (PAIR)
+      tmem_alloc_pair(&holder, 512);
+    else
+      tmem_alloc(&holder, 512);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (PAIR) cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = holder;
+  unsigned long long t0 = 0, t1 = 0;
+  if (WARP && warp == 0 && rank == 0) {
+    const uint32_t idesc = make_idesc_bf16_f32(PAIR ? 256 : 128, N);
+    const uint32_t a = smem_u32(smem), b = a + 16384;
+    uint32_t ph = 0;
+    t0 = globaltimer_ns();
+    for (int i = 0; i < iters; i += 4) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (PAIR)
+          umma_f16_ss_pair_warp(tmem, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc, 1);
+        else
+          umma_f16_ss_warp(tmem, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc, 1);
+      }
+      if ((i + 4) % per_commit == 0) {
+        if (PAIR)
+          umma_commit_pair_mc_warp(&bar, 0x1);
+        else
+          umma_commit_warp(&bar);
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      }
+    }
+    t1 = globaltimer_ns();
+    if (lane == 0) out[blockIdx.x] = t1 - t0;
+  }
+  if (!WARP && warp == 0 && rank == 0 && lane == 0) {
+    const uint32_t idesc = make_idesc_bf16_f32(PAIR ? 256 : 128, N);
+    const uint32_t a = smem_u32(smem), b = a + 16384;
+    uint32_t ph = 0;
+    t0 = globaltimer_ns();
+    for (int i = 0; i < iters; ++i) {
+      const int k = i & 3;
+      if (PAIR)
+        umma_f16_ss_pair(tmem, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc, 1);
+      else
+        umma_f16_ss(tmem, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc, 1);
+      if ((i + 1) % per_commit == 0) {
+        if (PAIR)
+          umma_commit_pair_mc(&bar, 0x1);
+        else
+          umma_commit(&bar);
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      }
+    }
+    t1 = globaltimer_ns();
+    out[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (PAIR) cluster_sync_all();
+  if (warp == 0) {
+    tc_fence_after();
+    if (PAIR)
+      tmem_dealloc_pair(tmem, 512);
+    else
+      tmem_dealloc(tmem, 512);
+  }
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 1024 * 8);
+  const size_t smem = 16384 + 32768 + 1024;
+  cudaFuncSetAttribute(umma_loop<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(umma_loop<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(umma_loop<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(umma_loop<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int iters = 4096;
+  for (int warpv = 0; warpv < 2; ++warpv)
+  for (int pair = 0; pair < 2; ++pair) {
+    for (int N : {64, 128, 160, 256}) {
+      for (int per_commit : {4, 8, 64}) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(pair ? 2 : 1);
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = pair ? 2 : 1;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t e;
+        if (warpv)
+          e = pair ? cudaLaunchKernelEx(&cfg, umma_loop<1, 1>, N, iters, per_commit, d)
+                   : cudaLaunchKernelEx(&cfg, umma_loop<0, 1>, N, iters, per_commit, d);
+        else
+          e = pair ? cudaLaunchKernelEx(&cfg, umma_loop<1, 0>, N, iters, per_commit, d)
+                   : cudaLaunchKernelEx(&cfg, umma_loop<0, 0>, N, iters, per_commit, d);
+        cudaDeviceSynchronize();
+        unsigned long long ns = 0;
+        cudaMemcpy(&ns, d, 8, cudaMemcpyDeviceToHost);
+        const double flops = 2.0 * (pair ? 256 : 128) * N * 16 * iters;
+        printf("%s %s N=%3d commit/%2d : %7.1f ns per MMA, %7.1f TFLOP/s per %s (%s)\n", warpv ? "warp-uniform" : "lane0-branch", pair ? "pair M=256" : "cta  M=128",
+               N, per_commit, ns / (double)iters, flops / ns / 1e3, pair ? "SM pair" : "SM", cudaGetErrorString(e));
+      }
+    }
+  }
+  return 0;
+}

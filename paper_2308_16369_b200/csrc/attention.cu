@@ -16,6 +16,7 @@
 //    QKV epilogue).  Flash-style online softmax with mma.sync m16n8k16 bf16 (first version).
 #include "common.cuh"
 #include "kernels.cuh"
+#include "gemm.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -27,226 +28,7 @@ namespace {
 constexpr float kLog2e = 1.4426950408889634f;
 
 // ---------------------------------------------------------------------------
-// Decode attention
-// ---------------------------------------------------------------------------
-template <int HD, int G>
-__global__ void __launch_bounds__(128)
-    decode_attn_kernel(DecodeAttnArgs a) {
-  constexpr int kThreads = 128;
-  constexpr int kLanesPerKey = HD / 8;            // 16 lanes x 8 dims (HD=128); 8 lanes (HD=64)
-  constexpr int kKeyGroups = kThreads / kLanesPerKey;
-  const int j = blockIdx.x;           // decode request index
-  const int kvh = blockIdx.y;         // kv head (local)
-  const int z = blockIdx.z;           // split
-  const int bs = a.block_size;
-  const int ctx = a.ctx[j];
-  const int nblk = (ctx + bs - 1) / bs;
-  const int b0 = z * a.blocks_per_split;
-  const int b1 = min(nblk, b0 + a.blocks_per_split);
-  const int nq = a.n_q_local;
-  const int q_head0 = kvh * G;
-  const size_t block_bytes = static_cast<size_t>(bs) * HD * 2;
-
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int S = a.stages;
-  uint8_t* ring = smem;                                                // S x (K block, V block)
-  float* s_p = reinterpret_cast<float*>(smem + S * 2 * block_bytes);   // [G][bs]
-  float* s_stat = s_p + G * bs;                                        // [G][2] m, scale | [G] sum
-  uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(s_stat + 4 * G) + 7) & ~uintptr_t(7));  // full[S]
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int grp = tid / kLanesPerKey, gl = tid % kLanesPerKey;
-
-  float* part_o = a.part_o;   // [d][nq][splits][HD]
-  float* part_lse = a.part_lse;  // [d][nq][splits]
-
-  if (b0 >= b1) {
-    if (a.splits > 1 && tid < G) {
-      part_lse[(static_cast<size_t>(j) * nq + q_head0 + tid) * a.splits + z] = -INFINITY;
-    }
-    return;
-  }
-
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-
-  const int* table = a.block_tables + static_cast<size_t>(j) * a.max_blocks;
-  const uint8_t* kbase = static_cast<const uint8_t*>(a.kcache);
-  const uint8_t* vbase = static_cast<const uint8_t*>(a.vcache);
-  const int n_local = b1 - b0;
-  uint64_t pol = 0;
-  if (tid == 0) {
-    pol = policy_evict_first();
-    for (int i = 0; i < min(S, n_local); ++i) {
-      const size_t blk = static_cast<size_t>(table[b0 + i]) * a.n_kv_local + kvh;
-      mbar_arrive_expect_tx(&bars[i], 2 * block_bytes);
-      bulk_load_1d(ring + (2 * i) * block_bytes, kbase + blk * block_bytes, block_bytes, &bars[i], pol);
-      bulk_load_1d(ring + (2 * i + 1) * block_bytes, vbase + blk * block_bytes, block_bytes, &bars[i], pol);
-    }
-  }
-
-  // q for all G heads, this lane's 8 dims, pre-scaled by softmax scale * log2(e)
-  const float qscale = a.scale * kLog2e;
-  float q[G][8];
-  {
-    const __nv_bfloat16* qrow = a.q + static_cast<size_t>(a.q_row0 + j) * a.q_ld;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(qrow + (q_head0 + g) * HD + gl * 8);
-      const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = unpack_bf16x2(w[i]);
-        q[g][2 * i] = f.x * qscale;
-        q[g][2 * i + 1] = f.y * qscale;
-      }
-    }
-  }
-
-  // PV ownership: thread owns dims (2*dp, 2*dp+1) for keys with key % 2 == kh
-  constexpr int kDimPairs = HD / 2;
-  const int dp = tid % kDimPairs;
-  const int kh = tid / kDimPairs;              // 0 or 1 (HD=128); 0..3 (HD=64)
-  constexpr int kKeyStride = kThreads / kDimPairs;
-  float acc[G][2];
-  float m_run[G], l_run[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    acc[g][0] = acc[g][1] = 0.f;
-    m_run[g] = -INFINITY;
-    l_run[g] = 0.f;
-  }
-
-  for (int i = 0; i < n_local; ++i) {
-    const int s = i % S;
-    const uint32_t ph = (i / S) & 1;
-    mbar_wait(&bars[s], ph);
-    const __nv_bfloat16* Kb = reinterpret_cast<const __nv_bfloat16*>(ring + (2 * s) * block_bytes);
-    const __nv_bfloat16* Vb = reinterpret_cast<const __nv_bfloat16*>(ring + (2 * s + 1) * block_bytes);
-    const int key0 = (b0 + i) * bs;
-    const int nkeys = min(bs, ctx - key0);
-
-    // scores (log2 domain)
-    for (int k = grp; k < bs; k += kKeyGroups) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(Kb + k * HD + gl * 8);
-      const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-      float kf[8];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const float2 f = unpack_bf16x2(w[t]);
-        kf[2 * t] = f.x;
-        kf[2 * t + 1] = f.y;
-      }
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        float d = 0.f;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) d = fmaf(q[g][t], kf[t], d);
-#pragma unroll
-        for (int off = kLanesPerKey / 2; off >= 1; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
-        if (gl == 0) s_p[g * bs + k] = (k < nkeys) ? d : -INFINITY;
-      }
-    }
-    __syncthreads();
-    // softmax statistics: warp w handles heads w, w+4, ...
-    for (int g = warp; g < G; g += 4) {
-      float mx = -INFINITY;
-      for (int k = lane; k < bs; k += 32) mx = fmaxf(mx, s_p[g * bs + k]);
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      const float m_old = (i == 0) ? -INFINITY : s_stat[2 * g];
-      const float m_new = (i == 0) ? mx : fmaxf(m_old, mx);
-      float sum = 0.f;
-      for (int k = lane; k < bs; k += 32) {
-        const float pv = exp2f(s_p[g * bs + k] - m_new);
-        s_p[g * bs + k] = pv;
-        sum += pv;
-      }
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-      if (lane == 0) {
-        s_stat[2 * g] = m_new;
-        s_stat[2 * g + 1] = (i == 0) ? 0.f : exp2f(m_old - m_new);
-        s_stat[2 * G + g] = sum;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float sc = s_stat[2 * g + 1];
-      const float bsum = s_stat[2 * G + g];
-      acc[g][0] *= sc;
-      acc[g][1] *= sc;
-      l_run[g] = l_run[g] * sc + bsum;
-      m_run[g] = s_stat[2 * g];
-    }
-    for (int k = kh; k < nkeys; k += kKeyStride) {
-      const float2 v = unpack_bf16x2(*reinterpret_cast<const uint32_t*>(Vb + k * HD + 2 * dp));
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float pv = s_p[g * bs + k];
-        acc[g][0] = fmaf(pv, v.x, acc[g][0]);
-        acc[g][1] = fmaf(pv, v.y, acc[g][1]);
-      }
-    }
-    __syncthreads();  // stage s and s_p free
-    if (tid == 0 && i + S < n_local) {
-      const size_t blk = static_cast<size_t>(table[b0 + i + S]) * a.n_kv_local + kvh;
-      mbar_arrive_expect_tx(&bars[s], 2 * block_bytes);
-      bulk_load_1d(ring + (2 * s) * block_bytes, kbase + blk * block_bytes, block_bytes, &bars[s], pol);
-      bulk_load_1d(ring + (2 * s + 1) * block_bytes, vbase + blk * block_bytes, block_bytes, &bars[s], pol);
-    }
-  }
-
-  // reduce the kKeyStride key-interleaved partial accumulators through shared memory
-  float* red = reinterpret_cast<float*>(ring);  // ring is free now: [kKeyStride][G][HD]
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    red[(kh * G + g) * HD + 2 * dp] = acc[g][0];
-    red[(kh * G + g) * HD + 2 * dp + 1] = acc[g][1];
-  }
-  __syncthreads();
-  for (int idx = tid; idx < G * HD; idx += kThreads) {
-    const int g = idx / HD, dd = idx % HD;
-    float o = 0.f;
-#pragma unroll
-    for (int t = 0; t < kKeyStride; ++t) o += red[(t * G + g) * HD + dd];
-    const float l = l_run[g];  // identical in every thread
-    const int qh = q_head0 + g;
-    if (a.splits == 1) {
-      a.out[static_cast<size_t>(a.q_row0 + j) * a.out_ld + qh * HD + dd] = __float2bfloat16_rn(o / l);
-    } else {
-      part_o[((static_cast<size_t>(j) * nq + qh) * a.splits + z) * HD + dd] = o / l;
-      if (dd == 0) part_lse[(static_cast<size_t>(j) * nq + qh) * a.splits + z] = m_run[g] + log2f(l);
-    }
-  }
-}
-
-__global__ void decode_combine_kernel(DecodeAttnArgs a, int HD) {
-  const int j = blockIdx.x, qh = blockIdx.y;
-  const int nq = a.n_q_local;
-  const float* lse = a.part_lse + (static_cast<size_t>(j) * nq + qh) * a.splits;
-  float mx = -INFINITY;
-  for (int z = 0; z < a.splits; ++z) mx = fmaxf(mx, lse[z]);
-  float den = 0.f;
-  for (int z = 0; z < a.splits; ++z) den += (lse[z] == -INFINITY) ? 0.f : exp2f(lse[z] - mx);
-  for (int dd = threadIdx.x; dd < HD; dd += blockDim.x) {
-    float o = 0.f;
-    for (int z = 0; z < a.splits; ++z) {
-      if (lse[z] == -INFINITY) continue;
-      o += exp2f(lse[z] - mx) * a.part_o[((static_cast<size_t>(j) * nq + qh) * a.splits + z) * HD + dd];
-    }
-    a.out[static_cast<size_t>(a.q_row0 + j) * a.out_ld + qh * HD + dd] = __float2bfloat16_rn(o / den);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Chunked-prefill attention (mma.sync m16n8k16 bf16, fp32 accumulate)
+// mma.sync / ldmatrix / cp.async helpers
 // ---------------------------------------------------------------------------
 SARATHI_DEVICE void ldmatrix_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -272,6 +54,254 @@ SARATHI_DEVICE void cp_async16(uint32_t dst, const void* src, bool valid) {
 SARATHI_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 SARATHI_DEVICE void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+
+// ---------------------------------------------------------------------------
+// Decode attention (paged KV, split-K over the sequence)
+//   grid (d, n_kv_local, splits); 160 threads: warps 0-3 compute, warp 4 = TMA producer.
+//   Each KV block (bs keys x hd) of K and of V is one 2D TMA load (128B swizzle) into an S-stage
+//   ring.  Compute warp w owns the 16-key groups w, w+4, ... of every block and runs, per group,
+//   S = Q K^T (mma.sync m16n8k16; the G query heads of the GQA group are the MMA rows, padded to
+//   16), its own online softmax (fp32, exp2 domain) and O += P V.  The four warps' (m, l, O) are
+//   merged once at the end; splits > 1 write (o, lse) partials for decode_combine.
+// ---------------------------------------------------------------------------
+template <int HD>
+__global__ void __launch_bounds__(160)
+    decode_attn_mma(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
+                    DecodeAttnArgs a) {
+  constexpr int NBOX = HD / 64;  // 128-byte TMA boxes per row
+  const int j = blockIdx.x, kvh = blockIdx.y, z = blockIdx.z;
+  const int G = a.n_q_local / a.n_kv_local;
+  const int bs = a.block_size;
+  const int ctx = a.ctx[j];
+  const int nblk = (ctx + bs - 1) / bs;
+  const int b0 = z * a.blocks_per_split;
+  const int b1 = min(nblk, b0 + a.blocks_per_split);
+  const int nq = a.n_q_local;
+  const int q_head0 = kvh * G;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+
+  if (b0 >= b1) {
+    if (a.splits > 1 && tid < G)
+      a.part_lse[(static_cast<size_t>(j) * nq + q_head0 + tid) * a.splits + z] = -INFINITY;
+    return;
+  }
+  const int S = a.stages;
+  const uint32_t half_bytes = static_cast<uint32_t>(bs) * 128;       // one 64-col box of a block
+  const uint32_t blk_bytes = half_bytes * NBOX;                       // K (or V) block
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(S) * 2 * blk_bytes);
+  uint64_t* empty = full + S;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);  // one arrive per compute warp
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int n_local = b1 - b0;
+  const int* table = a.block_tables + static_cast<size_t>(j) * a.max_blocks;
+
+  if (warp == 4) {
+    // ---------------- producer (warp-uniform; elected lane issues) ----------------
+    if (lane == 0) {
+      tma_prefetch_desc(&mapK);
+      tma_prefetch_desc(&mapV);
+      const uint64_t pol = policy_evict_first();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < n_local; ++i) {
+        mbar_wait(&empty[s], ph ^ 1);
+        const int row0 = (table[b0 + i] * a.n_kv_local + kvh) * bs;
+        uint8_t* kd = smem + static_cast<size_t>(s) * 2 * blk_bytes;
+        uint8_t* vd = kd + blk_bytes;
+        mbar_arrive_expect_tx(&full[s], 2 * blk_bytes);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx) {
+          tma_load_2d(kd + bx * half_bytes, &mapK, &full[s], bx * 64, row0, pol);
+          tma_load_2d(vd + bx * half_bytes, &mapV, &full[s], bx * 64, row0, pol);
+        }
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- compute warps ----------------
+  const float sl2 = a.scale * kLog2e;
+  // Q fragment (A operand, 16 x HD): row = head within the group (rows >= G are zero)
+  uint32_t qf[HD / 16][4];
+  {
+    const __nv_bfloat16* qrow = a.q + static_cast<size_t>(a.q_row0 + j) * a.q_ld + static_cast<size_t>(q_head0) * HD;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      const int c0 = kk * 16 + 2 * tig;
+      qf[kk][0] = gid < G ? *reinterpret_cast<const uint32_t*>(qrow + static_cast<size_t>(gid) * HD + c0) : 0u;
+      qf[kk][1] = gid + 8 < G ? *reinterpret_cast<const uint32_t*>(qrow + static_cast<size_t>(gid + 8) * HD + c0) : 0u;
+      qf[kk][2] = gid < G ? *reinterpret_cast<const uint32_t*>(qrow + static_cast<size_t>(gid) * HD + c0 + 8) : 0u;
+      qf[kk][3] = gid + 8 < G ? *reinterpret_cast<const uint32_t*>(qrow + static_cast<size_t>(gid + 8) * HD + c0 + 8) : 0u;
+    }
+  }
+  float o[HD / 8][4];
+#pragma unroll
+  for (int n = 0; n < HD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  const int ngroups = bs / 16;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int i = 0; i < n_local; ++i) {
+    mbar_wait(&full[s], ph);
+    const uint32_t kb = smem_u32(smem + static_cast<size_t>(s) * 2 * blk_bytes);
+    const uint32_t vb = kb + blk_bytes;
+    const int key_base = (b0 + i) * bs;
+    for (int grp = warp; grp < ngroups; grp += 4) {
+      const int k0 = grp * 16;  // key row within the block
+      float sacc[2][4];
+#pragma unroll
+      for (int n = 0; n < 2; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const int row = k0 + (lane & 7) + 8 * (lane >> 4);
+        const int ch = kk * 2 + ((lane >> 3) & 1);  // 16-B chunk in the row
+        const uint32_t addr = kb + (ch >> 3) * half_bytes + row * 128 + (((ch & 7) ^ (row & 7)) << 4);
+        uint32_t b0r, b1r, b2r, b3r;
+        ldmatrix_x4(addr, b0r, b1r, b2r, b3r);
+        mma_bf16_16816(sacc[0], qf[kk], b0r, b1r);
+        mma_bf16_16816(sacc[1], qf[kk], b2r, b3r);
+      }
+      // mask keys >= ctx, scale to log2 domain, online softmax per row
+      float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int key = key_base + k0 + n * 8 + 2 * tig + (e & 1);
+          const float v = key < ctx ? sacc[n][e] * sl2 : -INFINITY;
+          sacc[n][e] = v;
+          mx[e >> 1] = fmaxf(mx[e >> 1], v);
+        }
+      float sc[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+        const float mnew = fmaxf(mrow[r], mx[r]);
+        sc[r] = (mnew == -INFINITY) ? 1.f : exp2f(mrow[r] - mnew);
+        mrow[r] = mnew;
+      }
+      float rs[2] = {0.f, 0.f};
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float m = mrow[e >> 1];
+          const float pv = (m == -INFINITY) ? 0.f : exp2f(sacc[n][e] - m);
+          sacc[n][e] = pv;
+          rs[e >> 1] += pv;
+        }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], 1);
+        rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], 2);
+        lrow[r] = lrow[r] * sc[r] + rs[r];
+      }
+#pragma unroll
+      for (int n = 0; n < HD / 8; ++n) {
+        o[n][0] *= sc[0];
+        o[n][1] *= sc[0];
+        o[n][2] *= sc[1];
+        o[n][3] *= sc[1];
+      }
+      uint32_t pa[4];
+      pa[0] = pack_bf16x2(sacc[0][0], sacc[0][1]);
+      pa[1] = pack_bf16x2(sacc[0][2], sacc[0][3]);
+      pa[2] = pack_bf16x2(sacc[1][0], sacc[1][1]);
+      pa[3] = pack_bf16x2(sacc[1][2], sacc[1][3]);
+#pragma unroll
+      for (int n2 = 0; n2 < HD / 16; ++n2) {
+        const int row = k0 + (lane & 7) + 8 * ((lane >> 3) & 1);
+        const int ch = n2 * 2 + (lane >> 4);
+        const uint32_t addr = vb + (ch >> 3) * half_bytes + row * 128 + (((ch & 7) ^ (row & 7)) << 4);
+        uint32_t b0r, b1r, b2r, b3r;
+        ldmatrix_x4_trans(addr, b0r, b1r, b2r, b3r);
+        mma_bf16_16816(o[2 * n2], pa, b0r, b1r);
+        mma_bf16_16816(o[2 * n2 + 1], pa, b2r, b3r);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == S) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+
+  // ---------------- merge the 4 warps' partial softmax states ----------------
+  named_bar_sync(1, 128);  // all compute warps done with the ring
+  float* sm_m = reinterpret_cast<float*>(smem);  // [4][16]
+  float* sm_l = sm_m + 64;                       // [4][16]
+  float* sm_o = sm_l + 64;                       // [4][16][HD]
+  if (tig == 0) {
+    sm_m[warp * 16 + gid] = mrow[0];
+    sm_m[warp * 16 + gid + 8] = mrow[1];
+    sm_l[warp * 16 + gid] = lrow[0];
+    sm_l[warp * 16 + gid + 8] = lrow[1];
+  }
+#pragma unroll
+  for (int n = 0; n < HD / 8; ++n) {
+    const int col = n * 8 + 2 * tig;
+    sm_o[(warp * 16 + gid) * HD + col] = o[n][0];
+    sm_o[(warp * 16 + gid) * HD + col + 1] = o[n][1];
+    sm_o[(warp * 16 + gid + 8) * HD + col] = o[n][2];
+    sm_o[(warp * 16 + gid + 8) * HD + col + 1] = o[n][3];
+  }
+  named_bar_sync(1, 128);
+  for (int idx = tid; idx < G * HD; idx += 128) {
+    const int g = idx / HD, dd = idx % HD;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w * 16 + g]);
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float mw = sm_m[w * 16 + g];
+      const float f = mw == -INFINITY ? 0.f : exp2f(mw - M);
+      L += sm_l[w * 16 + g] * f;
+      O += sm_o[(w * 16 + g) * HD + dd] * f;
+    }
+    const int qh = q_head0 + g;
+    if (a.splits == 1) {
+      a.out[static_cast<size_t>(a.q_row0 + j) * a.out_ld + qh * HD + dd] = __float2bfloat16_rn(O / L);
+    } else {
+      a.part_o[((static_cast<size_t>(j) * nq + qh) * a.splits + z) * HD + dd] = O / L;
+      if (dd == 0) a.part_lse[(static_cast<size_t>(j) * nq + qh) * a.splits + z] = M + log2f(L);
+    }
+  }
+}
+
+__global__ void decode_combine_kernel(DecodeAttnArgs a, int HD) {
+  const int j = blockIdx.x, qh = blockIdx.y;
+  const int nq = a.n_q_local;
+  const float* lse = a.part_lse + (static_cast<size_t>(j) * nq + qh) * a.splits;
+  float mx = -INFINITY;
+  for (int z = 0; z < a.splits; ++z) mx = fmaxf(mx, lse[z]);
+  float den = 0.f;
+  for (int z = 0; z < a.splits; ++z) den += (lse[z] == -INFINITY) ? 0.f : exp2f(lse[z] - mx);
+  for (int dd = threadIdx.x; dd < HD; dd += blockDim.x) {
+    float o = 0.f;
+    for (int z = 0; z < a.splits; ++z) {
+      if (lse[z] == -INFINITY) continue;
+      o += exp2f(lse[z] - mx) * a.part_o[((static_cast<size_t>(j) * nq + qh) * a.splits + z) * HD + dd];
+    }
+    a.out[static_cast<size_t>(a.q_row0 + j) * a.out_ld + qh * HD + dd] = __float2bfloat16_rn(o / den);
+  }
+}
 
 // smem tile [rows][HD] bf16 with 16-byte chunks XOR-swizzled by (row % 8)
 template <int HD>
@@ -452,46 +482,41 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-template <int HD, int G>
-cudaError_t launch_decode_t(const DecodeAttnArgs& a, cudaStream_t st) {
-  const size_t block_bytes = static_cast<size_t>(a.block_size) * HD * 2;
-  const size_t smem = a.stages * 2 * block_bytes + (G * a.block_size + 4 * G + 8) * sizeof(float) + 8 * a.stages + 16;
+template <int HD>
+cudaError_t launch_decode_hd(const DecodeAttnArgs& a, const CUtensorMap& mk, const CUtensorMap& mv, cudaStream_t st) {
+  const size_t smem = decode_smem_bytes(HD, a.block_size, a.stages, 1);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(decode_attn_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(decode_attn_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
   dim3 grid(a.d, a.n_kv_local, a.splits);
-  decode_attn_kernel<HD, G><<<grid, 128, smem, st>>>(a);
+  decode_attn_mma<HD><<<grid, 160, smem, st>>>(mk, mv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || a.splits == 1) return e;
   decode_combine_kernel<<<dim3(a.d, a.n_q_local), 128, 0, st>>>(a, HD);
   return cudaGetLastError();
 }
 
-template <int HD>
-cudaError_t launch_decode_hd(const DecodeAttnArgs& a, cudaStream_t st) {
-  const int G = a.n_q_local / a.n_kv_local;
-  switch (G) {
-    case 1: return launch_decode_t<HD, 1>(a, st);
-    case 2: return launch_decode_t<HD, 2>(a, st);
-    case 4: return launch_decode_t<HD, 4>(a, st);
-    case 8: return launch_decode_t<HD, 8>(a, st);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
 }  // namespace
 
-size_t decode_smem_bytes(int head_dim, int block_size, int stages, int G) {
-  return stages * 2 * static_cast<size_t>(block_size) * head_dim * 2 + (G * block_size + 4 * G + 8) * sizeof(float) +
-         8 * stages + 16;
+size_t decode_smem_bytes(int head_dim, int block_size, int stages, int /*G*/) {
+  const size_t ring = static_cast<size_t>(stages) * 2 * block_size * head_dim * 2;
+  const size_t merge = (128 + 64 * static_cast<size_t>(head_dim)) * 4;
+  return std::max(ring, merge) + 16 * stages + 1024 + 64;
 }
 
-cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st) {
+bool make_tmap_kv(CUtensorMap* map, const void* pool, long long rows, int head_dim, int block_size) {
+  // 2D view [rows = num_blocks * n_kv * block_size][head_dim], 64-column boxes of block_size rows, SW128
+  return make_tmap_bf16(map, pool, static_cast<uint64_t>(rows), head_dim, head_dim, block_size);
+}
+
+cudaError_t launch_decode_attention(const DecodeAttnArgs& a, const CUtensorMap& mk, const CUtensorMap& mv,
+                                    cudaStream_t st) {
   if (a.d == 0) return cudaSuccess;
-  if (a.head_dim == 128) return launch_decode_hd<128>(a, st);
-  if (a.head_dim == 64) return launch_decode_hd<64>(a, st);
+  if (a.n_q_local / a.n_kv_local > 16) return cudaErrorInvalidValue;
+  if (a.head_dim == 128) return launch_decode_hd<128>(a, mk, mv, st);
+  if (a.head_dim == 64) return launch_decode_hd<64>(a, mk, mv, st);
   return cudaErrorInvalidValue;
 }
 

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda.h>
 
 namespace sarathi {
 
@@ -43,7 +44,10 @@ struct PrefillAttnArgs {
 };
 
 size_t decode_smem_bytes(int head_dim, int block_size, int stages, int G);
-cudaError_t launch_decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
+// TMA map over one layer's K or V pool viewed as [num_blocks * n_kv_local * block_size][head_dim].
+bool make_tmap_kv(CUtensorMap* map, const void* pool, long long rows, int head_dim, int block_size);
+cudaError_t launch_decode_attention(const DecodeAttnArgs& a, const CUtensorMap& kmap, const CUtensorMap& vmap,
+                                    cudaStream_t st);
 cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t st);
 
 // h[t][:] = float(E[tok[t]][:])

@@ -322,9 +322,15 @@ Status Model::alloc_kv(int64_t nb, int32_t bs) {
   const size_t per = static_cast<size_t>(nb) * nkv_l * bs * cfg.head_dim;
   kpool.resize(cfg.n_layers);
   vpool.resize(cfg.n_layers);
+  kmap.resize(cfg.n_layers);
+  vmap.resize(cfg.n_layers);
   for (int l = 0; l < cfg.n_layers; ++l) {
     SRET(dalloc(&kpool[l], per));
     SRET(dalloc(&vpool[l], per));
+    const long long rows = nb * static_cast<long long>(nkv_l) * bs;
+    if (!make_tmap_kv(&kmap[l], kpool[l], rows, cfg.head_dim, bs) ||
+        !make_tmap_kv(&vmap[l], vpool[l], rows, cfg.head_dim, bs))
+      return Status::err(SARATHI_ECUDA, "alloc_kv: tensor map encode failed");
   }
   num_blocks = nb;
   block_size = bs;
@@ -576,13 +582,16 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       splits = static_cast<int>(std::max<size_t>(1, std::min<size_t>(splits, part_cap / per_split)));
       da.blocks_per_split = (max_nblk + splits - 1) / splits;
       da.splits = (max_nblk + da.blocks_per_split - 1) / da.blocks_per_split;
-      da.stages = 3;
+      {
+        const size_t blk = static_cast<size_t>(block_size) * hd * 2;  // K (or V) block bytes
+        da.stages = static_cast<int>(std::max<size_t>(2, std::min<size_t>(4, (104 * 1024) / (2 * blk))));
+      }
       da.part_o = part_o;
       da.part_lse = part_lse;
       da.out = o;
       da.out_ld = q_dim_l;
       ob = op_begin();
-      SRET(check(launch_decode_attention(da, stream), "decode attention"));
+      SRET(check(launch_decode_attention(da, kmap[l], vmap[l], stream), "decode attention"));
       op_end(SARATHI_OP_DECODE_ATTN, ob);
       launches += da.splits > 1 ? 2 : 1;
     }

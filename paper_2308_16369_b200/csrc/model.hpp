@@ -64,6 +64,7 @@ struct Model {
   int block_size = 0;
   int max_blocks_per_req = 0;
   std::vector<__nv_bfloat16*> kpool, vpool;
+  std::vector<CUtensorMap> kmap, vmap;  // TMA maps of the pools (decode attention)
   BlockAllocator alloc;
   std::map<int64_t, int32_t> cached;
   // activations / workspaces (Tmax rows)

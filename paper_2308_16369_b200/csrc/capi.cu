@@ -199,14 +199,26 @@ int sarathi_debug_kv(const sarathi_model* m, int32_t layer, int64_t req_id, int3
   if (pos0 < 0 || n < 0 || pos0 + n > M.alloc.reserved(req_id)) return fail(SARATHI_EINVAL, "debug_kv: range");
   cudaStreamSynchronize(M.stream);
   const int hd = M.cfg.head_dim, bs = M.block_size;
+  // copy whole [n_kv_local][bs][hd] blocks, then gather the requested positions on the host
+  const size_t blk_elems = static_cast<size_t>(M.nkv_l) * bs * hd;
+  std::vector<uint16_t> kb(blk_elems), vb(blk_elems);
+  const auto& table = M.alloc.table(req_id);
+  int cur_blk = -1;
   for (int i = 0; i < n; ++i) {
-    const int64_t sl = M.alloc.slot(req_id, pos0 + i);
-    for (int hh = 0; hh < M.nkv_l; ++hh) {
-      const size_t row = (static_cast<size_t>(sl / bs) * M.nkv_l + hh) * bs + sl % bs;
-      const size_t dst = (static_cast<size_t>(i) * M.nkv_l + hh) * hd;
-      if (cudaMemcpy(host_k + dst, M.kpool[layer] + row * hd, hd * 2, cudaMemcpyDeviceToHost) != cudaSuccess ||
-          cudaMemcpy(host_v + dst, M.vpool[layer] + row * hd, hd * 2, cudaMemcpyDeviceToHost) != cudaSuccess)
+    const int pos = pos0 + i;
+    const int bi = pos / bs;
+    if (bi != cur_blk) {
+      const size_t off = static_cast<size_t>(table[bi]) * blk_elems;
+      if (cudaMemcpy(kb.data(), M.kpool[layer] + off, blk_elems * 2, cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(vb.data(), M.vpool[layer] + off, blk_elems * 2, cudaMemcpyDeviceToHost) != cudaSuccess)
         return fail(SARATHI_ECUDA, "debug_kv: copy failed");
+      cur_blk = bi;
+    }
+    for (int hh = 0; hh < M.nkv_l; ++hh) {
+      const size_t src = (static_cast<size_t>(hh) * bs + pos % bs) * hd;
+      const size_t dst = (static_cast<size_t>(i) * M.nkv_l + hh) * hd;
+      std::memcpy(host_k + dst, kb.data() + src, hd * 2);
+      std::memcpy(host_v + dst, vb.data() + src, hd * 2);
     }
   }
   return SARATHI_OK;

@@ -66,8 +66,28 @@ SARATHI_DEVICE int cta_of(long long u, const KParams& p) {
 }
 
 // Epilogue for one 16-token chunk of a 128-row tile.  Thread r (0..127) holds acc row r, tokens c0..c0+15.
+// RoPE table values (cos, sin) for row r and tokens c0..c0+15 (prefetched one chunk ahead).
+SARATHI_DEVICE void rope_load(const KParams& p, const EpiParams& ep, int r, int mt, int c0, int tvalid,
+                              const int* s_pos, float (&cs)[16], float (&sn)[16]) {
+  const int hd = ep.head_dim, half = hd >> 1;
+  const int m = mt * kBM + r;
+  const bool rope = m < p.M && (m / hd) < ep.n_q_local + ep.n_kv_local;
+  const int dd = (r % hd) % half;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    cs[j] = 1.f;
+    sn[j] = 0.f;
+    if (rope && c0 + j < tvalid) {
+      const size_t ti = static_cast<size_t>(s_pos[c0 + j]) * half + dd;
+      cs[j] = __ldg(ep.rope_cos + ti);
+      sn[j] = __ldg(ep.rope_sin + ti);
+    }
+  }
+}
+
 SARATHI_DEVICE void epilogue_chunk(const KParams& p, const EpiParams& ep, float (&v)[16], int r, int mt, int nt,
-                                   int c0, int tvalid, float* xbuf, const int* s_pos, const int* s_slot) {
+                                   int c0, int tvalid, float* xbuf, const int* s_pos, const int* s_slot,
+                                   const float (&cs)[16], const float (&sn)[16]) {
   const int m = mt * kBM + r;
   const long long t0 = static_cast<long long>(nt) * p.bn + c0;
   const int nv = min(16, tvalid - c0);  // valid tokens in this chunk (>= 1)
@@ -138,17 +158,6 @@ SARATHI_DEVICE void epilogue_chunk(const KParams& p, const EpiParams& ep, float 
       __nv_bfloat16* qout = static_cast<__nv_bfloat16*>(ep.out);
       __nv_bfloat16* cache = static_cast<__nv_bfloat16*>(rope ? ep.kcache : ep.vcache);
       const int kvh = isq ? 0 : (rope ? gh - ep.n_q_local : gh - ep.n_q_local - ep.n_kv_local);
-      float cs[16], sn[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {  // all table loads in flight before any store
-        cs[j] = 1.f;
-        sn[j] = 0.f;
-        if (rope && j < nv) {
-          const size_t ti = static_cast<size_t>(s_pos[c0 + j]) * half + dd;
-          cs[j] = __ldg(ep.rope_cos + ti);
-          sn[j] = __ldg(ep.rope_sin + ti);
-        }
-      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         if (j >= nv) continue;
@@ -347,16 +356,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ep.trace && blockIdx.x < 2 && et == 0 && seg < 64) ep.trace[blockIdx.x * 1024 + 512 + seg] = globaltimer_ns();
       const uint32_t trow = tmem + buf * 256 + ((quarter * 32u) << 16);
       const int nchunks = (tvalid + 15) / 16;
+      const bool rope = ep.mode == EPI_QKV_ROPE;
+      float cs[16], sn[16], csn[16], snn[16];  // current / next chunk RoPE values (registers)
       if (whole) {
+        if (rope) rope_load(p, ep, r, mt, 0, tvalid, s_pos, cs, sn);
         for (int ch = 0; ch < nchunks; ++ch) {
           uint32_t raw[16];
           tmem_ld_32x32b_x16(trow + ch * 16, raw);
           tmem_ld_wait();
           if (ch == nchunks - 1) release_tmem();
+          // prefetch the next chunk's RoPE table values; their latency overlaps this chunk
+          if (rope && ch + 1 < nchunks) rope_load(p, ep, r, mt, (ch + 1) * 16, tvalid, s_pos, csn, snn);
           float v[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
-          epilogue_chunk(p, ep, v, r, mt, nt, ch * 16, tvalid, xbuf, s_pos, s_slot);
+          epilogue_chunk(p, ep, v, r, mt, nt, ch * 16, tvalid, xbuf, s_pos, s_slot, cs, sn);
+          if (rope) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              cs[j] = csn[j];
+              sn[j] = snn[j];
+            }
+          }
         }
       } else {
         if (ep.mode == EPI_ADD_F32) {
@@ -405,7 +426,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (s_last) {
             __threadfence();
             const float* base = ep.ws + tile128 * p.max_slots * tile_elems;
+            if (rope) rope_load(p, ep, r, mt, 0, tvalid, s_pos, cs, sn);
             for (int ch = 0; ch < nchunks; ++ch) {
+              if (rope && ch + 1 < nchunks) rope_load(p, ep, r, mt, (ch + 1) * 16, tvalid, s_pos, csn, snn);
               float v[16];
 #pragma unroll
               for (int j = 0; j < 16; ++j) v[j] = 0.f;
@@ -423,7 +446,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                   for (int j = 0; j < 16; ++j) v[j] += t[q][j];
               }
-              epilogue_chunk(p, ep, v, r, mt, nt, ch * 16, tvalid, xbuf, s_pos, s_slot);
+              epilogue_chunk(p, ep, v, r, mt, nt, ch * 16, tvalid, xbuf, s_pos, s_slot, cs, sn);
+              if (rope) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                  cs[j] = csn[j];
+                  sn[j] = snn[j];
+                }
+              }
             }
           }
         }

@@ -1,0 +1,70 @@
+"""Parity at BASELINE.json's full size, in the launch configuration bench.py times: LLaMA-13B
+(40 layers, H=5120, 40 heads), one decode-maximal hybrid batch of the bench composition (chunk
+p=256 at prefix s=768 + d=64 decodes at context 1024, T=320), same setup code as bench.py.
+
+The fp64 oracle cannot replay 40 layers over 65 x 1024 tokens, so it checks sampled rows
+layer-locally (SURVEY §8(c) compare mode): for sampled layers it takes the GPU's own layer input
+h^{l-1} and the request's KV context read back from the paged cache and recomputes
+  * the row's own appended K and V (RoPE + append at its slot),
+  * the layer's update h^l - h^{l-1} (attention over [0, pos] + O-proj + FFN),
+and for the final residual the logits on a sampled vocabulary subset.  Max relative error
+<= 2e-2 (north star) on each."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import model as om
+from oracle.metrics import relative_error
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def _bf16(bits):
+    return synth.as_f64(bits)
+
+
+def test_llama13b_bench_composition_sampled_layer_local():
+    import torch
+    import bench
+    from paper_2308_16369_b200 import sarathi as S
+
+    cfg = synth.LLAMA_13B
+    p, s, d, ctx = 256, 768, 64, 1024
+    torch.cuda.set_device(0)
+    m, prefill, decodes = bench.setup_model(S, synth, cfg, p, s, d, ctx, 0, 1, 0, None, 0)
+    T = p + d
+    logits = np.zeros((T, cfg.vocab), dtype=np.float32)
+    m.run_hybrid_batch(prefill, decodes, flags=S.RETURN_ALL_ROWS | S.DUMP_LAYERS, logits_host=logits)
+    rows = [0, 131, 255, 256, 300, 319]
+    req = [0 if r < p else r - p + 1 for r in rows]
+    pos = np.array([s + r if r < p else ctx - 1 for r in rows])
+    errs = {}
+    for layer in (0, cfg.n_layers - 1):
+        h_in = m.hidden(layer - 1, T)[rows].astype(np.float64)
+        h_out = m.hidden(layer, T)[rows].astype(np.float64)
+        lw = om.layer_weights(cfg, 0, layer)
+        kctx, vctx = [], []
+        for rq, ps in zip(req, pos):
+            kb, vb = m.kv(layer, rq, 0, int(ps) + 1, cfg.n_kv_heads)
+            kctx.append(_bf16(kb))
+            vctx.append(_bf16(vb))
+        _, k_o, v_o = om.qkv_rows(cfg, lw, h_in, pos)
+        k_gpu = np.stack([k[-1] for k in kctx])
+        v_gpu = np.stack([v[-1] for v in vctx])
+        errs[f"k_append_l{layer}"] = relative_error(k_gpu, k_o)
+        errs[f"v_append_l{layer}"] = relative_error(v_gpu, v_o)
+        ref = om.layer_rows_from_input(cfg, lw, h_in, pos, kctx, vctx)
+        errs[f"delta_l{layer}"] = relative_error(h_out - h_in, ref - h_in)
+        errs[f"h_l{layer}"] = relative_error(h_out, ref)
+        del lw
+    h_fin = m.hidden(cfg.n_layers - 1, T)[rows].astype(np.float64)
+    vidx = np.arange(0, cfg.vocab, 16)
+    wl = _bf16(synth.lm_head_rows_bits(cfg, 0, vidx))
+    gf = _bf16(synth.final_gain_bits(cfg, 0))
+    ref_logits = om.logits_rows(cfg, gf, wl, h_fin)
+    errs["logits_sampled"] = relative_error(logits[rows][:, vidx], ref_logits)
+    m.close()
+    print("full-size layer-local errors:", {k: f"{v:.2e}" for k, v in errs.items()})
+    for k, v in errs.items():
+        assert v <= TOL, (k, v)

@@ -71,8 +71,8 @@ SARATHI_DEVICE void rope_load(const KParams& p, const EpiParams& ep, int r, int 
                               const int* s_pos, float (&cs)[16], float (&sn)[16]) {
   const int hd = ep.head_dim, half = hd >> 1;
   const int m = mt * kBM + r;
-  const bool rope = m < p.M && (m / hd) < ep.n_q_local + ep.n_kv_local;
-  const int dd = (r % hd) % half;
+  const bool rope = m < p.M && (m >> (hd == 128 ? 7 : 6)) < ep.n_q_local + ep.n_kv_local;
+  const int dd = r & (half - 1);
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     cs[j] = 1.f;
@@ -143,21 +143,22 @@ SARATHI_DEVICE void epilogue_chunk(const KParams& p, const EpiParams& ep, float 
     case EPI_QKV_ROPE: {
       // rows are head-aligned (128 % head_dim == 0): rotate-half partner of row r is r ^ half.
       const int hd = ep.head_dim, half = hd >> 1;
+      const int hd_shift = hd == 128 ? 7 : 6;
       named_bar_sync(2, 128);
 #pragma unroll
       for (int j = 0; j < 16; ++j) xbuf[r * kXPitch + j] = v[j];
       named_bar_sync(2, 128);
       if (m >= p.M) break;
-      const int d = r % hd;   // dim within head
-      const int gh = m / hd;  // head index in [q heads | k heads | v heads]
+      const int d = r & (hd - 1);     // dim within head
+      const int gh = m >> hd_shift;   // head index in [q heads | k heads | v heads]
       const bool rope = gh < ep.n_q_local + ep.n_kv_local;
       const bool isq = gh < ep.n_q_local;
       const int partner = r ^ half;
       const bool lowhalf = d < half;
-      const int dd = lowhalf ? d : d - half;
       __nv_bfloat16* qout = static_cast<__nv_bfloat16*>(ep.out);
       __nv_bfloat16* cache = static_cast<__nv_bfloat16*>(rope ? ep.kcache : ep.vcache);
       const int kvh = isq ? 0 : (rope ? gh - ep.n_q_local : gh - ep.n_q_local - ep.n_kv_local);
+      const int head_row = kvh * ep.block_size;  // + s_slot[t] = cache row of this token and kv head
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         if (j >= nv) continue;
@@ -165,15 +166,8 @@ SARATHI_DEVICE void epilogue_chunk(const KParams& p, const EpiParams& ep, float 
         const float xp = xbuf[partner * kXPitch + j];
         // x1 = low-half value, x2 = high-half value: y1 = x1 c - x2 s, y2 = x2 c + x1 s
         const float y = lowhalf ? (v[j] * cs[j] - xp * sn[j]) : (v[j] * cs[j] + xp * sn[j]);
-        __nv_bfloat16* dst;
-        if (isq) {
-          dst = qout + (static_cast<long long>(nt) * p.bn + t) * ep.ldo + m;
-        } else {
-          const int sl = s_slot[t];
-          const size_t row =
-              (static_cast<size_t>(sl / ep.block_size) * ep.n_kv_local + kvh) * ep.block_size + sl % ep.block_size;
-          dst = cache + row * hd + d;
-        }
+        __nv_bfloat16* dst = isq ? qout + (static_cast<long long>(nt) * p.bn + t) * ep.ldo + m
+                                 : cache + (static_cast<size_t>(s_slot[t] + head_row) << hd_shift) + d;
         *dst = __float2bfloat16_rn(y);
       }
       break;
@@ -346,7 +340,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(2, 128);
         for (int t = et; t < tvalid; t += 128) {
           s_pos[t] = __ldg(ep.pos + nt * p.bn + t);
-          s_slot[t] = __ldg(ep.slot + nt * p.bn + t);
+          const int sl = __ldg(ep.slot + nt * p.bn + t);
+          // paged-cache row of (slot, kv head 0): [block][n_kv][bs] -> (sl/bs)*n_kv*bs + sl%bs
+          s_slot[t] = (sl / ep.block_size) * ep.n_kv_local * ep.block_size + sl % ep.block_size;
         }
         named_bar_sync(2, 128);
       }

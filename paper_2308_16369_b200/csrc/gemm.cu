@@ -406,6 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t raw[16];
             tmem_ld_32x32b_x16(trow + ch * 16, raw);
             tmem_ld_wait();
+            // partial layout [token][row]: a warp store covers 128 contiguous bytes
 #pragma unroll
             for (int j = 0; j < 16; ++j) __stcg(wsp + static_cast<size_t>(ch * 16 + j) * kBM + r, __uint_as_float(raw[j]));
           }
@@ -423,25 +424,39 @@ __global__ void __launch_bounds__(kThreads, 1)
             __threadfence();
             const float* base = ep.ws + tile128 * p.max_slots * tile_elems;
             if (rope) rope_load(p, ep, r, mt, 0, tvalid, s_pos, cs, sn);
+            // vectorised, software-pipelined reduction: chunk ch+1's partials are in flight while
+            // chunk ch is summed (slot order kept -> deterministic)
+            constexpr int kMaxSlots = 2;  // prefetched slots; slots >= 2 (rare) are added unpipelined
+            // software-pipelined reduction: chunk ch+1's partials are in flight while chunk ch is summed
+            // (slot order kept -> deterministic); [token][row] layout keeps every load 128 B per warp
+            const float* colbase = base + r;
+            float cur[kMaxSlots][16], nxt[kMaxSlots][16];
+#pragma unroll
+            for (int q = 0; q < kMaxSlots; ++q)
+#pragma unroll
+              for (int j = 0; j < 16; ++j) cur[q][j] = q < nslot ? __ldcg(colbase + q * tile_elems + j * kBM) : 0.f;
             for (int ch = 0; ch < nchunks; ++ch) {
               if (rope && ch + 1 < nchunks) rope_load(p, ep, r, mt, (ch + 1) * 16, tvalid, s_pos, csn, snn);
+              if (ch + 1 < nchunks) {
+#pragma unroll
+                for (int q = 0; q < kMaxSlots; ++q)
+#pragma unroll
+                  for (int j = 0; j < 16; ++j)
+                    nxt[q][j] = q < nslot ? __ldcg(colbase + q * tile_elems + static_cast<size_t>((ch + 1) * 16 + j) * kBM)
+                                          : 0.f;
+              }
               float v[16];
 #pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = 0.f;
-              // all slots' loads of this chunk in flight before summing (slot order kept)
-              for (int s0 = 0; s0 < nslot; s0 += 4) {
-                float t[4][16];
+              for (int j = 0; j < 16; ++j) v[j] = cur[0][j] + cur[1][j];
+              for (int q = kMaxSlots; q < nslot; ++q) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const float* src = base + (s0 + q) * tile_elems + static_cast<size_t>(ch * 16) * kBM + r;
-#pragma unroll
-                  for (int j = 0; j < 16; ++j) t[q][j] = (s0 + q < nslot) ? __ldcg(src + j * kBM) : 0.f;
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-#pragma unroll
-                  for (int j = 0; j < 16; ++j) v[j] += t[q][j];
+                for (int j = 0; j < 16; ++j)
+                  v[j] += __ldcg(colbase + q * tile_elems + static_cast<size_t>(ch * 16 + j) * kBM);
               }
+#pragma unroll
+              for (int q = 0; q < kMaxSlots; ++q)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) cur[q][j] = nxt[q][j];
               epilogue_chunk(p, ep, v, r, mt, nt, ch * 16, tvalid, xbuf, s_pos, s_slot, cs, sn);
               if (rope) {
 #pragma unroll
@@ -538,6 +553,11 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
     return std::min(s, g);
   };
   int max_slots = slots_for(pairs);
+  // the reduction handles <= 4 contributors per tile: use fewer pairs if the split is finer
+  while (pairs > 1 && max_slots > 4) {
+    --pairs;
+    max_slots = slots_for(pairs);
+  }
   const size_t tile_elems = static_cast<size_t>(pl.bn) * kBM;
   const size_t tiles128 = static_cast<size_t>(pl.m_tiles) * pl.n_tiles;
   while (pairs > 1 && tiles128 * max_slots * tile_elems > ws_cap_floats) {

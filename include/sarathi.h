@@ -195,6 +195,14 @@ int sarathi_launch_count(const sarathi_model* m, int64_t* out);
 
 const char* sarathi_last_error(void);
 
+/* Host-only view of this library's Megatron tensor-parallel sharding (§2.3): for
+ * each row r of rank `rank`'s packed tensor (0 qkv, 1 o, 2 gate||up, 3 down, 16 embedding,
+ * 18 LM head) of `layer`, the generator tensor id tau[r], fp32 scale[r] and the flat index base[r]
+ * of element (r, 0) in the logical unsharded tensor (element (r, c) = base[r] + c).  rows/cols
+ * receive the shard shape; tau/scale/base may be NULL (shape query).  No CUDA. */
+int sarathi_shard_map(const sarathi_model_config* cfg, int32_t rank, int32_t world, int32_t layer, int32_t tensor,
+                      int32_t* tau, float* scale, int64_t* base, int32_t cap, int32_t* rows, int32_t* cols);
+
 /* ---- host-side scheduler (decode-maximal batching, §4.3) — no CUDA --------------------- */
 /* Policy (reading O-16): FCFS admission by (arrival, id) while fewer than B requests run and the
  * full (P+D)-token KV reservation fits in the sched's own block allocator (lowest-free-first,

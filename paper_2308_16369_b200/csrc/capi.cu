@@ -277,6 +277,30 @@ int sarathi_launch_count(const sarathi_model* m, int64_t* out) {
   return SARATHI_OK;
 }
 
+int sarathi_shard_map(const sarathi_model_config* cfg, int32_t rank, int32_t world, int32_t layer, int32_t tensor,
+                      int32_t* tau, float* scale, int64_t* base, int32_t cap, int32_t* rows, int32_t* cols) {
+  if (!cfg || !rows || !cols || world < 1 || rank < 0 || rank >= world)
+    return fail(SARATHI_EINVAL, "shard_map: bad argument");
+  std::vector<int> t;
+  std::vector<float> sc;
+  std::vector<long long> b;
+  sarathi::ShardDims d;
+  if (!sarathi::shard_map(cfg->n_layers, cfg->hidden, cfg->n_heads, cfg->n_kv_heads, cfg->head_dim, cfg->ffn_hidden,
+                          cfg->vocab, cfg->ffn_kind, rank, world, layer, tensor, &t, &sc, &b, &d))
+    return fail(SARATHI_EINVAL, "shard_map: bad tensor id");
+  *rows = d.rows;
+  *cols = d.cols;
+  if (tau || scale || base) {
+    if (cap < d.rows) return fail(SARATHI_EINVAL, "shard_map: cap too small");
+    for (int r = 0; r < d.rows; ++r) {
+      if (tau) tau[r] = t[r];
+      if (scale) scale[r] = sc[r];
+      if (base) base[r] = b[r];
+    }
+  }
+  return SARATHI_OK;
+}
+
 // ---- scheduler ----
 int sarathi_sched_create(int32_t B, int32_t C, int32_t policy, int32_t tile_adjust, int64_t num_blocks,
                          int32_t block_size, sarathi_sched** out) {

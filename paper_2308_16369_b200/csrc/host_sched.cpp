@@ -2,6 +2,7 @@
 #include "host_sched.hpp"
 
 #include <algorithm>
+#include <cmath>
 
 namespace sarathi {
 
@@ -140,6 +141,96 @@ std::vector<int64_t> Scheduler::complete() {
   have_plan_ = false;
   ++iteration_;
   return fin;
+}
+
+namespace {
+constexpr int kWQ = 0, kWK = 1, kWV = 2, kWO = 3, kWG = 4, kWU = 5, kWD = 6;
+constexpr int kEmbTau = 1 << 20, kWlmTau = (1 << 20) + 2;
+float weight_scale(double sigma) { return static_cast<float>(std::sqrt(3.0) * sigma / 16777216.0); }
+}  // namespace
+
+bool shard_map(int n_layers, int hidden, int n_heads, int n_kv_heads, int head_dim, int ffn_hidden, int vocab,
+               int ffn_kind, int rank, int world, int layer, int tensor, std::vector<int>* tau,
+               std::vector<float>* scale, std::vector<long long>* base, ShardDims* dims) {
+  const int H = hidden, hd = head_dim;
+  const int q_dim_l = n_heads / world * hd, kv_dim_l = n_kv_heads / world * hd;
+  const int h2_l = ffn_hidden / world, vocab_l = vocab / world;
+  const double s_in = 1.0 / std::sqrt(static_cast<double>(H));
+  const double depth = 1.0 / std::sqrt(2.0 * n_layers);
+  const double s_o = depth / std::sqrt(static_cast<double>(n_heads) * hd);
+  const double s_d = depth / std::sqrt(static_cast<double>(ffn_hidden));
+  int rows = 0, cols = 0;
+  switch (tensor) {
+    case 0: rows = q_dim_l + 2 * kv_dim_l; cols = H; break;
+    case 1: rows = H; cols = q_dim_l; break;
+    case 2: rows = ffn_kind == 0 ? 2 * h2_l : h2_l; cols = H; break;
+    case 3: rows = H; cols = h2_l; break;
+    case 16: rows = vocab; cols = H; break;
+    case 18: rows = vocab_l; cols = H; break;
+    default: return false;
+  }
+  tau->assign(rows, 0);
+  scale->assign(rows, 0.f);
+  base->assign(rows, 0);
+  for (int r = 0; r < rows; ++r) {
+    int kind = 0;
+    long long b = 0;
+    double sig = s_in;
+    switch (tensor) {
+      case 0: {  // [q_r ; k_r ; v_r]: the rank's heads of the logical Wq, Wk, Wv
+        long long lrow;
+        if (r < q_dim_l) {
+          kind = kWQ;
+          lrow = static_cast<long long>(rank) * q_dim_l + r;
+        } else if (r < q_dim_l + kv_dim_l) {
+          kind = kWK;
+          lrow = static_cast<long long>(rank) * kv_dim_l + (r - q_dim_l);
+        } else {
+          kind = kWV;
+          lrow = static_cast<long long>(rank) * kv_dim_l + (r - q_dim_l - kv_dim_l);
+        }
+        b = lrow * H;
+        break;
+      }
+      case 1:  // row-parallel: columns rank*q_dim_l .. of the logical [H][n_heads*hd]
+        kind = kWO;
+        sig = s_o;
+        b = static_cast<long long>(r) * n_heads * hd + static_cast<long long>(rank) * q_dim_l;
+        break;
+      case 2: {  // gate||up interleaved in 64-row blocks (SwiGLU) or W1 (GELU)
+        long long fl = r;
+        kind = kWG;
+        if (ffn_kind == 0) {
+          const int blk = r / 128, w2 = r % 128;
+          kind = w2 < 64 ? kWG : kWU;
+          fl = static_cast<long long>(blk) * 64 + (w2 % 64);
+        }
+        b = (static_cast<long long>(rank) * h2_l + fl) * H;
+        break;
+      }
+      case 3:  // row-parallel down
+        kind = kWD;
+        sig = s_d;
+        b = static_cast<long long>(r) * ffn_hidden + static_cast<long long>(rank) * h2_l;
+        break;
+      case 16:
+        (*tau)[r] = kEmbTau;
+        (*scale)[r] = weight_scale(1.0);
+        (*base)[r] = static_cast<long long>(r) * H;
+        continue;
+      case 18:
+        (*tau)[r] = kWlmTau;
+        (*scale)[r] = weight_scale(s_in);
+        (*base)[r] = (static_cast<long long>(rank) * vocab_l + r) * H;
+        continue;
+    }
+    (*tau)[r] = 16 * layer + kind;
+    (*scale)[r] = weight_scale(sig);
+    (*base)[r] = b;
+  }
+  dims->rows = rows;
+  dims->cols = cols;
+  return true;
 }
 
 }  // namespace sarathi

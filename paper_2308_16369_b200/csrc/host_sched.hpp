@@ -83,4 +83,17 @@ class Scheduler {
   PlanOut last_;
 };
 
+// Megatron tensor-parallel shard of one packed weight (§2.3): for every row r of the
+// rank-local packed tensor, the generator tensor id tau[r], fp32 scale[r] and the flat index base[r]
+// of element (r, 0) in the LOGICAL tensor (element (r, c) is base[r] + c).  tensor: 0 qkv
+// (column-parallel [q_r; k_r; v_r]), 1 o (row-parallel), 2 gate||up (column-parallel, 64-row
+// interleave) / W1, 3 down (row-parallel), 16 embedding (replicated), 18 LM head (vocab-parallel).
+// Host-only; returns false on a bad tensor id.
+struct ShardDims {
+  int rows = 0, cols = 0;
+};
+bool shard_map(int n_layers, int hidden, int n_heads, int n_kv_heads, int head_dim, int ffn_hidden, int vocab,
+               int ffn_kind, int rank, int world, int layer, int tensor, std::vector<int>* tau,
+               std::vector<float>* scale, std::vector<long long>* base, ShardDims* dims);
+
 }  // namespace sarathi

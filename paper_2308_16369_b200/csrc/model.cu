@@ -193,57 +193,14 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
     SRET(dalloc_padded(&w.down, H, h2_l));
     SRET(dalloc(&w.g1, H));
     SRET(dalloc(&w.g2, H));
-    // QKV: [q_r ; k_r ; v_r], column-parallel (rank's heads of the logical Wq, Wk, Wv)
-    fill(qkv_rows);
-    for (int r = 0; r < qkv_rows; ++r) {
-      long long lrow;
-      int kind;
-      if (r < q_dim_l) {
-        kind = kWQ;
-        lrow = static_cast<long long>(rank) * q_dim_l + r;
-      } else if (r < q_dim_l + kv_dim_l) {
-        kind = kWK;
-        lrow = static_cast<long long>(rank) * kv_dim_l + (r - q_dim_l);
-      } else {
-        kind = kWV;
-        lrow = static_cast<long long>(rank) * kv_dim_l + (r - q_dim_l - kv_dim_l);
-      }
-      tau[r] = 16 * l + kind;
-      scl[r] = weight_scale(s_in);
-      base[r] = lrow * H;
+    // rank-local shards of the logical weights (host_sched.cpp: shard_map), generated on device
+    ShardDims sd;
+    __nv_bfloat16* dsts[4] = {w.qkv, w.o, w.gu, w.down};
+    for (int t = 0; t < 4; ++t) {
+      shard_map(c.n_layers, H, c.n_heads, c.n_kv_heads, hd, c.ffn_hidden, c.vocab, c.ffn_kind, rank, world, l, t, &tau,
+                &scl, &base, &sd);
+      SRET(gen(dsts[t], sd.rows, sd.cols, 1));
     }
-    SRET(gen(w.qkv, qkv_rows, H, 1));
-    // O: row-parallel [H][q_dim_l] = columns rank*q_dim_l.. of the logical [H][nq*hd]
-    fill(H);
-    for (int r = 0; r < H; ++r) {
-      tau[r] = 16 * l + kWO;
-      scl[r] = weight_scale(s_o);
-      base[r] = static_cast<long long>(r) * c.n_heads * hd + static_cast<long long>(rank) * q_dim_l;
-    }
-    SRET(gen(w.o, H, q_dim_l, 1));
-    // gate||up interleaved in 64-row blocks (SwiGLU) or W1 (GELU)
-    fill(gu_rows);
-    for (int r = 0; r < gu_rows; ++r) {
-      int kind = kWG;
-      long long fl = r;
-      if (c.ffn_kind == SARATHI_FFN_SWIGLU) {
-        const int blk = r / 128, w2 = r % 128;
-        kind = w2 < 64 ? kWG : kWU;
-        fl = static_cast<long long>(blk) * 64 + (w2 % 64);
-      }
-      tau[r] = 16 * l + kind;
-      scl[r] = weight_scale(s_in);
-      base[r] = (static_cast<long long>(rank) * h2_l + fl) * H;
-    }
-    SRET(gen(w.gu, gu_rows, H, 1));
-    // down: row-parallel [H][h2_l]
-    fill(H);
-    for (int r = 0; r < H; ++r) {
-      tau[r] = 16 * l + kWD;
-      scl[r] = weight_scale(s_d);
-      base[r] = static_cast<long long>(r) * c.ffn_hidden + static_cast<long long>(rank) * h2_l;
-    }
-    SRET(gen(w.down, H, h2_l, 1));
     if (!make_tmap_weight(&w.m_qkv, w.qkv, qkv_rows, H) || !make_tmap_weight(&w.m_o, w.o, H, q_dim_l) ||
         !make_tmap_weight(&w.m_gu, w.gu, gu_rows, H) || !make_tmap_weight(&w.m_down, w.down, H, h2_l))
       return Status::err(SARATHI_ECUDA, "cuTensorMapEncodeTiled failed for a weight");
@@ -253,22 +210,20 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   }
   // embedding (replicated), final gain, LM head (vocab-parallel)
   SRET(dalloc(&emb, static_cast<size_t>(c.vocab) * H));
-  fill(c.vocab);
-  for (int r = 0; r < c.vocab; ++r) {
-    tau[r] = kEmbTau;
-    scl[r] = weight_scale(1.0);
-    base[r] = static_cast<long long>(r) * H;
+  {
+    ShardDims sd;
+    shard_map(c.n_layers, H, c.n_heads, c.n_kv_heads, hd, c.ffn_hidden, c.vocab, c.ffn_kind, rank, world, 0, 16, &tau,
+              &scl, &base, &sd);
   }
   SRET(gen(emb, c.vocab, H, 0));
   SRET(dalloc(&gf, H));
   SRET(check(launch_gaingen(gf, H, kGfTau, 0, seed, stream), "gaingen"));
   ++launches;
   SRET(dalloc_padded(&lm, vocab_l, H));
-  fill(vocab_l);
-  for (int r = 0; r < vocab_l; ++r) {
-    tau[r] = kWlmTau;
-    scl[r] = weight_scale(s_in);
-    base[r] = (static_cast<long long>(rank) * vocab_l + r) * H;
+  {
+    ShardDims sd;
+    shard_map(c.n_layers, H, c.n_heads, c.n_kv_heads, hd, c.ffn_hidden, c.vocab, c.ffn_kind, rank, world, 0, 18, &tau,
+              &scl, &base, &sd);
   }
   SRET(gen(lm, vocab_l, H, 1));
   if (!make_tmap_weight(&m_lm, lm, vocab_l, H)) return Status::err(SARATHI_ECUDA, "tensor map (lm head)");

@@ -33,7 +33,7 @@ EXPORTS = [
     "sarathi_sched_submit", "sarathi_sched_next", "sarathi_sched_complete", "sarathi_sched_idle_step",
     "sarathi_sched_done", "sarathi_sched_block_table", "sarathi_op_gemm", "sarathi_op_rmsnorm",
     "sarathi_request_truncate", "sarathi_last_io_bytes", "sarathi_set_profiling", "sarathi_op_times",
-    "sarathi_op_pack_weight",
+    "sarathi_op_pack_weight", "sarathi_shard_map",
 ]
 GEMM_W_PACKED = 0x100
 OP_NAMES = ["embed", "rmsnorm", "gemm_qkv", "prefill_attn", "decode_attn", "gemm_o", "gemm_gate_up",
@@ -108,6 +108,7 @@ def _load() -> C.CDLL:
         "sarathi_set_profiling": [VP, I32],
         "sarathi_op_times": [VP, P(C.c_double), P(I64), I32, I32],
         "sarathi_op_pack_weight": [VP, VP, I32, I32, VP],
+        "sarathi_shard_map": [P(ModelConfigC), I32, I32, I32, I32, P(I32), P(F), P(I64), I32, P(I32), P(I32)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -359,6 +360,19 @@ def op_gemm(W_ptr: int, X_ptr: int, out_ptr: int, M: int, N: int, K: int, mode: 
 def op_pack_weight(W_ptr: int, out_ptr: int, rows: int, cols: int, stream: int = 0):
     _check(lib.sarathi_op_pack_weight(C.c_void_p(W_ptr), C.c_void_p(out_ptr), rows, cols,
                                       C.c_void_p(stream) if stream else None))
+
+
+def shard_map(cfg: ModelConfigC, rank: int, world: int, layer: int, tensor: int):
+    """(tau[rows], scale[rows], base[rows], (rows, cols)) of a rank's packed weight shard (host-only)."""
+    rows, cols = C.c_int32(), C.c_int32()
+    _check(lib.sarathi_shard_map(C.byref(cfg), rank, world, layer, tensor, None, None, None, 0, C.byref(rows),
+                                 C.byref(cols)))
+    tau = np.zeros(rows.value, np.int32)
+    sc = np.zeros(rows.value, np.float32)
+    base = np.zeros(rows.value, np.int64)
+    _check(lib.sarathi_shard_map(C.byref(cfg), rank, world, layer, tensor, _p(tau, C.c_int32), _p(sc, C.c_float),
+                                 _p(base, C.c_int64), rows.value, C.byref(rows), C.byref(cols)))
+    return tau, sc, base, (rows.value, cols.value)
 
 
 def op_rmsnorm(h_ptr: int, g_ptr: int, out_ptr: int, R: int, H: int, eps: float, stream: int = 0):

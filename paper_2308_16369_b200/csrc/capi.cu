@@ -404,7 +404,7 @@ int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  GemmPlan pl = plan_gemm(M, N, K, sms, ws_floats, force_splits);
+  GemmPlan pl = plan_gemm(M, N, K, sms, ws_floats, force_splits, mode == EPI_ADD_F32);
   // pack W into the library's tile-major layout (the layout init_model generates weights in)
   static __nv_bfloat16* wp = nullptr;
   static size_t wp_elems = 0;

@@ -42,8 +42,12 @@ struct KParams {
   int M, N, KB;
   int bn, n_mma;          // tokens per tile; UMMAs per k-step (bn / n_mma tokens each, <= 256)
   int pm_tiles, n_tiles;  // 256-row pair tiles, token tiles
-  long long units;        // total (pair tile, k-block) work units = pm_tiles * n_tiles * KB
+  long long units;        // stream-K units = sk_tiles * KB (the first sk_tiles tiles are split)
   int ctas;               // number of CTA PAIRS (grid = 2 * ctas)
+  int sk_tiles;           // tiles processed stream-K (first), split across all pairs
+  int dp_per_pair;        // whole tiles per pair processed after the stream-K part
+  int dp_extra;           // pairs [0, dp_extra) take one more whole tile
+  int tiles;              // total pair-tiles = pm_tiles * n_tiles
   int stages;
   int nbuf;               // TMEM accumulator buffers (2 if bn <= 256)
   int max_slots;          // partial slots per tile
@@ -60,10 +64,40 @@ SARATHI_DEVICE float gelu_tanh_f(float x) {
 SARATHI_DEVICE long long unit_begin(int c, const KParams& p) {
   return (static_cast<long long>(c) * p.units) / p.ctas;
 }
-// CTA owning work unit u under the balanced partition above.
+// CTA pair owning stream-K unit u under the balanced partition above (units > 0).
 SARATHI_DEVICE int cta_of(long long u, const KParams& p) {
   return static_cast<int>(((u + 1) * p.ctas - 1) / p.units);
 }
+
+// Work of one CTA pair: first its stream-K range of units over the split tiles [0, sk_tiles) (so
+// their reductions overlap later work), then dp_per_pair whole tiles (reduction-free epilogues).
+struct SegIter {
+  long long u, u_end;
+  int dp_t, dp_end;
+  SARATHI_DEVICE void init(const KParams& p, int pair) {
+    u = unit_begin(pair, p);
+    u_end = unit_begin(pair + 1, p);
+    dp_t = p.sk_tiles + pair * p.dp_per_pair + min(pair, p.dp_extra);
+    dp_end = min(p.tiles, dp_t + p.dp_per_pair + (pair < p.dp_extra ? 1 : 0));
+  }
+  // next segment: tile, k-block range [kb0, kb1); false when done
+  SARATHI_DEVICE bool next(const KParams& p, int& tile, int& kb0, int& kb1) {
+    if (u < u_end) {
+      tile = static_cast<int>(u / p.KB);
+      kb0 = static_cast<int>(u % p.KB);
+      kb1 = static_cast<int>(min(static_cast<long long>(p.KB), kb0 + (u_end - u)));
+      u += kb1 - kb0;
+      return true;
+    }
+    if (dp_t < dp_end) {
+      tile = dp_t++;
+      kb0 = 0;
+      kb1 = p.KB;
+      return true;
+    }
+    return false;
+  }
+};
 
 // Epilogue for one 16-token chunk of a 128-row tile.  Thread r (0..127) holds acc row r, tokens c0..c0+15.
 // RoPE table values (cos, sin) for row r and tokens c0..c0+15 (prefetched one chunk ahead).
@@ -201,7 +235,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();   // 0 = leader (issues the pair MMAs)
   const int pair = blockIdx.x >> 1;
-  const long long u_begin = unit_begin(pair, p), u_end = unit_begin(pair + 1, p);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -232,39 +265,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     {
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
-      // incremental (tile, k-block, stage, phase) counters: no integer division in the hot loop
-      const long long n = u_end - u_begin;
-      int tile = static_cast<int>(u_begin / p.KB), kb = static_cast<int>(u_begin % p.KB);
-      int pt = tile / p.n_tiles, nt = tile % p.n_tiles;
+      // incremental (k-block, stage, phase) counters inside a segment: no division in the hot loop
+      const uint32_t tx = 2 * (stage_bytes - ((ep.dbg & 1) ? b_bytes : 0) - ((ep.dbg & 2) ? kABytes : 0));
       int s = 0;
       uint32_t ph = 0;
-      int wrow = ((pt * 2 + static_cast<int>(rank)) * p.KB + kb) * kWRowsPerTile;  // row in the 512-B view
-      const uint32_t tx = 2 * (stage_bytes - ((ep.dbg & 1) ? b_bytes : 0) - ((ep.dbg & 2) ? kABytes : 0));
-      for (long long i = 0; i < n; ++i) {
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* a = smem + static_cast<size_t>(s) * stage_bytes;
-        uint8_t* b = a + kABytes;
-        // both CTAs' bytes are counted on the leader's full[s] (pair TMA)
-        if (rank == 0) mbar_arrive_expect_tx_warp(&full[s], tx);
-        // W tile: the contiguous 16 KB pre-swizzled tile as 32 rows x 512 B (unswizzled map)
-        if (!(ep.dbg & 2)) tma_load_2d_pair_warp(a, &mapW, &full[s], 0, wrow, pol_w);
-        if (!(ep.dbg & 1))
-          for (int j = 0; j < p.n_mma; ++j)
-            tma_load_2d_pair_warp(b + j * (ni / 2) * kBK * 2, &mapX, &full[s], kb * kBK,
-                                  nt * p.bn + j * ni + static_cast<int>(rank) * (ni / 2), pol_x);
-        if (ep.trace && blockIdx.x < 2 && i < 256 && lane == 0) ep.trace[blockIdx.x * 1024 + i] = globaltimer_ns();
-        if (++s == p.stages) {
-          s = 0;
-          ph ^= 1;
-        }
-        wrow += kWRowsPerTile;
-        if (++kb == p.KB) {  // next tile
-          kb = 0;
-          if (++nt == p.n_tiles) {
-            nt = 0;
-            ++pt;
+      long long i = 0;
+      SegIter it;
+      it.init(p, pair);
+      int tile, kb0, kb1;
+      while (it.next(p, tile, kb0, kb1)) {
+        const int pt = tile / p.n_tiles, nt = tile % p.n_tiles;
+        int wrow = ((pt * 2 + static_cast<int>(rank)) * p.KB + kb0) * kWRowsPerTile;  // row in the 512-B view
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* a = smem + static_cast<size_t>(s) * stage_bytes;
+          uint8_t* b = a + kABytes;
+          // both CTAs' bytes are counted on the leader's full[s] (pair TMA)
+          if (rank == 0) mbar_arrive_expect_tx_warp(&full[s], tx);
+          // W tile: the contiguous 16 KB pre-swizzled tile as 32 rows x 512 B (unswizzled map)
+          if (!(ep.dbg & 2)) tma_load_2d_pair_warp(a, &mapW, &full[s], 0, wrow, pol_w);
+          if (!(ep.dbg & 1))
+            for (int j = 0; j < p.n_mma; ++j)
+              tma_load_2d_pair_warp(b + j * (ni / 2) * kBK * 2, &mapX, &full[s], kb * kBK,
+                                    nt * p.bn + j * ni + static_cast<int>(rank) * (ni / 2), pol_x);
+          if (ep.trace && blockIdx.x < 2 && i < 256 && lane == 0) ep.trace[blockIdx.x * 1024 + i] = globaltimer_ns();
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
           }
-          wrow = (pt * 2 + static_cast<int>(rank)) * p.KB * kWRowsPerTile;
+          wrow += kWRowsPerTile;
         }
       }
     }
@@ -274,10 +303,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = make_idesc_bf16_f32(2 * kBM, ni);
       int i = 0, seg = 0, s = 0;
       uint32_t ph = 0;
-      long long u = u_begin;
-      int kb0 = static_cast<int>(u_begin % p.KB);
-      while (u < u_end) {
-        const int kb1 = static_cast<int>(min(static_cast<long long>(p.KB), kb0 + (u_end - u)));
+      SegIter it;
+      it.init(p, pair);
+      int tile, kb0, kb1;
+      while (it.next(p, tile, kb0, kb1)) {
         const int buf = seg % p.nbuf;
         const uint32_t use = seg / p.nbuf;
         mbar_wait_cluster(&tempty[buf], (use & 1) ^ 1);  // both CTAs' epilogues drained it
@@ -307,8 +336,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             ph ^= 1;
           }
         }
-        u += kb1 - kb0;
-        kb0 = 0;  // every later segment starts a new tile
         ++seg;
       }
     }
@@ -319,12 +346,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = static_cast<int>(quarter * 32 + lane);    // accumulator row within this CTA's half
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
     int seg = 0;
-    long long u = u_begin;
     const size_t tile_elems = static_cast<size_t>(p.bn) * kBM;
-    while (u < u_end) {
-      const int tile = static_cast<int>(u / p.KB);
-      const int kb0 = static_cast<int>(u % p.KB);
-      const int kb1 = static_cast<int>(min(static_cast<long long>(p.KB), kb0 + (u_end - u)));
+    SegIter it;
+    it.init(p, pair);
+    int tile, kb0, kb1;
+    while (it.next(p, tile, kb0, kb1)) {
       const int pt = tile / p.n_tiles, nt = tile % p.n_tiles;
       const int mt = pt * 2 + static_cast<int>(rank);       // this CTA's 128-row tile
       const int buf = seg % p.nbuf;
@@ -469,7 +495,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      u += kb1 - kb0;
       ++seg;
     }
   }
@@ -524,7 +549,7 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
   return r == CUDA_SUCCESS;
 }
 
-GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int force_pairs) {
+GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int force_pairs, bool atomic_epilogue) {
   GemmPlan pl;
   pl.M = M;
   pl.N = N;
@@ -542,33 +567,73 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
   pl.box_rows = pl.bn / pl.n_mma / 2;  // each CTA of the pair holds half of every UMMA's tokens
   pl.pm_tiles = (M + 2 * kBM - 1) / (2 * kBM);
   pl.m_tiles = 2 * pl.pm_tiles;
-  const long long ptiles = static_cast<long long>(pl.pm_tiles) * pl.n_tiles;
-  pl.units = ptiles * KB;
-  // persistent grid: one CTA pair per 2 SMs, each pair with at least ~4 k-blocks of work
-  int pairs = static_cast<int>(std::min<long long>(num_sms / 2, std::max<long long>(1, pl.units / 4)));
-  if (force_pairs > 0) pairs = static_cast<int>(std::min<long long>(pl.units, force_pairs));
+  const int tiles = pl.pm_tiles * pl.n_tiles;
+  pl.tiles = tiles;
+  const int P = std::max(1, num_sms / 2);
+  // Work split (in k-block units; a split tile costs a partial write + a reduction, ~KB/2 units
+  // when it is exposed at the kernel end):
+  //  * residual-add epilogues reduce with red.add (no reduction pass): pure stream-K over all pairs;
+  //  * tiles <= P: one whole tile per pair (data-parallel) unless stream-K saves > KB/2 units;
+  //  * tiles > P: the tiles % P remainder stream-K first (reductions overlap the rest), then
+  //    tiles / P whole tiles per pair.
+  int pairs, sk_tiles, dp_per, dp_extra = 0;
+  if (force_pairs > 0) {
+    pairs = static_cast<int>(std::min<long long>(static_cast<long long>(tiles) * KB, force_pairs));
+    sk_tiles = tiles;
+    dp_per = 0;
+  } else if (atomic_epilogue) {
+    pairs = static_cast<int>(std::min<long long>(P, std::max<long long>(1, static_cast<long long>(tiles) * KB / 4)));
+    sk_tiles = tiles;
+    dp_per = 0;
+  } else if (tiles <= P) {
+    const int sk_pairs = static_cast<int>(std::min<long long>(P, std::max<long long>(1, static_cast<long long>(tiles) * KB / 4)));
+    const double sk_units = std::ceil(static_cast<double>(tiles) * KB / sk_pairs) + 0.5 * KB;
+    if (KB <= sk_units) {
+      pairs = tiles;
+      sk_tiles = 0;
+      dp_per = 1;
+    } else {
+      pairs = sk_pairs;
+      sk_tiles = tiles;
+      dp_per = 0;
+    }
+  } else {
+    pairs = P;
+    dp_per = tiles / P;
+    sk_tiles = tiles % P;
+    if (static_cast<long long>(sk_tiles) * KB < 4LL * P) {  // remainder too small to split: whole tiles
+      dp_extra = sk_tiles;
+      sk_tiles = 0;
+    }
+  }
+  const long long units = static_cast<long long>(sk_tiles) * KB;
   auto slots_for = [&](int g) {
-    const long long pc = pl.units / g;  // >= 1
+    if (units == 0) return 1;
+    const long long pc = std::max<long long>(1, units / g);
     const int s = pc >= KB ? 2 : static_cast<int>((KB + pc - 1) / pc) + 1;
     return std::min(s, g);
   };
   int max_slots = slots_for(pairs);
-  // the reduction handles <= 4 contributors per tile: use fewer pairs if the split is finer
-  while (pairs > 1 && max_slots > 4) {
+  // the reduction handles <= 4 contributors per tile (pure stream-K plans only)
+  while (dp_per == 0 && pairs > 1 && max_slots > 4) {
     --pairs;
     max_slots = slots_for(pairs);
   }
   const size_t tile_elems = static_cast<size_t>(pl.bn) * kBM;
   const size_t tiles128 = static_cast<size_t>(pl.m_tiles) * pl.n_tiles;
-  while (pairs > 1 && tiles128 * max_slots * tile_elems > ws_cap_floats) {
+  while (dp_per == 0 && pairs > 1 && tiles128 * max_slots * tile_elems > ws_cap_floats) {
     pairs = std::max(1, pairs / 2);
     max_slots = slots_for(pairs);
   }
   pl.ctas = pairs;
+  pl.sk_tiles = sk_tiles;
+  pl.dp_per_pair = dp_per;
+  pl.dp_extra = dp_extra;
+  pl.units = units;
   pl.max_slots = max_slots;
-  pl.splits = static_cast<int>((pl.units + pairs - 1) / pairs);  // units per pair (informational)
+  pl.splits = static_cast<int>((units + pairs - 1) / pairs) + dp_per * KB;  // units per pair (informational)
   pl.kb_per_split = pl.splits;
-  pl.ws_floats = tiles128 * max_slots * tile_elems;
+  pl.ws_floats = units > 0 ? tiles128 * max_slots * tile_elems : 0;
   pl.nbuf = pl.bn <= 256 ? 2 : 1;
   const size_t stage = kABytes + static_cast<size_t>(pl.bn / 2) * kBK * 2;
   const size_t budget = 226 * 1024 - 1024 - extra_smem(pl.bn);
@@ -609,6 +674,10 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   kp.n_tiles = pl.n_tiles;
   kp.units = pl.units;
   kp.ctas = pl.ctas;
+  kp.sk_tiles = pl.sk_tiles;
+  kp.dp_per_pair = pl.dp_per_pair;
+  kp.dp_extra = pl.dp_extra;
+  kp.tiles = pl.tiles;
   kp.stages = pl.stages;
   kp.nbuf = pl.nbuf;
   kp.max_slots = pl.max_slots;

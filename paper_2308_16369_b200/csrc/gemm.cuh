@@ -47,8 +47,12 @@ struct GemmPlan {
   int box_rows = 0;    // X TMA box rows (per CTA of the pair: half of one UMMA's tokens)
   int pm_tiles = 0;    // 256-row tiles (one per CTA pair)
   int m_tiles = 0, n_tiles = 0;  // 128-row tiles (2 * pm_tiles), token tiles
-  long long units = 0; // (pair tile, k-block) work units
+  long long units = 0; // stream-K (pair tile, k-block) units = sk_tiles * K/64
   int ctas = 0;        // persistent grid size in CTA PAIRS
+  int tiles = 0;       // pair-tiles (pm_tiles * n_tiles)
+  int sk_tiles = 0;    // tiles split stream-K across all pairs (processed first)
+  int dp_per_pair = 0; // whole tiles per pair processed after the stream-K part
+  int dp_extra = 0;    // pairs [0, dp_extra) take one extra whole tile
   int max_slots = 1;   // stream-K partial slots per tile
   int nbuf = 1;        // TMEM accumulator buffers
   int splits = 1, kb_per_split = 0;  // units per CTA (informational)
@@ -60,7 +64,9 @@ struct GemmPlan {
 // Persistent stream-K plan for C[N x M] = X[N x K] * W[M x K]^T on `num_sms` SMs (CTA pairs,
 // tcgen05 cta_group::2).  force_pairs > 0 fixes the grid (tests use it to exercise multi-pair
 // reductions of one tile).
-GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int force_pairs = 0);
+// atomic_epilogue: the epilogue is a residual add (split tiles reduce with red.add, no reduction pass).
+GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int force_pairs = 0,
+                   bool atomic_epilogue = false);
 
 // 2D bf16 K-major tensor map with 128B swizzle: rows x cols(=K), box = box_rows x 64.
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,

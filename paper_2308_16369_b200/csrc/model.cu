@@ -304,9 +304,10 @@ Status Model::alloc_kv(int64_t nb, int32_t bs) {
 }
 
 Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, int N, const EpiParams& ep_in) {
-  auto pk = std::make_tuple(M, N, K);
+  const bool atomic = ep_in.mode == EPI_ADD_F32;
+  auto pk = std::make_tuple(M, N, K * 2 + (atomic ? 1 : 0));
   auto it = plans.find(pk);
-  if (it == plans.end()) it = plans.emplace(pk, plan_gemm(M, N, K, num_sms, gemm_ws_floats)).first;
+  if (it == plans.end()) it = plans.emplace(pk, plan_gemm(M, N, K, num_sms, gemm_ws_floats, 0, atomic)).first;
   const GemmPlan& pl = it->second;
   auto xk = std::make_tuple(X, N, K, pl.box_rows);
   auto xi = xmaps.find(xk);

@@ -81,8 +81,10 @@ int sarathi_nccl_unique_id(void* out128);
 
 /* Creates the model on dist->device and generates this rank's weight shards ON DEVICE from the
  * counter-based generator spec (synth/__init__.py header; seed = weight_seed).  Weights are
- * packed in kernel layout: per layer QKV [(nq+2nkv)/t*hd, H], gate||up interleaved in 64-row
- * blocks [2*H2/t, H], O [H, nq*hd/t], down [H, H2/t]; embedding and final norm replicated; LM
+ * packed in kernel layout: per layer QKV [(nq+2nkv)/t*hd, H] (inside each head, row 32j+l is dim
+ * 16j+l for l < 16 and dim hd/2+16j+l-16 otherwise: rotate-half partners share a warp), gate||up
+ * interleaved in 16-row blocks [2*H2/t, H] (rows 32b..32b+15 gate features 16b.., the next 16 the
+ * matching up features), O [H, nq*hd/t], down [H, H2/t]; embedding and final norm replicated; LM
  * head vocab-parallel [ceil(V/t), H].  Ownership: the library owns all device memory.
  * Errors: EINVAL (bad config / divisibility by world), ECUDA (allocation), ENCCL. */
 int sarathi_init_model(const sarathi_model_config* cfg, const sarathi_dist* dist, uint64_t weight_seed,
@@ -186,7 +188,9 @@ int sarathi_debug_hidden(const sarathi_model* m, int32_t layer, float* host_out)
 /* K and V (bf16 bits, [n][n_kv/t][hd] each) of positions pos0..pos0+n-1 of a request, layer l. */
 int sarathi_debug_kv(const sarathi_model* m, int32_t layer, int64_t req_id, int32_t pos0, int32_t n,
                      uint16_t* host_k, uint16_t* host_v);
-/* Copies `count` bf16 values (bits) of a packed weight tensor, starting at element `offset`.
+/* Copies `count` bf16 values (bits) of a packed weight tensor, starting at element `offset`, in
+ * the packed ROW order of sarathi_init_model (QKV dims permuted inside heads, gate/up interleaved)
+ * with the tile-major storage undone. 
  * tensor: 0 qkv, 1 o, 2 gate||up, 3 down, 4 g1, 5 g2 (per layer); 16 emb, 17 final gain, 18 lm head. */
 int sarathi_debug_weight(const sarathi_model* m, int32_t layer, int32_t tensor, int64_t offset, int64_t count,
                          uint16_t* host_out);
@@ -245,7 +249,8 @@ int sarathi_sched_block_table(const sarathi_sched* s, int64_t req_id, int32_t* o
 /* ---- kernel-level entry points (device pointers, caller's stream) for parity tests ------ */
 /* out = X · Wᵀ on tcgen05: W bf16 [M][K] (K-major), X bf16 [N][K]; mode 0: out bf16 [N][M],
  * 1: out fp32 [N][M], 2: out fp32 += (residual add), 3: SiLU(gate)·up with gate/up interleaved in
- * 64-row blocks of W -> out bf16 [N][M/2], 4: GELU-tanh -> bf16.  K % 64 == 0, N >= 1.
+ * 16-row blocks of W (rows 32b..32b+15 gate of features 16b.., next 16 rows their up) -> out bf16
+ * [N][M/2], 4: GELU-tanh -> bf16.  K % 64 == 0, M % 8 == 0 (M % 128 == 0 for mode 3), N >= 1.
  * force_splits > 0 fixes the persistent stream-K grid size in CTA pairs (else one pair per 2 SMs).
  * mode | SARATHI_GEMM_W_PACKED: W is already in the tile-major layout of sarathi_op_pack_weight
  * (otherwise it is packed into a library-owned scratch buffer first, on the same stream). */

@@ -390,8 +390,8 @@ int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t 
   using namespace sarathi;
   const bool prepacked = (mode & SARATHI_GEMM_W_PACKED) != 0;
   mode &= ~SARATHI_GEMM_W_PACKED;
-  if (!W || !X || !out || M < 1 || N < 1 || K < 64 || K % 64 || mode < 0 || mode > 4)
-    return fail(SARATHI_EINVAL, "op_gemm: bad argument (K % 64 == 0, mode 0..4)");
+  if (!W || !X || !out || M < 8 || M % 8 || N < 1 || K < 64 || K % 64 || mode < 0 || mode > 4)
+    return fail(SARATHI_EINVAL, "op_gemm: bad argument (M % 8 == 0, K % 64 == 0, mode 0..4)");
   if (mode == EPI_SILU_MUL && M % 128) return fail(SARATHI_EINVAL, "op_gemm: SiLU mode needs M % 128 == 0");
   static float* ws = nullptr;
   static int* ctr = nullptr;
@@ -450,7 +450,8 @@ int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t 
               h[2048 + i] ? (h[2048 + i] - t0) * 1e-3 : -1.0, h[1280 + i] ? (h[1280 + i] - t0) * 1e-3 : -1.0,
               h[256 + i] ? (h[256 + i] - t0) * 1e-3 : -1.0);
     for (int sgm = 0; sgm < 64 && h[512 + sgm]; ++sgm)
-      fprintf(stderr, "seg %d epilogue wake %8.3f us\n", sgm, (h[512 + sgm] - t0) * 1e-3);
+      fprintf(stderr, "seg %d epilogue wake %8.3f us  done %8.3f us\n", sgm, (h[512 + sgm] - t0) * 1e-3,
+              h[576 + sgm] ? (h[576 + sgm] - t0) * 1e-3 : -1.0);
   }
   if (e != cudaSuccess) return fail(SARATHI_ECUDA, std::string("op_gemm: ") + cudaGetErrorString(e));
   return SARATHI_OK;

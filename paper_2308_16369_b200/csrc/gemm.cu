@@ -35,7 +35,6 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
 constexpr int kThreads = 192;
-constexpr int kXPitch = 17;                  // xbuf [128][17] fp32 (partner exchange)
 constexpr int kWRowsPerTile = 32;            // packed W viewed as rows of 256 elements (512 B)
 
 struct KParams {
@@ -99,14 +98,31 @@ struct SegIter {
   }
 };
 
-// Epilogue for one 16-token chunk of a 128-row tile.  Thread r (0..127) holds acc row r, tokens c0..c0+15.
-// RoPE table values (cos, sin) for row r and tokens c0..c0+15 (prefetched one chunk ahead).
-SARATHI_DEVICE void rope_load(const KParams& p, const EpiParams& ep, int r, int mt, int c0, int tvalid,
-                              const int* s_pos, float (&cs)[16], float (&sn)[16]) {
-  const int hd = ep.head_dim, half = hd >> 1;
-  const int m = mt * kBM + r;
-  const bool rope = m < p.M && (m >> (hd == 128 ? 7 : 6)) < ep.n_q_local + ep.n_kv_local;
-  const int dd = r & (half - 1);
+// ---------------------------------------------------------------------------
+// Epilogue.  The accumulator comes out of TMEM with thread = row (tcgen05.ld 32x32b: lane l of
+// warp quarter q holds row 32q + l of this CTA's 128-row tile) and registers = 16 consecutive
+// tokens.  Outputs are token-major ([token][feature]), so each warp transposes its 32 x 16 block
+// through a private 2 KB shared-memory buffer and writes 16-byte vectors (8 bf16 / 4 fp32 features
+// of one token) — the residual add is a vector red.global.add.v4.f32.  No cross-warp barrier.
+//
+// Row orders the packed weights are generated in (host_sched.cpp shard_map) so that every fused
+// epilogue is warp-local:
+//  * gate||up (SwiGLU): 16-row interleave — packed rows [32b, 32b+16) = gate features
+//    [16b, 16b+16), rows [32b+16, 32b+32) = the matching up features; lane l and l^16 of a warp
+//    hold g and u of the same feature (one shuffle).
+//  * QKV: inside each head, warp-slab j (rows 32j..32j+31 of the head) holds dims
+//    [16j, 16j+16) in lanes 0-15 and their rotate-half partners [hd/2 + 16j, ...) in lanes 16-31,
+//    so RoPE is one shuffle.  Q, K and V are stored in the natural dim order.
+// ---------------------------------------------------------------------------
+constexpr int kStageFloats = 16 * 32;  // per-warp transpose buffer (2 KB)
+
+SARATHI_DEVICE int qkv_dim_of_lane(int jw, uint32_t lane, int half) {
+  return (lane < 16 ? 0 : half) + 16 * jw + static_cast<int>(lane & 15);
+}
+
+// RoPE table values (cos, sin) of this lane's rotation index for the chunk's 16 tokens.
+SARATHI_DEVICE void rope_load(int dd, bool rope, int half, int c0, int tvalid, const int* s_pos, const EpiParams& ep,
+                              float (&cs)[16], float (&sn)[16]) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     cs[j] = 1.f;
@@ -119,91 +135,126 @@ SARATHI_DEVICE void rope_load(const KParams& p, const EpiParams& ep, int r, int 
   }
 }
 
-SARATHI_DEVICE void epilogue_chunk(const KParams& p, const EpiParams& ep, float (&v)[16], int r, int mt, int nt,
-                                   int c0, int tvalid, float* xbuf, const int* s_pos, const int* s_slot,
-                                   const float (&cs)[16], const float (&sn)[16]) {
-  const int m = mt * kBM + r;
-  const long long t0 = static_cast<long long>(nt) * p.bn + c0;
-  const int nv = min(16, tvalid - c0);  // valid tokens in this chunk (>= 1)
+struct QkvLane {  // per-warp / per-lane constants of the fused QKV epilogue
+  int gh;         // packed head index in [q heads | k heads | v heads]
+  int jw;         // warp slab within the head
+  int dd;         // rotation index of this lane (dim within the half)
+  bool rope;      // q or k head
+};
+
+SARATHI_DEVICE QkvLane qkv_lane(const EpiParams& ep, int mt, uint32_t q, uint32_t lane) {
+  QkvLane o;
+  const int hd_shift = ep.head_dim == 128 ? 7 : 6;
+  const int row0 = mt * kBM + static_cast<int>(q) * 32;
+  o.gh = row0 >> hd_shift;
+  o.jw = (row0 & (ep.head_dim - 1)) >> 5;
+  o.dd = 16 * o.jw + static_cast<int>(lane & 15);
+  o.rope = o.gh < ep.n_q_local + ep.n_kv_local;
+  return o;
+}
+
+SARATHI_DEVICE void red_add_v4(float* addr, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[16], uint32_t q, uint32_t lane, int mt,
+                             int nt, int c0, int tvalid, float* sbuf, const int* s_slot, const QkvLane& ql,
+                             const float (&cs)[16], const float (&sn)[16]) {
+  const int row0 = mt * kBM + static_cast<int>(q) * 32;  // first accumulator row of this warp
+  const long long tb = static_cast<long long>(nt) * p.bn + c0;
+  const int nv = min(16, tvalid - c0);
+  uint16_t* sb = reinterpret_cast<uint16_t*>(sbuf);
   switch (ep.mode) {
     case EPI_STORE_BF16:
     case EPI_GELU: {
-      if (m >= p.M) break;
-      __nv_bfloat16* out = static_cast<__nv_bfloat16*>(ep.out) + t0 * ep.ldo + m;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float x = ep.mode == EPI_GELU ? gelu_tanh_f(v[j]) : v[j];
-        if (j < nv) out[j * ep.ldo] = __float2bfloat16_rn(x);
+        sb[j * 32 + lane] = __bfloat16_as_ushort(__float2bfloat16_rn(x));
       }
-      break;
-    }
-    case EPI_STORE_F32: {
-      if (m >= p.M) break;
-      float* out = static_cast<float*>(ep.out) + t0 * ep.ldo + m;
+      __syncwarp();
+      const int g = static_cast<int>(lane & 3), m = row0 + g * 8;
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j < nv) out[j * ep.ldo] = v[j];
+      for (int pass = 0; pass < 2; ++pass) {
+        const int tok = pass * 8 + static_cast<int>(lane >> 2);
+        if (tok < nv && m < p.M)
+          *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + (tb + tok) * ep.ldo + m) =
+              *reinterpret_cast<const uint4*>(sb + tok * 32 + g * 8);
+      }
+      __syncwarp();
       break;
     }
+    case EPI_STORE_F32:
     case EPI_ADD_F32: {
-      if (m >= p.M) break;
-      float* out = static_cast<float*>(ep.out) + t0 * ep.ldo + m;
-      float o[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) o[j] = j < nv ? __ldcg(out + j * ep.ldo) : 0.f;  // 16 loads in flight
+      for (int j = 0; j < 16; ++j) sbuf[j * 32 + lane] = v[j];
+      __syncwarp();
+      const int g = static_cast<int>(lane & 7), m = row0 + g * 4;
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j < nv) out[j * ep.ldo] = o[j] + v[j];
+      for (int pass = 0; pass < 4; ++pass) {
+        const int tok = pass * 4 + static_cast<int>(lane >> 3);
+        if (tok < nv && m < p.M) {
+          const float4 x = *reinterpret_cast<const float4*>(sbuf + tok * 32 + g * 4);
+          float* dst = static_cast<float*>(ep.out) + (tb + tok) * ep.ldo + m;
+          if (ep.mode == EPI_ADD_F32)
+            red_add_v4(dst, x);
+          else
+            *reinterpret_cast<float4*>(dst) = x;
+        }
+      }
+      __syncwarp();
       break;
     }
     case EPI_SILU_MUL: {
-      // tile rows [0,64): gate features, [64,128): the matching up features (64-row interleave)
-      named_bar_sync(2, 128);  // xbuf free (previous chunk consumed)
-      if (r >= 64) {
+      // lanes 0-15: gate of features f0 + (l & 15); lanes 16-31: up of the same features.
+      // After one xor-16 exchange lanes 0-15 own tokens 0-7 and lanes 16-31 tokens 8-15.
+      const bool lo = lane < 16;
+      const int f0 = row0 >> 1;  // 16 output features per warp
 #pragma unroll
-        for (int j = 0; j < 16; ++j) xbuf[(r - 64) * kXPitch + j] = v[j];
+      for (int i = 0; i < 8; ++i) {
+        const float send = lo ? v[8 + i] : v[i];
+        const float y = __shfl_xor_sync(0xffffffffu, send, 16);
+        const float gv = lo ? v[i] : y, uv = lo ? y : v[8 + i];
+        sb[((lo ? 0 : 8) + i) * 16 + (lane & 15)] = __bfloat16_as_ushort(__float2bfloat16_rn(silu_f(gv) * uv));
       }
-      named_bar_sync(2, 128);
-      if (r < 64) {
-        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(ep.out) + t0 * ep.ldo + mt * 64 + r;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float u = xbuf[r * kXPitch + j];
-          if (j < nv) out[j * ep.ldo] = __float2bfloat16_rn(silu_f(v[j]) * u);
-        }
-      }
+      __syncwarp();
+      const int tok = static_cast<int>(lane >> 1), h8 = static_cast<int>(lane & 1) * 8;
+      if (tok < nv && row0 < p.M)
+        *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + (tb + tok) * ep.ldo + f0 + h8) =
+            *reinterpret_cast<const uint4*>(sb + tok * 16 + h8);
+      __syncwarp();
       break;
     }
     case EPI_QKV_ROPE: {
-      // rows are head-aligned (128 % head_dim == 0): rotate-half partner of row r is r ^ half.
-      const int hd = ep.head_dim, half = hd >> 1;
-      const int hd_shift = hd == 128 ? 7 : 6;
-      named_bar_sync(2, 128);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) xbuf[r * kXPitch + j] = v[j];
-      named_bar_sync(2, 128);
-      if (m >= p.M) break;
-      const int d = r & (hd - 1);     // dim within head
-      const int gh = m >> hd_shift;   // head index in [q heads | k heads | v heads]
-      const bool rope = gh < ep.n_q_local + ep.n_kv_local;
-      const bool isq = gh < ep.n_q_local;
-      const int partner = r ^ half;
-      const bool lowhalf = d < half;
-      __nv_bfloat16* qout = static_cast<__nv_bfloat16*>(ep.out);
-      __nv_bfloat16* cache = static_cast<__nv_bfloat16*>(rope ? ep.kcache : ep.vcache);
-      const int kvh = isq ? 0 : (rope ? gh - ep.n_q_local : gh - ep.n_q_local - ep.n_kv_local);
-      const int head_row = kvh * ep.block_size;  // + s_slot[t] = cache row of this token and kv head
+      const int half = ep.head_dim >> 1;
+      const bool lo = lane < 16;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        if (j >= nv) continue;
-        const int t = c0 + j;
-        const float xp = xbuf[partner * kXPitch + j];
+        const float xp = __shfl_xor_sync(0xffffffffu, v[j], 16);  // rotate-half partner
         // x1 = low-half value, x2 = high-half value: y1 = x1 c - x2 s, y2 = x2 c + x1 s
-        const float y = lowhalf ? (v[j] * cs[j] - xp * sn[j]) : (v[j] * cs[j] + xp * sn[j]);
-        __nv_bfloat16* dst = isq ? qout + (static_cast<long long>(nt) * p.bn + t) * ep.ldo + m
-                                 : cache + (static_cast<size_t>(s_slot[t] + head_row) << hd_shift) + d;
-        *dst = __float2bfloat16_rn(y);
+        const float y = ql.rope ? (lo ? v[j] * cs[j] - xp * sn[j] : v[j] * cs[j] + xp * sn[j]) : v[j];
+        sb[j * 32 + lane] = __bfloat16_as_ushort(__float2bfloat16_rn(y));
       }
+      __syncwarp();
+      if (row0 < p.M) {
+        const int hd_shift = ep.head_dim == 128 ? 7 : 6;
+        const bool isq = ql.gh < ep.n_q_local;
+        const int kvh = isq ? 0 : (ql.rope ? ql.gh - ep.n_q_local : ql.gh - ep.n_q_local - ep.n_kv_local);
+        __nv_bfloat16* cache = static_cast<__nv_bfloat16*>(ql.rope ? ep.kcache : ep.vcache);
+        const int g = static_cast<int>(lane & 3);  // 8-dim group: 0,1 low half; 2,3 high half
+        const int d = (g < 2 ? 0 : half) + 16 * ql.jw + (g & 1) * 8;
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+          const int tok = pass * 8 + static_cast<int>(lane >> 2);
+          if (tok >= nv) continue;
+          __nv_bfloat16* dst =
+              isq ? static_cast<__nv_bfloat16*>(ep.out) + (tb + tok) * ep.ldo + (ql.gh << hd_shift) + d
+                  : cache + (static_cast<size_t>(s_slot[c0 + tok] + kvh * ep.block_size) << hd_shift) + d;
+          *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(sb + tok * 32 + g * 8);
+        }
+      }
+      __syncwarp();
       break;
     }
     default:
@@ -219,8 +270,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t b_bytes = static_cast<uint32_t>(p.bn / 2) * kBK * 2;  // this CTA's half of the tokens
   const uint32_t stage_bytes = kABytes + b_bytes;
-  float* xbuf = reinterpret_cast<float*>(smem + p.ring_bytes);         // [128][17]
-  int* s_pos = reinterpret_cast<int*>(xbuf + kBM * kXPitch);           // [bn]
+  float* stage_buf = reinterpret_cast<float*>(smem + p.ring_bytes);    // [4 warps][16 x 32] transpose
+  int* s_pos = reinterpret_cast<int*>(stage_buf + 4 * kStageFloats);   // [bn]
   int* s_slot = s_pos + p.bn;                                          // [bn]
   uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_slot + p.bn) + 7) & ~uintptr_t(7));
   uint64_t* full = bars;                // local: this CTA's W + X bytes landed
@@ -344,9 +395,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int et = threadIdx.x - 64;                        // 0..127
     const uint32_t quarter = warp & 3;                      // TMEM lane quarter of this warp
     const int r = static_cast<int>(quarter * 32 + lane);    // accumulator row within this CTA's half
+    float* sbuf = stage_buf + quarter * kStageFloats;       // this warp's transpose buffer
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
     int seg = 0;
     const size_t tile_elems = static_cast<size_t>(p.bn) * kBM;
+    const bool rope_mode = ep.mode == EPI_QKV_ROPE;
+    const int half = ep.head_dim >> 1;
     SegIter it;
     it.init(p, pair);
     int tile, kb0, kb1;
@@ -356,13 +410,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int buf = seg % p.nbuf;
       const uint32_t use = seg / p.nbuf;
       const int tvalid = min(p.bn, p.N - nt * p.bn);
-      const bool whole = kb0 == 0 && kb1 == p.KB;
+      // whole tiles and residual adds (red.add of every contributor's partial) emit straight from TMEM
+      const bool direct = (kb0 == 0 && kb1 == p.KB) || ep.mode == EPI_ADD_F32;
+      QkvLane ql{};
+      if (rope_mode) ql = qkv_lane(ep, mt, quarter, lane);
       auto release_tmem = [&]() {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_leader + buf * 8);
       };
-      if (ep.mode == EPI_QKV_ROPE) {  // stage per-token metadata for the fused KV append
+      if (rope_mode) {  // stage per-token metadata for the fused KV append
         named_bar_sync(2, 128);
         for (int t = et; t < tvalid; t += 128) {
           s_pos[t] = __ldg(ep.pos + nt * p.bn + t);
@@ -378,22 +435,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ep.trace && blockIdx.x < 2 && et == 0 && seg < 64) ep.trace[blockIdx.x * 1024 + 512 + seg] = globaltimer_ns();
       const uint32_t trow = tmem + buf * 256 + ((quarter * 32u) << 16);
       const int nchunks = (tvalid + 15) / 16;
-      const bool rope = ep.mode == EPI_QKV_ROPE;
       float cs[16], sn[16], csn[16], snn[16];  // current / next chunk RoPE values (registers)
-      if (whole) {
-        if (rope) rope_load(p, ep, r, mt, 0, tvalid, s_pos, cs, sn);
+      if (direct) {
+        if (rope_mode) rope_load(ql.dd, ql.rope, half, 0, tvalid, s_pos, ep, cs, sn);
         for (int ch = 0; ch < nchunks; ++ch) {
           uint32_t raw[16];
           tmem_ld_32x32b_x16(trow + ch * 16, raw);
           tmem_ld_wait();
           if (ch == nchunks - 1) release_tmem();
           // prefetch the next chunk's RoPE table values; their latency overlaps this chunk
-          if (rope && ch + 1 < nchunks) rope_load(p, ep, r, mt, (ch + 1) * 16, tvalid, s_pos, csn, snn);
+          if (rope_mode && ch + 1 < nchunks) rope_load(ql.dd, ql.rope, half, (ch + 1) * 16, tvalid, s_pos, ep, csn, snn);
           float v[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
-          epilogue_chunk(p, ep, v, r, mt, nt, ch * 16, tvalid, xbuf, s_pos, s_slot, cs, sn);
-          if (rope) {
+          if (!(ep.dbg & 4)) epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_slot, ql, cs, sn);
+          if (rope_mode) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               cs[j] = csn[j];
@@ -402,99 +458,79 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else {
-        if (ep.mode == EPI_ADD_F32) {
-          // residual add: every contributor adds its partial straight into the fp32 residual
-          // (red.global.add; no partial buffer, no reduction pass)
-          const int m = mt * kBM + r;
-          for (int ch = 0; ch < nchunks; ++ch) {
-            uint32_t raw[16];
-            tmem_ld_32x32b_x16(trow + ch * 16, raw);
-            tmem_ld_wait();
-            if (ch == nchunks - 1) release_tmem();
-            if (m < p.M) {
-              float* out = static_cast<float*>(ep.out) + (static_cast<long long>(nt) * p.bn + ch * 16) * ep.ldo + m;
-              const int nv = min(16, tvalid - ch * 16);
+        // stream-K partial: slot = position of this pair among the tile's contributors; the last to
+        // arrive sums the slots in slot order (deterministic) and runs the fused epilogue
+        const int c_first = cta_of(static_cast<long long>(tile) * p.KB, p);
+        const int c_last = cta_of(static_cast<long long>(tile) * p.KB + p.KB - 1, p);
+        const int nslot = c_last - c_first + 1;
+        const int slot = pair - c_first;
+        const size_t tile128 = static_cast<size_t>(mt) * p.n_tiles + nt;
+        float* wsp = ep.ws + (tile128 * p.max_slots + slot) * tile_elems;
+        for (int ch = 0; ch < nchunks; ++ch) {
+          uint32_t raw[16];
+          tmem_ld_32x32b_x16(trow + ch * 16, raw);
+          tmem_ld_wait();
+          // partial layout [token][row]: a warp store covers 128 contiguous bytes
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (j < nv) atomicAdd(out + j * ep.ldo, __uint_as_float(raw[j]));
-            }
-          }
-        } else {
-          // stream-K partial: slot = position of this pair among the tile's contributors; the last to
-          // arrive sums the slots in slot order (deterministic) and runs the fused epilogue
-          const int c_first = cta_of(static_cast<long long>(tile) * p.KB, p);
-          const int c_last = cta_of(static_cast<long long>(tile) * p.KB + p.KB - 1, p);
-          const int nslot = c_last - c_first + 1;
-          const int slot = pair - c_first;
-          const size_t tile128 = static_cast<size_t>(mt) * p.n_tiles + nt;
-          float* wsp = ep.ws + (tile128 * p.max_slots + slot) * tile_elems;
-          for (int ch = 0; ch < nchunks; ++ch) {
-            uint32_t raw[16];
-            tmem_ld_32x32b_x16(trow + ch * 16, raw);
-            tmem_ld_wait();
-            // partial layout [token][row]: a warp store covers 128 contiguous bytes
-#pragma unroll
-            for (int j = 0; j < 16; ++j) __stcg(wsp + static_cast<size_t>(ch * 16 + j) * kBM + r, __uint_as_float(raw[j]));
-          }
-          release_tmem();
+          for (int j = 0; j < 16; ++j) __stcg(wsp + static_cast<size_t>(ch * 16 + j) * kBM + r, __uint_as_float(raw[j]));
+        }
+        release_tmem();
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (et == 0) {
+          int* ctr = ep.counters + tile128;
+          const int old = atomicAdd(ctr, 1);
+          s_last = (old == nslot - 1);
+          if (s_last) *ctr = 0;  // re-arm for the next launch
+        }
+        named_bar_sync(1, 128);
+        if (s_last) {
           __threadfence();
-          named_bar_sync(1, 128);
-          if (et == 0) {
-            int* ctr = ep.counters + tile128;
-            const int old = atomicAdd(ctr, 1);
-            s_last = (old == nslot - 1);
-            if (s_last) *ctr = 0;  // re-arm for the next launch
-          }
-          named_bar_sync(1, 128);
-          if (s_last) {
-            __threadfence();
-            const float* base = ep.ws + tile128 * p.max_slots * tile_elems;
-            if (rope) rope_load(p, ep, r, mt, 0, tvalid, s_pos, cs, sn);
-            // vectorised, software-pipelined reduction: chunk ch+1's partials are in flight while
-            // chunk ch is summed (slot order kept -> deterministic)
-            constexpr int kMaxSlots = 2;  // prefetched slots; slots >= 2 (rare) are added unpipelined
-            // software-pipelined reduction: chunk ch+1's partials are in flight while chunk ch is summed
-            // (slot order kept -> deterministic); [token][row] layout keeps every load 128 B per warp
-            const float* colbase = base + r;
-            float cur[kMaxSlots][16], nxt[kMaxSlots][16];
+          const float* base = ep.ws + tile128 * p.max_slots * tile_elems;
+          if (rope_mode) rope_load(ql.dd, ql.rope, half, 0, tvalid, s_pos, ep, cs, sn);
+          // software-pipelined reduction: chunk ch+1's partials are in flight while chunk ch is summed
+          // (slot order kept -> deterministic); [token][row] layout keeps every load 128 B per warp
+          constexpr int kMaxSlots = 2;  // prefetched slots; slots >= 2 (rare) are added unpipelined
+          const float* colbase = base + r;
+          float cur[kMaxSlots][16], nxt[kMaxSlots][16];
 #pragma unroll
-            for (int q = 0; q < kMaxSlots; ++q)
+          for (int q = 0; q < kMaxSlots; ++q)
 #pragma unroll
-              for (int j = 0; j < 16; ++j) cur[q][j] = q < nslot ? __ldcg(colbase + q * tile_elems + j * kBM) : 0.f;
-            for (int ch = 0; ch < nchunks; ++ch) {
-              if (rope && ch + 1 < nchunks) rope_load(p, ep, r, mt, (ch + 1) * 16, tvalid, s_pos, csn, snn);
-              if (ch + 1 < nchunks) {
-#pragma unroll
-                for (int q = 0; q < kMaxSlots; ++q)
-#pragma unroll
-                  for (int j = 0; j < 16; ++j)
-                    nxt[q][j] = q < nslot ? __ldcg(colbase + q * tile_elems + static_cast<size_t>((ch + 1) * 16 + j) * kBM)
-                                          : 0.f;
-              }
-              float v[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = cur[0][j] + cur[1][j];
-              for (int q = kMaxSlots; q < nslot; ++q) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                  v[j] += __ldcg(colbase + q * tile_elems + static_cast<size_t>(ch * 16 + j) * kBM);
-              }
+            for (int j = 0; j < 16; ++j) cur[q][j] = q < nslot ? __ldcg(colbase + q * tile_elems + j * kBM) : 0.f;
+          for (int ch = 0; ch < nchunks; ++ch) {
+            if (rope_mode && ch + 1 < nchunks) rope_load(ql.dd, ql.rope, half, (ch + 1) * 16, tvalid, s_pos, ep, csn, snn);
+            if (ch + 1 < nchunks) {
 #pragma unroll
               for (int q = 0; q < kMaxSlots; ++q)
 #pragma unroll
-                for (int j = 0; j < 16; ++j) cur[q][j] = nxt[q][j];
-              epilogue_chunk(p, ep, v, r, mt, nt, ch * 16, tvalid, xbuf, s_pos, s_slot, cs, sn);
-              if (rope) {
+                for (int j = 0; j < 16; ++j)
+                  nxt[q][j] = q < nslot ? __ldcg(colbase + q * tile_elems + static_cast<size_t>((ch + 1) * 16 + j) * kBM)
+                                        : 0.f;
+            }
+            float v[16];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                  cs[j] = csn[j];
-                  sn[j] = snn[j];
-                }
+            for (int j = 0; j < 16; ++j) v[j] = cur[0][j] + cur[1][j];
+            for (int q = kMaxSlots; q < nslot; ++q) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                v[j] += __ldcg(colbase + q * tile_elems + static_cast<size_t>(ch * 16 + j) * kBM);
+            }
+#pragma unroll
+            for (int q = 0; q < kMaxSlots; ++q)
+#pragma unroll
+              for (int j = 0; j < 16; ++j) cur[q][j] = nxt[q][j];
+            epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_slot, ql, cs, sn);
+            if (rope_mode) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                cs[j] = csn[j];
+                sn[j] = snn[j];
               }
             }
           }
         }
       }
+      if (ep.trace && blockIdx.x < 2 && et == 0 && seg < 64) ep.trace[blockIdx.x * 1024 + 576 + seg] = globaltimer_ns();
       ++seg;
     }
   }
@@ -531,7 +567,7 @@ uint32_t pow2_cols(int n) {
   return c;
 }
 
-size_t extra_smem(int bn) { return kBM * kXPitch * 4 + 2 * static_cast<size_t>(bn) * 4 + 3 * 8 * 8 + 64 + 64; }
+size_t extra_smem(int bn) { return 4 * kStageFloats * 4 + 2 * static_cast<size_t>(bn) * 4 + 3 * 8 * 8 + 64 + 64; }
 
 }  // namespace
 

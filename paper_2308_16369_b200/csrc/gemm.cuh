@@ -12,7 +12,7 @@ enum EpiMode : int {
   EPI_STORE_BF16 = 0,  // out[t, m] = bf16(acc)
   EPI_STORE_F32 = 1,   // out[t, m] = acc (fp32)
   EPI_ADD_F32 = 2,     // out[t, m] += acc (fp32 residual stream, fused residual add)
-  EPI_SILU_MUL = 3,    // gate/up interleaved in 64-row blocks: out[t, f] = bf16(silu(g) * u)
+  EPI_SILU_MUL = 3,    // gate/up interleaved in 16-row blocks: out[t, f] = bf16(silu(g) * u)
   EPI_GELU = 4,        // out[t, m] = bf16(gelu_tanh(acc))
   EPI_QKV_ROPE = 5,    // RoPE(q,k) at pos[t]; q -> out; k,v -> paged KV cache at slot[t]
 };
@@ -37,7 +37,7 @@ struct EpiParams {
   int* counters = nullptr;
   // debug: globaltimer stamps of the first CTA pair (producer issue / MMA full-wake / epilogue wake)
   unsigned long long* trace = nullptr;
-  int dbg = 0;  // debug: bit0 skip X loads, bit1 skip W loads (timing experiments only; results invalid)
+  int dbg = 0;  // debug: bit0 skip X loads, bit1 skip W loads, bit2 skip whole-tile epilogue stores (timing experiments only; results invalid)
 };
 
 struct GemmPlan {

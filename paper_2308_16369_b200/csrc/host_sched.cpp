@@ -178,17 +178,21 @@ bool shard_map(int n_layers, int hidden, int n_heads, int n_kv_heads, int head_d
     double sig = s_in;
     switch (tensor) {
       case 0: {  // [q_r ; k_r ; v_r]: the rank's heads of the logical Wq, Wk, Wv
-        long long lrow;
+        // inside each head, packed row 32j + l (l < 16) is dim 16j + l and row 32j + 16 + l is its
+        // rotate-half partner hd/2 + 16j + l (gemm.cu: RoPE is a warp-local shuffle)
+        int rr = r;
         if (r < q_dim_l) {
           kind = kWQ;
-          lrow = static_cast<long long>(rank) * q_dim_l + r;
         } else if (r < q_dim_l + kv_dim_l) {
           kind = kWK;
-          lrow = static_cast<long long>(rank) * kv_dim_l + (r - q_dim_l);
+          rr = r - q_dim_l;
         } else {
           kind = kWV;
-          lrow = static_cast<long long>(rank) * kv_dim_l + (r - q_dim_l - kv_dim_l);
+          rr = r - q_dim_l - kv_dim_l;
         }
+        const int head = rr / hd, pr = rr % hd, slab = pr / 32, l = pr % 32;
+        const int d = (l < 16 ? 0 : hd / 2) + 16 * slab + (l % 16);
+        const long long lrow = static_cast<long long>(rank) * (kind == kWQ ? q_dim_l : kv_dim_l) + head * hd + d;
         b = lrow * H;
         break;
       }
@@ -197,13 +201,13 @@ bool shard_map(int n_layers, int hidden, int n_heads, int n_kv_heads, int head_d
         sig = s_o;
         b = static_cast<long long>(r) * n_heads * hd + static_cast<long long>(rank) * q_dim_l;
         break;
-      case 2: {  // gate||up interleaved in 64-row blocks (SwiGLU) or W1 (GELU)
+      case 2: {  // gate||up interleaved in 16-row blocks (SwiGLU) or W1 (GELU)
         long long fl = r;
         kind = kWG;
         if (ffn_kind == 0) {
-          const int blk = r / 128, w2 = r % 128;
-          kind = w2 < 64 ? kWG : kWU;
-          fl = static_cast<long long>(blk) * 64 + (w2 % 64);
+          const int blk = r / 32, w2 = r % 32;
+          kind = w2 < 16 ? kWG : kWU;
+          fl = static_cast<long long>(blk) * 16 + (w2 % 16);
         }
         b = (static_cast<long long>(rank) * h2_l + fl) * H;
         break;

@@ -86,7 +86,7 @@ class Scheduler {
 // Megatron tensor-parallel shard of one packed weight (§2.3): for every row r of the
 // rank-local packed tensor, the generator tensor id tau[r], fp32 scale[r] and the flat index base[r]
 // of element (r, 0) in the LOGICAL tensor (element (r, c) is base[r] + c).  tensor: 0 qkv
-// (column-parallel [q_r; k_r; v_r]), 1 o (row-parallel), 2 gate||up (column-parallel, 64-row
+// (column-parallel [q_r; k_r; v_r]), 1 o (row-parallel), 2 gate||up (column-parallel, 16-row
 // interleave) / W1, 3 down (row-parallel), 16 embedding (replicated), 18 LM head (vocab-parallel).
 // Host-only; returns false on a bad tensor id.
 struct ShardDims {

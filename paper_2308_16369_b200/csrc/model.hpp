@@ -33,7 +33,7 @@ struct Status {
 struct LayerWeights {
   __nv_bfloat16* qkv = nullptr;   // [(nq_l + 2 nkv_l) hd][H]
   __nv_bfloat16* o = nullptr;     // [H][nq_l hd]
-  __nv_bfloat16* gu = nullptr;    // [2 H2_l][H] gate/up interleaved in 64-row blocks (SwiGLU) | [H2_l][H] (GELU)
+  __nv_bfloat16* gu = nullptr;    // [2 H2_l][H] gate/up interleaved in 16-row blocks (SwiGLU) | [H2_l][H] (GELU)
   __nv_bfloat16* down = nullptr;  // [H][H2_l]
   __nv_bfloat16* g1 = nullptr;    // [H]
   __nv_bfloat16* g2 = nullptr;    // [H]

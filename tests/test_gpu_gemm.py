@@ -59,11 +59,11 @@ def test_gemm_exact_bf16_out_and_residual_add(S, M, N, K, splits):
 
 
 def test_gemm_silu_mul_interleaved(S):
-    M, N, K = 512, 40, 256   # 4 tiles: rows [128i, 128i+64) gate, [128i+64, 128i+128) up
+    M, N, K = 512, 40, 256   # rows [32i, 32i+16) gate of features [16i, 16i+16), [32i+16, 32i+32) their up
     g = torch.Generator().manual_seed(3)
     W = (torch.randn(M, K, generator=g) / 16).to(torch.bfloat16)
     X = torch.randn(N, K, generator=g).to(torch.bfloat16)
-    acc = (X.double() @ W.double().T).reshape(N, M // 128, 2, 64)
+    acc = (X.double() @ W.double().T).reshape(N, M // 32, 2, 16)
     gate, up = acc[:, :, 0, :], acc[:, :, 1, :]
     ref = (gate / (1 + torch.exp(-gate)) * up).reshape(N, M // 2)
     out = torch.empty((N, M // 2), device="cuda", dtype=torch.bfloat16)

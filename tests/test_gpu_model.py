@@ -59,14 +59,17 @@ def test_device_weights_bit_exact(S):
     m = S.Model(S.config_from(cfg, 16), seed=11)
     H, hd = cfg.hidden, cfg.head_dim
     for l in range(cfg.n_layers):
-        qkv = m.weight(l, 0, 0, (cfg.q_dim + 2 * cfg.kv_dim) * H).reshape(-1, H)
+        qkv = m.weight(l, 0, 0, (cfg.q_dim + 2 * cfg.kv_dim) * H).reshape(-1, hd, H)
         ref = np.concatenate([synth.layer_tensor_bits(cfg, 11, l, k) for k in (synth.WQ, synth.WK, synth.WV)])
-        assert np.array_equal(qkv, ref)
+        # packed order inside a head: slab j = dims [16j, 16j+16) then [hd/2 + 16j, hd/2 + 16j + 16)
+        perm = np.concatenate([np.r_[16 * j:16 * j + 16, hd // 2 + 16 * j:hd // 2 + 16 * j + 16] for j in range(hd // 32)])
+        assert sorted(perm.tolist()) == list(range(hd))
+        assert np.array_equal(qkv, ref.reshape(-1, hd, H)[:, perm])
         assert np.array_equal(m.weight(l, 1, 0, H * cfg.q_dim).reshape(H, -1), synth.layer_tensor_bits(cfg, 11, l, synth.WO))
-        gu = m.weight(l, 2, 0, 2 * cfg.ffn_hidden * H).reshape(-1, 128, H)
-        g = synth.layer_tensor_bits(cfg, 11, l, synth.WG).reshape(-1, 64, H)
-        u = synth.layer_tensor_bits(cfg, 11, l, synth.WU).reshape(-1, 64, H)
-        assert np.array_equal(gu[:, :64], g) and np.array_equal(gu[:, 64:], u)
+        gu = m.weight(l, 2, 0, 2 * cfg.ffn_hidden * H).reshape(-1, 32, H)
+        g = synth.layer_tensor_bits(cfg, 11, l, synth.WG).reshape(-1, 16, H)
+        u = synth.layer_tensor_bits(cfg, 11, l, synth.WU).reshape(-1, 16, H)
+        assert np.array_equal(gu[:, :16], g) and np.array_equal(gu[:, 16:], u)
         assert np.array_equal(m.weight(l, 3, 0, H * cfg.ffn_hidden).reshape(H, -1), synth.layer_tensor_bits(cfg, 11, l, synth.WD))
         assert np.array_equal(m.weight(l, 4, 0, H), synth.layer_tensor_bits(cfg, 11, l, synth.G1))
         assert np.array_equal(m.weight(l, 5, 0, H), synth.layer_tensor_bits(cfg, 11, l, synth.G2))

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(160)
   const uint32_t half_bytes = static_cast<uint32_t>(bs) * 128;       // one 64-col box of a block
   const uint32_t blk_bytes = half_bytes * NBOX;                       // K (or V) block
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(S) * 2 * blk_bytes);
   uint64_t* empty = full + S;
   if (tid == 0) {

@@ -405,6 +405,13 @@ int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   GemmPlan pl = plan_gemm(M, N, K, sms, ws_floats, force_splits, mode == EPI_ADD_F32);
+  if (const char* st_env = getenv("SARATHI_GEMM_STAGES")) {  // timing experiments: fewer ring stages
+    const int want = atoi(st_env);
+    if (want >= 2 && want < pl.stages) {
+      pl.smem -= static_cast<size_t>(pl.stages - want) * (16384 + static_cast<size_t>(pl.bn / 2) * 128);
+      pl.stages = want;
+    }
+  }
   // pack W into the library's tile-major layout (the layout init_model generates weights in)
   static __nv_bfloat16* wp = nullptr;
   static size_t wp_elems = 0;
@@ -438,20 +445,8 @@ int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t 
   }
   const cudaError_t e = launch_gemm(mw, mx, pl, ep, st);
   if (tracing) {
-    unsigned long long h[4096];
     cudaStreamSynchronize(st);
-    cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
-    const unsigned long long t0 = h[0];
-    fprintf(stderr, "gemm trace M=%d N=%d K=%d pairs=%d stages=%d units/pair~%lld\n", M, N, K, pl.ctas, pl.stages,
-            pl.units / pl.ctas);
-    for (int i = 0; i < 256 && h[i]; ++i)
-      fprintf(stderr, "u%3d issue0 %8.3f issue1 %8.3f full0 %8.3f full1(relay) %8.3f mma %8.3f us\n", i,
-              (h[i] - t0) * 1e-3, h[1024 + i] ? (h[1024 + i] - t0) * 1e-3 : -1.0,
-              h[2048 + i] ? (h[2048 + i] - t0) * 1e-3 : -1.0, h[1280 + i] ? (h[1280 + i] - t0) * 1e-3 : -1.0,
-              h[256 + i] ? (h[256 + i] - t0) * 1e-3 : -1.0);
-    for (int sgm = 0; sgm < 64 && h[512 + sgm]; ++sgm)
-      fprintf(stderr, "seg %d epilogue wake %8.3f us  done %8.3f us\n", sgm, (h[512 + sgm] - t0) * 1e-3,
-              h[576 + sgm] ? (h[576 + sgm] - t0) * 1e-3 : -1.0);
+    dump_gemm_trace(trace, pl);
   }
   if (e != cudaSuccess) return fail(SARATHI_ECUDA, std::string("op_gemm: ") + cudaGetErrorString(e));
   return SARATHI_OK;

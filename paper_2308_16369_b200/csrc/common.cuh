@@ -225,6 +225,16 @@ SARATHI_DEVICE void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
 
 SARATHI_DEVICE void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
+// wait::ld that also "defines" r: the registers of an in-flight tcgen05.ld must not be read (or
+// copied) by compiled code before the wait, so they are tied to it as read-write operands.
+SARATHI_DEVICE void tmem_ld_wait_regs(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+}
+
 // UMMA shared-memory matrix descriptor, K-major operand, 128-byte swizzle:
 //   start address >> 4 in [0,14), LBO (ignored for swizzled K-major, 1) in [16,30),
 //   SBO = 1024 B (8 rows x 128 B) >> 4 in [32,46), version 1 in [46,48), layout 2 (SW128) in [61,64).

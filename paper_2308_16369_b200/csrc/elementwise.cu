@@ -175,8 +175,12 @@ cudaError_t launch_rmsnorm(float* h, const __nv_bfloat16* add, const __nv_bfloat
                            const int* rows, int R, int H, float eps, cudaStream_t st) {
   if (R == 0) return cudaSuccess;
   if (H % 4) return cudaErrorInvalidValue;
+  // one CTA per row, sized so that every row of a batch (T <= 512) is resident in ONE wave
+  // (a second partial wave doubles the latency of this latency-bound kernel)
   if (H <= 256 * 4 * 2) {
     rmsnorm_kernel<256, 2><<<R, 256, 0, st>>>(h, add, g, out, rows, H, eps);
+  } else if (H <= 256 * 4 * 5) {
+    rmsnorm_kernel<256, 5><<<R, 256, 0, st>>>(h, add, g, out, rows, H, eps);
   } else if (H <= 512 * 4 * 8) {
     rmsnorm_kernel<512, 8><<<R, 512, 0, st>>>(h, add, g, out, rows, H, eps);
   } else {

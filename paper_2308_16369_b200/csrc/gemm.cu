@@ -13,12 +13,13 @@
 // the number of 128-row tiles (QKV 120, O 40, gate/up 216, down 40, LM head 250 at LLaMA-13B).
 // A tile covered by several CTAs is reduced deterministically: each contributor writes an fp32
 // partial into its slot, the last to arrive (atomic counter) sums the slots in order and runs the
-// fused epilogue.  Warp roles (192 threads):
+// fused epilogue.  Warp roles (320 threads):
 //   warp 0      TMA producer: W tile [128 x 64] (evict_first) + X tile [bn x 64] (evict_last),
 //               128B swizzle, S-stage smem ring (full/empty mbarriers), runs across segments
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; tcgen05.commit frees stages and
 //               signals the epilogue per segment; TMEM double-buffered when bn <= 256
-//   warps 2..5  epilogue straight from TMEM (tcgen05.ld 32x32b.x16): residual add, SiLU*up,
+//   warps 2..9  epilogue straight from TMEM (tcgen05.ld 32x32b.x16; two warps per lane quarter,
+//               alternate 16-token chunks): residual add, SiLU*up,
 //               GELU, RoPE + paged KV append, bf16/fp32 stores, or the stream-K partial
 #include "common.cuh"
 #include "gemm.cuh"
@@ -34,7 +35,8 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;               // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+constexpr int kEpiThreads = 256;
 constexpr int kWRowsPerTile = 32;            // packed W viewed as rows of 256 elements (512 B)
 
 struct KParams {
@@ -54,10 +56,12 @@ struct KParams {
   uint32_t ring_bytes;
 };
 
-SARATHI_DEVICE float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+SARATHI_DEVICE float silu_f(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 SARATHI_DEVICE float gelu_tanh_f(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(k0 * (x + k1 * x * x * x)));  // |err| ~ 2^-11, below bf16 output ulp
+  return 0.5f * x * (1.0f + t);
 }
 
 SARATHI_DEVICE long long unit_begin(int c, const KParams& p) {
@@ -116,23 +120,21 @@ struct SegIter {
 // ---------------------------------------------------------------------------
 constexpr int kStageFloats = 16 * 32;  // per-warp transpose buffer (2 KB)
 
-SARATHI_DEVICE int qkv_dim_of_lane(int jw, uint32_t lane, int half) {
-  return (lane < 16 ? 0 : half) + 16 * jw + static_cast<int>(lane & 15);
-}
-
-// RoPE table values (cos, sin) of this lane's rotation index for the chunk's 16 tokens.
-SARATHI_DEVICE void rope_load(int dd, bool rope, int half, int c0, int tvalid, const int* s_pos, const EpiParams& ep,
-                              float (&cs)[16], float (&sn)[16]) {
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    cs[j] = 1.f;
-    sn[j] = 0.f;
-    if (rope && c0 + j < tvalid) {
-      const size_t ti = static_cast<size_t>(s_pos[c0 + j]) * half + dd;
-      cs[j] = __ldg(ep.rope_cos + ti);
-      sn[j] = __ldg(ep.rope_sin + ti);
-    }
-  }
+// RoPE angles are computed in registers (no table traffic: table loads from the epilogue cost an
+// L2/HBM round trip per 16-token chunk and dominated the QKV GEMM).  angle = pos * theta_i with
+// theta_i = base^(-2i/hd) held as an fp32 pair (hi + lo, from fp64 on the host), the product kept
+// exact with an FMA, reduced mod 2*pi by a 3-constant Cody-Waite step, then __sincosf on |r| <= pi
+// (abs error ~2^-21; angle error <= 2.3e-7 rad for pos <= 2e5, checked against fp64).
+SARATHI_DEVICE void rope_cos_sin(int pos, float th_hi, float th_lo, float& c, float& s) {
+  const float p = static_cast<float>(pos);
+  const float a_hi = p * th_hi;
+  const float a_lo = fmaf(p, th_hi, -a_hi) + p * th_lo;
+  const float k = rintf(a_hi * 0.15915494309189535f);  // round(a / 2pi)
+  float r = fmaf(-k, 6.28125f, a_hi);                   // 2pi = 6.28125 + 1.9353071795864769e-3 + ...
+  r = fmaf(-k, 1.9353071795864769e-3f, r);
+  r = fmaf(-k, 1.0253132e-11f, r);  // 2pi - 6.28125 - fp32(1.9353071795864769e-3)
+  r += a_lo;
+  __sincosf(r, &s, &c);
 }
 
 struct QkvLane {  // per-warp / per-lane constants of the fused QKV epilogue
@@ -140,6 +142,7 @@ struct QkvLane {  // per-warp / per-lane constants of the fused QKV epilogue
   int jw;         // warp slab within the head
   int dd;         // rotation index of this lane (dim within the half)
   bool rope;      // q or k head
+  float th_hi, th_lo;  // theta_dd = base^(-2 dd / hd) as hi + lo
 };
 
 SARATHI_DEVICE QkvLane qkv_lane(const EpiParams& ep, int mt, uint32_t q, uint32_t lane) {
@@ -150,6 +153,8 @@ SARATHI_DEVICE QkvLane qkv_lane(const EpiParams& ep, int mt, uint32_t q, uint32_
   o.jw = (row0 & (ep.head_dim - 1)) >> 5;
   o.dd = 16 * o.jw + static_cast<int>(lane & 15);
   o.rope = o.gh < ep.n_q_local + ep.n_kv_local;
+  o.th_hi = __ldg(ep.rope_theta + 2 * o.dd);
+  o.th_lo = __ldg(ep.rope_theta + 2 * o.dd + 1);
   return o;
 }
 
@@ -159,11 +164,11 @@ SARATHI_DEVICE void red_add_v4(float* addr, float4 v) {
 }
 
 SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[16], uint32_t q, uint32_t lane, int mt,
-                             int nt, int c0, int tvalid, float* sbuf, const int* s_slot, const QkvLane& ql,
-                             const float (&cs)[16], const float (&sn)[16]) {
+                             int nt, int c0, int tvalid, float* sbuf, const int* s_pos, const int* s_slot,
+                             const QkvLane& ql) {
   const int row0 = mt * kBM + static_cast<int>(q) * 32;  // first accumulator row of this warp
   const long long tb = static_cast<long long>(nt) * p.bn + c0;
-  const int nv = min(16, tvalid - c0);
+  const int nv = (ep.dbg & 8) ? 0 : min(16, tvalid - c0);  // dbg bit 3: no global stores
   uint16_t* sb = reinterpret_cast<uint16_t*>(sbuf);
   switch (ep.mode) {
     case EPI_STORE_BF16:
@@ -211,11 +216,12 @@ SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[1
       // After one xor-16 exchange lanes 0-15 own tokens 0-7 and lanes 16-31 tokens 8-15.
       const bool lo = lane < 16;
       const int f0 = row0 >> 1;  // 16 output features per warp
+      float y[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) y[i] = __shfl_xor_sync(0xffffffffu, lo ? v[8 + i] : v[i], 16);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float send = lo ? v[8 + i] : v[i];
-        const float y = __shfl_xor_sync(0xffffffffu, send, 16);
-        const float gv = lo ? v[i] : y, uv = lo ? y : v[8 + i];
+        const float gv = lo ? v[i] : y[i], uv = lo ? y[i] : v[8 + i];
         sb[((lo ? 0 : 8) + i) * 16 + (lane & 15)] = __bfloat16_as_ushort(__float2bfloat16_rn(silu_f(gv) * uv));
       }
       __syncwarp();
@@ -229,12 +235,26 @@ SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[1
     case EPI_QKV_ROPE: {
       const int half = ep.head_dim >> 1;
       const bool lo = lane < 16;
+      if (ql.rope) {
+        // branch-free, 8 tokens per batch so the shuffles, position loads and sincos of different
+        // tokens overlap (a per-token dependent chain cost ~150 cycles x 16 per chunk)
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float xp = __shfl_xor_sync(0xffffffffu, v[j], 16);  // rotate-half partner
-        // x1 = low-half value, x2 = high-half value: y1 = x1 c - x2 s, y2 = x2 c + x1 s
-        const float y = ql.rope ? (lo ? v[j] * cs[j] - xp * sn[j] : v[j] * cs[j] + xp * sn[j]) : v[j];
-        sb[j * 32 + lane] = __bfloat16_as_ushort(__float2bfloat16_rn(y));
+        for (int j0 = 0; j0 < 16; j0 += 8) {
+          float xp[8], c[8], sn[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) xp[j] = __shfl_xor_sync(0xffffffffu, v[j0 + j], 16);  // rotate-half partner
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rope_cos_sin(s_pos[min(c0 + j0 + j, tvalid - 1)], ql.th_hi, ql.th_lo, c[j], sn[j]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            // x1 = low-half value, x2 = high-half value: y1 = x1 c - x2 s, y2 = x2 c + x1 s
+            const float y = lo ? v[j0 + j] * c[j] - xp[j] * sn[j] : v[j0 + j] * c[j] + xp[j] * sn[j];
+            sb[(j0 + j) * 32 + lane] = __bfloat16_as_ushort(__float2bfloat16_rn(y));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sb[j * 32 + lane] = __bfloat16_as_ushort(__float2bfloat16_rn(v[j]));
       }
       __syncwarp();
       if (row0 < p.M) {
@@ -247,7 +267,7 @@ SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[1
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
           const int tok = pass * 8 + static_cast<int>(lane >> 2);
-          if (tok >= nv) continue;
+          if (tok >= nv || ((ep.dbg & 16) && !isq)) continue;  // dbg bit 4: no K/V cache stores
           __nv_bfloat16* dst =
               isq ? static_cast<__nv_bfloat16*>(ep.out) + (tb + tok) * ep.ldo + (ql.gh << hd_shift) + d
                   : cache + (static_cast<size_t>(s_slot[c0 + tok] + kvh * ep.block_size) << hd_shift) + d;
@@ -266,14 +286,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_pair(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, const KParams p,
                    const EpiParams ep) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem =
-      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base derived by pointer arithmetic from the __shared__ array (not an integer
+  // round trip), so every pointer below stays in the shared address space (STS/LDS, not generic ST/LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t b_bytes = static_cast<uint32_t>(p.bn / 2) * kBK * 2;  // this CTA's half of the tokens
   const uint32_t stage_bytes = kABytes + b_bytes;
-  float* stage_buf = reinterpret_cast<float*>(smem + p.ring_bytes);    // [4 warps][16 x 32] transpose
-  int* s_pos = reinterpret_cast<int*>(stage_buf + 4 * kStageFloats);   // [bn]
+  float* stage_buf = reinterpret_cast<float*>(smem + p.ring_bytes);    // [8 warps][16 x 32] transpose
+  int* s_pos = reinterpret_cast<int*>(stage_buf + 8 * kStageFloats);   // [bn]
   int* s_slot = s_pos + p.bn;                                          // [bn]
-  uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_slot + p.bn) + 7) & ~uintptr_t(7));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_slot + ((p.bn + 1) & ~1));  // 8-B aligned (bn is a multiple of 16)
   uint64_t* full = bars;                // local: this CTA's W + X bytes landed
   uint64_t* pfull = full + p.stages;    // leader only: the peer's stage landed (relayed)
   uint64_t* empty = pfull + p.stages;
@@ -295,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty[b], 16);  // 8 epilogue warps x 2 CTAs
     }
     fence_barrier_init();
   }
@@ -391,16 +412,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---------------- Epilogue (warps 2..5 of both CTAs) ----------------
-    const int et = threadIdx.x - 64;                        // 0..127
+    // ---------------- Epilogue (warps 2..9 of both CTAs) ----------------
+    // two warps per TMEM lane quarter (warp & 3); warp half `eh` takes chunks eh, eh + 2, ...
+    const int et = threadIdx.x - 64;                        // 0..255
+    const int ew = static_cast<int>(warp) - 2;              // 0..7
+    const int eh = ew >> 2;
     const uint32_t quarter = warp & 3;                      // TMEM lane quarter of this warp
     const int r = static_cast<int>(quarter * 32 + lane);    // accumulator row within this CTA's half
-    float* sbuf = stage_buf + quarter * kStageFloats;       // this warp's transpose buffer
+    float* sbuf = stage_buf + ew * kStageFloats;            // this warp's transpose buffer
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
     int seg = 0;
     const size_t tile_elems = static_cast<size_t>(p.bn) * kBM;
     const bool rope_mode = ep.mode == EPI_QKV_ROPE;
-    const int half = ep.head_dim >> 1;
     SegIter it;
     it.init(p, pair);
     int tile, kb0, kb1;
@@ -420,14 +443,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive_cluster(tempty_leader + buf * 8);
       };
       if (rope_mode) {  // stage per-token metadata for the fused KV append
-        named_bar_sync(2, 128);
-        for (int t = et; t < tvalid; t += 128) {
+        named_bar_sync(2, kEpiThreads);
+        for (int t = et; t < tvalid; t += kEpiThreads) {
           s_pos[t] = __ldg(ep.pos + nt * p.bn + t);
           const int sl = __ldg(ep.slot + nt * p.bn + t);
           // paged-cache row of (slot, kv head 0): [block][n_kv][bs] -> (sl/bs)*n_kv*bs + sl%bs
           s_slot[t] = (sl / ep.block_size) * ep.n_kv_local * ep.block_size + sl % ep.block_size;
         }
-        named_bar_sync(2, 128);
+        named_bar_sync(2, kEpiThreads);
       }
       if (lane == 0) mbar_wait(&tfull[buf], use & 1);
       __syncwarp();
@@ -435,25 +458,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ep.trace && blockIdx.x < 2 && et == 0 && seg < 64) ep.trace[blockIdx.x * 1024 + 512 + seg] = globaltimer_ns();
       const uint32_t trow = tmem + buf * 256 + ((quarter * 32u) << 16);
       const int nchunks = (tvalid + 15) / 16;
-      float cs[16], sn[16], csn[16], snn[16];  // current / next chunk RoPE values (registers)
       if (direct) {
-        if (rope_mode) rope_load(ql.dd, ql.rope, half, 0, tvalid, s_pos, ep, cs, sn);
-        for (int ch = 0; ch < nchunks; ++ch) {
+        // software-pipelined TMEM drain: this warp's next chunk (ch + 2) is in flight while ch is emitted
+        if (eh >= nchunks) {
+          release_tmem();
+        } else {
           uint32_t raw[16];
-          tmem_ld_32x32b_x16(trow + ch * 16, raw);
-          tmem_ld_wait();
-          if (ch == nchunks - 1) release_tmem();
-          // prefetch the next chunk's RoPE table values; their latency overlaps this chunk
-          if (rope_mode && ch + 1 < nchunks) rope_load(ql.dd, ql.rope, half, (ch + 1) * 16, tvalid, s_pos, ep, csn, snn);
-          float v[16];
+          tmem_ld_32x32b_x16(trow + eh * 16, raw);
+          tmem_ld_wait_regs(raw);
+          if (eh + 2 >= nchunks) release_tmem();
+          for (int ch = eh; ch < nchunks; ch += 2) {
+            uint32_t nraw[16];
+            const bool more = ch + 2 < nchunks;
+            if (more) tmem_ld_32x32b_x16(trow + (ch + 2) * 16, nraw);
+            float v[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
-          if (!(ep.dbg & 4)) epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_slot, ql, cs, sn);
-          if (rope_mode) {
+            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
+            if (!(ep.dbg & 4))
+              epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, ql);
+            if (ep.trace && blockIdx.x < 2 && et == 0 && seg == 0 && ch < 64)
+              ep.trace[blockIdx.x * 1024 + 640 + ch] = globaltimer_ns();
+            if (more) {
+              tmem_ld_wait_regs(nraw);
+              if (ch + 4 >= nchunks) release_tmem();
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              cs[j] = csn[j];
-              sn[j] = snn[j];
+              for (int j = 0; j < 16; ++j) raw[j] = nraw[j];
             }
           }
         }
@@ -466,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int slot = pair - c_first;
         const size_t tile128 = static_cast<size_t>(mt) * p.n_tiles + nt;
         float* wsp = ep.ws + (tile128 * p.max_slots + slot) * tile_elems;
-        for (int ch = 0; ch < nchunks; ++ch) {
+        for (int ch = eh; ch < nchunks; ch += 2) {
           uint32_t raw[16];
           tmem_ld_32x32b_x16(trow + ch * 16, raw);
           tmem_ld_wait();
@@ -476,18 +505,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         release_tmem();
         __threadfence();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiThreads);
         if (et == 0) {
           int* ctr = ep.counters + tile128;
           const int old = atomicAdd(ctr, 1);
           s_last = (old == nslot - 1);
           if (s_last) *ctr = 0;  // re-arm for the next launch
         }
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiThreads);
         if (s_last) {
           __threadfence();
           const float* base = ep.ws + tile128 * p.max_slots * tile_elems;
-          if (rope_mode) rope_load(ql.dd, ql.rope, half, 0, tvalid, s_pos, ep, cs, sn);
           // software-pipelined reduction: chunk ch+1's partials are in flight while chunk ch is summed
           // (slot order kept -> deterministic); [token][row] layout keeps every load 128 B per warp
           constexpr int kMaxSlots = 2;  // prefetched slots; slots >= 2 (rare) are added unpipelined
@@ -496,15 +524,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int q = 0; q < kMaxSlots; ++q)
 #pragma unroll
-            for (int j = 0; j < 16; ++j) cur[q][j] = q < nslot ? __ldcg(colbase + q * tile_elems + j * kBM) : 0.f;
-          for (int ch = 0; ch < nchunks; ++ch) {
-            if (rope_mode && ch + 1 < nchunks) rope_load(ql.dd, ql.rope, half, (ch + 1) * 16, tvalid, s_pos, ep, csn, snn);
-            if (ch + 1 < nchunks) {
+            for (int j = 0; j < 16; ++j)
+              cur[q][j] = q < nslot && eh < nchunks ? __ldcg(colbase + q * tile_elems + static_cast<size_t>(eh * 16 + j) * kBM) : 0.f;
+          for (int ch = eh; ch < nchunks; ch += 2) {
+            if (ch + 2 < nchunks) {
 #pragma unroll
               for (int q = 0; q < kMaxSlots; ++q)
 #pragma unroll
                 for (int j = 0; j < 16; ++j)
-                  nxt[q][j] = q < nslot ? __ldcg(colbase + q * tile_elems + static_cast<size_t>((ch + 1) * 16 + j) * kBM)
+                  nxt[q][j] = q < nslot ? __ldcg(colbase + q * tile_elems + static_cast<size_t>((ch + 2) * 16 + j) * kBM)
                                         : 0.f;
             }
             float v[16];
@@ -519,14 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int q = 0; q < kMaxSlots; ++q)
 #pragma unroll
               for (int j = 0; j < 16; ++j) cur[q][j] = nxt[q][j];
-            epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_slot, ql, cs, sn);
-            if (rope_mode) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                cs[j] = csn[j];
-                sn[j] = snn[j];
-              }
-            }
+            epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, ql);
           }
         }
       }
@@ -567,7 +588,7 @@ uint32_t pow2_cols(int n) {
   return c;
 }
 
-size_t extra_smem(int bn) { return 4 * kStageFloats * 4 + 2 * static_cast<size_t>(bn) * 4 + 3 * 8 * 8 + 64 + 64; }
+size_t extra_smem(int bn) { return 8 * kStageFloats * 4 + 2 * static_cast<size_t>(bn) * 4 + 3 * 8 * 8 + 64 + 64; }
 
 }  // namespace
 
@@ -690,6 +711,21 @@ bool make_tmap_weight(CUtensorMap* map, const void* w, int M, int K) {
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+void dump_gemm_trace(const unsigned long long* trace_dev, const GemmPlan& pl) {
+  static unsigned long long h[4096];
+  cudaMemcpy(h, trace_dev, sizeof(h), cudaMemcpyDeviceToHost);
+  const unsigned long long t0 = h[0];
+  fprintf(stderr, "gemm trace M=%d N=%d K=%d pairs=%d stages=%d units/pair~%lld\n", pl.M, pl.N, pl.K, pl.ctas, pl.stages,
+          pl.units / std::max(1, pl.ctas));
+  for (int i = 0; i < 256 && h[i]; ++i)
+    fprintf(stderr, "u%3d issue0 %8.3f issue1 %8.3f mma %8.3f us\n", i, (h[i] - t0) * 1e-3,
+            h[1024 + i] ? (h[1024 + i] - t0) * 1e-3 : -1.0, h[256 + i] ? (h[256 + i] - t0) * 1e-3 : -1.0);
+  for (int ch = 0; ch < 64 && h[640 + ch]; ++ch) fprintf(stderr, "seg0 chunk %d emitted %8.3f us\n", ch, (h[640 + ch] - t0) * 1e-3);
+  for (int sgm = 0; sgm < 64 && h[512 + sgm]; ++sgm)
+    fprintf(stderr, "seg %d epilogue wake %8.3f us  done %8.3f us\n", sgm, (h[512 + sgm] - t0) * 1e-3,
+            h[576 + sgm] ? (h[576 + sgm] - t0) * 1e-3 : -1.0);
 }
 
 cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const GemmPlan& pl, const EpiParams& ep,

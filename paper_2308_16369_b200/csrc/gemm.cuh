@@ -24,8 +24,7 @@ struct EpiParams {
   // EPI_QKV_ROPE
   const int* pos = nullptr;
   const int* slot = nullptr;
-  const float* rope_cos = nullptr;  // [max_pos][head_dim/2]
-  const float* rope_sin = nullptr;
+  const float* rope_theta = nullptr;  // [head_dim/2][2]: theta_i = base^(-2i/hd) as fp32 hi, lo
   void* kcache = nullptr;  // bf16 [num_blocks][n_kv_local][block_size][head_dim]
   void* vcache = nullptr;
   int head_dim = 128;
@@ -78,5 +77,8 @@ bool make_tmap_weight(CUtensorMap* map, const void* w, int M, int K);
 // mapW: make_tmap_weight map; mapX: activation [N][K] map (make_tmap_bf16, box rows plan.box_rows).
 cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const GemmPlan& plan, const EpiParams& ep,
                         cudaStream_t stream);
+
+// Debug: prints the globaltimer trace (EpiParams.trace, 4096 u64) of the first CTA pair to stderr.
+void dump_gemm_trace(const unsigned long long* trace_dev, const GemmPlan& plan);
 
 }  // namespace sarathi

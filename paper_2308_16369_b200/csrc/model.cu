@@ -13,6 +13,8 @@
 // then logits = RMSNorm(h[rows]; g_f) Wlm^T for the R requested rows (vocab-parallel under TP).
 #include "model.hpp"
 
+#include <cstdlib>
+
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -231,18 +233,14 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   // RoPE tables (fp64 on host -> fp32), reading O-7
   {
     const int half = hd / 2;
-    std::vector<float> cs(static_cast<size_t>(c.max_seq_len) * half), sn(cs.size());
-    for (int p = 0; p < c.max_seq_len; ++p)
-      for (int i = 0; i < half; ++i) {
-        const double inv = std::pow(static_cast<double>(c.rope_base), -(2.0 * i) / hd);
-        const double ang = p * inv;
-        cs[static_cast<size_t>(p) * half + i] = static_cast<float>(std::cos(ang));
-        sn[static_cast<size_t>(p) * half + i] = static_cast<float>(std::sin(ang));
-      }
-    SRET(dalloc(&rope_cos, cs.size()));
-    SRET(dalloc(&rope_sin, sn.size()));
-    SRET(check(cudaMemcpy(rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice), "H2D rope"));
-    SRET(check(cudaMemcpy(rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice), "H2D rope"));
+    std::vector<float> th(static_cast<size_t>(half) * 2);
+    for (int i = 0; i < half; ++i) {
+      const double inv = std::pow(static_cast<double>(c.rope_base), -(2.0 * i) / hd);
+      th[2 * i] = static_cast<float>(inv);
+      th[2 * i + 1] = static_cast<float>(inv - static_cast<double>(th[2 * i]));
+    }
+    SRET(dalloc(&rope_theta, th.size()));
+    SRET(check(cudaMemcpy(rope_theta, th.data(), th.size() * 4, cudaMemcpyHostToDevice), "H2D rope"));
   }
 
   // activations / workspaces
@@ -320,6 +318,23 @@ Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, 
   ep.ws = gemm_ws;
   ep.counters = gemm_counters;
   ++launches;
+  // debug: SARATHI_MODEL_TRACE=<epilogue mode>:<N> traces the first such launch with N tokens
+  static const char* trace_env = getenv("SARATHI_MODEL_TRACE");
+  static bool traced = false;
+  const char* colon = trace_env ? strchr(trace_env, ':') : nullptr;
+  if (colon && !traced && atoi(trace_env) == ep.mode && atoi(colon + 1) == N) {
+    traced = true;
+    unsigned long long* tr = nullptr;
+    cudaMalloc(&tr, 4096 * 8);
+    cudaMemsetAsync(tr, 0, 4096 * 8, stream);
+    ep.trace = tr;
+    if (const char* d = getenv("SARATHI_GEMM_DBG")) ep.dbg = atoi(d);  // traced launch only
+    const Status st = check(launch_gemm(mw, xi->second, pl, ep, stream), "gemm launch");
+    cudaStreamSynchronize(stream);
+    dump_gemm_trace(tr, pl);
+    cudaFree(tr);
+    return st;
+  }
   return check(launch_gemm(mw, xi->second, pl, ep, stream), "gemm launch");
 }
 
@@ -479,8 +494,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     e.ldo = q_dim_l;
     e.pos = d_pos;
     e.slot = d_slot;
-    e.rope_cos = rope_cos;
-    e.rope_sin = rope_sin;
+    e.rope_theta = rope_theta;
     e.kcache = kpool[l];
     e.vcache = vpool[l];
     e.head_dim = hd;

@@ -56,8 +56,7 @@ struct Model {
   std::vector<LayerWeights> layers;
   std::vector<void*> allocations;
   // rope tables [max_seq_len][hd/2]
-  float* rope_cos = nullptr;
-  float* rope_sin = nullptr;
+  float* rope_theta = nullptr;  // [hd/2][2] RoPE frequencies (fp64 -> fp32 hi + lo)
   // KV cache
   bool kv_ready = false;
   int64_t num_blocks = 0;

@@ -140,6 +140,14 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   if (q_dim_l % 64) return Status::err(SARATHI_EINVAL, "init_model: local q dim must be a multiple of 64");
   if (qkv_rows % 128 && hd == 128) return Status::err(SARATHI_EINVAL, "init_model: qkv rows not tile aligned");
   SRET(check(cudaSetDevice(device), "cudaSetDevice"));
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    const char* pr = getenv("SARATHI_AUX_PRIORITY");  // experiment: "low" | "high" (default)
+    SRET(check(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, pr && pr[0] == 'l' ? lo : hi), "aux stream"));
+    SRET(check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event"));
+    SRET(check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event"));
+  }
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device);
 
   if (world > 1) {
@@ -338,7 +346,7 @@ Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, 
   return check(launch_gemm(mw, xi->second, pl, ep, stream), "gemm launch");
 }
 
-cudaEvent_t Model::op_begin() {
+cudaEvent_t Model::op_begin(cudaStream_t s) {
   if (!profiling) return nullptr;
   if (ev_used + 2 > ev_pool.size()) {
     for (int i = 0; i < 256; ++i) {
@@ -348,14 +356,14 @@ cudaEvent_t Model::op_begin() {
     }
   }
   cudaEvent_t b = ev_pool[ev_used++];
-  cudaEventRecord(b, stream);
+  cudaEventRecord(b, s ? s : stream);
   return b;
 }
 
-void Model::op_end(int op, cudaEvent_t b) {
+void Model::op_end(int op, cudaEvent_t b, cudaStream_t s) {
   if (!b) return;
   cudaEvent_t e = ev_pool[ev_used++];
-  cudaEventRecord(e, stream);
+  cudaEventRecord(e, s ? s : stream);
   pending_ops.emplace_back(op, b, e);
 }
 
@@ -521,10 +529,17 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       pa.scale = scale;
       pa.out = o;
       pa.out_ld = q_dim_l;
-      ob = op_begin();
-      SRET(check(launch_prefill_attention(pa, stream), "prefill attention"));
-      op_end(SARATHI_OP_PREFILL_ATTN, ob);
+      // with decodes in the batch, the chunk's attention overlaps the decode attention (side stream)
+      cudaStream_t ps = d > 0 ? aux : stream;
+      if (d > 0) {
+        SRET(check(cudaEventRecord(ev_fork, stream), "fork"));
+        SRET(check(cudaStreamWaitEvent(aux, ev_fork, 0), "fork"));
+      }
+      ob = op_begin(ps);
+      SRET(check(launch_prefill_attention(pa, ps), "prefill attention"));
+      op_end(SARATHI_OP_PREFILL_ATTN, ob, ps);
       ++launches;
+      if (d > 0) SRET(check(cudaEventRecord(ev_join, aux), "join"));
     }
     if (d > 0) {
       DecodeAttnArgs da;
@@ -564,6 +579,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       SRET(check(launch_decode_attention(da, kmap[l], vmap[l], stream), "decode attention"));
       op_end(SARATHI_OP_DECODE_ATTN, ob);
       launches += da.splits > 1 ? 2 : 1;
+      if (p > 0) SRET(check(cudaStreamWaitEvent(stream, ev_join, 0), "join"));
     }
     // O-projection (postproj) + residual / TP all-reduce
     EpiParams eo;
@@ -671,6 +687,12 @@ void Model::destroy() {
   }
   for (void* p : allocations) cudaFree(p);
   allocations.clear();
+  if (aux) cudaStreamSynchronize(aux);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (aux) cudaStreamDestroy(aux);
+  aux = nullptr;
+  ev_fork = ev_join = nullptr;
   for (int i = 0; i < 2; ++i) {
     if (meta_host_buf[i]) cudaFreeHost(meta_host_buf[i]);
     if (meta_ev[i]) cudaEventDestroy(meta_ev[i]);

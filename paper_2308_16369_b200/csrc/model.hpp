@@ -44,6 +44,10 @@ struct Model {
   sarathi_model_config cfg{};
   int rank = 0, world = 1, device = 0;
   cudaStream_t stream = nullptr;
+  // side stream: the chunked-prefill attention runs concurrently with the (HBM-bound) decode
+  // attention of the same layer (fork after the QKV GEMM, join before the O GEMM)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int num_sms = 148;
   uint64_t seed = 0;
   // sharded sizes
@@ -55,7 +59,6 @@ struct Model {
   CUtensorMap m_lm;
   std::vector<LayerWeights> layers;
   std::vector<void*> allocations;
-  // rope tables [max_seq_len][hd/2]
   float* rope_theta = nullptr;  // [hd/2][2] RoPE frequencies (fp64 -> fp32 hi + lo)
   // KV cache
   bool kv_ready = false;
@@ -102,8 +105,8 @@ struct Model {
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending_ops;
   double op_ms[SARATHI_NUM_OPS] = {0};
   int64_t op_count[SARATHI_NUM_OPS] = {0};
-  cudaEvent_t op_begin();
-  void op_end(int op, cudaEvent_t b);
+  cudaEvent_t op_begin(cudaStream_t s = nullptr);
+  void op_end(int op, cudaEvent_t b, cudaStream_t s = nullptr);
   Status collect_op_times();
 
   Status init(const sarathi_model_config& c, const sarathi_dist& d, uint64_t seed);

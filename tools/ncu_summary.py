@@ -1,6 +1,10 @@
 """Summarise an ncu report (.ncu-rep) into a short text file for profiles/.
 
     python tools/ncu_summary.py gpurun_out/prof.ncu-rep [--top 12] > profiles/rNN_name.txt
+    [--traffic-json profiles/ncu_traffic.json --workload W --key decode_attention --match decode_attn]
+
+--traffic-json records dram__bytes_read.sum + dram__bytes_write.sum per launch (mean over the
+launches whose name contains --match) for bench.py's roofline `traffic` field.
 
 Per kernel: duration, DRAM bytes read/written (traffic), DRAM / L2 / SM / tensor-pipe utilisation,
 registers, achieved occupancy; then the hottest SASS lines by warp-stall samples.
@@ -8,6 +12,8 @@ registers, achieved occupancy; then the hottest SASS lines by warp-stall samples
 import argparse
 import csv
 import io
+import json
+import os
 import subprocess
 
 METRICS = [
@@ -35,8 +41,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("report")
     ap.add_argument("--top", type=int, default=12)
+    ap.add_argument("--traffic-json")
+    ap.add_argument("--workload")
+    ap.add_argument("--key")
+    ap.add_argument("--match")
     a = ap.parse_args()
-    raw = list(csv.reader(io.StringIO(ncu(["-i", a.report, "--page", "raw", "--csv"]))))
+    raw = list(csv.reader(io.StringIO(ncu(["-i", a.report, "--page", "raw", "--csv", "--print-units", "base"]))))
     hdr, units = raw[0], raw[1]
     name_i = hdr.index("Kernel Name")
     print(f"# ncu summary of {a.report}")
@@ -46,6 +56,14 @@ def main():
             if key in hdr:
                 i = hdr.index(key)
                 print(f"  {label:16s} {row[i]:>14s} {units[i]}")
+    if a.traffic_json:
+        rd, wr = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+        vals = [float(r[rd].replace(",", "")) + float(r[wr].replace(",", "")) for r in raw[2:] if a.match in r[name_i]]
+        assert vals, f"no launch matching {a.match}"
+        db = json.load(open(a.traffic_json)) if os.path.exists(a.traffic_json) else {}
+        db.setdefault(a.workload, {})[a.key] = {"dram_bytes_per_launch": round(sum(vals) / len(vals)),
+                                                "launches": len(vals), "source": os.path.basename(a.report)}
+        json.dump(db, open(a.traffic_json, "w"), indent=1)
     src = ncu(["-i", a.report, "--page", "source", "--csv", "--print-source", "sass"])
     blocks, cur = [], None
     for r in csv.reader(io.StringIO(src)):

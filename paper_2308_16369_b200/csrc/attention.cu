@@ -482,6 +482,291 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Chunked-prefill attention on the 5th-gen tensor cores (tcgen05 / TMEM / TMA).
+//   CTA = (128-query tile of the chunk, query head); 256 threads, query row r = TMEM lane r is
+//   owned by two threads (one per 64-key / hd/2 column half).  Per key tile t (128 keys = 128/bs paged blocks, TMA-loaded K-major SW128):
+//     S_t  = Q K_t^T        UMMA M=128, N=128, K=hd into TMEM (two S buffers: S_{t+1} is issued
+//                           before the softmax of S_t, so the tensor core overlaps the softmax)
+//     P_t  = exp2(S_t*c - m) bf16 -> smem (K-major SW128, the A operand of the next UMMA)
+//     O_t  = P_t V_t        UMMA M=128, N=hd, K=128 keys, B = V tile read MN-major (no transpose)
+//     O    = O * alpha + O_t  in registers (online softmax, fp32; reading O-9: key j <= s + i)
+//   Issue (TMA + UMMA) is warp 0, warp-uniform with one elected lane.
+// ---------------------------------------------------------------------------
+constexpr int kPBQ = 128;  // queries per CTA
+constexpr int kPBK = 128;  // keys per tile
+
+// MN-major SW128 UMMA smem descriptor: 64-element (128 B) rows along MN, MN atoms LBO apart,
+// 8-row K groups SBO apart (CuTe canonical ((8,n),(8,k)):((1,LBO),(8,SBO)) in 16-B units).
+SARATHI_DEVICE uint64_t make_desc_mn_sw128(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
+template <int HD>
+struct PtcSmem {
+  static constexpr uint32_t kQ = kPBQ * HD * 2;   // Q tile  [HD/64][128 rows][64] SW128
+  static constexpr uint32_t kKV = kPBK * HD * 2;  // K or V tile [HD/64][128 keys][64]
+  static constexpr uint32_t kP = kPBQ * kPBK * 2; // P [2][128 rows][64 keys]
+  static constexpr uint32_t kRed = 2 * kPBQ * 4;  // per-half row maxima / sums
+  static constexpr uint32_t kTotal = kQ + 4 * kKV + kP + kRed + 256 + 1024;  // + barriers + align slack
+};
+
+SARATHI_DEVICE float ex2_approx(float x) {  // 2^x, MUFU.EX2 (x = -inf -> 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 256 threads: warp w owns TMEM lane quarter (w & 3) -> query rows 32(w&3)..+31, and column half
+// ch = w >> 2 of every S tile (keys 64ch..64ch+63) and of O (dims (hd/2)ch..); the two halves of a
+// row exchange their maxima through shared memory once per tile.
+template <int HD>
+__global__ void __launch_bounds__(256, 1)
+    prefill_attn_tc(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
+                    const __grid_constant__ CUtensorMap mapV, const PrefillAttnArgs a) {
+  using L = PtcSmem<HD>;
+  constexpr int kHalves = HD / 64;
+  constexpr int kOC = HD / 2;  // O columns per column half
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + L::kQ;          // [2 buffers]
+  uint8_t* sV = sK + 2 * L::kKV;     // [2 buffers]
+  uint8_t* sP = sV + 2 * L::kKV;
+  float* red = reinterpret_cast<float*>(sP + L::kP);  // [2 halves][128 rows]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(red) + L::kRed);
+  uint64_t* q_full = bars;        // 1
+  uint64_t* k_full = bars + 1;    // [2]
+  uint64_t* v_full = bars + 3;    // [2]
+  uint64_t* s_done = bars + 5;    // [2]
+  uint64_t* o_done = bars + 7;    // 1
+  uint32_t* holder = reinterpret_cast<uint32_t*>(bars + 8);
+
+  const uint32_t warp = warp_id_uniform(), lane = lane_id();
+  const uint32_t quarter = warp & 3, chh = warp >> 2;
+  const int r = static_cast<int>(quarter * 32 + lane);  // query row within the tile == TMEM lane
+  const int qt = blockIdx.x, qh = blockIdx.y;
+  const int kvh = qh * a.n_kv_local / a.n_q_local;
+  const int q0 = qt * kPBQ;
+  const int s0 = a.start, p = a.p, bs = a.block_size;
+  const int kv_len = s0 + p;
+  const int key_end = s0 + min(q0 + kPBQ, p);  // keys this tile needs: [0, key_end)
+  const int ntiles = (key_end + kPBK - 1) / kPBK;
+  const int last_blk = (kv_len - 1) / bs;      // last block of the request holding valid keys
+  const bool tr0 = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+
+  if (tr0) a.trace[254] = globaltimer_ns();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *holder;
+  const uint32_t tS[2] = {tmem, tmem + 128};
+  const uint32_t tO = tmem + 256;
+
+  // K (or V) tile load: every paged block of the tile (indices past the request clamp to its last
+  // block, so every smem byte the UMMAs read is finite; those keys are masked).  K_t is free once
+  // S_t is done, V_t once PV_t is done, so they are refilled at different points.
+  auto load_tile = [&](int t, int buf, bool is_v) {
+    uint64_t* bar = is_v ? &v_full[buf] : &k_full[buf];
+    uint8_t* dst = (is_v ? sV : sK) + buf * L::kKV;
+    const CUtensorMap* map = is_v ? &mapV : &mapK;
+    mbar_arrive_expect_tx_warp(bar, kPBK * HD * 2);
+    for (int kb = 0; kb < kPBK; kb += bs) {
+      const int bi = min((t * kPBK + kb) / bs, last_blk);
+      const int row = (a.block_table[bi] * a.n_kv_local + kvh) * bs;
+#pragma unroll
+      for (int h = 0; h < kHalves; ++h) tma_load_2d_warp(dst + h * (kPBK * 128) + kb * 128, map, bar, h * 64, row);
+    }
+  };
+  const uint32_t idesc_s = make_idesc_bf16_f32(kPBQ, kPBK);
+  const uint32_t idesc_o = make_idesc_bf16_f32(kPBQ, HD) | (1u << 16);  // B (V) MN-major
+  auto issue_s = [&](int t) {  // S_t = Q K_t^T into tS[t & 1]
+    const int buf = t & 1;
+    mbar_wait(&k_full[buf], (t >> 1) & 1);
+    tc_fence_after();
+    const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + buf * L::kKV);
+#pragma unroll
+    for (int k = 0; k < HD / 16; ++k) {
+      const uint32_t off = (k >> 2) * (kPBQ * 128) + (k & 3) * 32;  // hd half, 32 B step in the row
+      umma_f16_ss_warp(tS[buf], make_desc_k_sw128(qa + off), make_desc_k_sw128(kb + (k >> 2) * (kPBK * 128) + (k & 3) * 32),
+                       idesc_s, k > 0 ? 1u : 0u);
+    }
+    umma_commit_warp(&s_done[buf]);
+  };
+
+  if (warp == 0) {
+    mbar_arrive_expect_tx_warp(q_full, L::kQ);
+#pragma unroll
+    for (int h = 0; h < kHalves; ++h)
+      tma_load_2d_warp(sQ + h * (kPBQ * 128), &mapQ, q_full, qh * HD + h * 64, a.q_row0 + q0);
+    load_tile(0, 0, false);
+    load_tile(0, 0, true);
+    if (ntiles > 1) {
+      load_tile(1, 1, false);
+      load_tile(1, 1, true);
+    }
+    mbar_wait(q_full, 0);
+    issue_s(0);
+  }
+
+  const float c2 = a.scale * kLog2e;
+  const int qpos = s0 + q0 + r;  // absolute position of this row's query
+  // online softmax with a lazily refreshed running max (the FA4 rule): P = exp2(S c2 - m) is used
+  // with a stale m until the tile max exceeds it by more than 8 (P <= 2^8, exact in fp32/bf16
+  // range); O accumulates in TMEM across tiles and is rescaled there only when m moves
+  float m = -INFINITY, l = 0.f;  // l: this column half's partial row sum
+  const uint32_t lane_off = (quarter * 32u) << 16;
+  uint8_t* prow = sP + chh * (kPBQ * 128) + r * 128;  // this row's 64-key slice of P (k-block chh)
+  const int c_key0 = static_cast<int>(chh) * 64;
+
+  for (int t = 0; t < ntiles; ++t) {
+    const int buf = t & 1;
+    const bool tr = tr0 && t < 32;
+    if (tr) a.trace[t * 8 + 0] = globaltimer_ns();
+    if (warp == 0 && t + 1 < ntiles) issue_s(t + 1);  // overlaps this tile's softmax
+    mbar_wait(&s_done[buf], (t >> 1) & 1);
+    tc_fence_after();
+    if (tr) a.trace[t * 8 + 1] = globaltimer_ns();
+    if (warp == 0 && t + 2 < ntiles) load_tile(t + 2, buf, false);  // K_t consumed by S_t
+    // this half of the S row in registers: 4 loads in flight, one wait
+    uint32_t sr[4][16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x16(tS[buf] + lane_off + c_key0 + c * 16, sr[c]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_ld_wait_regs(sr[c]);
+    const int kbase = t * kPBK + c_key0;
+    const bool need_mask = t * kPBK + kPBK - 1 > s0 + q0;  // (CTA-uniform) some key lies past a query
+    float mt = -INFINITY;
+    if (need_mask) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float v = __uint_as_float(sr[c][j]);
+          mt = kbase + c * 16 + j <= qpos ? fmaxf(mt, v) : mt;
+        }
+    } else {
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(sr[c][j]));
+      mt = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+    }
+    red[chh * kPBQ + r] = mt;
+    // PV_{t-1} must be complete before P is overwritten and before O is rescaled
+    if (t > 0) {
+      mbar_wait(o_done, (t - 1) & 1);
+      tc_fence_after();
+      if (warp == 0 && t + 1 < ntiles) load_tile(t + 1, (t + 1) & 1, true);  // V_{t-1} consumed by PV_{t-1}
+    }
+    named_bar_sync(1, 256);  // both halves' maxima posted
+    mt = fmaxf(mt, red[(chh ^ 1) * kPBQ + r]) * c2;
+    if (tr) a.trace[t * 8 + 2] = globaltimer_ns();
+    const bool refresh = mt > m + 8.f;  // also true on the first tile (m = -inf)
+    if (t > 0 && __any_sync(0xffffffffu, refresh)) {  // warp-collective TMEM rescale of this O half
+      const float alpha = refresh ? ex2_approx(m - mt) : 1.f;
+#pragma unroll
+      for (int c = 0; c < kOC; c += 16) {
+        uint32_t ov[16];
+        tmem_ld_32x32b_x16(tO + lane_off + chh * kOC + c, ov);
+        tmem_ld_wait_regs(ov);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * alpha);
+        tmem_st_32x32b_x16(tO + lane_off + chh * kOC + c, ov);
+      }
+      tmem_st_wait();
+      l *= alpha;
+    }
+    if (refresh) m = mt;
+    // P = exp2(S c2 - m) -> bf16 smem (K-major SW128 rows), partial row sum
+    const float mneg = -m;
+    float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float pv[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float e = ex2_approx(fmaf(__uint_as_float(sr[c][j]), c2, mneg));
+        pv[j] = (!need_mask || kbase + c * 16 + j <= qpos) ? e : 0.f;
+        rs4[j & 3] += pv[j];
+      }
+#pragma unroll
+      for (int h8 = 0; h8 < 2; ++h8) {
+        const int chunk = c * 2 + h8;  // 16-B chunk (8 keys) within the 128-B row
+        uint4 w;
+        w.x = pack_bf16x2(pv[h8 * 8 + 0], pv[h8 * 8 + 1]);
+        w.y = pack_bf16x2(pv[h8 * 8 + 2], pv[h8 * 8 + 3]);
+        w.z = pack_bf16x2(pv[h8 * 8 + 4], pv[h8 * 8 + 5]);
+        w.w = pack_bf16x2(pv[h8 * 8 + 6], pv[h8 * 8 + 7]);
+        *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) << 4)) = w;
+      }
+    }
+    l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+    fence_proxy_async_shared();  // P (generic-proxy stores) -> visible to the tensor core
+    tc_fence_before();
+    __syncthreads();  // P complete; S_buf reads, O rescales and red[] reads done
+    if (tr) a.trace[t * 8 + 3] = globaltimer_ns();
+    if (warp == 0) {  // O += P_t V_t  (TMEM accumulate)
+      mbar_wait(&v_full[buf], (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + buf * L::kKV);
+#pragma unroll
+      for (int k = 0; k < kPBK / 16; ++k)
+        umma_f16_ss_warp(tO, make_desc_k_sw128(pa + (k >> 2) * (kPBQ * 128) + (k & 3) * 32),
+                         make_desc_mn_sw128(vb + k * 2048, kPBK * 128, 1024), idesc_o, (t > 0 || k > 0) ? 1u : 0u);
+      umma_commit_warp(o_done);
+    }
+  }
+  mbar_wait(o_done, (ntiles - 1) & 1);
+  tc_fence_after();
+  if (tr0) a.trace[255] = globaltimer_ns();
+  red[chh * kPBQ + r] = l;
+  named_bar_sync(1, 256);
+  const float inv = 1.f / (l + red[(chh ^ 1) * kPBQ + r]);
+
+  // O rows (bf16): this warp's half of the row's dims; rows past the chunk are not written
+  {
+    __nv_bfloat16* dst = a.out + static_cast<size_t>(a.q_row0 + q0 + r) * a.out_ld + qh * HD + chh * kOC;
+    const bool valid = q0 + r < p;
+#pragma unroll
+    for (int c = 0; c < kOC; c += 16) {
+      uint32_t ov[16];
+      tmem_ld_32x32b_x16(tO + lane_off + chh * kOC + c, ov);
+      tmem_ld_wait_regs(ov);
+      if (valid) {
+#pragma unroll
+        for (int h8 = 0; h8 < 16; h8 += 8) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(ov[h8 + 0]) * inv, __uint_as_float(ov[h8 + 1]) * inv);
+          w.y = pack_bf16x2(__uint_as_float(ov[h8 + 2]) * inv, __uint_as_float(ov[h8 + 3]) * inv);
+          w.z = pack_bf16x2(__uint_as_float(ov[h8 + 4]) * inv, __uint_as_float(ov[h8 + 5]) * inv);
+          w.w = pack_bf16x2(__uint_as_float(ov[h8 + 6]) * inv, __uint_as_float(ov[h8 + 7]) * inv);
+          *reinterpret_cast<uint4*>(dst + c + h8) = w;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 template <int HD>
 cudaError_t launch_decode_hd(const DecodeAttnArgs& a, const CUtensorMap& mk, const CUtensorMap& mv, cudaStream_t st) {
   const size_t smem = decode_smem_bytes(HD, a.block_size, a.stages, 1);
@@ -520,8 +805,29 @@ cudaError_t launch_decode_attention(const DecodeAttnArgs& a, const CUtensorMap& 
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t st) {
+template <int HD>
+cudaError_t launch_prefill_tc(const PrefillAttnArgs& a, const CUtensorMap& mq, const CUtensorMap& mk,
+                              const CUtensorMap& mv, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_attn_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(PtcSmem<HD>::kTotal));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((a.p + kPBQ - 1) / kPBQ, a.n_q_local);
+  prefill_attn_tc<HD><<<grid, 256, PtcSmem<HD>::kTotal, st>>>(mq, mk, mv, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, const CUtensorMap* qmap, const CUtensorMap* kmap,
+                                     const CUtensorMap* vmap, cudaStream_t st) {
   if (a.p == 0) return cudaSuccess;
+  const bool tc = qmap && kmap && vmap && (a.block_size == 16 || a.block_size == 32 || a.block_size == 64 ||
+                                           a.block_size == 128);
+  if (tc && a.head_dim == 128) return launch_prefill_tc<128>(a, *qmap, *kmap, *vmap, st);
+  if (tc && a.head_dim == 64) return launch_prefill_tc<64>(a, *qmap, *kmap, *vmap, st);
+  // mma.sync kernel: block sizes the tcgen05 tile (128 keys) does not tile
   dim3 grid((a.p + 63) / 64, a.n_q_local);
   if (a.head_dim == 128) {
     const size_t smem = (64 + 4 * 64) * 128 * 2;

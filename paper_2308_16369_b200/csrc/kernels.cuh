@@ -41,6 +41,7 @@ struct PrefillAttnArgs {
   float scale = 0.f;
   __nv_bfloat16* out = nullptr;
   int out_ld = 0;
+  unsigned long long* trace = nullptr;  // debug: globaltimer stamps of CTA (0,0) (tcgen05 kernel)
 };
 
 size_t decode_smem_bytes(int head_dim, int block_size, int stages, int G);
@@ -48,7 +49,10 @@ size_t decode_smem_bytes(int head_dim, int block_size, int stages, int G);
 bool make_tmap_kv(CUtensorMap* map, const void* pool, long long rows, int head_dim, int block_size);
 cudaError_t launch_decode_attention(const DecodeAttnArgs& a, const CUtensorMap& kmap, const CUtensorMap& vmap,
                                     cudaStream_t st);
-cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, cudaStream_t st);
+// Chunked-prefill attention.  With the TMA maps (q: [Tmax][q_ld] box 128 x 64; K/V: make_tmap_kv) and
+// block_size in {16, 32, 64, 128} it runs the tcgen05 kernel, otherwise the mma.sync kernel.
+cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, const CUtensorMap* qmap, const CUtensorMap* kmap,
+                                     const CUtensorMap* vmap, cudaStream_t st);
 
 // h[t][:] = float(E[tok[t]][:])
 cudaError_t launch_embedding(const int* tok, const __nv_bfloat16* E, float* h, int T, int H, cudaStream_t st);

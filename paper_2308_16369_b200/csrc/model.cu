@@ -13,6 +13,7 @@
 // then logits = RMSNorm(h[rows]; g_f) Wlm^T for the R requested rows (vocab-parallel under TP).
 #include "model.hpp"
 
+#include <cstdio>
 #include <cstdlib>
 
 #include <dlfcn.h>
@@ -256,6 +257,8 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   SRET(dalloc(&h, static_cast<size_t>(Tmax) * H));
   SRET(dalloc(&a, static_cast<size_t>(Tmax) * H));
   SRET(dalloc(&q, static_cast<size_t>(Tmax) * q_dim_l));
+  if (!make_tmap_bf16(&m_q, q, static_cast<uint64_t>(Tmax), q_dim_l, q_dim_l, 128))
+    return Status::err(SARATHI_ECUDA, "tensor map (q)");
   SRET(dalloc(&o, static_cast<size_t>(Tmax) * q_dim_l));
   SRET(dalloc(&f, static_cast<size_t>(Tmax) * h2_l));
   SRET(dalloc(&ar, static_cast<size_t>(Tmax) * H));
@@ -288,6 +291,10 @@ Status Model::alloc_kv(int64_t nb, int32_t bs) {
   for (int l = 0; l < cfg.n_layers; ++l) {
     SRET(dalloc(&kpool[l], per));
     SRET(dalloc(&vpool[l], per));
+    // zero once: slots never written (past a request's length inside a block, or in blocks a tile
+    // rounds up to) are read by the attention kernels under a zero probability; they must be finite
+    SRET(check(cudaMemsetAsync(kpool[l], 0, per * 2, stream), "memset kv"));
+    SRET(check(cudaMemsetAsync(vpool[l], 0, per * 2, stream), "memset kv"));
     const long long rows = nb * static_cast<long long>(nkv_l) * bs;
     if (!make_tmap_kv(&kmap[l], kpool[l], rows, cfg.head_dim, bs) ||
         !make_tmap_kv(&vmap[l], vpool[l], rows, cfg.head_dim, bs))
@@ -536,7 +543,29 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
         SRET(check(cudaStreamWaitEvent(aux, ev_fork, 0), "fork"));
       }
       ob = op_begin(ps);
-      SRET(check(launch_prefill_attention(pa, ps), "prefill attention"));
+      static const char* ptrace = getenv("SARATHI_PREFILL_TRACE");  // debug: stamps of one launch with p == N
+      static bool ptraced = false;
+      unsigned long long* trbuf = nullptr;
+      if (ptrace && !ptraced && atoi(ptrace) == p && l == 1) {
+        ptraced = true;
+        cudaMalloc(&trbuf, 256 * 8);
+        cudaMemsetAsync(trbuf, 0, 256 * 8, ps);
+        pa.trace = trbuf;
+      }
+      SRET(check(launch_prefill_attention(pa, &m_q, &kmap[l], &vmap[l], ps), "prefill attention"));
+      if (trbuf) {
+        unsigned long long hb[256];
+        cudaStreamSynchronize(ps);
+        cudaMemcpy(hb, trbuf, sizeof(hb), cudaMemcpyDeviceToHost);
+        const unsigned long long t0 = hb[254];
+        for (int t = 0; t < 32 && hb[t * 8]; ++t) {
+          fprintf(stderr, "prefill tile %2d:", t);
+          for (int k = 0; k < 7; ++k) fprintf(stderr, " %8.3f", hb[t * 8 + k] ? (hb[t * 8 + k] - t0) * 1e-3 : -1.0);
+          fprintf(stderr, "\n");
+        }
+        fprintf(stderr, "prefill last PV done %8.3f us\n", (hb[255] - t0) * 1e-3);
+        cudaFree(trbuf);
+      }
       op_end(SARATHI_OP_PREFILL_ATTN, ob, ps);
       ++launches;
       if (d > 0) SRET(check(cudaEventRecord(ev_join, aux), "join"));

@@ -57,6 +57,7 @@ struct Model {
   __nv_bfloat16* gf = nullptr;   // [H]
   __nv_bfloat16* lm = nullptr;   // [vocab_l][H]
   CUtensorMap m_lm;
+  CUtensorMap m_q;  // q buffer [Tmax][q_dim_l], box 128 x 64 (tcgen05 prefill attention)
   std::vector<LayerWeights> layers;
   std::vector<void*> allocations;
   float* rope_theta = nullptr;  // [hd/2][2] RoPE frequencies (fp64 -> fp32 hi + lo)

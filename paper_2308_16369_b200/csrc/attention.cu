@@ -69,6 +69,8 @@ template <int HD>
 __global__ void __launch_bounds__(160)
     decode_attn_mma(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
                     DecodeAttnArgs a) {
+  griddep_launch_dependents();
+  griddep_wait();  // q comes from the QKV GEMM (PDL)
   constexpr int NBOX = HD / 64;  // 128-byte TMA boxes per row
   const int j = blockIdx.x, kvh = blockIdx.y, z = blockIdx.z;
   const int G = a.n_q_local / a.n_kv_local;
@@ -286,6 +288,8 @@ __global__ void __launch_bounds__(160)
 }
 
 __global__ void decode_combine_kernel(DecodeAttnArgs a, int HD) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int j = blockIdx.x, qh = blockIdx.y;
   const int nq = a.n_q_local;
   const float* lse = a.part_lse + (static_cast<size_t>(j) * nq + qh) * a.splits;
@@ -776,10 +780,10 @@ cudaError_t launch_decode_hd(const DecodeAttnArgs& a, const CUtensorMap& mk, con
     configured = true;
   }
   dim3 grid(a.d, a.n_kv_local, a.splits);
-  decode_attn_mma<HD><<<grid, 160, smem, st>>>(mk, mv, a);
+  launch_pdl(decode_attn_mma<HD>, grid, dim3(160), smem, st, mk, mv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || a.splits == 1) return e;
-  decode_combine_kernel<<<dim3(a.d, a.n_q_local), 128, 0, st>>>(a, HD);
+  launch_pdl(decode_combine_kernel, dim3(a.d, a.n_q_local), dim3(128), 0, st, a, HD);
   return cudaGetLastError();
 }
 

@@ -3,6 +3,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cuda.h>
@@ -49,6 +51,13 @@ SARATHI_DEVICE float2 unpack_bf16x2(uint32_t v) {
   __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&v);
   return __bfloat1622float2(b);
 }
+
+// Programmatic dependent launch (PDL): a kernel launched with programmatic stream serialization
+// may start while its predecessor drains; griddep_wait() blocks until the predecessor grid has
+// completed and its memory is visible (a no-op without a programmatic dependency);
+// griddep_launch_dependents() lets the successor grid start launching.
+SARATHI_DEVICE void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+SARATHI_DEVICE void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 SARATHI_DEVICE void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
@@ -389,6 +398,24 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16_f32(uint32_t M, uint32_t 
          | (0u << 16)         // b K-major
          | ((N >> 3) << 17)   // n_dim
          | ((M >> 4) << 24);  // m_dim
+}
+
+// Host: launch with programmatic stream serialization (PDL) unless SARATHI_PDL=0.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace sarathi

@@ -8,10 +8,20 @@
 
 namespace sarathi {
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SARATHI_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 namespace {
 
 __global__ void embedding_kernel(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ E,
                                  float* __restrict__ h, int H) {
+  griddep_launch_dependents();
+  griddep_wait();  // h is read by the previous step's kernels
   const int t = blockIdx.x;
   const __nv_bfloat16* src = E + static_cast<size_t>(tok[t]) * H;
   float* dst = h + static_cast<size_t>(t) * H;
@@ -50,6 +60,8 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h
                                                            __nv_bfloat16* __restrict__ out, const int* __restrict__ rows,
                                                            int H, float eps) {
   __shared__ float sred[kThreads / 32];
+  griddep_launch_dependents();
+  griddep_wait();  // h / add come from the preceding GEMM (PDL)
   const int r = blockIdx.x;
   const int row = rows ? rows[r] : r;
   float* x = h + static_cast<size_t>(row) * H;
@@ -167,7 +179,7 @@ __global__ void gaingen_kernel(__nv_bfloat16* __restrict__ dst, int n, int tau, 
 
 cudaError_t launch_embedding(const int* tok, const __nv_bfloat16* E, float* h, int T, int H, cudaStream_t st) {
   if (T == 0) return cudaSuccess;
-  embedding_kernel<<<T, 256, 0, st>>>(tok, E, h, H);
+  launch_pdl(embedding_kernel, dim3(T), dim3(256), 0, st, tok, E, h, H);
   return cudaGetLastError();
 }
 
@@ -178,11 +190,11 @@ cudaError_t launch_rmsnorm(float* h, const __nv_bfloat16* add, const __nv_bfloat
   // one CTA per row, sized so that every row of a batch (T <= 512) is resident in ONE wave
   // (a second partial wave doubles the latency of this latency-bound kernel)
   if (H <= 256 * 4 * 2) {
-    rmsnorm_kernel<256, 2><<<R, 256, 0, st>>>(h, add, g, out, rows, H, eps);
+    launch_pdl(rmsnorm_kernel<256, 2>, dim3(R), dim3(256), 0, st, h, add, g, out, rows, H, eps);
   } else if (H <= 256 * 4 * 5) {
-    rmsnorm_kernel<256, 5><<<R, 256, 0, st>>>(h, add, g, out, rows, H, eps);
+    launch_pdl(rmsnorm_kernel<256, 5>, dim3(R), dim3(256), 0, st, h, add, g, out, rows, H, eps);
   } else if (H <= 512 * 4 * 8) {
-    rmsnorm_kernel<512, 8><<<R, 512, 0, st>>>(h, add, g, out, rows, H, eps);
+    launch_pdl(rmsnorm_kernel<512, 8>, dim3(R), dim3(512), 0, st, h, add, g, out, rows, H, eps);
   } else {
     return cudaErrorInvalidValue;
   }

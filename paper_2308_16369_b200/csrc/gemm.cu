@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();   // 0 = leader (issues the pair MMAs)
+  griddep_launch_dependents();
   const int pair = blockIdx.x >> 1;
 
   if (threadIdx.x == 0) {
@@ -331,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *holder;
   const int ni = p.bn / p.n_mma;  // tokens per UMMA (multiple of 16, <= 256)
+  if (warp != 0) griddep_wait();  // the producer waits after prefetching its first W tiles
 
   if (warp == 0) {
     // ---------------- TMA producer (whole warp, warp-uniform; one elected lane issues) ----------------
@@ -345,17 +347,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       SegIter it;
       it.init(p, pair);
       int tile, kb0, kb1;
+      // PDL: weights do not depend on the previous kernel, so the first ring's W tiles are fetched
+      // before the grid-dependency wait (overlapping the predecessor's tail); X loads come after it
+      int npre = 0;
+      {
+        SegIter it0 = it;
+        if (it0.next(p, tile, kb0, kb1)) {
+          npre = min(p.stages, kb1 - kb0);
+          const int pt = tile / p.n_tiles;
+          const int wrow0 = ((pt * 2 + static_cast<int>(rank)) * p.KB + kb0) * kWRowsPerTile;
+          for (int j = 0; j < npre; ++j) {
+            uint8_t* a = smem + static_cast<size_t>(j) * stage_bytes;
+            if (rank == 0) mbar_arrive_expect_tx_warp(&full[j], tx);
+            if (!(ep.dbg & 2)) tma_load_2d_pair_warp(a, &mapW, &full[j], 0, wrow0 + j * kWRowsPerTile, pol_w);
+          }
+        }
+      }
+      griddep_wait();
       while (it.next(p, tile, kb0, kb1)) {
         const int pt = tile / p.n_tiles, nt = tile % p.n_tiles;
         int wrow = ((pt * 2 + static_cast<int>(rank)) * p.KB + kb0) * kWRowsPerTile;  // row in the 512-B view
         for (int kb = kb0; kb < kb1; ++kb, ++i) {
-          mbar_wait(&empty[s], ph ^ 1);
           uint8_t* a = smem + static_cast<size_t>(s) * stage_bytes;
           uint8_t* b = a + kABytes;
-          // both CTAs' bytes are counted on the leader's full[s] (pair TMA)
-          if (rank == 0) mbar_arrive_expect_tx_warp(&full[s], tx);
-          // W tile: the contiguous 16 KB pre-swizzled tile as 32 rows x 512 B (unswizzled map)
-          if (!(ep.dbg & 2)) tma_load_2d_pair_warp(a, &mapW, &full[s], 0, wrow, pol_w);
+          if (i >= npre) {
+            mbar_wait(&empty[s], ph ^ 1);
+            // both CTAs' bytes are counted on the leader's full[s] (pair TMA)
+            if (rank == 0) mbar_arrive_expect_tx_warp(&full[s], tx);
+            // W tile: the contiguous 16 KB pre-swizzled tile as 32 rows x 512 B (unswizzled map)
+            if (!(ep.dbg & 2)) tma_load_2d_pair_warp(a, &mapW, &full[s], 0, wrow, pol_w);
+          }
           if (!(ep.dbg & 1))
             for (int j = 0; j < p.n_mma; ++j)
               tma_load_2d_pair_warp(b + j * (ni / 2) * kBK * 2, &mapX, &full[s], kb * kBK,
@@ -671,14 +692,15 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
     return std::min(s, g);
   };
   int max_slots = slots_for(pairs);
-  // the reduction handles <= 4 contributors per tile (pure stream-K plans only)
-  while (dp_per == 0 && pairs > 1 && max_slots > 4) {
+  // the partial reduction handles <= 4 contributors per tile (pure stream-K plans only; residual
+  // adds reduce with red.add and have no partial slots)
+  while (!atomic_epilogue && dp_per == 0 && pairs > 1 && max_slots > 4) {
     --pairs;
     max_slots = slots_for(pairs);
   }
   const size_t tile_elems = static_cast<size_t>(pl.bn) * kBM;
   const size_t tiles128 = static_cast<size_t>(pl.m_tiles) * pl.n_tiles;
-  while (dp_per == 0 && pairs > 1 && tiles128 * max_slots * tile_elems > ws_cap_floats) {
+  while (!atomic_epilogue && dp_per == 0 && pairs > 1 && tiles128 * max_slots * tile_elems > ws_cap_floats) {
     pairs = std::max(1, pairs / 2);
     max_slots = slots_for(pairs);
   }
@@ -690,7 +712,7 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
   pl.max_slots = max_slots;
   pl.splits = static_cast<int>((units + pairs - 1) / pairs) + dp_per * KB;  // units per pair (informational)
   pl.kb_per_split = pl.splits;
-  pl.ws_floats = units > 0 ? tiles128 * max_slots * tile_elems : 0;
+  pl.ws_floats = units > 0 && !atomic_epilogue ? tiles128 * max_slots * tile_elems : 0;
   pl.nbuf = pl.bn <= 256 ? 2 : 1;
   const size_t stage = kABytes + static_cast<size_t>(pl.bn / 2) * kBK * 2;
   const size_t budget = 226 * 1024 - 1024 - extra_smem(pl.bn);
@@ -760,13 +782,15 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (see the producer)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, gemm_bf16_pair, mapW, mapX, kp, ep);
 }
 

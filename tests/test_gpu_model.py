@@ -116,3 +116,18 @@ def test_default_rows_and_errors_leave_state_unchanged(S):
     assert np.max(np.abs(out[0] - ref2)) / np.max(np.abs(ref2)) < TOL
     assert np.max(np.abs(out[1] - ref1)) / np.max(np.abs(ref1)) < TOL
     m.close()
+
+
+@pytest.mark.parametrize("hd,n_kv,C,bs", [(128, 2, 300, 64), (64, 8, 200, 16), (128, 4, 260, 128)])
+def test_prefill_attention_multitile(S, hd, n_kv, C, bs):
+    """Chunks larger than one 128-query tile and prefixes spanning several 128-key tiles (the
+    tcgen05 prefill kernel: ragged last q-tile, causal diagonal inside a key tile, K/V ring refills,
+    lazy max refresh), GQA and MHA, block sizes 16/64/128 — end to end against the fp64 oracle."""
+    H = 512
+    cfg = synth.ModelConfig(f"mid-hd{hd}", 1, H, H // hd, n_kv, hd, 768, 256, max_seq_len=1024)
+    # request 1: 700-token prompt in chunks of C (s = 0, C, 2C, ...); 2 and 3 decode alongside
+    reqs = [(2, 40, 6, 0), (3, 9, 8, 0), (1, 700, 2, 1)]
+    steps = gh.run_schedule(S, cfg, reqs, B=3, C=C, num_blocks=1024 // bs * 3, block_size=bs,
+                            weight_seed=7, max_tokens=C + 3)
+    _check(steps)
+    assert max(p[0][2] for p in (s.plan for s in steps) if p[0] is not None) > 128

@@ -165,7 +165,7 @@ SARATHI_DEVICE void red_add_v4(float* addr, float4 v) {
 
 SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[16], uint32_t q, uint32_t lane, int mt,
                              int nt, int c0, int tvalid, float* sbuf, const int* s_pos, const int* s_slot,
-                             const QkvLane& ql) {
+                             const int* s_consec, const QkvLane& ql) {
   const int row0 = mt * kBM + static_cast<int>(q) * 32;  // first accumulator row of this warp
   const long long tb = static_cast<long long>(nt) * p.bn + c0;
   const int nv = (ep.dbg & 8) ? 0 : min(16, tvalid - c0);  // dbg bit 3: no global stores
@@ -238,13 +238,32 @@ SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[1
       if (ql.rope) {
         // branch-free, 8 tokens per batch so the shuffles, position loads and sincos of different
         // tokens overlap (a per-token dependent chain cost ~150 cycles x 16 per chunk)
+        // consecutive positions (prefill chunks): angle-addition recurrence from the chunk's first
+        // position, 4 FMAs per token instead of a reduction + sincos (error growth ~16 ulp)
+        const bool consec = s_consec[c0 >> 4] != 0;
+        float cd = 1.f, sd = 0.f, cr = 1.f, sr = 0.f;
+        if (consec) {
+          rope_cos_sin(1, ql.th_hi, ql.th_lo, cd, sd);
+          rope_cos_sin(s_pos[c0], ql.th_hi, ql.th_lo, cr, sr);
+        }
 #pragma unroll
         for (int j0 = 0; j0 < 16; j0 += 8) {
           float xp[8], c[8], sn[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) xp[j] = __shfl_xor_sync(0xffffffffu, v[j0 + j], 16);  // rotate-half partner
+          if (consec) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) rope_cos_sin(s_pos[min(c0 + j0 + j, tvalid - 1)], ql.th_hi, ql.th_lo, c[j], sn[j]);
+            for (int j = 0; j < 8; ++j) {
+              c[j] = cr;
+              sn[j] = sr;
+              const float cn = fmaf(cr, cd, -sr * sd);
+              sr = fmaf(sr, cd, cr * sd);
+              cr = cn;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) rope_cos_sin(s_pos[min(c0 + j0 + j, tvalid - 1)], ql.th_hi, ql.th_lo, c[j], sn[j]);
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             // x1 = low-half value, x2 = high-half value: y1 = x1 c - x2 s, y2 = x2 c + x1 s
@@ -294,7 +313,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* stage_buf = reinterpret_cast<float*>(smem + p.ring_bytes);    // [8 warps][16 x 32] transpose
   int* s_pos = reinterpret_cast<int*>(stage_buf + 8 * kStageFloats);   // [bn]
   int* s_slot = s_pos + p.bn;                                          // [bn]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_slot + ((p.bn + 1) & ~1));  // 8-B aligned (bn is a multiple of 16)
+  int* s_consec = s_slot + p.bn;                                       // [32] chunk has consecutive positions
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_consec + 32);         // 8-B aligned (bn is a multiple of 16)
   uint64_t* full = bars;                // local: this CTA's W + X bytes landed
   uint64_t* pfull = full + p.stages;    // leader only: the peer's stage landed (relayed)
   uint64_t* empty = pfull + p.stages;
@@ -472,6 +492,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           s_slot[t] = (sl / ep.block_size) * ep.n_kv_local * ep.block_size + sl % ep.block_size;
         }
         named_bar_sync(2, kEpiThreads);
+        if (et < (tvalid + 15) / 16) {  // chunk et: positions p0, p0+1, ... (a prefill chunk) -> RoPE recurrence
+          const int c0 = et * 16, n = min(16, tvalid - c0);
+          int ok = 1;
+          for (int j = 1; j < n; ++j) ok &= s_pos[c0 + j] == s_pos[c0] + j;
+          s_consec[et] = ok;
+        }
+        named_bar_sync(2, kEpiThreads);
       }
       if (lane == 0) mbar_wait(&tfull[buf], use & 1);
       __syncwarp();
@@ -496,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
             if (!(ep.dbg & 4))
-              epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, ql);
+              epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql);
             if (ep.trace && blockIdx.x < 2 && et == 0 && seg == 0 && ch < 64)
               ep.trace[blockIdx.x * 1024 + 640 + ch] = globaltimer_ns();
             if (more) {
@@ -568,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int q = 0; q < kMaxSlots; ++q)
 #pragma unroll
               for (int j = 0; j < 16; ++j) cur[q][j] = nxt[q][j];
-            epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, ql);
+            epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql);
           }
         }
       }
@@ -609,7 +636,7 @@ uint32_t pow2_cols(int n) {
   return c;
 }
 
-size_t extra_smem(int bn) { return 8 * kStageFloats * 4 + 2 * static_cast<size_t>(bn) * 4 + 3 * 8 * 8 + 64 + 64; }
+size_t extra_smem(int bn) { return 8 * kStageFloats * 4 + 32 * 4 + 2 * static_cast<size_t>(bn) * 4 + 3 * 8 * 8 + 64 + 64; }
 
 }  // namespace
 

@@ -200,6 +200,57 @@ __global__ void __launch_bounds__(192, 1) umma_gemm_like(int kblocks, int S, int
   }
 }
 
+// Two commits per 8-UMMA group (one per stage of a 2-stage group, as a GEMM with 4 UMMAs per
+// k-block would need): is the cost per commit instruction or per commit group?
+__global__ void __launch_bounds__(128, 1) umma_two_commits(int N, int iters, int dual, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bars[16];
+  __shared__ uint32_t holder;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 16; ++i) mbar_init(&bars[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc_pair(&holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = holder;
+  const int S = 6;  // groups in flight
+  if (warp == 0 && rank == 0) {
+    const uint32_t idesc = make_idesc_bf16_f32(256, N);
+    const uint32_t a = smem_u32(smem), b = a + 16384;
+    const unsigned long long t0 = globaltimer_ns();
+    const int groups = iters / 8;
+    for (int g = 0; g < groups; ++g) {
+      const int s = g % S;
+      if (g >= S) {
+        mbar_wait(&bars[2 * s], ((g / S) - 1) & 1);
+        if (dual) mbar_wait(&bars[2 * s + 1], ((g / S) - 1) & 1);
+        tc_fence_after();
+      }
+      for (int k = 0; k < 8; ++k) {
+        umma_f16_ss_pair_warp(tmem, make_desc_k_sw128(a + (k & 3) * 32), make_desc_k_sw128(b + (k & 3) * 32), idesc, 1);
+        if (dual && k == 3) umma_commit_pair_mc_warp(&bars[2 * s + 1], 0x1);  // mid-group commit
+      }
+      umma_commit_pair_mc_warp(&bars[2 * s], 0x1);
+    }
+    for (int g = groups - S; g < groups; ++g)
+      if (g >= 0) mbar_wait(&bars[2 * (g % S)], (g / S) & 1);
+    const unsigned long long t1 = globaltimer_ns();
+    if (lane == 0) out[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
+  }
+}
+
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 1024 * 8);
@@ -287,6 +338,26 @@ int main() {
       cudaMemcpy(&ns, d, 8, cudaMemcpyDeviceToHost);
       printf("gemm-like pair 2xN=160 rotate=%d mask=%d spin=%d: %7.1f ns per k-block (8 UMMAs) (%s)\n", rotate, mask, spin, ns / (double)kb,
              cudaGetErrorString(e ? e : cudaGetLastError()));
+    }
+  cudaFuncSetAttribute(umma_two_commits, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (int N : {128, 160})
+    for (int dual : {0, 1}) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(2);
+      cfg.blockDim = dim3(128);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, umma_two_commits, N, 4096, dual, d);
+      cudaDeviceSynchronize();
+      unsigned long long ns = 0;
+      cudaMemcpy(&ns, d, 8, cudaMemcpyDeviceToHost);
+      printf("two-commit test pair N=%d dual=%d: %7.1f ns per MMA (%s)\n", N, dual, ns / 4096.0, cudaGetErrorString(e ? e : cudaGetLastError()));
     }
   return 0;
 }

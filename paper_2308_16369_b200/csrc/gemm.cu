@@ -25,6 +25,7 @@
 #include "gemm.cuh"
 
 #include <algorithm>
+#include <vector>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -329,6 +330,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_ctarank();   // 0 = leader (issues the pair MMAs)
   griddep_launch_dependents();
   const int pair = blockIdx.x >> 1;
+  // debug trace: CTA pair (dbg >> 8) records its timeline (tb = 0 / 1 for its two CTAs)
+  const int tb = static_cast<int>(blockIdx.x) - 2 * (ep.dbg >> 8);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < p.n_mma; ++j)
               tma_load_2d_pair_warp(b + j * (ni / 2) * kBK * 2, &mapX, &full[s], kb * kBK,
                                     nt * p.bn + j * ni + static_cast<int>(rank) * (ni / 2), pol_x);
-          if (ep.trace && blockIdx.x < 2 && i < 256 && lane == 0) ep.trace[blockIdx.x * 1024 + i] = globaltimer_ns();
+          if (ep.trace && tb < 2 && i < 256 && lane == 0) ep.trace[tb * 1024 + i] = globaltimer_ns();
           if (++s == p.stages) {
             s = 0;
             ph ^= 1;
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb, ++i) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          if (ep.trace && blockIdx.x == 0 && lane == 0 && i < 256) ep.trace[256 + i] = globaltimer_ns();
+          if (ep.trace && tb == 0 && lane == 0 && i < 256) ep.trace[256 + i] = globaltimer_ns();
           {
             // warp-uniform issue (operands stay in uniform registers), one elected lane issues
             const uint32_t a = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
@@ -504,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_wait(&tfull[buf], use & 1);
       __syncwarp();
       tc_fence_after();
-      if (ep.trace && blockIdx.x < 2 && et == 0 && seg < 64) ep.trace[blockIdx.x * 1024 + 512 + seg] = globaltimer_ns();
+      if (ep.trace && tb < 2 && et == 0 && seg < 64) ep.trace[tb * 1024 + 512 + seg] = globaltimer_ns();
       const uint32_t trow = tmem + buf * 256 + ((quarter * 32u) << 16);
       const int nchunks = (tvalid + 15) / 16;
       if (direct) {
@@ -525,8 +528,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
             if (!(ep.dbg & 4))
               epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql);
-            if (ep.trace && blockIdx.x < 2 && et == 0 && seg == 0 && ch < 64)
-              ep.trace[blockIdx.x * 1024 + 640 + ch] = globaltimer_ns();
+            if (ep.trace && tb < 2 && et == 0 && seg == 0 && ch < 64)
+              ep.trace[tb * 1024 + 640 + ch] = globaltimer_ns();
             if (more) {
               tmem_ld_wait_regs(nraw);
               if (ch + 4 >= nchunks) release_tmem();
@@ -543,16 +546,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nslot = c_last - c_first + 1;
         const int slot = pair - c_first;
         const size_t tile128 = static_cast<size_t>(mt) * p.n_tiles + nt;
-        float* wsp = ep.ws + (tile128 * p.max_slots + slot) * tile_elems;
-        for (int ch = eh; ch < nchunks; ch += 2) {
+        // partial layout [chunk][lane quarter][token quad j][lane][4 tokens] (fp32): a thread keeps its
+        // row's 16 tokens as four float4, and each warp-wide 16-B vector access is 512 contiguous bytes
+        const size_t qoff = static_cast<size_t>(quarter) * 512 + lane * 4;  // + (ch * 4 * 512) + j * 128
+        float* wsp = ep.ws + (tile128 * p.max_slots + slot) * tile_elems + qoff;
+        if (eh >= nchunks) {
+          release_tmem();
+        } else {
+          // TMEM drain pipelined like the direct path; TMEM is released right after the last load
           uint32_t raw[16];
-          tmem_ld_32x32b_x16(trow + ch * 16, raw);
-          tmem_ld_wait();
-          // partial layout [token][row]: a warp store covers 128 contiguous bytes
+          tmem_ld_32x32b_x16(trow + eh * 16, raw);
+          tmem_ld_wait_regs(raw);
+          if (eh + 2 >= nchunks) release_tmem();
+          for (int ch = eh; ch < nchunks; ch += 2) {
+            uint32_t nraw[16];
+            const bool more = ch + 2 < nchunks;
+            if (more) tmem_ld_32x32b_x16(trow + (ch + 2) * 16, nraw);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) __stcg(wsp + static_cast<size_t>(ch * 16 + j) * kBM + r, __uint_as_float(raw[j]));
+            for (int j = 0; j < 4; ++j)
+              __stcg(reinterpret_cast<float4*>(wsp + ch * 2048 + j * 128),
+                     make_float4(__uint_as_float(raw[4 * j]), __uint_as_float(raw[4 * j + 1]),
+                                 __uint_as_float(raw[4 * j + 2]), __uint_as_float(raw[4 * j + 3])));
+            if (more) {
+              tmem_ld_wait_regs(nraw);
+              if (ch + 4 >= nchunks) release_tmem();
+#pragma unroll
+              for (int j = 0; j < 16; ++j) raw[j] = nraw[j];
+            }
+          }
         }
-        release_tmem();
         __threadfence();
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
@@ -562,51 +584,59 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (s_last) *ctr = 0;  // re-arm for the next launch
         }
         named_bar_sync(1, kEpiThreads);
-        if (s_last) {
+        if (s_last && eh < nchunks) {
           __threadfence();
-          const float* base = ep.ws + tile128 * p.max_slots * tile_elems;
-          // software-pipelined reduction: chunk ch+1's partials are in flight while chunk ch is summed
-          // (slot order kept -> deterministic); [token][row] layout keeps every load 128 B per warp
-          constexpr int kMaxSlots = 2;  // prefetched slots; slots >= 2 (rare) are added unpipelined
-          const float* colbase = base + r;
-          float cur[kMaxSlots][16], nxt[kMaxSlots][16];
+          const float* rowbase = ep.ws + tile128 * p.max_slots * tile_elems + qoff;
+          // slots summed in slot order (deterministic); slot 0 of the next chunk is in flight while
+          // this chunk is summed and emitted (A/B register buffers, no copies)
+          auto load1 = [&](int ch, float4 (&buf)[4]) {
 #pragma unroll
-          for (int q = 0; q < kMaxSlots; ++q)
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              cur[q][j] = q < nslot && eh < nchunks ? __ldcg(colbase + q * tile_elems + static_cast<size_t>(eh * 16 + j) * kBM) : 0.f;
-          for (int ch = eh; ch < nchunks; ch += 2) {
-            if (ch + 2 < nchunks) {
-#pragma unroll
-              for (int q = 0; q < kMaxSlots; ++q)
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                  nxt[q][j] = q < nslot ? __ldcg(colbase + q * tile_elems + static_cast<size_t>((ch + 2) * 16 + j) * kBM)
-                                        : 0.f;
-            }
+            for (int j = 0; j < 4; ++j) buf[j] = __ldcg(reinterpret_cast<const float4*>(rowbase + ch * 2048 + j * 128));
+          };
+          auto sum_emit = [&](int ch, const float4 (&buf)[4]) {
             float v[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = cur[0][j] + cur[1][j];
-            for (int q = kMaxSlots; q < nslot; ++q) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                v[j] += __ldcg(colbase + q * tile_elems + static_cast<size_t>(ch * 16 + j) * kBM);
+            for (int j = 0; j < 4; ++j) {
+              v[4 * j + 0] = buf[j].x;
+              v[4 * j + 1] = buf[j].y;
+              v[4 * j + 2] = buf[j].z;
+              v[4 * j + 3] = buf[j].w;
             }
+            for (int q = 1; q < nslot; ++q) {
 #pragma unroll
-            for (int q = 0; q < kMaxSlots; ++q)
-#pragma unroll
-              for (int j = 0; j < 16; ++j) cur[q][j] = nxt[q][j];
+              for (int j = 0; j < 4; ++j) {
+                const float4 x = __ldcg(reinterpret_cast<const float4*>(rowbase + q * tile_elems + ch * 2048 + j * 128));
+                v[4 * j + 0] += x.x;
+                v[4 * j + 1] += x.y;
+                v[4 * j + 2] += x.z;
+                v[4 * j + 3] += x.w;
+              }
+            }
             epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql);
+          };
+          float4 A[4], B[4];
+          load1(eh, A);
+          for (int ch = eh; ch < nchunks; ch += 4) {
+            if (ch + 2 < nchunks) load1(ch + 2, B);
+            sum_emit(ch, A);
+            if (ch + 2 < nchunks) {
+              if (ch + 4 < nchunks) load1(ch + 4, A);
+              sum_emit(ch + 2, B);
+            }
           }
         }
       }
-      if (ep.trace && blockIdx.x < 2 && et == 0 && seg < 64) ep.trace[blockIdx.x * 1024 + 576 + seg] = globaltimer_ns();
+      if (ep.trace && tb < 2 && et == 0 && seg < 64) ep.trace[tb * 1024 + 576 + seg] = globaltimer_ns();
       ++seg;
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (ep.trace && threadIdx.x == 0) {
+    ep.trace[2048 + blockIdx.x] = globaltimer_ns();  // per-CTA end (debug)
+    if (blockIdx.x == 0) ep.trace[2047] = 1;
+  }
   cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
@@ -772,6 +802,22 @@ void dump_gemm_trace(const unsigned long long* trace_dev, const GemmPlan& pl) {
   for (int i = 0; i < 256 && h[i]; ++i)
     fprintf(stderr, "u%3d issue0 %8.3f issue1 %8.3f mma %8.3f us\n", i, (h[i] - t0) * 1e-3,
             h[1024 + i] ? (h[1024 + i] - t0) * 1e-3 : -1.0, h[256 + i] ? (h[256 + i] - t0) * 1e-3 : -1.0);
+  {
+    int n = 0;
+    std::vector<double> ends;
+    for (int b = 0; b < 2 * pl.ctas && 2048 + b < 4096; ++b)
+      if (h[2048 + b]) {
+        ends.push_back((h[2048 + b] - t0) * 1e-3);
+        ++n;
+      }
+    std::sort(ends.begin(), ends.end());
+    if (n) fprintf(stderr, "CTA end times (us): min %.2f p25 %.2f p50 %.2f p75 %.2f max %.2f (n=%d)\n", ends[0],
+                   ends[n / 4], ends[n / 2], ends[3 * n / 4], ends[n - 1], n);
+    if (getenv("SARATHI_TRACE_ALL")) {
+      for (int b = 0; b < 2 * pl.ctas; b += 2)
+        fprintf(stderr, "pair %d end %.2f\n", b / 2, h[2048 + b] ? (h[2048 + b] - t0) * 1e-3 : -1.0);
+    }
+  }
   for (int ch = 0; ch < 64 && h[640 + ch]; ++ch) fprintf(stderr, "seg0 chunk %d emitted %8.3f us\n", ch, (h[640 + ch] - t0) * 1e-3);
   for (int sgm = 0; sgm < 64 && h[512 + sgm]; ++sgm)
     fprintf(stderr, "seg %d epilogue wake %8.3f us  done %8.3f us\n", sgm, (h[512 + sgm] - t0) * 1e-3,

@@ -25,22 +25,44 @@ def _bf16(bits):
 
 
 def test_llama13b_bench_composition_sampled_layer_local():
+    _layer_local(synth.LLAMA_13B, 256, 768, 64, 1024, (0, synth.LLAMA_13B.n_layers - 1))
+
+
+# Per-rank shard shapes of the other BASELINE.json configs at full width (SURVEY §8(a) reference
+# sizes), two layers each: LLaMA-33B TP1 (52 heads, H2 17920; [33B-1] d=22 at 2K), LLaMA-2-70B
+# TP8 rank (8 query heads sharing ONE KV head: GQA group 8, H2/8, V/8; [70B-8]) and the GPT-3
+# 175B-shape TP8 rank (12 heads, 2-matrix GELU FFN, H2/8, V/8).  Same kernels and per-GPU GEMM /
+# attention shapes as the sharded model; the residual is this rank's alone.
+SHARDS = {
+    "llama33b-tp1": (synth.dataclasses.replace(synth.LLAMA_33B, n_layers=2, max_seq_len=2048), 256, 768, 22, 2048),
+    "llama70b-tp8-rank": (synth.ModelConfig("llama2-70b-tp8-rank", 2, 8192, 8, 1, 128, 3584, 4000, max_seq_len=2048),
+                          256, 1024, 26, 2048),
+    "gpt3-tp8-rank": (synth.ModelConfig("gpt3-tp8-rank", 2, 12288, 12, 12, 128, 6144, 6288, ffn_kind=synth.FFN_GELU,
+                                        max_seq_len=2048), 256, 1024, 26, 2048),
+}
+
+
+@pytest.mark.parametrize("name", sorted(SHARDS))
+def test_config_shards_sampled_layer_local(name):
+    cfg, p, s, d, ctx = SHARDS[name]
+    _layer_local(cfg, p, s, d, ctx, (0, 1))
+
+
+def _layer_local(cfg, p, s, d, ctx, layers):
     import torch
     import bench
     from paper_2308_16369_b200 import sarathi as S
 
-    cfg = synth.LLAMA_13B
-    p, s, d, ctx = 256, 768, 64, 1024
     torch.cuda.set_device(0)
     m, prefill, decodes = bench.setup_model(S, synth, cfg, p, s, d, ctx, 0, 1, 0, None, 0)
     T = p + d
     logits = np.zeros((T, cfg.vocab), dtype=np.float32)
     m.run_hybrid_batch(prefill, decodes, flags=S.RETURN_ALL_ROWS | S.DUMP_LAYERS, logits_host=logits)
-    rows = [0, 131, 255, 256, 300, 319]
+    rows = [0, p // 2 + 3, p - 1, p, p + d // 2, T - 1]  # chunk rows (incl. its last) and decode rows
     req = [0 if r < p else r - p + 1 for r in rows]
     pos = np.array([s + r if r < p else ctx - 1 for r in rows])
     errs = {}
-    for layer in (0, cfg.n_layers - 1):
+    for layer in layers:
         h_in = m.hidden(layer - 1, T)[rows].astype(np.float64)
         h_out = m.hidden(layer, T)[rows].astype(np.float64)
         lw = om.layer_weights(cfg, 0, layer)

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(160)
     const uint32_t kb = smem_u32(smem + static_cast<size_t>(s) * 2 * blk_bytes);
     const uint32_t vb = kb + blk_bytes;
     const int key_base = (b0 + i) * bs;
-    for (int grp = warp; grp < ngroups; grp += 4) {
+    for (int grp = warp; grp < (a.dbg & 1 ? 0 : ngroups); grp += 4) {
       const int k0 = grp * 16;  // key row within the block
       float sacc[2][4];
 #pragma unroll

@@ -26,6 +26,7 @@ struct DecodeAttnArgs {
   float* part_lse = nullptr;  // [d][n_q_local][splits]
   __nv_bfloat16* out = nullptr;  // [T][out_ld]; row q_row0 + j
   int out_ld = 0;
+  int dbg = 0;  // timing experiments only: bit0 = consumers skip the math (pure K/V streaming)
 };
 
 struct PrefillAttnArgs {

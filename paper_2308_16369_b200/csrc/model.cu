@@ -600,6 +600,8 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
         const size_t blk = static_cast<size_t>(block_size) * hd * 2;  // K (or V) block bytes
         da.stages = static_cast<int>(std::max<size_t>(2, std::min<size_t>(4, (104 * 1024) / (2 * blk))));
       }
+      static const int dec_dbg = getenv("SARATHI_DECODE_DBG") ? atoi(getenv("SARATHI_DECODE_DBG")) : 0;
+      da.dbg = dec_dbg;
       da.part_o = part_o;
       da.part_lse = part_lse;
       da.out = o;

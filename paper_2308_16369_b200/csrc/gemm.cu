@@ -718,7 +718,11 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
     sk_tiles = tiles;
     dp_per = 0;
   } else if (atomic_epilogue) {
+    // residual adds reduce with red.add: split-K.  With tiles <= pairs, split every tile the same
+    // number of ways (pairs = tiles * floor(P / tiles)) so each pair's k-range lies inside ONE tile:
+    // one red.add epilogue per pair instead of two for ranges straddling a tile boundary
     pairs = static_cast<int>(std::min<long long>(P, std::max<long long>(1, static_cast<long long>(tiles) * KB / 4)));
+    if (tiles <= P && !getenv("SARATHI_GEMM_SK_ANY")) pairs = tiles * std::max(1, std::min(P / tiles, KB / 4));
     sk_tiles = tiles;
     dp_per = 0;
   } else if (tiles <= P) {

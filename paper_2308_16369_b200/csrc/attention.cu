@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 namespace sarathi {
 
@@ -556,15 +557,12 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t warp = warp_id_uniform(), lane = lane_id();
   const uint32_t quarter = warp & 3, chh = warp >> 2;
   const int r = static_cast<int>(quarter * 32 + lane);  // query row within the tile == TMEM lane
-  const int qt = blockIdx.x, qh = blockIdx.y;
-  const int kvh = qh * a.n_kv_local / a.n_q_local;
-  const int q0 = qt * kPBQ;
   const int s0 = a.start, p = a.p, bs = a.block_size;
   const int kv_len = s0 + p;
-  const int key_end = s0 + min(q0 + kPBQ, p);  // keys this tile needs: [0, key_end)
-  const int ntiles = (key_end + kPBK - 1) / kPBK;
   const int last_blk = (kv_len - 1) / bs;      // last block of the request holding valid keys
-  const bool tr0 = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+  const int ntq = (p + kPBQ - 1) / kPBQ;
+  const int n_items = ntq * a.n_q_local;
+  const bool tr0 = a.trace && blockIdx.x == 0 && threadIdx.x == 0;
 
   if (tr0) a.trace[254] = globaltimer_ns();
   if (threadIdx.x == 0) {
@@ -578,6 +576,15 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem = *holder;
   const uint32_t tS[2] = {tmem, tmem + 128};
   const uint32_t tO = tmem + 256;
+  // the CTA walks (q-tile, head) items it = blockIdx.x, + gridDim.x, ...; g = the CTA's running
+  // key-tile count, so every ring barrier keeps one phase sequence across items
+  int g0 = 0, n_done = 0;
+  for (int it = static_cast<int>(blockIdx.x); it < n_items; it += static_cast<int>(gridDim.x), ++n_done) {
+  const int qt = it % ntq, qh = it / ntq;
+  const int kvh = qh * a.n_kv_local / a.n_q_local;
+  const int q0 = qt * kPBQ;
+  const int key_end = s0 + min(q0 + kPBQ, p);  // keys this tile needs: [0, key_end)
+  const int ntiles = (key_end + kPBK - 1) / kPBK;
 
   // K (or V) tile load: every paged block of the tile (indices past the request clamp to its last
   // block, so every smem byte the UMMAs read is finite; those keys are masked).  K_t is free once
@@ -596,9 +603,9 @@ __global__ void __launch_bounds__(256, 1)
   };
   const uint32_t idesc_s = make_idesc_bf16_f32(kPBQ, kPBK);
   const uint32_t idesc_o = make_idesc_bf16_f32(kPBQ, HD) | (1u << 16);  // B (V) MN-major
-  auto issue_s = [&](int t) {  // S_t = Q K_t^T into tS[t & 1]
-    const int buf = t & 1;
-    mbar_wait(&k_full[buf], (t >> 1) & 1);
+  auto issue_s = [&](int t) {  // S_t = Q K_t^T into tS[(g0 + t) & 1]
+    const int g = g0 + t, buf = g & 1;
+    mbar_wait(&k_full[buf], (g >> 1) & 1);
     tc_fence_after();
     const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + buf * L::kKV);
 #pragma unroll
@@ -615,13 +622,13 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
     for (int h = 0; h < kHalves; ++h)
       tma_load_2d_warp(sQ + h * (kPBQ * 128), &mapQ, q_full, qh * HD + h * 64, a.q_row0 + q0);
-    load_tile(0, 0, false);
-    load_tile(0, 0, true);
+    load_tile(0, g0 & 1, false);
+    load_tile(0, g0 & 1, true);
     if (ntiles > 1) {
-      load_tile(1, 1, false);
-      load_tile(1, 1, true);
+      load_tile(1, (g0 + 1) & 1, false);
+      load_tile(1, (g0 + 1) & 1, true);
     }
-    mbar_wait(q_full, 0);
+    mbar_wait(q_full, n_done & 1);
     issue_s(0);
   }
 
@@ -636,11 +643,11 @@ __global__ void __launch_bounds__(256, 1)
   const int c_key0 = static_cast<int>(chh) * 64;
 
   for (int t = 0; t < ntiles; ++t) {
-    const int buf = t & 1;
-    const bool tr = tr0 && t < 32;
+    const int g = g0 + t, buf = g & 1;
+    const bool tr = tr0 && n_done == 0 && t < 32;
     if (tr) a.trace[t * 8 + 0] = globaltimer_ns();
     if (warp == 0 && t + 1 < ntiles) issue_s(t + 1);  // overlaps this tile's softmax
-    mbar_wait(&s_done[buf], (t >> 1) & 1);
+    mbar_wait(&s_done[buf], (g >> 1) & 1);
     tc_fence_after();
     if (tr) a.trace[t * 8 + 1] = globaltimer_ns();
     if (warp == 0 && t + 2 < ntiles) load_tile(t + 2, buf, false);  // K_t consumed by S_t
@@ -672,9 +679,9 @@ __global__ void __launch_bounds__(256, 1)
     red[chh * kPBQ + r] = mt;
     // PV_{t-1} must be complete before P is overwritten and before O is rescaled
     if (t > 0) {
-      mbar_wait(o_done, (t - 1) & 1);
+      mbar_wait(o_done, (g - 1) & 1);
       tc_fence_after();
-      if (warp == 0 && t + 1 < ntiles) load_tile(t + 1, (t + 1) & 1, true);  // V_{t-1} consumed by PV_{t-1}
+      if (warp == 0 && t + 1 < ntiles) load_tile(t + 1, (g + 1) & 1, true);  // V_{t-1} consumed by PV_{t-1}
     }
     named_bar_sync(1, 256);  // both halves' maxima posted
     mt = fmaxf(mt, red[(chh ^ 1) * kPBQ + r]) * c2;
@@ -724,7 +731,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();  // P complete; S_buf reads, O rescales and red[] reads done
     if (tr) a.trace[t * 8 + 3] = globaltimer_ns();
     if (warp == 0) {  // O += P_t V_t  (TMEM accumulate)
-      mbar_wait(&v_full[buf], (t >> 1) & 1);
+      mbar_wait(&v_full[buf], (g >> 1) & 1);
       tc_fence_after();
       const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + buf * L::kKV);
 #pragma unroll
@@ -734,9 +741,9 @@ __global__ void __launch_bounds__(256, 1)
       umma_commit_warp(o_done);
     }
   }
-  mbar_wait(o_done, (ntiles - 1) & 1);
+  mbar_wait(o_done, (g0 + ntiles - 1) & 1);
   tc_fence_after();
-  if (tr0) a.trace[255] = globaltimer_ns();
+  if (tr0 && n_done == 0) a.trace[255] = globaltimer_ns();
   red[chh * kPBQ + r] = l;
   named_bar_sync(1, 256);
   const float inv = 1.f / (l + red[(chh ^ 1) * kPBQ + r]);
@@ -763,6 +770,11 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   }
+  g0 += ntiles;
+  tc_fence_before();
+  __syncthreads();  // O / red / Q / K,V buffers free for the next item
+  tc_fence_after();
+  }  // item loop
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -819,8 +831,10 @@ cudaError_t launch_prefill_tc(const PrefillAttnArgs& a, const CUtensorMap& mq, c
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((a.p + kPBQ - 1) / kPBQ, a.n_q_local);
-  prefill_attn_tc<HD><<<grid, 256, PtcSmem<HD>::kTotal, st>>>(mq, mk, mv, a);
+  const int items = (a.p + kPBQ - 1) / kPBQ * a.n_q_local;
+  static const int cap = getenv("SARATHI_PREFILL_CTAS") ? atoi(getenv("SARATHI_PREFILL_CTAS")) : 0;  // experiment
+  const int ctas = cap > 0 ? std::min(cap, items) : items;
+  prefill_attn_tc<HD><<<ctas, 256, PtcSmem<HD>::kTotal, st>>>(mq, mk, mv, a);
   return cudaGetLastError();
 }
 

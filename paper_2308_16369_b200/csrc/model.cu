@@ -495,6 +495,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   SRET(dump_h(0));
   const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
   bool pending_ar = false;  // TP: down-proj partial in `ar` not yet added to h
+  static const bool no_aux = getenv("SARATHI_NO_AUX") != nullptr;  // experiment: serial attention
   for (int l = 0; l < cfg.n_layers; ++l) {
     LayerWeights& w = layers[l];
     ob = op_begin();
@@ -537,8 +538,9 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       pa.out = o;
       pa.out_ld = q_dim_l;
       // with decodes in the batch, the chunk's attention overlaps the decode attention (side stream)
-      cudaStream_t ps = d > 0 ? aux : stream;
-      if (d > 0) {
+      const bool side = d > 0 && !no_aux;
+      cudaStream_t ps = side ? aux : stream;
+      if (side) {
         SRET(check(cudaEventRecord(ev_fork, stream), "fork"));
         SRET(check(cudaStreamWaitEvent(aux, ev_fork, 0), "fork"));
       }
@@ -568,7 +570,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       }
       op_end(SARATHI_OP_PREFILL_ATTN, ob, ps);
       ++launches;
-      if (d > 0) SRET(check(cudaEventRecord(ev_join, aux), "join"));
+      if (side) SRET(check(cudaEventRecord(ev_join, aux), "join"));
     }
     if (d > 0) {
       DecodeAttnArgs da;
@@ -610,7 +612,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       SRET(check(launch_decode_attention(da, kmap[l], vmap[l], stream), "decode attention"));
       op_end(SARATHI_OP_DECODE_ATTN, ob);
       launches += da.splits > 1 ? 2 : 1;
-      if (p > 0) SRET(check(cudaStreamWaitEvent(stream, ev_join, 0), "join"));
+      if (p > 0 && !no_aux) SRET(check(cudaStreamWaitEvent(stream, ev_join, 0), "join"));
     }
     // O-projection (postproj) + residual / TP all-reduce
     EpiParams eo;

@@ -321,8 +321,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* pfull = full + p.stages;    // leader only: the peer's stage landed (relayed)
   uint64_t* empty = pfull + p.stages;
   uint64_t* tfull = empty + p.stages;   // [2]
-  uint64_t* tempty = tfull + 2;         // [2] (leader's are the ones waited on)
-  uint32_t* holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + 2;         // [3] (leader's are the ones waited on)
+  uint32_t* holder = reinterpret_cast<uint32_t*>(tempty + 3);
   __shared__ int s_last;
 
   const uint32_t warp = warp_id_uniform();
@@ -339,10 +339,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&pfull[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 16);  // 8 epilogue warps x 2 CTAs
-    }
+    for (int b = 0; b < 2; ++b) mbar_init(&tfull[b], 1);
+    for (int b = 0; b < 3; ++b) mbar_init(&tempty[b], 16);  // 8 epilogue warps x 2 CTAs
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -356,6 +354,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *holder;
   const int ni = p.bn / p.n_mma;  // tokens per UMMA (multiple of 16, <= 256)
+  // TMEM slot ring (two UMMAs per k-step, 3 * ni <= 512): segment s accumulates into slots
+  // (2s mod 3, 2s+1 mod 3) of ni columns, so segment s+1 only needs the first half of segment s's
+  // accumulator drained (its other slot was freed a segment earlier) and the next mainloop overlaps
+  // most of the epilogue.  Otherwise: two 256-column buffers (bn <= 256) or one.
+  const bool ring = p.n_mma == 2 && 3 * ni <= 512;
   if (warp != 0) griddep_wait();  // the producer waits after prefetching its first W tiles
 
   if (warp == 0) {
@@ -423,12 +426,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       SegIter it;
       it.init(p, pair);
       int tile, kb0, kb1;
+      int uses[3] = {0, 0, 0};
       while (it.next(p, tile, kb0, kb1)) {
         const int buf = seg % p.nbuf;
         const uint32_t use = seg / p.nbuf;
-        mbar_wait_cluster(&tempty[buf], (use & 1) ^ 1);  // both CTAs' epilogues drained it
+        uint32_t d0, d1;
+        int tb_idx;  // tfull barrier of this segment
+        if (ring) {
+          const int sa = (2 * seg) % 3, sb = (2 * seg + 1) % 3;
+          for (int k : {sa, sb}) {  // both CTAs' epilogues drained the slot's previous use
+            if (uses[k]) mbar_wait_cluster(&tempty[k], (uses[k] - 1) & 1);
+            ++uses[k];
+          }
+          d0 = tmem + sa * ni;
+          d1 = tmem + sb * ni;
+          tb_idx = seg & 1;
+        } else {
+          mbar_wait_cluster(&tempty[buf], (use & 1) ^ 1);  // both CTAs' epilogues drained it
+          d0 = tmem + buf * 256;
+          d1 = d0 + ni;
+          tb_idx = buf;
+        }
         tc_fence_after();
-        const uint32_t d0 = tmem + buf * 256;
         for (int kb = kb0; kb < kb1; ++kb, ++i) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
@@ -442,11 +461,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
               umma_f16_ss_pair_warp(d0, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc, acc);
               if (p.n_mma == 2)
-                umma_f16_ss_pair_warp(d0 + ni, make_desc_k_sw128(a + k * 32),
+                umma_f16_ss_pair_warp(d1, make_desc_k_sw128(a + k * 32),
                                       make_desc_k_sw128(b + (ni / 2) * 128 + k * 32), idesc, acc);
             }
             umma_commit_pair_mc_warp(&empty[s], 0x3);
-            if (kb == kb1 - 1) umma_commit_pair_mc_warp(&tfull[buf], 0x3);
+            if (kb == kb1 - 1) umma_commit_pair_mc_warp(&tfull[tb_idx], 0x3);
           }
           if (++s == p.stages) {
             s = 0;
@@ -482,10 +501,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool direct = (kb0 == 0 && kb1 == p.KB) || ep.mode == EPI_ADD_F32;
       QkvLane ql{};
       if (rope_mode) ql = qkv_lane(ep, mt, quarter, lane);
-      auto release_tmem = [&]() {
+      const int nchunks = (tvalid + 15) / 16;
+      // accumulator column of chunk ch and the TMEM releases this warp owes (see `ring`)
+      const int nA = ring ? ni / 16 : (1 << 30);
+      const int sA = (2 * seg) % 3, sB = (2 * seg + 1) % 3;
+      auto tcol = [&](int ch) -> uint32_t {
+        if (!ring) return static_cast<uint32_t>(buf * 256 + ch * 16);
+        return static_cast<uint32_t>(ch < nA ? sA * ni + ch * 16 : sB * ni + (ch - nA) * 16);
+      };
+      auto arrive_slot = [&](int k) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(tempty_leader + buf * 8);
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + k * 8);
+      };
+      auto last_of = [&](int lim) {  // this warp's last chunk below lim (-1 if none)
+        if (lim <= eh) return -1;
+        return eh + ((lim - 1 - eh) / 2) * 2;
+      };
+      const int lastA = last_of(min(nA, nchunks)), lastAll = last_of(nchunks);
+      auto release_tmem = [&]() {  // everything this warp owes for the segment
+        if (ring) {
+          arrive_slot(sA);
+          arrive_slot(sB);
+        } else {
+          arrive_slot(buf);
+        }
+      };
+      auto after_load = [&](int c) {  // chunk c's accumulator is in registers
+        if (ring) {
+          if (c == lastA) arrive_slot(sA);
+          if (c == lastAll) arrive_slot(sB);  // (with A when this warp has no half-B chunk)
+        } else if (c == lastAll) {
+          arrive_slot(buf);
+        }
       };
       if (rope_mode) {  // stage per-token metadata for the fused KV append
         named_bar_sync(2, kEpiThreads);
@@ -504,25 +552,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         named_bar_sync(2, kEpiThreads);
       }
-      if (lane == 0) mbar_wait(&tfull[buf], use & 1);
+      if (lane == 0) {
+        if (ring)
+          mbar_wait(&tfull[seg & 1], (seg >> 1) & 1);
+        else
+          mbar_wait(&tfull[buf], use & 1);
+      }
       __syncwarp();
       tc_fence_after();
       if (ep.trace && tb < 2 && et == 0 && seg < 64) ep.trace[tb * 1024 + 512 + seg] = globaltimer_ns();
-      const uint32_t trow = tmem + buf * 256 + ((quarter * 32u) << 16);
-      const int nchunks = (tvalid + 15) / 16;
+      const uint32_t trow = tmem + ((quarter * 32u) << 16);
       if (direct) {
         // software-pipelined TMEM drain: this warp's next chunk (ch + 2) is in flight while ch is emitted
         if (eh >= nchunks) {
           release_tmem();
         } else {
           uint32_t raw[16];
-          tmem_ld_32x32b_x16(trow + eh * 16, raw);
+          tmem_ld_32x32b_x16(trow + tcol(eh), raw);
           tmem_ld_wait_regs(raw);
-          if (eh + 2 >= nchunks) release_tmem();
+          after_load(eh);
           for (int ch = eh; ch < nchunks; ch += 2) {
             uint32_t nraw[16];
             const bool more = ch + 2 < nchunks;
-            if (more) tmem_ld_32x32b_x16(trow + (ch + 2) * 16, nraw);
+            if (more) tmem_ld_32x32b_x16(trow + tcol(ch + 2), nraw);
             float v[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
@@ -532,7 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               ep.trace[tb * 1024 + 640 + ch] = globaltimer_ns();
             if (more) {
               tmem_ld_wait_regs(nraw);
-              if (ch + 4 >= nchunks) release_tmem();
+              after_load(ch + 2);
 #pragma unroll
               for (int j = 0; j < 16; ++j) raw[j] = nraw[j];
             }
@@ -555,13 +607,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           // TMEM drain pipelined like the direct path; TMEM is released right after the last load
           uint32_t raw[16];
-          tmem_ld_32x32b_x16(trow + eh * 16, raw);
+          tmem_ld_32x32b_x16(trow + tcol(eh), raw);
           tmem_ld_wait_regs(raw);
-          if (eh + 2 >= nchunks) release_tmem();
+          after_load(eh);
           for (int ch = eh; ch < nchunks; ch += 2) {
             uint32_t nraw[16];
             const bool more = ch + 2 < nchunks;
-            if (more) tmem_ld_32x32b_x16(trow + (ch + 2) * 16, nraw);
+            if (more) tmem_ld_32x32b_x16(trow + tcol(ch + 2), nraw);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               __stcg(reinterpret_cast<float4*>(wsp + ch * 2048 + j * 128),
@@ -569,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  __uint_as_float(raw[4 * j + 2]), __uint_as_float(raw[4 * j + 3])));
             if (more) {
               tmem_ld_wait_regs(nraw);
-              if (ch + 4 >= nchunks) release_tmem();
+              after_load(ch + 2);
 #pragma unroll
               for (int j = 0; j < 16; ++j) raw[j] = nraw[j];
             }
@@ -727,7 +779,9 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
     dp_per = 0;
   } else if (tiles <= P) {
     const int sk_pairs = static_cast<int>(std::min<long long>(P, std::max<long long>(1, static_cast<long long>(tiles) * KB / 4)));
-    const double sk_units = std::ceil(static_cast<double>(tiles) * KB / sk_pairs) + 0.5 * KB;
+    // cost model in k-block units: a split tile adds a partial write + reduction ~ sk_cost * KB
+    static const double sk_cost = getenv("SARATHI_GEMM_SK_COST") ? atof(getenv("SARATHI_GEMM_SK_COST")) : 0.5;
+    const double sk_units = std::ceil(static_cast<double>(tiles) * KB / sk_pairs) + sk_cost * KB;
     if (KB <= sk_units) {
       pairs = tiles;
       sk_tiles = 0;
@@ -853,7 +907,7 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   kp.stages = pl.stages;
   kp.nbuf = pl.nbuf;
   kp.max_slots = pl.max_slots;
-  kp.tmem_cols = pl.nbuf == 2 ? 512 : pow2_cols(pl.bn);
+  kp.tmem_cols = (pl.nbuf == 2 || (pl.n_mma == 2 && 3 * (pl.bn / 2) <= 512)) ? 512 : pow2_cols(pl.bn);
   kp.ring_bytes = static_cast<uint32_t>(pl.stages * (kABytes + static_cast<size_t>(pl.bn / 2) * kBK * 2));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pl.ctas);

@@ -601,6 +601,8 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       {
         const size_t blk = static_cast<size_t>(block_size) * hd * 2;  // K (or V) block bytes
         da.stages = static_cast<int>(std::max<size_t>(2, std::min<size_t>(4, (104 * 1024) / (2 * blk))));
+        static const int st_env = getenv("SARATHI_DECODE_STAGES") ? atoi(getenv("SARATHI_DECODE_STAGES")) : 0;
+        if (st_env >= 2) da.stages = st_env;  // experiment
       }
       static const int dec_dbg = getenv("SARATHI_DECODE_DBG") ? atoi(getenv("SARATHI_DECODE_DBG")) : 0;
       da.dbg = dec_dbg;

@@ -774,7 +774,9 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
     // number of ways (pairs = tiles * floor(P / tiles)) so each pair's k-range lies inside ONE tile:
     // one red.add epilogue per pair instead of two for ranges straddling a tile boundary
     pairs = static_cast<int>(std::min<long long>(P, std::max<long long>(1, static_cast<long long>(tiles) * KB / 4)));
-    if (tiles <= P && !getenv("SARATHI_GEMM_SK_ANY")) pairs = tiles * std::max(1, std::min(P / tiles, KB / 4));
+    // (only for wide token tiles: with small bn the red.add epilogue is cheap and every pair counts)
+    if (tiles <= P && pl.bn >= 128 && !getenv("SARATHI_GEMM_SK_ANY"))
+      pairs = tiles * std::max(1, std::min(P / tiles, KB / 4));
     sk_tiles = tiles;
     dp_per = 0;
   } else if (tiles <= P) {

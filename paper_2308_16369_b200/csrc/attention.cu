@@ -2,18 +2,19 @@
 // the prefill and decodes happen separately. The attention operation for decode requests is
 // batched together, while the attention in prefill chunk is processed separately").
 //
-//  * decode_attention: one query per decode request against its paged KV (keys [0, ctx-1]),
-//    split-K over the sequence; each CTA owns (request, kv head, split) and streams whole
-//    contiguous KV blocks ([bs x hd] bf16, 16 KB at bs=64, hd=128) into a shared-memory ring with
-//    cp.async.bulk + mbarrier (TMA bulk engine), computes q.k with 16-lane dot products and
-//    warp-shuffle reductions, and runs the online softmax in fp32 (exp2 domain).  All G = n_q/n_kv
-//    query heads of a GQA group share one KV stream.  Partial (o, lse) per split are merged by
-//    decode_combine.  HBM-bound by design (decode attention "does not benefit
-//    from batch size").
-//  * prefill_attention: the chunk's p queries at positions s..s+p-1 against keys [0, s+i]
-//    (progressive causal mask, PAPER.md L362-369 Fig. fig-attn-chunk-prefills; inclusive,
-//    reading O-9) over the request's paged cache (prefix + the chunk itself, appended by the
-//    QKV epilogue).  Flash-style online softmax with mma.sync m16n8k16 bf16 (first version).
+//  * decode_attn_mma: one query per decode request against its paged KV (keys [0, ctx-1]), split-K
+//    over the sequence when there are few requests; each CTA owns (request, kv head, split), a
+//    producer warp TMA-loads whole (block, head) K and V tiles (SW128) into a 3-stage ring, and 4
+//    compute warps run QK^T / PV with mma.sync (the G query heads of a GQA group are the MMA rows)
+//    and a per-warp online softmax merged once.  Partial (o, lse) per split are merged by
+//    decode_combine.  HBM-bound by design (decode attention "does not benefit from
+//    batch size"); it streams at ~0.97 of the measured HBM copy bandwidth.
+//  * prefill_attn_tc: the chunk's p queries at positions s..s+p-1 against keys [0, s+i]
+//    (progressive causal mask, PAPER.md L362-369 Fig. fig-attn-chunk-prefills; inclusive, reading
+//    O-9) over the request's paged cache (prefix + the chunk itself, appended by the QKV epilogue),
+//    on the 5th-gen tensor cores: S and O accumulate in TMEM, P goes through shared memory.
+//  * prefill_attn_kernel: the mma.sync flash kernel, kept for block sizes the 128-key tcgen05 tile
+//    does not divide.
 #include "common.cuh"
 #include "kernels.cuh"
 #include "gemm.cuh"

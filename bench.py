@@ -228,6 +228,7 @@ def ours(args):
     for _ in range(args.steps):
         step(prefill, decodes)
     ops = m.op_times(reset=True)
+    kops = m.op_kernel_times(reset=True)  # in-kernel device spans of the same GEMM launches
     # the same decodes without the chunk: decode attention alone on the GPU (in the hybrid step the
     # chunked-prefill attention runs beside it on a side stream and shares the SMs)
     for _ in range(args.steps):
@@ -284,6 +285,13 @@ def ours(args):
                    "weight_gbs": round(byts / avg / 1e9, 1) if avg else 0,
                    "frac_tensor": round(flops / avg / 1e12 / sus, 3) if avg else 0,
                    "frac_tensor_burst": round(flops / avg / 1e12 / peaks["bf16_tflops"], 3) if avg else 0}
+        # the event-timed figure above includes launch gaps and event overhead of the profiled pass;
+        # the kernel's own device span (first CTA start -> last CTA end, globaltimer) beside it
+        kt_ms, kn = kops.get(k, (0.0, 0))
+        if kn:
+            kavg = kt_ms / kn / 1e3
+            gemm[k]["us_kernel"] = round(kavg * 1e6, 2)
+            gemm[k]["frac_tensor_kernel"] = round(flops / kavg / 1e12 / sus, 3)
     per_layer_ops = {k: {"ms_total": round(v[0], 3), "launches": v[1]} for k, v in ops.items() if v[1]}
     traffic = ncu_traffic("decode_attention", args.workload)
     roofline = {"kernel": "decode_attention", "bound": "hbm", "achieved": round(da_gbs, 1),

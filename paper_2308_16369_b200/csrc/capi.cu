@@ -148,6 +148,21 @@ int sarathi_op_times(sarathi_model* m, double* ms_out, int64_t* counts_out, int3
   return SARATHI_OK;
 }
 
+int sarathi_op_kernel_times(sarathi_model* m, double* ms_out, int64_t* counts_out, int32_t n, int32_t reset) {
+  if (!m || !ms_out || !counts_out || n < SARATHI_NUM_OPS) return fail(SARATHI_EINVAL, "op_kernel_times: bad argument");
+  const sarathi::Status s = m->m.collect_op_times();
+  if (s.code != SARATHI_OK) return from(s);
+  for (int i = 0; i < SARATHI_NUM_OPS; ++i) {
+    ms_out[i] = m->m.op_kms[i];
+    counts_out[i] = m->m.op_kcount[i];
+    if (reset) {
+      m->m.op_kms[i] = 0;
+      m->m.op_kcount[i] = 0;
+    }
+  }
+  return SARATHI_OK;
+}
+
 int sarathi_run_hybrid_batch(sarathi_model* m, const sarathi_prefill_chunk* prefill, const sarathi_decode_set* decodes,
                              float* logits, int32_t flags) {
   if (!m) return fail(SARATHI_EINVAL, "run_hybrid_batch: NULL model");

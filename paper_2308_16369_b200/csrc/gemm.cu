@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();   // 0 = leader (issues the pair MMAs)
   griddep_launch_dependents();
+  if (ep.span_start && threadIdx.x == 0) atomicMin(ep.span_start, globaltimer_ns());
   const int pair = blockIdx.x >> 1;
   // debug trace: CTA pair (dbg >> 8) records its timeline (tb = 0 / 1 for its two CTAs)
   const int tb = static_cast<int>(blockIdx.x) - 2 * (ep.dbg >> 8);
@@ -685,6 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (ep.span_end && threadIdx.x == 0) atomicMax(ep.span_end, globaltimer_ns());
   if (ep.trace && threadIdx.x == 0) {
     ep.trace[2048 + blockIdx.x] = globaltimer_ns();  // per-CTA end (debug)
     if (blockIdx.x == 0) ep.trace[2047] = 1;

@@ -36,6 +36,8 @@ struct EpiParams {
   int* counters = nullptr;
   // debug: globaltimer stamps of the first CTA pair (producer issue / MMA full-wake / epilogue wake)
   unsigned long long* trace = nullptr;
+  unsigned long long* span_start = nullptr;  // profiling: atomicMin of CTA start times (globaltimer)
+  unsigned long long* span_end = nullptr;    // profiling: atomicMax of CTA end times
   int dbg = 0;  // debug: bit0 skip X loads, bit1 skip W loads, bit2 skip whole-tile epilogue stores (timing experiments only; results invalid)
 };
 

@@ -316,7 +316,7 @@ Status Model::alloc_kv(int64_t nb, int32_t bs) {
   return Status::ok();
 }
 
-Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, int N, const EpiParams& ep_in) {
+Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, int N, const EpiParams& ep_in, int op) {
   const bool atomic = ep_in.mode == EPI_ADD_F32;
   auto pk = std::make_tuple(M, N, K * 2 + (atomic ? 1 : 0));
   auto it = plans.find(pk);
@@ -333,6 +333,18 @@ Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, 
   ep.ws = gemm_ws;
   ep.counters = gemm_counters;
   ++launches;
+  if (profiling && op >= 0) {  // device span of this launch (sarathi_op_kernel_times)
+    if (!span_buf) {
+      SRET(dalloc(&span_buf, 2 * kSpanCap));
+      SRET(check(cudaMemsetAsync(span_buf, 0xFF, kSpanCap * 8, stream), "span init"));
+      SRET(check(cudaMemsetAsync(span_buf + kSpanCap, 0, kSpanCap * 8, stream), "span init"));
+    }
+    if (static_cast<int>(span_ops.size()) < kSpanCap) {
+      ep.span_start = span_buf + span_ops.size();
+      ep.span_end = span_buf + kSpanCap + span_ops.size();
+      span_ops.push_back(op);
+    }
+  }
   // debug: SARATHI_MODEL_TRACE=<epilogue mode>:<N> traces the first such launch with N tokens
   static const char* trace_env = getenv("SARATHI_MODEL_TRACE");
   static bool traced = false;
@@ -384,6 +396,20 @@ Status Model::collect_op_times() {
   }
   pending_ops.clear();
   ev_used = 0;
+  if (!span_ops.empty()) {
+    std::vector<unsigned long long> hs(2 * kSpanCap);
+    SRET(check(cudaMemcpy(hs.data(), span_buf, hs.size() * 8, cudaMemcpyDeviceToHost), "span read"));
+    for (size_t i = 0; i < span_ops.size(); ++i) {
+      const unsigned long long a = hs[i], b = hs[kSpanCap + i];
+      if (b > a) {
+        op_kms[span_ops[i]] += (b - a) * 1e-6;
+        op_kcount[span_ops[i]] += 1;
+      }
+    }
+    span_ops.clear();
+    SRET(check(cudaMemsetAsync(span_buf, 0xFF, kSpanCap * 8, stream), "span init"));
+    SRET(check(cudaMemsetAsync(span_buf + kSpanCap, 0, kSpanCap * 8, stream), "span init"));
+  }
   return Status::ok();
 }
 
@@ -518,7 +544,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     e.n_kv_local = nkv_l;
     e.block_size = block_size;
     ob = op_begin();
-    SRET(gemm(w.m_qkv, qkv_rows, H, a, H, T, e));
+    SRET(gemm(w.m_qkv, qkv_rows, H, a, H, T, e, SARATHI_OP_GEMM_QKV));
     op_end(SARATHI_OP_GEMM_QKV, ob);
     if (p > 0) {
       PrefillAttnArgs pa;
@@ -628,7 +654,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       eo.ldo = H;
     }
     ob = op_begin();
-    SRET(gemm(w.m_o, H, q_dim_l, o, q_dim_l, T, eo));
+    SRET(gemm(w.m_o, H, q_dim_l, o, q_dim_l, T, eo, SARATHI_OP_GEMM_O));
     op_end(SARATHI_OP_GEMM_O, ob);
     if (world > 1) {
       ob = op_begin();
@@ -645,7 +671,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     ef.out = f;
     ef.ldo = h2_l;
     ob = op_begin();
-    SRET(gemm(w.m_gu, gu_rows, H, a, H, T, ef));
+    SRET(gemm(w.m_gu, gu_rows, H, a, H, T, ef, SARATHI_OP_GEMM_GATE_UP));
     op_end(SARATHI_OP_GEMM_GATE_UP, ob);
     EpiParams ed;
     if (world == 1) {
@@ -658,7 +684,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       ed.ldo = H;
     }
     ob = op_begin();
-    SRET(gemm(w.m_down, H, h2_l, f, h2_l, T, ed));
+    SRET(gemm(w.m_down, H, h2_l, f, h2_l, T, ed, SARATHI_OP_GEMM_DOWN));
     op_end(SARATHI_OP_GEMM_DOWN, ob);
     if (world > 1) {
       ob = op_begin();

@@ -106,6 +106,12 @@ struct Model {
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending_ops;
   double op_ms[SARATHI_NUM_OPS] = {0};
   int64_t op_count[SARATHI_NUM_OPS] = {0};
+  // in-kernel device spans of profiled GEMM launches (first CTA start -> last CTA end, globaltimer)
+  static constexpr int kSpanCap = 4096;
+  unsigned long long* span_buf = nullptr;  // [kSpanCap] starts (atomicMin) | [kSpanCap] ends (atomicMax)
+  std::vector<int> span_ops;
+  double op_kms[SARATHI_NUM_OPS] = {0};
+  int64_t op_kcount[SARATHI_NUM_OPS] = {0};
   cudaEvent_t op_begin(cudaStream_t s = nullptr);
   void op_end(int op, cudaEvent_t b, cudaStream_t s = nullptr);
   Status collect_op_times();
@@ -116,7 +122,7 @@ struct Model {
   void destroy();
 
   // helpers
-  Status gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, int N, const EpiParams& ep);
+  Status gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, int N, const EpiParams& ep, int op = -1);
   Status check(cudaError_t e, const char* what);
   template <typename T>
   Status dalloc(T** p, size_t count);

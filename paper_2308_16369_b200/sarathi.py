@@ -32,7 +32,7 @@ EXPORTS = [
     "sarathi_launch_count", "sarathi_last_error", "sarathi_sched_create", "sarathi_sched_destroy",
     "sarathi_sched_submit", "sarathi_sched_next", "sarathi_sched_complete", "sarathi_sched_idle_step",
     "sarathi_sched_done", "sarathi_sched_block_table", "sarathi_op_gemm", "sarathi_op_rmsnorm",
-    "sarathi_request_truncate", "sarathi_last_io_bytes", "sarathi_set_profiling", "sarathi_op_times",
+    "sarathi_request_truncate", "sarathi_last_io_bytes", "sarathi_set_profiling", "sarathi_op_times", "sarathi_op_kernel_times",
     "sarathi_op_pack_weight", "sarathi_shard_map",
 ]
 GEMM_W_PACKED = 0x100
@@ -107,6 +107,7 @@ def _load() -> C.CDLL:
         "sarathi_last_io_bytes": [VP, P(I64), P(I64)],
         "sarathi_set_profiling": [VP, I32],
         "sarathi_op_times": [VP, P(C.c_double), P(I64), I32, I32],
+        "sarathi_op_kernel_times": [VP, P(C.c_double), P(I64), I32, I32],
         "sarathi_op_pack_weight": [VP, VP, I32, I32, VP],
         "sarathi_shard_map": [P(ModelConfigC), I32, I32, I32, I32, P(I32), P(F), P(I64), I32, P(I32), P(I32)],
     }
@@ -255,6 +256,13 @@ class Model:
         ms = np.zeros(len(OP_NAMES), dtype=np.float64)
         cnt = np.zeros(len(OP_NAMES), dtype=np.int64)
         _check(lib.sarathi_op_times(self.h, _p(ms, C.c_double), _p(cnt, C.c_int64), len(OP_NAMES), int(reset)))
+        return {n: (float(ms[i]), int(cnt[i])) for i, n in enumerate(OP_NAMES)}
+
+    def op_kernel_times(self, reset: bool = True):
+        """{op name: (total ms, launches)} of in-kernel device spans (GEMMs) since the last reset."""
+        ms = np.zeros(len(OP_NAMES), dtype=np.float64)
+        cnt = np.zeros(len(OP_NAMES), dtype=np.int64)
+        _check(lib.sarathi_op_kernel_times(self.h, _p(ms, C.c_double), _p(cnt, C.c_int64), len(OP_NAMES), int(reset)))
         return {n: (float(ms[i]), int(cnt[i])) for i, n in enumerate(OP_NAMES)}
 
     def slot_mapping(self) -> np.ndarray:

@@ -53,6 +53,11 @@ SARATHI_DEVICE void cp_async16(uint32_t dst, const void* src, bool valid) {
   const int sz = valid ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(sz) : "memory");
 }
+SARATHI_DEVICE float ex2_approx(float x) {  // 2^x, MUFU.EX2 (x = -inf -> 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 SARATHI_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 SARATHI_DEVICE void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -190,22 +195,28 @@ __global__ void __launch_bounds__(160)
           sacc[n][e] = v;
           mx[e >> 1] = fmaxf(mx[e >> 1], v);
         }
-      float sc[2];
+      // lazily refreshed running max (FA4 rule): keep a stale m until the group max exceeds it by
+      // more than 8 (p <= 2^8), so the O / l rescale runs only when some lane's max really moved
+      float sc[2] = {1.f, 1.f};
+      bool need = false;
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
         mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-        const float mnew = fmaxf(mrow[r], mx[r]);
-        sc[r] = (mnew == -INFINITY) ? 1.f : exp2f(mrow[r] - mnew);
-        mrow[r] = mnew;
+        if (mx[r] > mrow[r] + 8.f) {  // also the first finite max (mrow = -inf)
+          sc[r] = (mrow[r] == -INFINITY) ? 1.f : exp2f(mrow[r] - mx[r]);
+          mrow[r] = mx[r];
+          need = true;
+        }
       }
+      const bool rescale = __any_sync(0xffffffffu, need);
       float rs[2] = {0.f, 0.f};
 #pragma unroll
       for (int n = 0; n < 2; ++n)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float m = mrow[e >> 1];
-          const float pv = (m == -INFINITY) ? 0.f : exp2f(sacc[n][e] - m);
+          const float pv = (m == -INFINITY) ? 0.f : ex2_approx(sacc[n][e] - m);
           sacc[n][e] = pv;
           rs[e >> 1] += pv;
         }
@@ -215,12 +226,14 @@ __global__ void __launch_bounds__(160)
         rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], 2);
         lrow[r] = lrow[r] * sc[r] + rs[r];
       }
+      if (rescale) {
 #pragma unroll
-      for (int n = 0; n < HD / 8; ++n) {
-        o[n][0] *= sc[0];
-        o[n][1] *= sc[0];
-        o[n][2] *= sc[1];
-        o[n][3] *= sc[1];
+        for (int n = 0; n < HD / 8; ++n) {
+          o[n][0] *= sc[0];
+          o[n][1] *= sc[0];
+          o[n][2] *= sc[1];
+          o[n][3] *= sc[1];
+        }
       }
       uint32_t pa[4];
       pa[0] = pack_bf16x2(sacc[0][0], sacc[0][1]);
@@ -524,11 +537,6 @@ struct PtcSmem {
   static constexpr uint32_t kTotal = kQ + 4 * kKV + kP + kRed + 256 + 1024;  // + barriers + align slack
 };
 
-SARATHI_DEVICE float ex2_approx(float x) {  // 2^x, MUFU.EX2 (x = -inf -> 0)
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 // 256 threads: warp w owns TMEM lane quarter (w & 3) -> query rows 32(w&3)..+31, and column half
 // ch = w >> 2 of every S tile (keys 64ch..64ch+63) and of O (dims (hd/2)ch..); the two halves of a

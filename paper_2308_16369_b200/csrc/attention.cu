@@ -184,49 +184,32 @@ __global__ void __launch_bounds__(160)
         mma_bf16_16816(sacc[0], qf[kk], b0r, b1r);
         mma_bf16_16816(sacc[1], qf[kk], b2r, b3r);
       }
-      // mask keys >= ctx, scale to log2 domain, online softmax per row
+      // scale to the log2 domain; keys >= ctx masked (only the request's last block has any)
       float mx[2] = {-INFINITY, -INFINITY};
+      const bool tail = key_base + bs > ctx;
 #pragma unroll
       for (int n = 0; n < 2; ++n)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int key = key_base + k0 + n * 8 + 2 * tig + (e & 1);
-          const float v = key < ctx ? sacc[n][e] * sl2 : -INFINITY;
+          const float v = (!tail || key < ctx) ? sacc[n][e] * sl2 : -INFINITY;
           sacc[n][e] = v;
           mx[e >> 1] = fmaxf(mx[e >> 1], v);
         }
-      // lazily refreshed running max (FA4 rule): keep a stale m until the group max exceeds it by
-      // more than 8 (p <= 2^8), so the O / l rescale runs only when some lane's max really moved
+      // lazily refreshed running max (FA4 rule): a row keeps a stale m until its max exceeds it by
+      // more than 8 (p <= 2^8).  The quad reduction and the O rescale run only when some lane of the
+      // warp saw such a max; the row sums stay per-lane partials (reduced once, at the merge).
       float sc[2] = {1.f, 1.f};
-      bool need = false;
+      if (__any_sync(0xffffffffu, mx[0] > mrow[0] + 8.f || mx[1] > mrow[1] + 8.f)) {
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-        if (mx[r] > mrow[r] + 8.f) {  // also the first finite max (mrow = -inf)
-          sc[r] = (mrow[r] == -INFINITY) ? 1.f : exp2f(mrow[r] - mx[r]);
-          mrow[r] = mx[r];
-          need = true;
+        for (int r = 0; r < 2; ++r) {
+          mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+          mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+          if (mx[r] > mrow[r] + 8.f) {  // also the first finite max (mrow = -inf); quad-uniform
+            sc[r] = (mrow[r] == -INFINITY) ? 1.f : exp2f(mrow[r] - mx[r]);
+            mrow[r] = mx[r];
+          }
         }
-      }
-      const bool rescale = __any_sync(0xffffffffu, need);
-      float rs[2] = {0.f, 0.f};
-#pragma unroll
-      for (int n = 0; n < 2; ++n)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float m = mrow[e >> 1];
-          const float pv = (m == -INFINITY) ? 0.f : ex2_approx(sacc[n][e] - m);
-          sacc[n][e] = pv;
-          rs[e >> 1] += pv;
-        }
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], 1);
-        rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], 2);
-        lrow[r] = lrow[r] * sc[r] + rs[r];
-      }
-      if (rescale) {
 #pragma unroll
         for (int n = 0; n < HD / 8; ++n) {
           o[n][0] *= sc[0];
@@ -235,6 +218,15 @@ __global__ void __launch_bounds__(160)
           o[n][3] *= sc[1];
         }
       }
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float m = mrow[e >> 1];
+          const float pv = (m == -INFINITY) ? 0.f : ex2_approx(sacc[n][e] - m);
+          sacc[n][e] = pv;
+          lrow[e >> 1] = (e & 1) || n ? lrow[e >> 1] + pv : lrow[e >> 1] * sc[e >> 1] + pv;
+        }
       uint32_t pa[4];
       pa[0] = pack_bf16x2(sacc[0][0], sacc[0][1]);
       pa[1] = pack_bf16x2(sacc[0][2], sacc[0][3]);
@@ -260,6 +252,11 @@ __global__ void __launch_bounds__(160)
   }
 
   // ---------------- merge the 4 warps' partial softmax states ----------------
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {  // per-lane partial row sums -> the row's sum over its 4 lanes
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
+  }
   named_bar_sync(1, 128);  // all compute warps done with the ring
   float* sm_m = reinterpret_cast<float*>(smem);  // [4][16]
   float* sm_l = sm_m + 64;                       // [4][16]

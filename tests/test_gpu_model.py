@@ -118,7 +118,8 @@ def test_default_rows_and_errors_leave_state_unchanged(S):
     m.close()
 
 
-@pytest.mark.parametrize("hd,n_kv,C,bs", [(128, 2, 300, 64), (64, 8, 200, 16), (128, 4, 260, 128)])
+@pytest.mark.parametrize("hd,n_kv,C,bs", [(128, 2, 300, 64), (64, 8, 200, 16), (128, 4, 260, 128),
+                                           (128, 4, 700, 64)])  # the last: one 700-token chunk, T > 512
 def test_prefill_attention_multitile(S, hd, n_kv, C, bs):
     """Chunks larger than one 128-query tile and prefixes spanning several 128-key tiles (the
     tcgen05 prefill kernel: ragged last q-tile, causal diagonal inside a key tile, K/V ring refills,
@@ -131,3 +132,5 @@ def test_prefill_attention_multitile(S, hd, n_kv, C, bs):
                             weight_seed=7, max_tokens=C + 3)
     _check(steps)
     assert max(p[0][2] for p in (s.plan for s in steps) if p[0] is not None) > 128
+    if C > 512:  # GEMMs with two token tiles (T > 512) and prefill q-tiles 0..5
+        assert max(len(s.gpu_slots) for s in steps) > 512

@@ -410,10 +410,11 @@ int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t 
   if (mode == EPI_SILU_MUL && M % 128) return fail(SARATHI_EINVAL, "op_gemm: SiLU mode needs M % 128 == 0");
   static float* ws = nullptr;
   static int* ctr = nullptr;
-  static size_t ws_floats = static_cast<size_t>(32) << 20;
+  static size_t ws_floats = static_cast<size_t>(64) << 20;  // lower half slot partials, upper half red.add
   if (!ws) {
     if (cudaMalloc(&ws, ws_floats * 4) != cudaSuccess || cudaMalloc(&ctr, (1 << 16) * 4) != cudaSuccess ||
-        cudaMemset(ctr, 0, (1 << 16) * 4) != cudaSuccess)
+        cudaMemset(ctr, 0, (1 << 16) * 4) != cudaSuccess ||
+        cudaMemset(ws + ws_floats / 2, 0, ws_floats / 2 * 4) != cudaSuccess)
       return fail(SARATHI_ECUDA, "op_gemm: workspace allocation failed");
   }
   int dev = 0, sms = 148;
@@ -449,6 +450,7 @@ int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t 
   ep.out = out;
   ep.ldo = mode == EPI_SILU_MUL ? M / 2 : M;
   ep.ws = ws;
+  ep.ws_red = ws + ws_floats / 2;
   ep.counters = ctr;
   if (const char* d = getenv("SARATHI_GEMM_DBG")) ep.dbg = atoi(d);
   static unsigned long long* trace = nullptr;

@@ -54,6 +54,7 @@ struct KParams {
   int stages;
   int nbuf;               // TMEM accumulator buffers (2 if bn <= 256)
   int max_slots;          // partial slots per tile
+  int red_partials;       // split tiles accumulate in ONE zeroed fp32 slot by red.add (many contributors)
   uint32_t tmem_cols;
   uint32_t ring_bytes;
 };
@@ -602,7 +603,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // partial layout [chunk][lane quarter][token quad j][lane][4 tokens] (fp32): a thread keeps its
         // row's 16 tokens as four float4, and each warp-wide 16-B vector access is 512 contiguous bytes
         const size_t qoff = static_cast<size_t>(quarter) * 512 + lane * 4;  // + (ch * 4 * 512) + j * 128
-        float* wsp = ep.ws + (tile128 * p.max_slots + slot) * tile_elems + qoff;
+        float* wsp = p.red_partials ? ep.ws_red + tile128 * tile_elems + qoff
+                                    : ep.ws + (tile128 * p.max_slots + slot) * tile_elems + qoff;
         if (eh >= nchunks) {
           release_tmem();
         } else {
@@ -616,10 +618,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool more = ch + 2 < nchunks;
             if (more) tmem_ld_32x32b_x16(trow + tcol(ch + 2), nraw);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              __stcg(reinterpret_cast<float4*>(wsp + ch * 2048 + j * 128),
-                     make_float4(__uint_as_float(raw[4 * j]), __uint_as_float(raw[4 * j + 1]),
-                                 __uint_as_float(raw[4 * j + 2]), __uint_as_float(raw[4 * j + 3])));
+            for (int j = 0; j < 4; ++j) {
+              const float4 x = make_float4(__uint_as_float(raw[4 * j]), __uint_as_float(raw[4 * j + 1]),
+                                           __uint_as_float(raw[4 * j + 2]), __uint_as_float(raw[4 * j + 3]));
+              if (p.red_partials)
+                red_add_v4(wsp + ch * 2048 + j * 128, x);
+              else
+                __stcg(reinterpret_cast<float4*>(wsp + ch * 2048 + j * 128), x);
+            }
             if (more) {
               tmem_ld_wait_regs(nraw);
               after_load(ch + 2);
@@ -639,7 +645,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(1, kEpiThreads);
         if (s_last && eh < nchunks) {
           __threadfence();
-          const float* rowbase = ep.ws + tile128 * p.max_slots * tile_elems + qoff;
+          float* rowbase = p.red_partials ? ep.ws_red + tile128 * tile_elems + qoff
+                                          : ep.ws + tile128 * p.max_slots * tile_elems + qoff;
+          const int nsum = p.red_partials ? 1 : nslot;  // red.add already summed every contributor
           // slots summed in slot order (deterministic); slot 0 of the next chunk is in flight while
           // this chunk is summed and emitted (A/B register buffers, no copies)
           auto load1 = [&](int ch, float4 (&buf)[4]) {
@@ -655,7 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               v[4 * j + 2] = buf[j].z;
               v[4 * j + 3] = buf[j].w;
             }
-            for (int q = 1; q < nslot; ++q) {
+            for (int q = 1; q < nsum; ++q) {
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 const float4 x = __ldcg(reinterpret_cast<const float4*>(rowbase + q * tile_elems + ch * 2048 + j * 128));
@@ -676,6 +684,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (ch + 4 < nchunks) load1(ch + 4, A);
               sum_emit(ch + 2, B);
             }
+          }
+          if (p.red_partials) {  // re-zero this thread's part of the slot for the next launch
+            for (int ch = eh; ch < nchunks; ch += 2)
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                __stcg(reinterpret_cast<float4*>(rowbase + ch * 2048 + j * 128), make_float4(0.f, 0.f, 0.f, 0.f));
           }
         }
       }
@@ -812,15 +826,22 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
     return std::min(s, g);
   };
   int max_slots = slots_for(pairs);
-  // the partial reduction handles <= 4 contributors per tile (pure stream-K plans only; residual
-  // adds reduce with red.add and have no partial slots)
-  while (!atomic_epilogue && dp_per == 0 && pairs > 1 && max_slots > 4) {
+  const size_t tile_elems = static_cast<size_t>(pl.bn) * kBM;
+  const size_t tiles128 = static_cast<size_t>(pl.m_tiles) * pl.n_tiles;
+  // more than 4 contributors per split tile (few row tiles, e.g. a TP-8 rank's QKV): accumulate the
+  // partials by red.add into one zeroed fp32 slot per tile (the last contributor reads it once, runs
+  // the epilogue and re-zeroes it) instead of shrinking the grid to <= 4 slots
+  pl.red_partials = 0;
+  if (!atomic_epilogue && dp_per == 0 && max_slots > 4 && tiles128 * tile_elems <= ws_cap_floats / 2) {
+    pl.red_partials = 1;
+    max_slots = 1;
+  }
+  while (!atomic_epilogue && !pl.red_partials && dp_per == 0 && pairs > 1 && max_slots > 4) {
     --pairs;
     max_slots = slots_for(pairs);
   }
-  const size_t tile_elems = static_cast<size_t>(pl.bn) * kBM;
-  const size_t tiles128 = static_cast<size_t>(pl.m_tiles) * pl.n_tiles;
-  while (!atomic_epilogue && dp_per == 0 && pairs > 1 && tiles128 * max_slots * tile_elems > ws_cap_floats) {
+  while (!atomic_epilogue && !pl.red_partials && dp_per == 0 && pairs > 1 &&
+         tiles128 * max_slots * tile_elems > ws_cap_floats / 2) {
     pairs = std::max(1, pairs / 2);
     max_slots = slots_for(pairs);
   }
@@ -832,7 +853,7 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
   pl.max_slots = max_slots;
   pl.splits = static_cast<int>((units + pairs - 1) / pairs) + dp_per * KB;  // units per pair (informational)
   pl.kb_per_split = pl.splits;
-  pl.ws_floats = units > 0 && !atomic_epilogue ? tiles128 * max_slots * tile_elems : 0;
+  pl.ws_floats = units > 0 && !atomic_epilogue && !pl.red_partials ? tiles128 * max_slots * tile_elems : 0;
   pl.nbuf = pl.bn <= 256 ? 2 : 1;
   const size_t stage = kABytes + static_cast<size_t>(pl.bn / 2) * kBK * 2;
   const size_t budget = 226 * 1024 - 1024 - extra_smem(pl.bn);
@@ -911,6 +932,7 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   kp.stages = pl.stages;
   kp.nbuf = pl.nbuf;
   kp.max_slots = pl.max_slots;
+  kp.red_partials = pl.red_partials;
   kp.tmem_cols = (pl.nbuf == 2 || (pl.n_mma == 2 && 3 * (pl.bn / 2) <= 512)) ? 512 : pow2_cols(pl.bn);
   kp.ring_bytes = static_cast<uint32_t>(pl.stages * (kABytes + static_cast<size_t>(pl.bn / 2) * kBK * 2));
   cudaLaunchConfig_t cfg = {};

@@ -33,6 +33,7 @@ struct EpiParams {
   int block_size = 64;
   // split-K workspace (fp32 partials) + per-tile arrival counters (kept zero between launches)
   float* ws = nullptr;
+  float* ws_red = nullptr;  // zero-initialised fp32 tiles for red.add partials (kept zero between launches)
   int* counters = nullptr;
   // debug: globaltimer stamps of the first CTA pair (producer issue / MMA full-wake / epilogue wake)
   unsigned long long* trace = nullptr;
@@ -55,6 +56,7 @@ struct GemmPlan {
   int dp_per_pair = 0; // whole tiles per pair processed after the stream-K part
   int dp_extra = 0;    // pairs [0, dp_extra) take one extra whole tile
   int max_slots = 1;   // stream-K partial slots per tile
+  int red_partials = 0;  // split tiles accumulate by red.add into ONE zeroed slot (ws_red)
   int nbuf = 1;        // TMEM accumulator buffers
   int splits = 1, kb_per_split = 0;  // units per CTA (informational)
   int stages = 0;
@@ -62,6 +64,8 @@ struct GemmPlan {
   size_t ws_floats = 0;  // stream-K workspace needed
 };
 
+// Workspace convention (ws_cap_floats): slot partials use the lower half, red.add partials the
+// upper half, which the caller zeroes once (EpiParams.ws_red = ws + ws_cap_floats / 2).
 // Persistent stream-K plan for C[N x M] = X[N x K] * W[M x K]^T on `num_sms` SMs (CTA pairs,
 // tcgen05 cta_group::2).  force_pairs > 0 fixes the grid (tests use it to exercise multi-pair
 // reductions of one tile).

@@ -268,8 +268,9 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
     SRET(dalloc(&logits_local, static_cast<size_t>(Tmax) * vocab_l));
     SRET(dalloc(&logits_gather, static_cast<size_t>(world) * Tmax * vocab_l));
   }
-  gemm_ws_floats = static_cast<size_t>(48) << 20;
+  gemm_ws_floats = static_cast<size_t>(96) << 20;  // lower half: slot partials; upper half: red.add partials
   SRET(dalloc(&gemm_ws, gemm_ws_floats));
+  SRET(check(cudaMemset(gemm_ws + gemm_ws_floats / 2, 0, gemm_ws_floats / 2 * sizeof(float)), "zero ws"));
   SRET(dalloc(&gemm_counters, 1 << 16));
   SRET(check(cudaMemset(gemm_counters, 0, (1 << 16) * sizeof(int)), "memset"));
   part_cap = static_cast<size_t>(32) << 20;
@@ -331,6 +332,7 @@ Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, 
   }
   EpiParams ep = ep_in;
   ep.ws = gemm_ws;
+  ep.ws_red = gemm_ws + gemm_ws_floats / 2;
   ep.counters = gemm_counters;
   ++launches;
   if (profiling && op >= 0) {  // device span of this launch (sarathi_op_kernel_times)
@@ -616,10 +618,18 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       da.scale = scale;
       int max_nblk = 0;
       for (int j = 0; j < d; ++j) max_nblk = std::max(max_nblk, (dec->positions[j] + 1 + block_size - 1) / block_size);
+      // split the sequence until the grid fills the 2-CTA-per-SM slots in whole waves: at least one
+      // wave, and the partial last wave wastes <= 10 % of the slots (e.g. 13B TP8 rank: 64 x 5 CTAs
+      // is 1.08 waves -> 6 splits)
       const int base_ctas = d * nkv_l;
+      const int slots = 2 * num_sms;
+      auto waste = [&](int sp) {
+        const long long c = static_cast<long long>(base_ctas) * sp;
+        const long long w = (c + slots - 1) / slots;
+        return static_cast<double>(w * slots - c) / static_cast<double>(w * slots);
+      };
       int splits = 1;
-      const int target = 2 * num_sms;
-      if (base_ctas < target) splits = std::min(max_nblk, (target + base_ctas - 1) / base_ctas);
+      while (splits < max_nblk && (static_cast<long long>(base_ctas) * splits < slots || waste(splits) > 0.10)) ++splits;
       const size_t per_split = static_cast<size_t>(d) * nq_l * hd;
       splits = static_cast<int>(std::max<size_t>(1, std::min<size_t>(splits, part_cap / per_split)));
       da.blocks_per_split = (max_nblk + splits - 1) / splits;

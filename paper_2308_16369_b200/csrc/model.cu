@@ -618,18 +618,26 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       da.scale = scale;
       int max_nblk = 0;
       for (int j = 0; j < d; ++j) max_nblk = std::max(max_nblk, (dec->positions[j] + 1 + block_size - 1) / block_size);
-      // split the sequence until the grid fills the 2-CTA-per-SM slots in whole waves: at least one
-      // wave, and the partial last wave wastes <= 10 % of the slots (e.g. 13B TP8 rank: 64 x 5 CTAs
-      // is 1.08 waves -> 6 splits)
+      // split the sequence (flash-decoding) by a small cost model in microseconds: whole waves of
+      // 2-CTA-per-SM slots x (fixed per-CTA cost + blocks per split x per-block stream time), plus
+      // the combine kernel when split.  13B TP1 (2560 CTAs) stays unsplit; a 70B TP-8 rank (26
+      // requests x 1 KV head, 32 blocks) splits ~11 ways into one wave.
       const int base_ctas = d * nkv_l;
       const int slots = 2 * num_sms;
-      auto waste = [&](int sp) {
-        const long long c = static_cast<long long>(base_ctas) * sp;
-        const long long w = (c + slots - 1) / slots;
-        return static_cast<double>(w * slots - c) / static_cast<double>(w * slots);
-      };
       int splits = 1;
-      while (splits < max_nblk && (static_cast<long long>(base_ctas) * splits < slots || waste(splits) > 0.10)) ++splits;
+      double best = 1e30;
+      for (int sp = 1; sp <= max_nblk; ++sp) {
+        const int bps = (max_nblk + sp - 1) / sp;
+        const int n = (max_nblk + bps - 1) / bps;
+        if (n != sp) continue;  // same partition as a smaller split count
+        const long long ctas = static_cast<long long>(base_ctas) * n;
+        const double waves = static_cast<double>((ctas + slots - 1) / slots);
+        const double t = waves * (2.0 + 1.5 * bps) + (n > 1 ? 3.0 : 0.0);
+        if (t < best - 1e-9) {
+          best = t;
+          splits = n;
+        }
+      }
       const size_t per_split = static_cast<size_t>(d) * nq_l * hd;
       splits = static_cast<int>(std::max<size_t>(1, std::min<size_t>(splits, part_cap / per_split)));
       da.blocks_per_split = (max_nblk + splits - 1) / splits;

@@ -511,7 +511,6 @@ __global__ void __launch_bounds__(128)
 //   Issue (TMA + UMMA) is warp 0, warp-uniform with one elected lane.
 // ---------------------------------------------------------------------------
 constexpr int kPBQ = 128;  // queries per CTA
-constexpr int kPBK = 128;  // keys per tile
 
 // MN-major SW128 UMMA smem descriptor: 64-element (128 B) rows along MN, MN atoms LBO apart,
 // 8-row K groups SBO apart (CuTe canonical ((8,n),(8,k)):((1,LBO),(8,SBO)) in 16-B units).
@@ -525,32 +524,39 @@ SARATHI_DEVICE uint64_t make_desc_mn_sw128(uint32_t smem_addr, uint32_t lbo_byte
   return d;
 }
 
-template <int HD>
+// BK = keys per tile.  BK = 128 (default): 1 CTA per SM (197 KB smem at HD 128, 512 TMEM columns).
+// BK = 64: 256 TMEM columns and <= 100 KB smem (V single-buffered at HD 128), so a prefill CTA leaves
+// room on its SM for the decode-attention CTAs running concurrently on the other stream.
+template <int HD, int BK>
 struct PtcSmem {
+  static constexpr bool kVdb = BK == 128 || HD == 64;  // V double-buffered
   static constexpr uint32_t kQ = kPBQ * HD * 2;   // Q tile  [HD/64][128 rows][64] SW128
-  static constexpr uint32_t kKV = kPBK * HD * 2;  // K or V tile [HD/64][128 keys][64]
-  static constexpr uint32_t kP = kPBQ * kPBK * 2; // P [2][128 rows][64 keys]
+  static constexpr uint32_t kKV = BK * HD * 2;    // K or V tile [HD/64][BK keys][64]
+  static constexpr uint32_t kP = kPBQ * BK * 2;   // P [BK/64][128 rows][64 keys]
   static constexpr uint32_t kRed = 2 * kPBQ * 4;  // per-half row maxima / sums
-  static constexpr uint32_t kTotal = kQ + 4 * kKV + kP + kRed + 256 + 1024;  // + barriers + align slack
+  static constexpr uint32_t kTotal = kQ + (kVdb ? 4 : 3) * kKV + kP + kRed + 256 + 1024;  // + barriers + align slack
+  static constexpr uint32_t kTmemCols = BK == 128 ? 512 : 256;
 };
 
 
 // 256 threads: warp w owns TMEM lane quarter (w & 3) -> query rows 32(w&3)..+31, and column half
 // ch = w >> 2 of every S tile (keys 64ch..64ch+63) and of O (dims (hd/2)ch..); the two halves of a
 // row exchange their maxima through shared memory once per tile.
-template <int HD>
-__global__ void __launch_bounds__(256, 1)
+template <int HD, int BK>
+__global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
     prefill_attn_tc(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
                     const __grid_constant__ CUtensorMap mapV, const PrefillAttnArgs a) {
-  using L = PtcSmem<HD>;
+  using L = PtcSmem<HD, BK>;
   constexpr int kHalves = HD / 64;
   constexpr int kOC = HD / 2;  // O columns per column half
+  constexpr int kCH = BK / 2;  // S columns (keys) per column half
+  constexpr int kNC = kCH / 16;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + L::kQ;          // [2 buffers]
-  uint8_t* sV = sK + 2 * L::kKV;     // [2 buffers]
-  uint8_t* sP = sV + 2 * L::kKV;
+  uint8_t* sV = sK + 2 * L::kKV;     // [2 buffers] (kVdb) or [1]
+  uint8_t* sP = sV + (L::kVdb ? 2 : 1) * L::kKV;
   float* red = reinterpret_cast<float*>(sP + L::kP);  // [2 halves][128 rows]
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(red) + L::kRed);
   uint64_t* q_full = bars;        // 1
@@ -575,13 +581,13 @@ __global__ void __launch_bounds__(256, 1)
     for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc(holder, 512);
+  if (warp == 0) tmem_alloc(holder, L::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *holder;
-  const uint32_t tS[2] = {tmem, tmem + 128};
-  const uint32_t tO = tmem + 256;
+  const uint32_t tS[2] = {tmem, tmem + BK};
+  const uint32_t tO = tmem + 2 * BK;
   // the CTA walks (q-tile, head) items it = blockIdx.x, + gridDim.x, ...; g = the CTA's running
   // key-tile count, so every ring barrier keeps one phase sequence across items
   int g0 = 0, n_done = 0;
@@ -590,7 +596,7 @@ __global__ void __launch_bounds__(256, 1)
   const int kvh = qh * a.n_kv_local / a.n_q_local;
   const int q0 = qt * kPBQ;
   const int key_end = s0 + min(q0 + kPBQ, p);  // keys this tile needs: [0, key_end)
-  const int ntiles = (key_end + kPBK - 1) / kPBK;
+  const int ntiles = (key_end + BK - 1) / BK;
 
   // K (or V) tile load: every paged block of the tile (indices past the request clamp to its last
   // block, so every smem byte the UMMAs read is finite; those keys are masked).  K_t is free once
@@ -599,15 +605,15 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* bar = is_v ? &v_full[buf] : &k_full[buf];
     uint8_t* dst = (is_v ? sV : sK) + buf * L::kKV;
     const CUtensorMap* map = is_v ? &mapV : &mapK;
-    mbar_arrive_expect_tx_warp(bar, kPBK * HD * 2);
-    for (int kb = 0; kb < kPBK; kb += bs) {
-      const int bi = min((t * kPBK + kb) / bs, last_blk);
+    mbar_arrive_expect_tx_warp(bar, BK * HD * 2);
+    for (int kb = 0; kb < BK; kb += bs) {
+      const int bi = min((t * BK + kb) / bs, last_blk);
       const int row = (a.block_table[bi] * a.n_kv_local + kvh) * bs;
 #pragma unroll
-      for (int h = 0; h < kHalves; ++h) tma_load_2d_warp(dst + h * (kPBK * 128) + kb * 128, map, bar, h * 64, row);
+      for (int h = 0; h < kHalves; ++h) tma_load_2d_warp(dst + h * (BK * 128) + kb * 128, map, bar, h * 64, row);
     }
   };
-  const uint32_t idesc_s = make_idesc_bf16_f32(kPBQ, kPBK);
+  const uint32_t idesc_s = make_idesc_bf16_f32(kPBQ, BK);
   const uint32_t idesc_o = make_idesc_bf16_f32(kPBQ, HD) | (1u << 16);  // B (V) MN-major
   auto issue_s = [&](int t) {  // S_t = Q K_t^T into tS[(g0 + t) & 1]
     const int g = g0 + t, buf = g & 1;
@@ -617,7 +623,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
     for (int k = 0; k < HD / 16; ++k) {
       const uint32_t off = (k >> 2) * (kPBQ * 128) + (k & 3) * 32;  // hd half, 32 B step in the row
-      umma_f16_ss_warp(tS[buf], make_desc_k_sw128(qa + off), make_desc_k_sw128(kb + (k >> 2) * (kPBK * 128) + (k & 3) * 32),
+      umma_f16_ss_warp(tS[buf], make_desc_k_sw128(qa + off), make_desc_k_sw128(kb + (k >> 2) * (BK * 128) + (k & 3) * 32),
                        idesc_s, k > 0 ? 1u : 0u);
     }
     umma_commit_warp(&s_done[buf]);
@@ -629,10 +635,10 @@ __global__ void __launch_bounds__(256, 1)
     for (int h = 0; h < kHalves; ++h)
       tma_load_2d_warp(sQ + h * (kPBQ * 128), &mapQ, q_full, qh * HD + h * 64, a.q_row0 + q0);
     load_tile(0, g0 & 1, false);
-    load_tile(0, g0 & 1, true);
+    load_tile(0, L::kVdb ? (g0 & 1) : 0, true);
     if (ntiles > 1) {
       load_tile(1, (g0 + 1) & 1, false);
-      load_tile(1, (g0 + 1) & 1, true);
+      if (L::kVdb) load_tile(1, (g0 + 1) & 1, true);
     }
     mbar_wait(q_full, n_done & 1);
     issue_s(0);
@@ -645,8 +651,10 @@ __global__ void __launch_bounds__(256, 1)
   // range); O accumulates in TMEM across tiles and is rescaled there only when m moves
   float m = -INFINITY, l = 0.f;  // l: this column half's partial row sum
   const uint32_t lane_off = (quarter * 32u) << 16;
-  uint8_t* prow = sP + chh * (kPBQ * 128) + r * 128;  // this row's 64-key slice of P (k-block chh)
-  const int c_key0 = static_cast<int>(chh) * 64;
+  // this row's slice of P: k-block chh (BK 128) or 16-B chunks 4chh.. of the one k-block (BK 64)
+  uint8_t* prow = sP + (BK == 128 ? chh * (kPBQ * 128) : 0) + r * 128;
+  const int chunk0 = BK == 128 ? 0 : 4 * static_cast<int>(chh);
+  const int c_key0 = static_cast<int>(chh) * kCH;
 
   for (int t = 0; t < ntiles; ++t) {
     const int g = g0 + t, buf = g & 1;
@@ -658,17 +666,17 @@ __global__ void __launch_bounds__(256, 1)
     if (tr) a.trace[t * 8 + 1] = globaltimer_ns();
     if (warp == 0 && t + 2 < ntiles) load_tile(t + 2, buf, false);  // K_t consumed by S_t
     // this half of the S row in registers: 4 loads in flight, one wait
-    uint32_t sr[4][16];
+    uint32_t sr[kNC][16];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x16(tS[buf] + lane_off + c_key0 + c * 16, sr[c]);
+    for (int c = 0; c < kNC; ++c) tmem_ld_32x32b_x16(tS[buf] + lane_off + c_key0 + c * 16, sr[c]);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_ld_wait_regs(sr[c]);
-    const int kbase = t * kPBK + c_key0;
-    const bool need_mask = t * kPBK + kPBK - 1 > s0 + q0;  // (CTA-uniform) some key lies past a query
+    for (int c = 0; c < kNC; ++c) tmem_ld_wait_regs(sr[c]);
+    const int kbase = t * BK + c_key0;
+    const bool need_mask = t * BK + BK - 1 > s0 + q0;  // (CTA-uniform) some key lies past a query
     float mt = -INFINITY;
     if (need_mask) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < kNC; ++c)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const float v = __uint_as_float(sr[c][j]);
@@ -677,7 +685,7 @@ __global__ void __launch_bounds__(256, 1)
     } else {
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < kNC; ++c)
 #pragma unroll
         for (int j = 0; j < 16; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(sr[c][j]));
       mt = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
@@ -687,7 +695,13 @@ __global__ void __launch_bounds__(256, 1)
     if (t > 0) {
       mbar_wait(o_done, (g - 1) & 1);
       tc_fence_after();
-      if (warp == 0 && t + 1 < ntiles) load_tile(t + 1, (g + 1) & 1, true);  // V_{t-1} consumed by PV_{t-1}
+      if (warp == 0) {  // V_{t-1} consumed by PV_{t-1}
+        if (L::kVdb) {
+          if (t + 1 < ntiles) load_tile(t + 1, (g + 1) & 1, true);
+        } else {
+          load_tile(t, 0, true);
+        }
+      }
     }
     named_bar_sync(1, 256);  // both halves' maxima posted
     mt = fmaxf(mt, red[(chh ^ 1) * kPBQ + r]) * c2;
@@ -712,7 +726,7 @@ __global__ void __launch_bounds__(256, 1)
     const float mneg = -m;
     float rs4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < kNC; ++c) {
       float pv[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -722,7 +736,7 @@ __global__ void __launch_bounds__(256, 1)
       }
 #pragma unroll
       for (int h8 = 0; h8 < 2; ++h8) {
-        const int chunk = c * 2 + h8;  // 16-B chunk (8 keys) within the 128-B row
+        const int chunk = chunk0 + c * 2 + h8;  // 16-B chunk (8 keys) within the 128-B row
         uint4 w;
         w.x = pack_bf16x2(pv[h8 * 8 + 0], pv[h8 * 8 + 1]);
         w.y = pack_bf16x2(pv[h8 * 8 + 2], pv[h8 * 8 + 3]);
@@ -737,13 +751,14 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();  // P complete; S_buf reads, O rescales and red[] reads done
     if (tr) a.trace[t * 8 + 3] = globaltimer_ns();
     if (warp == 0) {  // O += P_t V_t  (TMEM accumulate)
-      mbar_wait(&v_full[buf], (g >> 1) & 1);
+      if (L::kVdb) mbar_wait(&v_full[buf], (g >> 1) & 1);
+      else mbar_wait(&v_full[0], g & 1);
       tc_fence_after();
-      const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + buf * L::kKV);
+      const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + (L::kVdb ? buf : 0) * L::kKV);
 #pragma unroll
-      for (int k = 0; k < kPBK / 16; ++k)
+      for (int k = 0; k < BK / 16; ++k)
         umma_f16_ss_warp(tO, make_desc_k_sw128(pa + (k >> 2) * (kPBQ * 128) + (k & 3) * 32),
-                         make_desc_mn_sw128(vb + k * 2048, kPBK * 128, 1024), idesc_o, (t > 0 || k > 0) ? 1u : 0u);
+                         make_desc_mn_sw128(vb + k * 2048, BK * 128, 1024), idesc_o, (t > 0 || k > 0) ? 1u : 0u);
       umma_commit_warp(o_done);
     }
   }
@@ -785,7 +800,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, L::kTmemCols);
   }
 }
 
@@ -827,20 +842,21 @@ cudaError_t launch_decode_attention(const DecodeAttnArgs& a, const CUtensorMap& 
   return cudaErrorInvalidValue;
 }
 
-template <int HD>
+template <int HD, int BK>
 cudaError_t launch_prefill_tc(const PrefillAttnArgs& a, const CUtensorMap& mq, const CUtensorMap& mk,
                               const CUtensorMap& mv, cudaStream_t st) {
+  using L = PtcSmem<HD, BK>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_attn_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(PtcSmem<HD>::kTotal));
+    cudaError_t e = cudaFuncSetAttribute(prefill_attn_tc<HD, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(L::kTotal));
     if (e != cudaSuccess) return e;
     configured = true;
   }
   const int items = (a.p + kPBQ - 1) / kPBQ * a.n_q_local;
   static const int cap = getenv("SARATHI_PREFILL_CTAS") ? atoi(getenv("SARATHI_PREFILL_CTAS")) : 0;  // experiment
   const int ctas = cap > 0 ? std::min(cap, items) : items;
-  prefill_attn_tc<HD><<<ctas, 256, PtcSmem<HD>::kTotal, st>>>(mq, mk, mv, a);
+  prefill_attn_tc<HD, BK><<<ctas, 256, L::kTotal, st>>>(mq, mk, mv, a);
   return cudaGetLastError();
 }
 
@@ -849,8 +865,16 @@ cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, const CUtensorMap
   if (a.p == 0) return cudaSuccess;
   const bool tc = qmap && kmap && vmap && (a.block_size == 16 || a.block_size == 32 || a.block_size == 64 ||
                                            a.block_size == 128);
-  if (tc && a.head_dim == 128) return launch_prefill_tc<128>(a, *qmap, *kmap, *vmap, st);
-  if (tc && a.head_dim == 64) return launch_prefill_tc<64>(a, *qmap, *kmap, *vmap, st);
+  // 128-key tiles; SARATHI_PREFILL_BK=64 selects the narrow tile (2 CTAs or a CTA + decode CTAs per
+  // SM).  Measured: TP-1 step unchanged, TP-8 rank shapes 2-4 % slower, so not the default.
+  static const bool narrow = getenv("SARATHI_PREFILL_BK") && atoi(getenv("SARATHI_PREFILL_BK")) == 64;
+  const bool bk128 = a.block_size == 128 || !narrow;
+  if (tc && a.head_dim == 128)
+    return bk128 ? launch_prefill_tc<128, 128>(a, *qmap, *kmap, *vmap, st)
+                 : launch_prefill_tc<128, 64>(a, *qmap, *kmap, *vmap, st);
+  if (tc && a.head_dim == 64)
+    return bk128 ? launch_prefill_tc<64, 128>(a, *qmap, *kmap, *vmap, st)
+                 : launch_prefill_tc<64, 64>(a, *qmap, *kmap, *vmap, st);
   // mma.sync kernel: block sizes the tcgen05 tile (128 keys) does not tile
   dim3 grid((a.p + 63) / 64, a.n_q_local);
   if (a.head_dim == 128) {

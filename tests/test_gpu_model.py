@@ -3,6 +3,9 @@ variants): logits of every row and the residual after every layer within 2e-2 re
 (north star); slot mappings, block tables and the schedule bit-exact; device-generated weights
 bit-exact to the synth spec."""
 import dataclasses
+import os
+import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -134,3 +137,16 @@ def test_prefill_attention_multitile(S, hd, n_kv, C, bs):
     assert max(p[0][2] for p in (s.plan for s in steps) if p[0] is not None) > 128
     if C > 512:  # GEMMs with two token tiles (T > 512) and prefill q-tiles 0..5
         assert max(len(s.gpu_slots) for s in steps) > 512
+
+
+@pytest.mark.skipif(os.environ.get("SARATHI_PREFILL_BK") == "64", reason="this process already runs the narrow tile")
+def test_prefill_attention_narrow_tile():
+    """The 64-key prefill tile (SARATHI_PREFILL_BK=64: single-buffered V at hd 128, 2 CTAs per SM),
+    read once per process, so the multitile cases rerun in a child process (bs 128 keeps the wide tile)."""
+    env = dict(os.environ, SARATHI_PREFILL_BK="64")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m", "gpu", "-k",
+                        "prefill_attention_multitile", "-p", "no:cacheprovider"],
+                       env=env, capture_output=True, text=True, timeout=900,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "4 passed" in r.stdout

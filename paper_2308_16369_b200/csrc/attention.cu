@@ -527,12 +527,12 @@ SARATHI_DEVICE uint64_t make_desc_mn_sw128(uint32_t smem_addr, uint32_t lbo_byte
 // BK = keys per tile.  BK = 128 (default): 1 CTA per SM (197 KB smem at HD 128, 512 TMEM columns).
 // BK = 64: 256 TMEM columns and <= 100 KB smem (V single-buffered at HD 128), so a prefill CTA leaves
 // room on its SM for the decode-attention CTAs running concurrently on the other stream.
-template <int HD, int BK>
+template <int HD, int BK, bool PT>
 struct PtcSmem {
   static constexpr bool kVdb = BK == 128 || HD == 64;  // V double-buffered
   static constexpr uint32_t kQ = kPBQ * HD * 2;   // Q tile  [HD/64][128 rows][64] SW128
   static constexpr uint32_t kKV = BK * HD * 2;    // K or V tile [HD/64][BK keys][64]
-  static constexpr uint32_t kP = kPBQ * BK * 2;   // P [BK/64][128 rows][64 keys]
+  static constexpr uint32_t kP = PT ? 0 : kPBQ * BK * 2;  // P [BK/64][128 rows][64 keys] (PT: in TMEM)
   static constexpr uint32_t kRed = 2 * kPBQ * 4;  // per-half row maxima / sums
   static constexpr uint32_t kTotal = kQ + (kVdb ? 4 : 3) * kKV + kP + kRed + 256 + 1024;  // + barriers + align slack
   static constexpr uint32_t kTmemCols = BK == 128 ? 512 : 256;
@@ -542,11 +542,18 @@ struct PtcSmem {
 // 256 threads: warp w owns TMEM lane quarter (w & 3) -> query rows 32(w&3)..+31, and column half
 // ch = w >> 2 of every S tile (keys 64ch..64ch+63) and of O (dims (hd/2)ch..); the two halves of a
 // row exchange their maxima through shared memory once per tile.
-template <int HD, int BK>
+//
+// PT (P in TMEM, BK = 128): three S buffers + O fill the 512 columns; P_t is written bf16-packed
+// over the columns of S_t the same thread just read and feeds PV_t as the TMEM A operand, so the
+// softmax of tile t never waits for PV_{t-1} (only an O rescale does), and there is no P smem
+// image, proxy fence or smem traffic.  S_{t+1} goes to buffer (t+1) mod 3, whose P_{t-2} was
+// consumed by PV_{t-2}, which warp 0 waited for before the tile-(t-1) barrier.
+template <int HD, int BK, bool PT>
 __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
     prefill_attn_tc(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
                     const __grid_constant__ CUtensorMap mapV, const PrefillAttnArgs a) {
-  using L = PtcSmem<HD, BK>;
+  static_assert(!PT || BK == 128, "P in TMEM needs the 128-key tile");
+  using L = PtcSmem<HD, BK, PT>;
   constexpr int kHalves = HD / 64;
   constexpr int kOC = HD / 2;  // O columns per column half
   constexpr int kCH = BK / 2;  // S columns (keys) per column half
@@ -562,9 +569,9 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
   uint64_t* q_full = bars;        // 1
   uint64_t* k_full = bars + 1;    // [2]
   uint64_t* v_full = bars + 3;    // [2]
-  uint64_t* s_done = bars + 5;    // [2]
-  uint64_t* o_done = bars + 7;    // 1
-  uint32_t* holder = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* s_done = bars + 5;    // [2] ([3] with PT)
+  uint64_t* o_done = bars + 8;    // 1
+  uint32_t* holder = reinterpret_cast<uint32_t*>(bars + 9);
 
   const uint32_t warp = warp_id_uniform(), lane = lane_id();
   const uint32_t quarter = warp & 3, chh = warp >> 2;
@@ -577,8 +584,9 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
   const bool tr0 = a.trace && blockIdx.x == 0 && threadIdx.x == 0;
 
   if (tr0) a.trace[254] = globaltimer_ns();
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < 384) a.trace[256 + 2 * blockIdx.x] = globaltimer_ns();
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 9; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(holder, L::kTmemCols);
@@ -586,8 +594,10 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *holder;
-  const uint32_t tS[2] = {tmem, tmem + BK};
-  const uint32_t tO = tmem + 2 * BK;
+  auto tS = [&](int b) { return tmem + static_cast<uint32_t>(b * BK); };  // S buffer b
+  const uint32_t tO = tmem + (PT ? 3 : 2) * BK;
+  auto sbuf = [](int g) { return PT ? g % 3 : g & 1; };          // S buffer of key tile g
+  auto sphase = [](int g) { return PT ? (g / 3) & 1 : (g >> 1) & 1; };
   // the CTA walks (q-tile, head) items it = blockIdx.x, + gridDim.x, ...; g = the CTA's running
   // key-tile count, so every ring barrier keeps one phase sequence across items
   int g0 = 0, n_done = 0;
@@ -615,18 +625,18 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
   };
   const uint32_t idesc_s = make_idesc_bf16_f32(kPBQ, BK);
   const uint32_t idesc_o = make_idesc_bf16_f32(kPBQ, HD) | (1u << 16);  // B (V) MN-major
-  auto issue_s = [&](int t) {  // S_t = Q K_t^T into tS[(g0 + t) & 1]
-    const int g = g0 + t, buf = g & 1;
+  auto issue_s = [&](int t) {  // S_t = Q K_t^T into tS[sbuf(g0 + t)]
+    const int g = g0 + t, buf = g & 1, sb = sbuf(g);
     mbar_wait(&k_full[buf], (g >> 1) & 1);
     tc_fence_after();
     const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + buf * L::kKV);
 #pragma unroll
     for (int k = 0; k < HD / 16; ++k) {
       const uint32_t off = (k >> 2) * (kPBQ * 128) + (k & 3) * 32;  // hd half, 32 B step in the row
-      umma_f16_ss_warp(tS[buf], make_desc_k_sw128(qa + off), make_desc_k_sw128(kb + (k >> 2) * (BK * 128) + (k & 3) * 32),
+      umma_f16_ss_warp(tS(sb), make_desc_k_sw128(qa + off), make_desc_k_sw128(kb + (k >> 2) * (BK * 128) + (k & 3) * 32),
                        idesc_s, k > 0 ? 1u : 0u);
     }
-    umma_commit_warp(&s_done[buf]);
+    umma_commit_warp(&s_done[sb]);
   };
 
   if (warp == 0) {
@@ -657,18 +667,18 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
   const int c_key0 = static_cast<int>(chh) * kCH;
 
   for (int t = 0; t < ntiles; ++t) {
-    const int g = g0 + t, buf = g & 1;
+    const int g = g0 + t, buf = g & 1, sb = sbuf(g);
     const bool tr = tr0 && n_done == 0 && t < 32;
     if (tr) a.trace[t * 8 + 0] = globaltimer_ns();
     if (warp == 0 && t + 1 < ntiles) issue_s(t + 1);  // overlaps this tile's softmax
-    mbar_wait(&s_done[buf], (g >> 1) & 1);
+    mbar_wait(&s_done[sb], sphase(g));
     tc_fence_after();
     if (tr) a.trace[t * 8 + 1] = globaltimer_ns();
     if (warp == 0 && t + 2 < ntiles) load_tile(t + 2, buf, false);  // K_t consumed by S_t
     // this half of the S row in registers: 4 loads in flight, one wait
     uint32_t sr[kNC][16];
 #pragma unroll
-    for (int c = 0; c < kNC; ++c) tmem_ld_32x32b_x16(tS[buf] + lane_off + c_key0 + c * 16, sr[c]);
+    for (int c = 0; c < kNC; ++c) tmem_ld_32x32b_x16(tS(sb) + lane_off + c_key0 + c * 16, sr[c]);
 #pragma unroll
     for (int c = 0; c < kNC; ++c) tmem_ld_wait_regs(sr[c]);
     const int kbase = t * BK + c_key0;
@@ -692,7 +702,7 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
     }
     red[chh * kPBQ + r] = mt;
     // PV_{t-1} must be complete before P is overwritten and before O is rescaled
-    if (t > 0) {
+    if (!PT && t > 0) {
       mbar_wait(o_done, (g - 1) & 1);
       tc_fence_after();
       if (warp == 0) {  // V_{t-1} consumed by PV_{t-1}
@@ -708,6 +718,10 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
     if (tr) a.trace[t * 8 + 2] = globaltimer_ns();
     const bool refresh = mt > m + 8.f;  // also true on the first tile (m = -inf)
     if (t > 0 && __any_sync(0xffffffffu, refresh)) {  // warp-collective TMEM rescale of this O half
+      if (PT) {  // PV_{t-1} must be complete
+        mbar_wait(o_done, (g - 1) & 1);
+        tc_fence_after();
+      }
       const float alpha = refresh ? ex2_approx(m - mt) : 1.f;
 #pragma unroll
       for (int c = 0; c < kOC; c += 16) {
@@ -722,9 +736,10 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
       l *= alpha;
     }
     if (refresh) m = mt;
-    // P = exp2(S c2 - m) -> bf16 smem (K-major SW128 rows), partial row sum
+    // P = exp2(S c2 - m) -> bf16 (smem K-major SW128 rows, or TMEM over S_t with PT), partial row sum
     const float mneg = -m;
     float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t pk[PT ? kNC * 8 : 1];
 #pragma unroll
     for (int c = 0; c < kNC; ++c) {
       float pv[16];
@@ -734,19 +749,36 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
         pv[j] = (!need_mask || kbase + c * 16 + j <= qpos) ? e : 0.f;
         rs4[j & 3] += pv[j];
       }
+      if constexpr (PT) {
 #pragma unroll
-      for (int h8 = 0; h8 < 2; ++h8) {
-        const int chunk = chunk0 + c * 2 + h8;  // 16-B chunk (8 keys) within the 128-B row
-        uint4 w;
-        w.x = pack_bf16x2(pv[h8 * 8 + 0], pv[h8 * 8 + 1]);
-        w.y = pack_bf16x2(pv[h8 * 8 + 2], pv[h8 * 8 + 3]);
-        w.z = pack_bf16x2(pv[h8 * 8 + 4], pv[h8 * 8 + 5]);
-        w.w = pack_bf16x2(pv[h8 * 8 + 6], pv[h8 * 8 + 7]);
-        *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) << 4)) = w;
+        for (int j = 0; j < 8; ++j) pk[c * 8 + j] = pack_bf16x2(pv[2 * j], pv[2 * j + 1]);
+      } else {
+#pragma unroll
+        for (int h8 = 0; h8 < 2; ++h8) {
+          const int chunk = chunk0 + c * 2 + h8;  // 16-B chunk (8 keys) within the 128-B row
+          uint4 w;
+          w.x = pack_bf16x2(pv[h8 * 8 + 0], pv[h8 * 8 + 1]);
+          w.y = pack_bf16x2(pv[h8 * 8 + 2], pv[h8 * 8 + 3]);
+          w.z = pack_bf16x2(pv[h8 * 8 + 4], pv[h8 * 8 + 5]);
+          w.w = pack_bf16x2(pv[h8 * 8 + 6], pv[h8 * 8 + 7]);
+          *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) << 4)) = w;
+        }
       }
     }
     l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
-    fence_proxy_async_shared();  // P (generic-proxy stores) -> visible to the tensor core
+    if constexpr (PT) {  // this half's 64 keys -> 32 packed columns at the start of its S columns
+#pragma unroll
+      for (int q = 0; q < kNC / 2; ++q)
+        tmem_st_32x32b_x16(tS(sb) + lane_off + c_key0 + q * 16, *reinterpret_cast<const uint32_t(*)[16]>(&pk[q * 16]));
+      tmem_st_wait();
+      if (warp == 0 && t > 0) {  // V_{t-1} consumed by PV_{t-1} (also orders S_{t+2} after PV_{t-1})
+        mbar_wait(o_done, (g - 1) & 1);
+        tc_fence_after();
+        if (t + 1 < ntiles) load_tile(t + 1, (g + 1) & 1, true);
+      }
+    } else {
+      fence_proxy_async_shared();  // P (generic-proxy stores) -> visible to the tensor core
+    }
     tc_fence_before();
     __syncthreads();  // P complete; S_buf reads, O rescales and red[] reads done
     if (tr) a.trace[t * 8 + 3] = globaltimer_ns();
@@ -756,9 +788,14 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
       tc_fence_after();
       const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + (L::kVdb ? buf : 0) * L::kKV);
 #pragma unroll
-      for (int k = 0; k < BK / 16; ++k)
-        umma_f16_ss_warp(tO, make_desc_k_sw128(pa + (k >> 2) * (kPBQ * 128) + (k & 3) * 32),
-                         make_desc_mn_sw128(vb + k * 2048, BK * 128, 1024), idesc_o, (t > 0 || k > 0) ? 1u : 0u);
+      for (int k = 0; k < BK / 16; ++k) {
+        const uint64_t bdesc = make_desc_mn_sw128(vb + k * 2048, BK * 128, 1024);
+        if constexpr (PT)  // keys 16k..: column half k/4, packed columns 8(k mod 4)..
+          umma_f16_ts_warp(tO, tS(sb) + (k >> 2) * 64 + (k & 3) * 8, bdesc, idesc_o, (t > 0 || k > 0) ? 1u : 0u);
+        else
+          umma_f16_ss_warp(tO, make_desc_k_sw128(pa + (k >> 2) * (kPBQ * 128) + (k & 3) * 32), bdesc, idesc_o,
+                           (t > 0 || k > 0) ? 1u : 0u);
+      }
       umma_commit_warp(o_done);
     }
   }
@@ -802,6 +839,7 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
     tc_fence_after();
     tmem_dealloc(tmem, L::kTmemCols);
   }
+  if (a.trace && threadIdx.x == 0 && blockIdx.x < 384) a.trace[257 + 2 * blockIdx.x] = globaltimer_ns();
 }
 
 template <int HD>
@@ -813,7 +851,10 @@ cudaError_t launch_decode_hd(const DecodeAttnArgs& a, const CUtensorMap& mk, con
     configured = true;
   }
   dim3 grid(a.d, a.n_kv_local, a.splits);
-  launch_pdl(decode_attn_mma<HD>, grid, dim3(160), smem, st, mk, mv, a);
+  if (a.no_pdl)
+    decode_attn_mma<HD><<<grid, 160, smem, st>>>(mk, mv, a);
+  else
+    launch_pdl(decode_attn_mma<HD>, grid, dim3(160), smem, st, mk, mv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || a.splits == 1) return e;
   launch_pdl(decode_combine_kernel, dim3(a.d, a.n_q_local), dim3(128), 0, st, a, HD);
@@ -842,13 +883,13 @@ cudaError_t launch_decode_attention(const DecodeAttnArgs& a, const CUtensorMap& 
   return cudaErrorInvalidValue;
 }
 
-template <int HD, int BK>
+template <int HD, int BK, bool PT = false>
 cudaError_t launch_prefill_tc(const PrefillAttnArgs& a, const CUtensorMap& mq, const CUtensorMap& mk,
                               const CUtensorMap& mv, cudaStream_t st) {
-  using L = PtcSmem<HD, BK>;
+  using L = PtcSmem<HD, BK, PT>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_attn_tc<HD, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(prefill_attn_tc<HD, BK, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(L::kTotal));
     if (e != cudaSuccess) return e;
     configured = true;
@@ -856,7 +897,7 @@ cudaError_t launch_prefill_tc(const PrefillAttnArgs& a, const CUtensorMap& mq, c
   const int items = (a.p + kPBQ - 1) / kPBQ * a.n_q_local;
   static const int cap = getenv("SARATHI_PREFILL_CTAS") ? atoi(getenv("SARATHI_PREFILL_CTAS")) : 0;  // experiment
   const int ctas = cap > 0 ? std::min(cap, items) : items;
-  prefill_attn_tc<HD, BK><<<ctas, 256, L::kTotal, st>>>(mq, mk, mv, a);
+  prefill_attn_tc<HD, BK, PT><<<ctas, 256, L::kTotal, st>>>(mq, mk, mv, a);
   return cudaGetLastError();
 }
 
@@ -869,12 +910,16 @@ cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, const CUtensorMap
   // SM).  Measured: TP-1 step unchanged, TP-8 rank shapes 2-4 % slower, so not the default.
   static const bool narrow = getenv("SARATHI_PREFILL_BK") && atoi(getenv("SARATHI_PREFILL_BK")) == 64;
   const bool bk128 = a.block_size == 128 || !narrow;
+  // P in TMEM (default); SARATHI_PREFILL_PT=0 selects the smem P image
+  static const bool pt = !(getenv("SARATHI_PREFILL_PT") && atoi(getenv("SARATHI_PREFILL_PT")) == 0);
   if (tc && a.head_dim == 128)
-    return bk128 ? launch_prefill_tc<128, 128>(a, *qmap, *kmap, *vmap, st)
-                 : launch_prefill_tc<128, 64>(a, *qmap, *kmap, *vmap, st);
+    return !bk128 ? launch_prefill_tc<128, 64>(a, *qmap, *kmap, *vmap, st)
+           : pt   ? launch_prefill_tc<128, 128, true>(a, *qmap, *kmap, *vmap, st)
+                  : launch_prefill_tc<128, 128>(a, *qmap, *kmap, *vmap, st);
   if (tc && a.head_dim == 64)
-    return bk128 ? launch_prefill_tc<64, 128>(a, *qmap, *kmap, *vmap, st)
-                 : launch_prefill_tc<64, 64>(a, *qmap, *kmap, *vmap, st);
+    return !bk128 ? launch_prefill_tc<64, 64>(a, *qmap, *kmap, *vmap, st)
+           : pt   ? launch_prefill_tc<64, 128, true>(a, *qmap, *kmap, *vmap, st)
+                  : launch_prefill_tc<64, 128>(a, *qmap, *kmap, *vmap, st);
   // mma.sync kernel: block sizes the tcgen05 tile (128 keys) does not tile
   dim3 grid((a.p + 63) / 64, a.n_q_local);
   if (a.head_dim == 128) {

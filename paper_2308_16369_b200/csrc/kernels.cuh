@@ -27,6 +27,10 @@ struct DecodeAttnArgs {
   __nv_bfloat16* out = nullptr;  // [T][out_ld]; row q_row0 + j
   int out_ld = 0;
   int dbg = 0;  // timing experiments only: bit0 = consumers skip the math (pure K/V streaming)
+  // 0: launched with programmatic dependent launch (CTAs become resident while the QKV GEMM
+  // drains).  1: plain launch, so a concurrently pending prefill-attention grid on the
+  // high-priority stream is dispatched first when the GEMM completes.
+  int no_pdl = 0;
 };
 
 struct PrefillAttnArgs {

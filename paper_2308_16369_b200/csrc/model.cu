@@ -28,6 +28,13 @@ namespace sarathi {
 
 namespace {
 
+// debug (SARATHI_PREFILL_TRACE): the time a stream reaches this point
+__global__ void stamp_kernel(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
+
 // ---- NCCL, resolved at run time (only needed for world > 1) ----
 struct NcclApi {
   bool ok = false;
@@ -578,13 +585,14 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       unsigned long long* trbuf = nullptr;
       if (ptrace && !ptraced && atoi(ptrace) == p && l == 1) {
         ptraced = true;
-        cudaMalloc(&trbuf, 256 * 8);
-        cudaMemsetAsync(trbuf, 0, 256 * 8, ps);
+        cudaMalloc(&trbuf, 1024 * 8);
+        cudaMemsetAsync(trbuf, 0, 1024 * 8, ps);
         pa.trace = trbuf;
+        stamp_kernel<<<1, 1, 0, ps>>>(trbuf + 1000);
       }
       SRET(check(launch_prefill_attention(pa, &m_q, &kmap[l], &vmap[l], ps), "prefill attention"));
       if (trbuf) {
-        unsigned long long hb[256];
+        unsigned long long hb[1024];
         cudaStreamSynchronize(ps);
         cudaMemcpy(hb, trbuf, sizeof(hb), cudaMemcpyDeviceToHost);
         const unsigned long long t0 = hb[254];
@@ -594,6 +602,12 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
           fprintf(stderr, "\n");
         }
         fprintf(stderr, "prefill last PV done %8.3f us\n", (hb[255] - t0) * 1e-3);
+        unsigned long long s_min = ~0ull;
+        for (int b = 0; b < 384 && hb[256 + 2 * b]; ++b) s_min = std::min(s_min, hb[256 + 2 * b]);
+        fprintf(stderr, "prefill stream ready %8.3f us before the first CTA\n", (s_min - hb[1000]) * 1e-3);
+        for (int b = 0; b < 384 && hb[256 + 2 * b]; ++b)
+          fprintf(stderr, "prefill cta %3d: start %8.3f end %8.3f us\n", b, (hb[256 + 2 * b] - s_min) * 1e-3,
+                  (hb[257 + 2 * b] - s_min) * 1e-3);
         cudaFree(trbuf);
       }
       op_end(SARATHI_OP_PREFILL_ATTN, ob, ps);
@@ -650,6 +664,8 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       }
       static const int dec_dbg = getenv("SARATHI_DECODE_DBG") ? atoi(getenv("SARATHI_DECODE_DBG")) : 0;
       da.dbg = dec_dbg;
+      static const int dec_nopdl = getenv("SARATHI_DECODE_NOPDL") ? atoi(getenv("SARATHI_DECODE_NOPDL")) : 0;
+      da.no_pdl = (dec_nopdl == 1 && p > 0 && !no_aux) || dec_nopdl == 2;
       da.part_o = part_o;
       da.part_lse = part_lse;
       da.out = o;

@@ -139,11 +139,13 @@ def test_prefill_attention_multitile(S, hd, n_kv, C, bs):
         assert max(len(s.gpu_slots) for s in steps) > 512
 
 
-@pytest.mark.skipif(os.environ.get("SARATHI_PREFILL_BK") == "64", reason="this process already runs the narrow tile")
-def test_prefill_attention_narrow_tile():
-    """The 64-key prefill tile (SARATHI_PREFILL_BK=64: single-buffered V at hd 128, 2 CTAs per SM),
-    read once per process, so the multitile cases rerun in a child process (bs 128 keeps the wide tile)."""
-    env = dict(os.environ, SARATHI_PREFILL_BK="64")
+@pytest.mark.skipif(os.environ.get("SARATHI_PREFILL_VARIANT_CHILD") == "1", reason="child process")
+@pytest.mark.parametrize("env", [{"SARATHI_PREFILL_BK": "64"}, {"SARATHI_PREFILL_PT": "0"}])
+def test_prefill_attention_variants(env):
+    """The non-default prefill kernels, selected once per process by environment, rerun the
+    multitile cases in a child process: the 64-key tile (SARATHI_PREFILL_BK=64: single-buffered V
+    at hd 128, 2 CTAs per SM; bs 128 keeps the wide tile) and the smem P image (SARATHI_PREFILL_PT=0)."""
+    env = dict(os.environ, SARATHI_PREFILL_VARIANT_CHILD="1", **env)
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m", "gpu", "-k",
                         "prefill_attention_multitile", "-p", "no:cacheprovider"],
                        env=env, capture_output=True, text=True, timeout=900,

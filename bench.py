@@ -234,6 +234,7 @@ def ours(args):
     for _ in range(args.steps):
         step(None, decodes)
     ops_dec = m.op_times(reset=True)
+    kops_dec = m.op_kernel_times(reset=True)
     m.set_profiling(False)
     # e2e: host buffers through the public API (H2D metadata + D2H logits every step), wall clock
     host_logits = np.empty((R, cfg.vocab), dtype=np.float32)
@@ -293,6 +294,11 @@ def ours(args):
             gemm[k]["us_kernel"] = round(kavg * 1e6, 2)
             gemm[k]["frac_tensor_kernel"] = round(flops / kavg / 1e12 / sus, 3)
     per_layer_ops = {k: {"ms_total": round(v[0], 3), "launches": v[1]} for k, v in ops.items() if v[1]}
+    # device spans (first CTA start after its grid dependency -> last CTA end, globaltimer) of the
+    # attention kernels: CUDA events on a stream running beside another grid are stamped late
+    def span_us(kd, k):
+        t_ms, n = kd.get(k, (0.0, 0))
+        return round(t_ms / n * 1e3, 2) if n else None
     traffic = ncu_traffic("decode_attention", args.workload)
     roofline = {"kernel": "decode_attention", "bound": "hbm", "achieved": round(da_gbs, 1),
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(da_gbs / peaks["hbm_gbs"], 3),
@@ -301,8 +307,10 @@ def ours(args):
                 "algorithmic_bytes_per_launch": da_bytes,
                 "avg_launch_us": round(da_avg_s * 1e6, 2), "peak_source": peaks["source"],
                 "note": "hybrid step: the chunk's prefill attention runs concurrently on a side stream",
+                "span_us": span_us(kops, "decode_attn"),
+                "prefill_attn_span_us": span_us(kops, "prefill_attn"),
                 "alone": {"achieved": round(dd_gbs, 1), "frac": round(dd_gbs / peaks["hbm_gbs"], 3),
-                          "avg_launch_us": round(dd_avg_s * 1e6, 2),
+                          "avg_launch_us": round(dd_avg_s * 1e6, 2), "span_us": span_us(kops_dec, "decode_attn"),
                           "pass": "decode-only steps of the same decodes (no concurrent kernel)"}}
 
     out = {

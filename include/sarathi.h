@@ -176,9 +176,11 @@ int sarathi_last_io_bytes(const sarathi_model* m, int64_t* h2d, int64_t* d2h);
 #define SARATHI_NUM_OPS 11
 int sarathi_set_profiling(sarathi_model* m, int32_t enable);
 int sarathi_op_times(sarathi_model* m, double* ms_out, int64_t* counts_out, int32_t n, int32_t reset);
-/* Device spans of the profiled layer GEMMs (QKV, O, gate||up, down): first CTA start to last CTA
- * end by the SM global timer, i.e. kernel time without launch gaps or event overhead; same
- * accumulate / reset / synchronise semantics as sarathi_op_times (ops without spans read 0). */
+/* Device spans of the profiled layer GEMMs (QKV, O, gate||up, down) and attention kernels (decode:
+ * the main kernel after its grid dependency resolves, not the split combine; prefill: the tcgen05
+ * kernel): first CTA start to last CTA end by the SM global timer, i.e. kernel time without launch
+ * gaps or event overhead; same accumulate / reset / synchronise semantics as sarathi_op_times (ops
+ * without spans read 0). */
 int sarathi_op_kernel_times(sarathi_model* m, double* ms_out, int64_t* counts_out, int32_t n, int32_t reset);
 
 /* ---- debug / parity hooks (host outputs, synchronise the stream) ------------------------ */

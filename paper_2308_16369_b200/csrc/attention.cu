@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(160)
                     DecodeAttnArgs a) {
   griddep_launch_dependents();
   griddep_wait();  // q comes from the QKV GEMM (PDL)
+  if (a.span_start && threadIdx.x == 0) atomicMin(a.span_start, globaltimer_ns());
   constexpr int NBOX = HD / 64;  // 128-byte TMA boxes per row
   const int j = blockIdx.x, kvh = blockIdx.y, z = blockIdx.z;
   const int G = a.n_q_local / a.n_kv_local;
@@ -297,6 +298,7 @@ __global__ void __launch_bounds__(160)
       if (dd == 0) a.part_lse[(static_cast<size_t>(j) * nq + qh) * a.splits + z] = M + log2f(L);
     }
   }
+  if (a.span_end && threadIdx.x == 0) atomicMax(a.span_end, globaltimer_ns());
 }
 
 __global__ void decode_combine_kernel(DecodeAttnArgs a, int HD) {
@@ -585,6 +587,7 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
 
   if (tr0) a.trace[254] = globaltimer_ns();
   if (a.trace && threadIdx.x == 0 && blockIdx.x < 384) a.trace[256 + 2 * blockIdx.x] = globaltimer_ns();
+  if (a.span_start && threadIdx.x == 0) atomicMin(a.span_start, globaltimer_ns());
   if (threadIdx.x == 0) {
     for (int i = 0; i < 9; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
@@ -840,6 +843,7 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
     tmem_dealloc(tmem, L::kTmemCols);
   }
   if (a.trace && threadIdx.x == 0 && blockIdx.x < 384) a.trace[257 + 2 * blockIdx.x] = globaltimer_ns();
+  if (a.span_end && threadIdx.x == 0) atomicMax(a.span_end, globaltimer_ns());
 }
 
 template <int HD>

@@ -31,6 +31,9 @@ struct DecodeAttnArgs {
   // drains).  1: plain launch, so a concurrently pending prefill-attention grid on the
   // high-priority stream is dispatched first when the GEMM completes.
   int no_pdl = 0;
+  // profiling (sarathi_op_kernel_times): min CTA start / max CTA end, globaltimer ns, or null
+  unsigned long long* span_start = nullptr;
+  unsigned long long* span_end = nullptr;
 };
 
 struct PrefillAttnArgs {
@@ -47,6 +50,8 @@ struct PrefillAttnArgs {
   __nv_bfloat16* out = nullptr;
   int out_ld = 0;
   unsigned long long* trace = nullptr;  // debug: globaltimer stamps of CTA (0,0) (tcgen05 kernel)
+  unsigned long long* span_start = nullptr;  // profiling, as DecodeAttnArgs (tcgen05 kernel)
+  unsigned long long* span_end = nullptr;
 };
 
 size_t decode_smem_bytes(int head_dim, int block_size, int stages, int G);

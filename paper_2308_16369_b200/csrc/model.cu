@@ -324,6 +324,22 @@ Status Model::alloc_kv(int64_t nb, int32_t bs) {
   return Status::ok();
 }
 
+Status Model::take_span(int op, unsigned long long** start, unsigned long long** end) {
+  *start = *end = nullptr;
+  if (!profiling) return Status::ok();
+  if (!span_buf) {
+    SRET(dalloc(&span_buf, 2 * kSpanCap));
+    SRET(check(cudaMemsetAsync(span_buf, 0xFF, kSpanCap * 8, stream), "span init"));
+    SRET(check(cudaMemsetAsync(span_buf + kSpanCap, 0, kSpanCap * 8, stream), "span init"));
+  }
+  if (static_cast<int>(span_ops.size()) < kSpanCap) {
+    *start = span_buf + span_ops.size();
+    *end = span_buf + kSpanCap + span_ops.size();
+    span_ops.push_back(op);
+  }
+  return Status::ok();
+}
+
 Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, int N, const EpiParams& ep_in, int op) {
   const bool atomic = ep_in.mode == EPI_ADD_F32;
   auto pk = std::make_tuple(M, N, K * 2 + (atomic ? 1 : 0));
@@ -342,18 +358,7 @@ Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, 
   ep.ws_red = gemm_ws + gemm_ws_floats / 2;
   ep.counters = gemm_counters;
   ++launches;
-  if (profiling && op >= 0) {  // device span of this launch (sarathi_op_kernel_times)
-    if (!span_buf) {
-      SRET(dalloc(&span_buf, 2 * kSpanCap));
-      SRET(check(cudaMemsetAsync(span_buf, 0xFF, kSpanCap * 8, stream), "span init"));
-      SRET(check(cudaMemsetAsync(span_buf + kSpanCap, 0, kSpanCap * 8, stream), "span init"));
-    }
-    if (static_cast<int>(span_ops.size()) < kSpanCap) {
-      ep.span_start = span_buf + span_ops.size();
-      ep.span_end = span_buf + kSpanCap + span_ops.size();
-      span_ops.push_back(op);
-    }
-  }
+  if (op >= 0) SRET(take_span(op, &ep.span_start, &ep.span_end));
   // debug: SARATHI_MODEL_TRACE=<epilogue mode>:<N> traces the first such launch with N tokens
   static const char* trace_env = getenv("SARATHI_MODEL_TRACE");
   static bool traced = false;
@@ -375,7 +380,10 @@ Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, 
 }
 
 cudaEvent_t Model::op_begin(cudaStream_t s) {
-  if (!profiling) return nullptr;
+  // debug: SARATHI_SPANS_ONLY keeps the device spans but drops the per-op events, whose records
+  // between kernels break the programmatic-dependent-launch chains (true launch gaps)
+  static const bool spans_only = getenv("SARATHI_SPANS_ONLY") != nullptr;
+  if (!profiling || spans_only) return nullptr;
   if (ev_used + 2 > ev_pool.size()) {
     for (int i = 0; i < 256; ++i) {
       cudaEvent_t e;
@@ -414,6 +422,18 @@ Status Model::collect_op_times() {
         op_kms[span_ops[i]] += (b - a) * 1e-6;
         op_kcount[span_ops[i]] += 1;
       }
+    }
+    static const int dump = getenv("SARATHI_SPAN_DUMP") ? atoi(getenv("SARATHI_SPAN_DUMP")) : 0;
+    static bool dumped = false;
+    if (dump > 0 && !dumped && !span_ops.empty()) {  // debug: timeline of the first `dump` spans
+      dumped = true;
+      const unsigned long long t0 = hs[0];
+      unsigned long long prev_end = hs[kSpanCap];
+      for (size_t i = 0; i < span_ops.size() && static_cast<int>(i) < dump; ++i)
+        fprintf(stderr, "span op %2d: %9.3f .. %9.3f us (%7.3f us; gap from previous end %7.3f)\n", span_ops[i],
+                (hs[i] - t0) * 1e-3, (hs[kSpanCap + i] - t0) * 1e-3, (hs[kSpanCap + i] - hs[i]) * 1e-3,
+                i ? (static_cast<double>(hs[i]) - static_cast<double>(prev_end)) * 1e-3 : 0.0),
+            prev_end = std::max(prev_end, hs[kSpanCap + i]);
     }
     span_ops.clear();
     SRET(check(cudaMemsetAsync(span_buf, 0xFF, kSpanCap * 8, stream), "span init"));
@@ -590,6 +610,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
         pa.trace = trbuf;
         stamp_kernel<<<1, 1, 0, ps>>>(trbuf + 1000);
       }
+      SRET(take_span(SARATHI_OP_PREFILL_ATTN, &pa.span_start, &pa.span_end));
       SRET(check(launch_prefill_attention(pa, &m_q, &kmap[l], &vmap[l], ps), "prefill attention"));
       if (trbuf) {
         unsigned long long hb[1024];
@@ -671,6 +692,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       da.out = o;
       da.out_ld = q_dim_l;
       ob = op_begin();
+      SRET(take_span(SARATHI_OP_DECODE_ATTN, &da.span_start, &da.span_end));
       SRET(check(launch_decode_attention(da, kmap[l], vmap[l], stream), "decode attention"));
       op_end(SARATHI_OP_DECODE_ATTN, ob);
       launches += da.splits > 1 ? 2 : 1;

@@ -123,6 +123,8 @@ struct Model {
 
   // helpers
   Status gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, int N, const EpiParams& ep, int op = -1);
+  // profiling: a (start, end) device-span slot for one launch of op (null pointers when off / full)
+  Status take_span(int op, unsigned long long** start, unsigned long long** end);
   Status check(cudaError_t e, const char* what);
   template <typename T>
   Status dalloc(T** p, size_t count);

@@ -259,7 +259,8 @@ class Model:
         return {n: (float(ms[i]), int(cnt[i])) for i, n in enumerate(OP_NAMES)}
 
     def op_kernel_times(self, reset: bool = True):
-        """{op name: (total ms, launches)} of in-kernel device spans (GEMMs) since the last reset."""
+        """{op name: (total ms, launches)} of in-kernel device spans (GEMMs, decode and prefill attention)
+        since the last reset."""
         ms = np.zeros(len(OP_NAMES), dtype=np.float64)
         cnt = np.zeros(len(OP_NAMES), dtype=np.int64)
         _check(lib.sarathi_op_kernel_times(self.h, _p(ms, C.c_double), _p(cnt, C.c_int64), len(OP_NAMES), int(reset)))

@@ -68,7 +68,7 @@ def main():
                "ms_per_layer": round(per_layer, 4), "projected_ms_per_step_compute_only": round(per_layer * L_full, 3),
                "projected_tokens_per_s_compute_only": round((p + d) / (per_layer * L_full) * 1e3, 1),
                "op_us_per_layer": {k: round(v[0] / max(v[1], 1) * 1e3, 2) for k, v in ops.items() if v[1]},
-               "gemm_kernel_us": {k: round(v[0] / max(v[1], 1) * 1e3, 2) for k, v in kops.items() if v[1]},
+               "kernel_span_us": {k: round(v[0] / max(v[1], 1) * 1e3, 2) for k, v in kops.items() if v[1]},
                "note": "one TP rank's compute on one B200; all-reduces not included"}
         print(json.dumps(row), flush=True)
         m.close()

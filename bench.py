@@ -230,7 +230,7 @@ def ours(args):
     ops = m.op_times(reset=True)
     kops = m.op_kernel_times(reset=True)  # in-kernel device spans of the same GEMM launches
     # the same decodes without the chunk: decode attention alone on the GPU (in the hybrid step the
-    # chunked-prefill attention runs beside it on a side stream and shares the SMs)
+    # chunked-prefill attention runs concurrently with it and shares the SMs)
     for _ in range(args.steps):
         step(None, decodes)
     ops_dec = m.op_times(reset=True)
@@ -306,7 +306,7 @@ def ours(args):
                 "traffic_source": traffic["source"] if traffic else None,
                 "algorithmic_bytes_per_launch": da_bytes,
                 "avg_launch_us": round(da_avg_s * 1e6, 2), "peak_source": peaks["source"],
-                "note": "hybrid step: the chunk's prefill attention runs concurrently on a side stream",
+                "note": "hybrid step: the chunk's prefill attention runs concurrently (attention chain)",
                 "span_us": span_us(kops, "decode_attn"),
                 "prefill_attn_span_us": span_us(kops, "prefill_attn"),
                 "alone": {"achieved": round(dd_gbs, 1), "frac": round(dd_gbs / peaks["hbm_gbs"], 3),

@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(160)
     decode_attn_mma(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
                     DecodeAttnArgs a) {
   griddep_launch_dependents();
-  griddep_wait();  // q comes from the QKV GEMM (PDL)
+  if (!a.wait_at_end) griddep_wait();  // q comes from the QKV GEMM (PDL)
+  const bool last_cta = blockIdx.x == gridDim.x - 1 && blockIdx.y == gridDim.y - 1 && blockIdx.z == gridDim.z - 1;
   if (a.span_start && threadIdx.x == 0) atomicMin(a.span_start, globaltimer_ns());
   constexpr int NBOX = HD / 64;  // 128-byte TMA boxes per row
   const int j = blockIdx.x, kvh = blockIdx.y, z = blockIdx.z;
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(160)
   if (b0 >= b1) {
     if (a.splits > 1 && tid < G)
       a.part_lse[(static_cast<size_t>(j) * nq + q_head0 + tid) * a.splits + z] = -INFINITY;
+    if (a.wait_at_end && last_cta) griddep_wait();
     return;
   }
   const int S = a.stages;
@@ -298,6 +300,9 @@ __global__ void __launch_bounds__(160)
       if (dd == 0) a.part_lse[(static_cast<size_t>(j) * nq + qh) * a.splits + z] = M + log2f(L);
     }
   }
+  // attention chain: the grid must not complete before the prefill grid; one CTA waiting is
+  // enough (the others keep their SM slots free for the rest of the grid)
+  if (a.wait_at_end && last_cta) griddep_wait();
   if (a.span_end && threadIdx.x == 0) atomicMax(a.span_end, globaltimer_ns());
 }
 
@@ -585,6 +590,10 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
   const int n_items = ntq * a.n_q_local;
   const bool tr0 = a.trace && blockIdx.x == 0 && threadIdx.x == 0;
 
+  // PDL (attention chain): wait for the QKV GEMM, THEN let the decode attention launch, so the
+  // decode grid starts only after q / K / V are complete
+  griddep_wait();
+  griddep_launch_dependents();
   if (tr0) a.trace[254] = globaltimer_ns();
   if (a.trace && threadIdx.x == 0 && blockIdx.x < 384) a.trace[256 + 2 * blockIdx.x] = globaltimer_ns();
   if (a.span_start && threadIdx.x == 0) atomicMin(a.span_start, globaltimer_ns());
@@ -901,7 +910,10 @@ cudaError_t launch_prefill_tc(const PrefillAttnArgs& a, const CUtensorMap& mq, c
   const int items = (a.p + kPBQ - 1) / kPBQ * a.n_q_local;
   static const int cap = getenv("SARATHI_PREFILL_CTAS") ? atoi(getenv("SARATHI_PREFILL_CTAS")) : 0;  // experiment
   const int ctas = cap > 0 ? std::min(cap, items) : items;
-  prefill_attn_tc<HD, BK, PT><<<ctas, 256, L::kTotal, st>>>(mq, mk, mv, a);
+  if (a.pdl)
+    launch_pdl(prefill_attn_tc<HD, BK, PT>, dim3(ctas), dim3(256), L::kTotal, st, mq, mk, mv, a);
+  else
+    prefill_attn_tc<HD, BK, PT><<<ctas, 256, L::kTotal, st>>>(mq, mk, mv, a);
   return cudaGetLastError();
 }
 

@@ -31,6 +31,11 @@ struct DecodeAttnArgs {
   // drains).  1: plain launch, so a concurrently pending prefill-attention grid on the
   // high-priority stream is dispatched first when the GEMM completes.
   int no_pdl = 0;
+  // 1: this launch directly follows the chunk's prefill attention in the same stream (the
+  // "attention chain"): the prefill grid waited for the QKV GEMM before triggering this launch,
+  // so q / K / V are complete when the CTAs start; the grid's last CTA instead waits for the
+  // prefill grid at its END, so the O projection after it (PDL) sees both attention outputs.
+  int wait_at_end = 0;
   // profiling (sarathi_op_kernel_times): min CTA start / max CTA end, globaltimer ns, or null
   unsigned long long* span_start = nullptr;
   unsigned long long* span_end = nullptr;
@@ -50,6 +55,7 @@ struct PrefillAttnArgs {
   __nv_bfloat16* out = nullptr;
   int out_ld = 0;
   unsigned long long* trace = nullptr;  // debug: globaltimer stamps of CTA (0,0) (tcgen05 kernel)
+  int pdl = 0;  // launch with programmatic dependent launch (attention chain; tcgen05 kernel)
   unsigned long long* span_start = nullptr;  // profiling, as DecodeAttnArgs (tcgen05 kernel)
   unsigned long long* span_end = nullptr;
 };

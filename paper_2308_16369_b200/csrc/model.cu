@@ -551,6 +551,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   const float scale = 1.0f / std::sqrt(static_cast<float>(hd));
   bool pending_ar = false;  // TP: down-proj partial in `ar` not yet added to h
   static const bool no_aux = getenv("SARATHI_NO_AUX") != nullptr;  // experiment: serial attention
+  static const bool attn_chain = !(getenv("SARATHI_ATTN_CHAIN") && atoi(getenv("SARATHI_ATTN_CHAIN")) == 0);
   for (int l = 0; l < cfg.n_layers; ++l) {
     LayerWeights& w = layers[l];
     ob = op_begin();
@@ -575,6 +576,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     ob = op_begin();
     SRET(gemm(w.m_qkv, qkv_rows, H, a, H, T, e, SARATHI_OP_GEMM_QKV));
     op_end(SARATHI_OP_GEMM_QKV, ob);
+    const bool chain = attn_chain && p > 0 && d > 0 && !no_aux;
     if (p > 0) {
       PrefillAttnArgs pa;
       pa.q = q;
@@ -592,8 +594,13 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       pa.scale = scale;
       pa.out = o;
       pa.out_ld = q_dim_l;
-      // with decodes in the batch, the chunk's attention overlaps the decode attention (side stream)
-      const bool side = d > 0 && !no_aux;
+      pa.pdl = chain;
+      // with decodes in the batch, the chunk's attention overlaps the decode attention: by default
+      // both run in the main stream as an "attention chain" (prefill, PDL-launched, waits for QKV
+      // and then triggers the decode grid, whose CTAs wait for the prefill grid at their end), so
+      // the prefill CTAs take their SMs first and no cross-stream fork / join is needed;
+      // SARATHI_ATTN_CHAIN=0 puts the prefill on the high-priority side stream instead
+      const bool side = d > 0 && !no_aux && !chain;
       cudaStream_t ps = side ? aux : stream;
       if (side) {
         SRET(check(cudaEventRecord(ev_fork, stream), "fork"));
@@ -687,6 +694,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       da.dbg = dec_dbg;
       static const int dec_nopdl = getenv("SARATHI_DECODE_NOPDL") ? atoi(getenv("SARATHI_DECODE_NOPDL")) : 0;
       da.no_pdl = (dec_nopdl == 1 && p > 0 && !no_aux) || dec_nopdl == 2;
+      da.wait_at_end = chain;
       da.part_o = part_o;
       da.part_lse = part_lse;
       da.out = o;
@@ -696,7 +704,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       SRET(check(launch_decode_attention(da, kmap[l], vmap[l], stream), "decode attention"));
       op_end(SARATHI_OP_DECODE_ATTN, ob);
       launches += da.splits > 1 ? 2 : 1;
-      if (p > 0 && !no_aux) SRET(check(cudaStreamWaitEvent(stream, ev_join, 0), "join"));
+      if (p > 0 && !no_aux && !chain) SRET(check(cudaStreamWaitEvent(stream, ev_join, 0), "join"));
     }
     // O-projection (postproj) + residual / TP all-reduce
     EpiParams eo;

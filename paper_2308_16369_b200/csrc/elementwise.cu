@@ -58,10 +58,12 @@ template <int kThreads, int kVec>
 __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h, const __nv_bfloat16* __restrict__ add,
                                                            const __nv_bfloat16* __restrict__ g,
                                                            __nv_bfloat16* __restrict__ out, const int* __restrict__ rows,
-                                                           int H, float eps) {
+                                                           int H, float eps, unsigned long long* span_start,
+                                                           unsigned long long* span_end) {
   __shared__ float sred[kThreads / 32];
   griddep_launch_dependents();
   griddep_wait();  // h / add come from the preceding GEMM (PDL)
+  if (span_start && threadIdx.x == 0) atomicMin(span_start, globaltimer_ns());
   const int r = blockIdx.x;
   const int row = rows ? rows[r] : r;
   float* x = h + static_cast<size_t>(row) * H;
@@ -97,6 +99,7 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h
       *reinterpret_cast<uint2*>(o + i) = pk;
     }
   }
+  if (span_end && threadIdx.x == 0) atomicMax(span_end, globaltimer_ns());
 }
 
 __global__ void residual_add_kernel(float* __restrict__ h, const __nv_bfloat16* __restrict__ add, size_t n) {
@@ -184,17 +187,18 @@ cudaError_t launch_embedding(const int* tok, const __nv_bfloat16* E, float* h, i
 }
 
 cudaError_t launch_rmsnorm(float* h, const __nv_bfloat16* add, const __nv_bfloat16* g, __nv_bfloat16* out,
-                           const int* rows, int R, int H, float eps, cudaStream_t st) {
+                           const int* rows, int R, int H, float eps, cudaStream_t st, unsigned long long* span_start,
+                           unsigned long long* span_end) {
   if (R == 0) return cudaSuccess;
   if (H % 4) return cudaErrorInvalidValue;
   // one CTA per row, sized so that every row of a batch (T <= 512) is resident in ONE wave
   // (a second partial wave doubles the latency of this latency-bound kernel)
   if (H <= 256 * 4 * 2) {
-    launch_pdl(rmsnorm_kernel<256, 2>, dim3(R), dim3(256), 0, st, h, add, g, out, rows, H, eps);
+    launch_pdl(rmsnorm_kernel<256, 2>, dim3(R), dim3(256), 0, st, h, add, g, out, rows, H, eps, span_start, span_end);
   } else if (H <= 256 * 4 * 5) {
-    launch_pdl(rmsnorm_kernel<256, 5>, dim3(R), dim3(256), 0, st, h, add, g, out, rows, H, eps);
+    launch_pdl(rmsnorm_kernel<256, 5>, dim3(R), dim3(256), 0, st, h, add, g, out, rows, H, eps, span_start, span_end);
   } else if (H <= 512 * 4 * 8) {
-    launch_pdl(rmsnorm_kernel<512, 8>, dim3(R), dim3(512), 0, st, h, add, g, out, rows, H, eps);
+    launch_pdl(rmsnorm_kernel<512, 8>, dim3(R), dim3(512), 0, st, h, add, g, out, rows, H, eps, span_start, span_end);
   } else {
     return cudaErrorInvalidValue;
   }

@@ -76,7 +76,8 @@ cudaError_t launch_embedding(const int* tok, const __nv_bfloat16* E, float* h, i
 // out[r][:] = bf16(RMSNorm(h[row(r)]) * g); row(r) = rows ? rows[r] : r.
 // If add != nullptr (TP all-reduced partial, bf16): h[row] += add[row] first and h is updated.
 cudaError_t launch_rmsnorm(float* h, const __nv_bfloat16* add, const __nv_bfloat16* g, __nv_bfloat16* out,
-                           const int* rows, int R, int H, float eps, cudaStream_t st);
+                           const int* rows, int R, int H, float eps, cudaStream_t st,
+                           unsigned long long* span_start = nullptr, unsigned long long* span_end = nullptr);
 
 // h[t][:] += add[t][:] (bf16 -> fp32), no norm (last layer under TP before the final norm)
 cudaError_t launch_residual_add(float* h, const __nv_bfloat16* add, int T, int H, cudaStream_t st);

@@ -555,7 +555,11 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   for (int l = 0; l < cfg.n_layers; ++l) {
     LayerWeights& w = layers[l];
     ob = op_begin();
-    SRET(check(launch_rmsnorm(h, pending_ar ? ar : nullptr, w.g1, a, nullptr, T, H, cfg.rms_eps, stream), "rmsnorm1"));
+    {
+      unsigned long long *sp0, *sp1;
+      SRET(take_span(SARATHI_OP_RMSNORM, &sp0, &sp1));
+      SRET(check(launch_rmsnorm(h, pending_ar ? ar : nullptr, w.g1, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1), "rmsnorm1"));
+    }
     op_end(SARATHI_OP_RMSNORM, ob);
     ++launches;
     pending_ar = false;
@@ -726,7 +730,11 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       op_end(SARATHI_OP_ALLREDUCE, ob);
     }
     ob = op_begin();
-    SRET(check(launch_rmsnorm(h, world > 1 ? ar : nullptr, w.g2, a, nullptr, T, H, cfg.rms_eps, stream), "rmsnorm2"));
+    {
+      unsigned long long *sp0, *sp1;
+      SRET(take_span(SARATHI_OP_RMSNORM, &sp0, &sp1));
+      SRET(check(launch_rmsnorm(h, world > 1 ? ar : nullptr, w.g2, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1), "rmsnorm2"));
+    }
     op_end(SARATHI_OP_RMSNORM, ob);
     ++launches;
     // FFN

@@ -62,6 +62,13 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h
                                                            unsigned long long* span_end) {
   __shared__ float sred[kThreads / 32];
   griddep_launch_dependents();
+  // g is a weight: fetched before the grid dependency resolves (overlaps the predecessor's tail)
+  uint2 gv[kVec];
+#pragma unroll
+  for (int c = 0; c < kVec; ++c) {
+    const int i = (c * kThreads + threadIdx.x) * 4;
+    if (i < H) gv[c] = *reinterpret_cast<const uint2*>(g + i);
+  }
   griddep_wait();  // h / add come from the preceding GEMM (PDL)
   if (span_start && threadIdx.x == 0) atomicMin(span_start, globaltimer_ns());
   const int r = blockIdx.x;
@@ -91,8 +98,7 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h
   for (int c = 0; c < kVec; ++c) {
     const int i = (c * kThreads + threadIdx.x) * 4;
     if (i < H) {
-      const uint2 graw = *reinterpret_cast<const uint2*>(g + i);
-      const float2 g0 = unpack_bf16x2(graw.x), g1 = unpack_bf16x2(graw.y);
+      const float2 g0 = unpack_bf16x2(gv[c].x), g1 = unpack_bf16x2(gv[c].y);
       uint2 pk;
       pk.x = pack_bf16x2(v[c].x * inv * g0.x, v[c].y * inv * g0.y);
       pk.y = pack_bf16x2(v[c].z * inv * g1.x, v[c].w * inv * g1.y);

@@ -140,15 +140,18 @@ def test_prefill_attention_multitile(S, hd, n_kv, C, bs):
 
 
 @pytest.mark.skipif(os.environ.get("SARATHI_PREFILL_VARIANT_CHILD") == "1", reason="child process")
-@pytest.mark.parametrize("env", [{"SARATHI_PREFILL_BK": "64"}, {"SARATHI_PREFILL_PT": "0"}])
-def test_prefill_attention_variants(env):
-    """The non-default prefill kernels, selected once per process by environment, rerun the
-    multitile cases in a child process: the 64-key tile (SARATHI_PREFILL_BK=64: single-buffered V
-    at hd 128, 2 CTAs per SM; bs 128 keeps the wide tile) and the smem P image (SARATHI_PREFILL_PT=0)."""
+@pytest.mark.parametrize("env,select,n", [({"SARATHI_PREFILL_BK": "64"}, "prefill_attention_multitile", 4),
+                                          ({"SARATHI_PREFILL_PT": "0"}, "prefill_attention_multitile", 4),
+                                          ({"SARATHI_ATTN_CHAIN": "0"}, "prefill_attention_multitile or config1", 5)])
+def test_prefill_attention_variants(env, select, n):
+    """The non-default attention paths, selected once per process by environment, rerun hybrid-batch
+    cases in a child process: the 64-key prefill tile (SARATHI_PREFILL_BK=64: single-buffered V at
+    hd 128, 2 CTAs per SM; bs 128 keeps the wide tile), the smem P image (SARATHI_PREFILL_PT=0) and
+    the side-stream + event-join overlap instead of the attention chain (SARATHI_ATTN_CHAIN=0)."""
     env = dict(os.environ, SARATHI_PREFILL_VARIANT_CHILD="1", **env)
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m", "gpu", "-k",
-                        "prefill_attention_multitile", "-p", "no:cacheprovider"],
+                        select, "-p", "no:cacheprovider"],
                        env=env, capture_output=True, text=True, timeout=900,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
-    assert "4 passed" in r.stdout
+    assert f"{n} passed" in r.stdout

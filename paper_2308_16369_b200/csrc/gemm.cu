@@ -634,8 +634,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        if (ep.trace && tb < 2 && et == 0 && seg < 32) ep.trace[tb * 1024 + 704 + seg] = globaltimer_ns();
         __threadfence();
         named_bar_sync(1, kEpiThreads);
+        if (ep.trace && tb < 2 && et == 0 && seg < 32) ep.trace[tb * 1024 + 736 + seg] = globaltimer_ns();
         if (et == 0) {
           int* ctr = ep.counters + tile128;
           const int old = atomicAdd(ctr, 1);
@@ -903,8 +905,10 @@ void dump_gemm_trace(const unsigned long long* trace_dev, const GemmPlan& pl) {
   }
   for (int ch = 0; ch < 64 && h[640 + ch]; ++ch) fprintf(stderr, "seg0 chunk %d emitted %8.3f us\n", ch, (h[640 + ch] - t0) * 1e-3);
   for (int sgm = 0; sgm < 64 && h[512 + sgm]; ++sgm)
-    fprintf(stderr, "seg %d epilogue wake %8.3f us  done %8.3f us\n", sgm, (h[512 + sgm] - t0) * 1e-3,
-            h[576 + sgm] ? (h[576 + sgm] - t0) * 1e-3 : -1.0);
+    fprintf(stderr, "seg %d epilogue wake %8.3f us  done %8.3f us  (partial stored %8.3f, fenced %8.3f)\n", sgm,
+            (h[512 + sgm] - t0) * 1e-3, h[576 + sgm] ? (h[576 + sgm] - t0) * 1e-3 : -1.0,
+            sgm < 32 && h[704 + sgm] ? (h[704 + sgm] - t0) * 1e-3 : -1.0,
+            sgm < 32 && h[736 + sgm] ? (h[736 + sgm] - t0) * 1e-3 : -1.0);
 }
 
 cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const GemmPlan& pl, const EpiParams& ep,

@@ -587,7 +587,9 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
   const int kv_len = s0 + p;
   const int last_blk = (kv_len - 1) / bs;      // last block of the request holding valid keys
   const int ntq = (p + kPBQ - 1) / kPBQ;
-  const int n_items = ntq * a.n_q_local;
+  const int ksplit = a.ksplit > 1 ? a.ksplit : 1;
+  const int n_items = ntq * a.n_q_local * ksplit;
+  int& s_merge = *reinterpret_cast<int*>(bars + 10);  // key split: "this CTA merges the pair"
   const bool tr0 = a.trace && blockIdx.x == 0 && threadIdx.x == 0;
 
   // PDL (attention chain): wait for the QKV GEMM, THEN let the decode attention launch, so the
@@ -614,11 +616,13 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
   // key-tile count, so every ring barrier keeps one phase sequence across items
   int g0 = 0, n_done = 0;
   for (int it = static_cast<int>(blockIdx.x); it < n_items; it += static_cast<int>(gridDim.x), ++n_done) {
-  const int qt = it % ntq, qh = it / ntq;
+  const int qt = it % ntq, qh = (it / ntq) % a.n_q_local, ks = it / (ntq * a.n_q_local);
   const int kvh = qh * a.n_kv_local / a.n_q_local;
   const int q0 = qt * kPBQ;
   const int key_end = s0 + min(q0 + kPBQ, p);  // keys this tile needs: [0, key_end)
-  const int ntiles = (key_end + BK - 1) / BK;
+  const int ntiles_all = (key_end + BK - 1) / BK;
+  const int tb0 = ks * ntiles_all / ksplit;  // this item's key tiles [tb0, tb0 + ntiles)
+  const int ntiles = (ks + 1) * ntiles_all / ksplit - tb0;
 
   // K (or V) tile load: every paged block of the tile (indices past the request clamp to its last
   // block, so every smem byte the UMMAs read is finite; those keys are masked).  K_t is free once
@@ -629,7 +633,7 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
     const CUtensorMap* map = is_v ? &mapV : &mapK;
     mbar_arrive_expect_tx_warp(bar, BK * HD * 2);
     for (int kb = 0; kb < BK; kb += bs) {
-      const int bi = min((t * BK + kb) / bs, last_blk);
+      const int bi = min(((tb0 + t) * BK + kb) / bs, last_blk);
       const int row = (a.block_table[bi] * a.n_kv_local + kvh) * bs;
 #pragma unroll
       for (int h = 0; h < kHalves; ++h) tma_load_2d_warp(dst + h * (BK * 128) + kb * 128, map, bar, h * 64, row);
@@ -693,8 +697,8 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
     for (int c = 0; c < kNC; ++c) tmem_ld_32x32b_x16(tS(sb) + lane_off + c_key0 + c * 16, sr[c]);
 #pragma unroll
     for (int c = 0; c < kNC; ++c) tmem_ld_wait_regs(sr[c]);
-    const int kbase = t * BK + c_key0;
-    const bool need_mask = t * BK + BK - 1 > s0 + q0;  // (CTA-uniform) some key lies past a query
+    const int kbase = (tb0 + t) * BK + c_key0;
+    const bool need_mask = (tb0 + t) * BK + BK - 1 > s0 + q0;  // (CTA-uniform) some key lies past a query
     float mt = -INFINITY;
     if (need_mask) {
 #pragma unroll
@@ -816,8 +820,87 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
   if (tr0 && n_done == 0) a.trace[255] = globaltimer_ns();
   red[chh * kPBQ + r] = l;
   named_bar_sync(1, 256);
-  const float inv = 1.f / (l + red[(chh ^ 1) * kPBQ + r]);
+  const float l_row = l + red[(chh ^ 1) * kPBQ + r];
+  const float inv = 1.f / l_row;
 
+  if (ksplit > 1) {
+    // key split: unnormalised O half-row + (m, l) of this key range, then the pair's last CTA merges
+    const int pq = qh * ntq + qt;
+    const size_t prow = (static_cast<size_t>(pq) * ksplit + ks) * kPBQ + r;
+    // O partial layout [pair][range][head_dim / 4][128 rows] float4: a warp's 32 rows of one
+    // 4-dim group are 512 contiguous bytes (coalesced writes here and reads in the merge)
+    float4* po4 = reinterpret_cast<float4*>(a.part_o) + (static_cast<size_t>(pq) * ksplit + ks) * (HD / 4) * kPBQ;
+#pragma unroll
+    for (int c = 0; c < kOC; c += 16) {
+      uint32_t ov[16];
+      tmem_ld_32x32b_x16(tO + lane_off + chh * kOC + c, ov);
+      tmem_ld_wait_regs(ov);
+#pragma unroll
+      for (int j = 0; j < 16; j += 4)
+        __stcg(po4 + ((chh * kOC + c + j) >> 2) * kPBQ + r,
+               make_float4(__uint_as_float(ov[j]), __uint_as_float(ov[j + 1]), __uint_as_float(ov[j + 2]),
+                           __uint_as_float(ov[j + 3])));
+    }
+    if (chh == 0) __stcg(reinterpret_cast<float2*>(a.part_ml + 2 * prow), make_float2(m, l_row));
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int old = atomicAdd(a.counters + pq, 1);
+      s_merge = old == ksplit - 1;
+      if (s_merge) a.counters[pq] = 0;  // re-arm for the next launch
+    }
+    __syncthreads();
+    if (s_merge && q0 + r < p) {
+      __threadfence();
+      const size_t row0 = static_cast<size_t>(pq) * ksplit * kPBQ + r;  // + i * kPBQ per range
+      // ksplit <= 4 (host): every range's (m, l) and O loads are issued before they are used
+      float mi[4], li[4], wi[4];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 ml = i < ksplit ? __ldcg(reinterpret_cast<const float2*>(a.part_ml + 2 * (row0 + i * kPBQ)))
+                                     : make_float2(-INFINITY, 0.f);
+        mi[i] = ml.x;
+        li[i] = ml.y;
+        mx = fmaxf(mx, ml.x);
+      }
+      float lsum = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        wi[i] = mi[i] == -INFINITY ? 0.f : exp2f(mi[i] - mx);  // ranges past ksplit: m = -inf
+        lsum = fmaf(wi[i], li[i], lsum);
+      }
+      const float linv = 1.f / lsum;
+      __nv_bfloat16* dst = a.out + static_cast<size_t>(a.q_row0 + q0 + r) * a.out_ld + qh * HD + chh * kOC;
+#pragma unroll 2
+      for (int c = 0; c < kOC; c += 8) {
+        float4 x[4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4* src = reinterpret_cast<const float4*>(a.part_o) +
+                              (static_cast<size_t>(pq) * ksplit + i) * (HD / 4) * kPBQ +
+                              ((chh * kOC + c) >> 2) * kPBQ + r;
+          x[i][0] = i < ksplit ? __ldcg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+          x[i][1] = i < ksplit ? __ldcg(src + kPBQ) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float w = wi[i] * linv;
+          acc[0] = fmaf(x[i][0].x, w, acc[0]); acc[1] = fmaf(x[i][0].y, w, acc[1]);
+          acc[2] = fmaf(x[i][0].z, w, acc[2]); acc[3] = fmaf(x[i][0].w, w, acc[3]);
+          acc[4] = fmaf(x[i][1].x, w, acc[4]); acc[5] = fmaf(x[i][1].y, w, acc[5]);
+          acc[6] = fmaf(x[i][1].z, w, acc[6]); acc[7] = fmaf(x[i][1].w, w, acc[7]);
+        }
+        uint4 o4;
+        o4.x = pack_bf16x2(acc[0], acc[1]);
+        o4.y = pack_bf16x2(acc[2], acc[3]);
+        o4.z = pack_bf16x2(acc[4], acc[5]);
+        o4.w = pack_bf16x2(acc[6], acc[7]);
+        *reinterpret_cast<uint4*>(dst + c) = o4;
+      }
+    }
+  } else
   // O rows (bf16): this warp's half of the row's dims; rows past the chunk are not written
   {
     __nv_bfloat16* dst = a.out + static_cast<size_t>(a.q_row0 + q0 + r) * a.out_ld + qh * HD + chh * kOC;
@@ -907,7 +990,7 @@ cudaError_t launch_prefill_tc(const PrefillAttnArgs& a, const CUtensorMap& mq, c
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int items = (a.p + kPBQ - 1) / kPBQ * a.n_q_local;
+  const int items = (a.p + kPBQ - 1) / kPBQ * a.n_q_local * std::max(1, a.ksplit);
   static const int cap = getenv("SARATHI_PREFILL_CTAS") ? atoi(getenv("SARATHI_PREFILL_CTAS")) : 0;  // experiment
   const int ctas = cap > 0 ? std::min(cap, items) : items;
   if (a.pdl)

@@ -56,6 +56,14 @@ struct PrefillAttnArgs {
   int out_ld = 0;
   unsigned long long* trace = nullptr;  // debug: globaltimer stamps of CTA (0,0) (tcgen05 kernel)
   int pdl = 0;  // launch with programmatic dependent launch (attention chain; tcgen05 kernel)
+  // key split (tcgen05 kernel): each (q-tile, head) pair's key tiles are divided into ksplit
+  // contiguous ranges, one CTA each; ranges write unnormalised fp32 O + (m, l) partials and the last
+  // CTA of the pair to finish merges them (flash-decoding style) into out.  The host keeps ksplit
+  // <= the key-tile count of the first q-tile, so no range is empty.
+  int ksplit = 1;
+  float* part_o = nullptr;   // [pairs][ksplit][128 rows][head_dim]
+  float* part_ml = nullptr;  // [pairs][ksplit][128 rows][2] (running max in log2 units, row sum)
+  int* counters = nullptr;   // [pairs], zero between launches (the merging CTA re-zeroes)
   unsigned long long* span_start = nullptr;  // profiling, as DecodeAttnArgs (tcgen05 kernel)
   unsigned long long* span_end = nullptr;
 };

@@ -283,6 +283,12 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   part_cap = static_cast<size_t>(32) << 20;
   SRET(dalloc(&part_o, part_cap));
   SRET(dalloc(&part_lse, part_cap / 64 + 1024));
+  pp_rows = static_cast<size_t>(64) << 10;  // 64 K rows of head_dim floats (32 MB at hd 128)
+  SRET(dalloc(&pp_o, pp_rows * hd));
+  SRET(dalloc(&pp_ml, 2 * pp_rows));
+  pp_pairs = ((Tmax + 127) / 128) * nq_l;
+  SRET(dalloc(&pp_ctr, pp_pairs));
+  SRET(check(cudaMemset(pp_ctr, 0, pp_pairs * sizeof(int)), "memset"));
   SRET(check(cudaStreamSynchronize(stream), "init sync"));
   return Status::ok();
 }
@@ -599,6 +605,38 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       pa.out = o;
       pa.out_ld = q_dim_l;
       pa.pdl = chain;
+      {
+        // key split for few (q-tile, head) pairs: when the chunk's attention (≈ 2.1 µs per
+        // 128-key tile per CTA, the measured per-tile chain) would outlast the decode attention
+        // beside it (its wave cost model below), or has the GPU to itself, its key tiles are
+        // divided over up to 4 CTAs per pair (merged by the last; no range may be empty)
+        const int ntq = (p + 127) / 128, pairs = ntq * nq_l;
+        const int first_tiles = (pre->start_pos + std::min(128, p) + 127) / 128;
+        const double est_p = 2.1 * ((pre->start_pos + p + 127) / 128);
+        double est_d = 0.0;
+        if (d > 0) {
+          int mb = 0;
+          for (int j = 0; j < d; ++j) mb = std::max(mb, (dec->positions[j] + 1 + block_size - 1) / block_size);
+          const long long ctas = static_cast<long long>(d) * nkv_l;
+          est_d = 1e30;
+          for (int sp = 1; sp <= mb; ++sp) {
+            const int bps = (mb + sp - 1) / sp;
+            const double waves = static_cast<double>((ctas * sp + 2 * num_sms - 1) / (2 * num_sms));
+            est_d = std::min(est_d, waves * (2.0 + 1.5 * bps) + (sp > 1 ? 3.0 : 0.0));
+          }
+        }
+        int ks = 1;
+        if (d > 0 ? est_p > 1.5 * est_d : 2 * pairs <= num_sms)
+          ks = d > 0 ? static_cast<int>(std::ceil(est_p / std::max(est_d, 1.0))) : num_sms / pairs;
+        static const int ks_env = getenv("SARATHI_PREFILL_KSPLIT") ? atoi(getenv("SARATHI_PREFILL_KSPLIT")) : 0;
+        if (ks_env > 0) ks = ks_env;
+        ks = std::min({ks, 4, first_tiles, std::max(1, num_sms / pairs)});
+        if (static_cast<size_t>(pairs) * ks * 128 > pp_rows || pairs > pp_pairs) ks = 1;
+        pa.ksplit = std::max(1, ks);
+        pa.part_o = pp_o;
+        pa.part_ml = pp_ml;
+        pa.counters = pp_ctr;
+      }
       // with decodes in the batch, the chunk's attention overlaps the decode attention: by default
       // both run in the main stream as an "attention chain" (prefill, PDL-launched, waits for QKV
       // and then triggers the decode grid, whose CTAs wait for the prefill grid at their end), so

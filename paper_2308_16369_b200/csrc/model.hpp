@@ -83,6 +83,12 @@ struct Model {
   float* part_o = nullptr;
   float* part_lse = nullptr;
   size_t part_cap = 0;  // floats in part_o
+  // chunked-prefill key-split partials (PrefillAttnArgs::ksplit): O rows, (m, l), per-pair counters
+  float* pp_o = nullptr;
+  float* pp_ml = nullptr;
+  int* pp_ctr = nullptr;
+  size_t pp_rows = 0;  // 128-row x ksplit capacity of pp_o in rows of head_dim floats
+  int pp_pairs = 0;    // counters
   int* meta_dev = nullptr;
   int* meta_host_buf[2] = {nullptr, nullptr};  // pinned, double-buffered
   cudaEvent_t meta_ev[2] = {nullptr, nullptr};

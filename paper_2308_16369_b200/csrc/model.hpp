@@ -44,8 +44,9 @@ struct Model {
   sarathi_model_config cfg{};
   int rank = 0, world = 1, device = 0;
   cudaStream_t stream = nullptr;
-  // side stream: the chunked-prefill attention runs concurrently with the (HBM-bound) decode
-  // attention of the same layer (fork after the QKV GEMM, join before the O GEMM)
+  // side stream, used only with SARATHI_ATTN_CHAIN=0 (the default "attention chain" keeps both
+  // attentions in the main stream): the chunked-prefill attention runs concurrently with the
+  // decode attention of the same layer (fork after the QKV GEMM, join before the O GEMM)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int num_sms = 148;

@@ -146,6 +146,7 @@ struct QkvLane {  // per-warp / per-lane constants of the fused QKV epilogue
   int dd;         // rotation index of this lane (dim within the half)
   bool rope;      // q or k head
   float th_hi, th_lo;  // theta_dd = base^(-2 dd / hd) as hi + lo
+  float cd, sd;        // cos / sin of one position step (theta_dd): the consecutive-position recurrence
 };
 
 SARATHI_DEVICE QkvLane qkv_lane(const EpiParams& ep, int mt, uint32_t q, uint32_t lane) {
@@ -158,6 +159,7 @@ SARATHI_DEVICE QkvLane qkv_lane(const EpiParams& ep, int mt, uint32_t q, uint32_
   o.rope = o.gh < ep.n_q_local + ep.n_kv_local;
   o.th_hi = __ldg(ep.rope_theta + 2 * o.dd);
   o.th_lo = __ldg(ep.rope_theta + 2 * o.dd + 1);
+  rope_cos_sin(1, o.th_hi, o.th_lo, o.cd, o.sd);
   return o;
 }
 
@@ -244,11 +246,9 @@ SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[1
         // consecutive positions (prefill chunks): angle-addition recurrence from the chunk's first
         // position, 4 FMAs per token instead of a reduction + sincos (error growth ~16 ulp)
         const bool consec = s_consec[c0 >> 4] != 0;
-        float cd = 1.f, sd = 0.f, cr = 1.f, sr = 0.f;
-        if (consec) {
-          rope_cos_sin(1, ql.th_hi, ql.th_lo, cd, sd);
-          rope_cos_sin(s_pos[c0], ql.th_hi, ql.th_lo, cr, sr);
-        }
+        const float cd = ql.cd, sd = ql.sd;
+        float cr = 1.f, sr = 0.f;
+        if (consec) rope_cos_sin(s_pos[c0], ql.th_hi, ql.th_lo, cr, sr);
 #pragma unroll
         for (int j0 = 0; j0 < 16; j0 += 8) {
           float xp[8], c[8], sn[8];

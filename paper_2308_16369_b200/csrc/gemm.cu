@@ -240,7 +240,7 @@ SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[1
     case EPI_QKV_ROPE: {
       const int half = ep.head_dim >> 1;
       const bool lo = lane < 16;
-      if (ql.rope) {
+      if (ql.rope && !(ep.dbg & 32)) {  // dbg bit 5: no RoPE math (timing only)
         // branch-free, 8 tokens per batch so the shuffles, position loads and sincos of different
         // tokens overlap (a per-token dependent chain cost ~150 cycles x 16 per chunk)
         // consecutive positions (prefill chunks): angle-addition recurrence from the chunk's first

@@ -17,7 +17,8 @@ from oracle import model as om
 from oracle.metrics import relative_error
 
 pytestmark = pytest.mark.gpu
-TOL = 2e-2
+TOL = 2e-2       # north-star contract
+REGRESS = 8e-3   # regression bound on every compared quantity (observed 0.3-3.5e-3)
 
 
 def _bf16(bits):
@@ -90,3 +91,4 @@ def _layer_local(cfg, p, s, d, ctx, layers):
     print("full-size layer-local errors:", {k: f"{v:.2e}" for k, v in errs.items()})
     for k, v in errs.items():
         assert v <= TOL, (k, v)
+        assert v <= REGRESS, (k, v)

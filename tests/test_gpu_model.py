@@ -16,7 +16,9 @@ from tests import gpu_harness as gh
 from tests.test_oracle_sched import CONFIG1_EXPECTED
 
 pytestmark = pytest.mark.gpu
-TOL = 2e-2
+TOL = 2e-2       # north-star contract (BASELINE.json): max relative error
+REGRESS = 8e-3   # regression bound: observed 1-3.5e-3 (bf16 operands, fp32 accumulate / residual; SURVEY
+                 # §8(c) error model: a branch far above ~5e-3 is a bug, not rounding)
 CONFIG1 = [(1, 5, 12, 0), (2, 11, 12, 0), (3, 16, 12, 0), (0, 64, 4, 3)]
 
 
@@ -32,8 +34,10 @@ def _check(steps, expected_plans=None):
     for s in steps:
         assert np.array_equal(s.gpu_slots, s.ref_slots)
     errs = gh.worst_errors(steps)
+    print("worst errors", errs)
     assert errs["logits"] <= TOL, errs
     assert errs["hidden"] <= TOL, errs
+    assert errs["logits"] <= REGRESS and errs["hidden"] <= REGRESS, errs
     return errs
 
 

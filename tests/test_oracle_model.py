@@ -202,7 +202,9 @@ def test_dense_mask_equals_key_range_loop():
 # Scalar-loop brute force of one whole forward at H = 8 (pure Python, no NumPy algebra).
 # ---------------------------------------------------------------------------
 
-def _scalar_forward(w: om.ModelWeights, toks):
+def _scalar_forward(w: om.ModelWeights, toks, trace=None):
+    """Pure-Python loops; `trace` (optional dict) receives per layer l the residual entering the
+    layer ("h_in", l) and the post-RoPE q / k and v of every token ("q"/"k"/"v", l)."""
     cfg = w.cfg
     H, hd, nq, nkv = cfg.hidden, cfg.head_dim, cfg.n_heads, cfg.n_kv_heads
     W = lambda a: a.tolist()
@@ -224,16 +226,21 @@ def _scalar_forward(w: om.ModelWeights, toks):
             out[i + half] = b * math.cos(th) + a * math.sin(th)
         return out
 
+    gelu = cfg.ffn_kind == synth.FFN_GELU
     hs = [W(w.emb[t]) for t in toks]
-    for lw in w.layers:
-        wq, wk, wv, wo, wg, wu, wd = map(W, (lw.wq, lw.wk, lw.wv, lw.wo, lw.wg, lw.wu, lw.wd))
-        Ks, Vs, new = [], [], []
+    for l, lw in enumerate(w.layers):
+        wq, wk, wv, wo, wg, wd = map(W, (lw.wq, lw.wk, lw.wv, lw.wo, lw.wg, lw.wd))
+        wu = None if gelu else W(lw.wu)
+        Ks, Vs, new, Qs = [], [], [], []
+        if trace is not None:
+            trace[("h_in", l)] = [list(h) for h in hs]
         for i, h in enumerate(hs):
             a = norm(h, W(lw.g1))
             q, k, v = mv(wq, a), mv(wk, a), mv(wv, a)
             qh = [rot(q[j * hd:(j + 1) * hd], i) for j in range(nq)]
             Ks.append([rot(k[j * hd:(j + 1) * hd], i) for j in range(nkv)])
             Vs.append([v[j * hd:(j + 1) * hd] for j in range(nkv)])
+            Qs.append(qh)
             o = []
             for j in range(nq):
                 kv = j * nkv // nq
@@ -244,20 +251,116 @@ def _scalar_forward(w: om.ModelWeights, toks):
                 o += [sum(e[t] / z * Vs[t][kv][c] for t in range(i + 1)) for c in range(hd)]
             u = [h[c] + x for c, x in enumerate(mv(wo, o))]
             b = norm(u, W(lw.g2))
-            gate, up = mv(wg, b), mv(wu, b)
-            f = [gate[r] / (1 + math.exp(-gate[r])) * up[r] for r in range(len(gate))]
+            if gelu:  # ffn_ln1 -> GELU-tanh -> ffn_ln2 (Table; reading O-1)
+                z = mv(wg, b)
+                f = [0.5 * x * (1 + math.tanh(math.sqrt(2 / math.pi) * (x + 0.044715 * x * x * x))) for x in z]
+            else:
+                gate, up = mv(wg, b), mv(wu, b)
+                f = [gate[r] / (1 + math.exp(-gate[r])) * up[r] for r in range(len(gate))]
             new.append([u[c] + x for c, x in enumerate(mv(wd, f))])
+        if trace is not None:
+            trace[("q", l)], trace[("k", l)], trace[("v", l)] = Qs, Ks, Vs
         hs = new
     wlm = W(w.wlm)
     return [mv(wlm, norm(h, W(w.gf))) for h in hs]
 
 
-def test_forward_full_matches_scalar_loops():
-    w = om.model_weights(MICRO, 9)
+MICRO_GELU = dataclasses.replace(MICRO, name="micro-gelu", n_layers=2, ffn_kind=synth.FFN_GELU, ffn_hidden=32)
+
+
+@pytest.mark.parametrize("cfg", [MICRO, MICRO_GELU], ids=["swiglu", "gelu"])
+def test_forward_full_matches_scalar_loops(cfg):
+    """Whole forward vs pure-Python loops; the GELU case pins the 2-matrix ffn branch
+    (GELU-tanh after W1, then W2; Table), which has no HF twin."""
+    w = om.model_weights(cfg, 9)
     toks = [3, 15, 0, 3, 7]
     ref = np.array(_scalar_forward(w, toks))
     ours = om.forward_full(w, toks).logits
     assert np.max(np.abs(ours - ref)) < 1e-12 * max(1.0, np.max(np.abs(ref)))
+
+
+def test_gelu_ffn_branch_order():
+    """ffn() GELU branch = W2 . GELU(W1 b): applying GELU after W2 instead (a plausible slip)
+    or using SiLU gives a different answer, so the scalar-loop pin above really covers it."""
+    w = om.model_weights(MICRO_GELU, 4)
+    lw = w.layers[0]
+    b = np.random.default_rng(0).standard_normal((3, MICRO_GELU.hidden))
+    got = om.ffn(MICRO_GELU, lw, b)
+    z = b @ lw.wg.T
+    ref = np.array([[sum(0.5 * x * (1 + math.tanh(math.sqrt(2 / math.pi) * (x + 0.044715 * x ** 3))) * lw.wd[c, r]
+                         for r, x in enumerate(row)) for c in range(MICRO_GELU.hidden)] for row in z])
+    assert np.max(np.abs(got - ref)) < 1e-12
+    assert np.max(np.abs(om.gelu_tanh(z @ lw.wd.T) - ref)) > 1e-3
+
+
+def test_qkv_rows_matches_scalar_loops():
+    """Post-RoPE q, k and v of qkv_rows (the full-size KV-append checker) vs the scalar loops'
+    per-token q/k/v at every position (RoPE at the row's own position, P:L214 fused QKV)."""
+    for cfg in (MICRO, MICRO_GELU):
+        w = om.model_weights(cfg, 9)
+        toks = [3, 15, 0, 3, 7, 11]
+        tr = {}
+        _scalar_forward(w, toks, tr)
+        for l in range(cfg.n_layers):
+            h_in = np.array(tr[("h_in", l)])
+            pos = np.arange(len(toks))
+            q, k, v = om.qkv_rows(cfg, w.layers[l], h_in, pos)
+            assert np.max(np.abs(q - np.array(tr[("q", l)]))) < 1e-12
+            assert np.max(np.abs(k - np.array(tr[("k", l)]))) < 1e-12
+            assert np.max(np.abs(v - np.array(tr[("v", l)]))) < 1e-12
+            # a subset of rows at their own positions gives the same rows (no dependence on batch)
+            sel = np.array([5, 1])
+            q2, k2, _ = om.qkv_rows(cfg, w.layers[l], h_in[sel], pos[sel])
+            assert np.max(np.abs(q2 - q[sel])) < 1e-12 and np.max(np.abs(k2 - k[sel])) < 1e-12
+
+
+@pytest.mark.parametrize("which", ["tiny", "gqa"])
+def test_layer_local_helpers_equal_incremental_replay(which, tiny_w, gqa_w):
+    """layer_rows_from_input / qkv_rows / logits_rows (the checkers behind the full-size GPU
+    parity tests) equal the incremental replay's per-layer rows, appended K/V and logits for
+    chunk rows and decode rows, including positions at 16- and 64-token block boundaries."""
+    w = tiny_w if which == "tiny" else gqa_w
+    cfg = w.cfg
+    V = cfg.vocab
+    toks = {r: synth.tokens(23, r, 0, 80, V) for r in (0, 1, 2)}
+    o = om.IncrementalOracle(w)
+    o.run_batch(om.PrefillItem(1, 0, toks[1][:16]), [])          # request 1 cached [0, 16)
+    o.run_batch(om.PrefillItem(2, 0, toks[2][:63]), [])          # request 2 cached [0, 63)
+    o.run_batch(om.PrefillItem(0, 0, toks[0][:15]), [])
+    # hybrid batch: chunk of request 0 at s = 15 (rows at positions 15, 16, ... 31, 32) + decodes
+    # of request 1 at position 16 and request 2 at 63 (block boundaries for bs 16 / 64)
+    res = o.run_batch(om.PrefillItem(0, 15, toks[0][15:33]),
+                      [om.DecodeItem(1, 16, toks[1][16]), om.DecodeItem(2, 63, toks[2][63])])
+    p = 18
+    rows = [0, 1, p - 1, p, p + 1]
+    req = [0, 0, 0, 1, 2]
+    pos = np.array([15, 16, 32, 16, 63])
+    assert np.array_equal(res.positions[rows], pos)
+    for l in range(cfg.n_layers):
+        h_in = res.layer_inputs[l][rows]
+        kctx = [o.kv[r][l][0][:ps + 1] for r, ps in zip(req, pos)]
+        vctx = [o.kv[r][l][1][:ps + 1] for r, ps in zip(req, pos)]
+        got = om.layer_rows_from_input(cfg, w.layers[l], h_in, pos, kctx, vctx)
+        assert _rel(got, res.hidden[l][rows]) < 1e-12, l
+        _, k, v = om.qkv_rows(cfg, w.layers[l], h_in, pos)
+        assert np.max(np.abs(k - np.stack([kc[-1] for kc in kctx]))) < 1e-12
+        assert np.max(np.abs(v - np.stack([vc[-1] for vc in vctx]))) < 1e-12
+        # dropping the row's own key (key_end = pos - 1, reading O-9 violated) is detected
+        short = [kc[:-1] for kc in kctx]
+        bad = om.layer_rows_from_input(cfg, w.layers[l], h_in[1:], pos[1:] - 1, short[1:], [vc[:-1] for vc in vctx][1:])
+        assert _rel(bad, res.hidden[l][rows[1:]]) > 1e-6
+    vidx = np.arange(3, V, 7)
+    lg = om.logits_rows(cfg, w.gf, w.wlm[vidx], res.hidden[-1][rows])
+    assert _rel(lg, res.logits[rows][:, vidx]) < 1e-12
+
+
+def test_relative_error_hand_example():
+    """||gpu - ref||_inf / ||ref||_inf (reading O-20) on hand-computed values."""
+    from oracle.metrics import relative_error
+    assert relative_error([1.0, 2.5, -3.0], [1.0, 2.0, -4.0]) == pytest.approx(0.25, abs=0)
+    assert relative_error([[0.5, -1.0]], [[0.0, 0.0]]) == 1.0       # zero reference: absolute error
+    assert relative_error(np.float32([2.0]), np.float64([2.0])) == 0.0
+    assert relative_error([-8.0, 1.0], [-10.0, 0.0]) == pytest.approx(0.2)   # sign-aware, inf-norm of ref
 
 
 # ---------------------------------------------------------------------------

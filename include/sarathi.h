@@ -93,7 +93,9 @@ int sarathi_init_model(const sarathi_model_config* cfg, const sarathi_dist* dist
 void sarathi_destroy(sarathi_model* m);
 
 /* Allocates the paged KV pools: per layer K and V, bf16 [num_blocks][n_kv/t][block_size][hd].
- * block_size: multiple of 16 in [16, 256].  Call once, after init, before any request.
+ * block_size: 16, 32, 64 or 128 (each divides the 128-key tile of the tcgen05 prefill-attention
+ * kernel, and the decode kernel's 2-stage K/V ring fits shared memory at head_dim 128).
+ * Call once, after init, before any request.
  * Errors: EINVAL, ESTATE (already allocated), ECUDA (out of memory). */
 int sarathi_alloc_kv(sarathi_model* m, int64_t num_blocks, int32_t block_size);
 
@@ -239,14 +241,17 @@ typedef struct {
 int sarathi_sched_create(int32_t B, int32_t C, int32_t policy, int32_t tile_adjust, int64_t num_blocks,
                          int32_t block_size, sarathi_sched** out);
 void sarathi_sched_destroy(sarathi_sched* s);
-/* P >= 1, D >= 0.  EINVAL on duplicate id. */
+/* P >= 1, D >= 0.  EINVAL on duplicate id; ENOKV when ceil((P+D)/block_size) > num_blocks (the
+ * request could never be admitted and, under strict FCFS, would block every later request). */
 int sarathi_sched_submit(sarathi_sched* s, int64_t req_id, int32_t P, int32_t D, int32_t arrival_iter);
 /* Forms the next plan.  Returns 1 with a plan, 0 if idle (nothing eligible this iteration; call
  * sarathi_sched_idle_step), <0 on error.  dec_req[cap], dec_pos[cap], admitted[cap] receive the
- * decode items and newly admitted ids; EINVAL if cap is too small. */
+ * decode items and newly admitted ids (each at most B entries); EINVAL, with the scheduler
+ * unchanged, if cap < B. */
 int sarathi_sched_next(sarathi_sched* s, sarathi_plan* plan, int64_t* dec_req, int32_t* dec_pos, int64_t* admitted,
                        int32_t cap);
-/* Marks the last plan as executed; finished[cap] receives requests that completed (free their KV). */
+/* Marks the last plan as executed; finished[cap] receives requests that completed (free their KV;
+ * at most B).  EINVAL, with the scheduler unchanged, if finished != NULL and cap < B. */
 int sarathi_sched_complete(sarathi_sched* s, int64_t* finished, int32_t cap, int32_t* n_finished);
 int sarathi_sched_idle_step(sarathi_sched* s);
 int sarathi_sched_done(const sarathi_sched* s, int32_t* done);

@@ -178,6 +178,10 @@ class Scheduler:
     def submit(self, req_id: int, P: int, D: int, arrival_iter: int = 0) -> None:
         if req_id in self.reqs or P < 1 or D < 0:
             raise ValueError("bad request")
+        if self.alloc.blocks_for(P + D) > self.alloc.num_blocks:
+            # never admissible: under strict FCFS it would block every later request (S: every
+            # request eventually finishes; reading O-16)
+            raise ValueError("P+D reservation exceeds the block pool")
         self.reqs[req_id] = ReqState(req_id, P, D, arrival_iter)
 
     def _running(self) -> List[ReqState]:

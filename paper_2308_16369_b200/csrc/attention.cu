@@ -13,8 +13,7 @@
 //    (progressive causal mask, PAPER.md L362-369 Fig. fig-attn-chunk-prefills; inclusive, reading
 //    O-9) over the request's paged cache (prefix + the chunk itself, appended by the QKV epilogue),
 //    on the 5th-gen tensor cores: S and O accumulate in TMEM, P goes through shared memory.
-//  * prefill_attn_kernel: the mma.sync flash kernel, kept for block sizes the 128-key tcgen05 tile
-//    does not divide.
+//    Every block size alloc_kv accepts (16/32/64/128) divides its 128-key tile.
 #include "common.cuh"
 #include "kernels.cuh"
 #include "gemm.cuh"
@@ -325,186 +324,6 @@ __global__ void decode_combine_kernel(DecodeAttnArgs a, int HD) {
     a.out[static_cast<size_t>(a.q_row0 + j) * a.out_ld + qh * HD + dd] = __float2bfloat16_rn(o / den);
   }
 }
-
-// smem tile [rows][HD] bf16 with 16-byte chunks XOR-swizzled by (row % 8)
-template <int HD>
-SARATHI_DEVICE uint32_t swz(int row, int chunk) {
-  return static_cast<uint32_t>(row * (HD * 2) + ((chunk ^ (row & 7)) << 4));
-}
-
-template <int HD>
-__global__ void __launch_bounds__(128)
-    prefill_attn_kernel(PrefillAttnArgs a) {
-  constexpr int BQ = 64, BK = 64;
-  constexpr int kChunks = HD / 8;  // 16-byte chunks per row
-  const int qt = blockIdx.x, qh = blockIdx.y;
-  const int kvh = qh * a.n_kv_local / a.n_q_local;
-  const int q0 = qt * BQ;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gid = lane >> 2, tig = lane & 3;
-  const int s0 = a.start;          // cached prefix length s
-  const int p = a.p;
-  const int kv_len = s0 + p;
-  const int q_hi = min(q0 + BQ, p);  // exclusive
-  const int key_end = s0 + q_hi;     // keys needed: [0, key_end)
-  const int ntiles = (key_end + BK - 1) / BK;
-  const int bs = a.block_size;
-
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* sQ = smem;                         // BQ x HD
-  uint8_t* sK = sQ + BQ * HD * 2;             // 2 x BK x HD
-  uint8_t* sV = sK + 2 * BK * HD * 2;         // 2 x BK x HD
-  const uint32_t sQa = smem_u32(sQ), sKa = smem_u32(sK), sVa = smem_u32(sV);
-
-  // load Q tile
-  for (int c = tid; c < BQ * kChunks; c += 128) {
-    const int r = c / kChunks, ch = c % kChunks;
-    const int qi = q0 + r;
-    const __nv_bfloat16* src = a.q + static_cast<size_t>(a.q_row0 + min(qi, p - 1)) * a.q_ld + qh * HD + ch * 8;
-    cp_async16(sQa + swz<HD>(r, ch), src, qi < p);
-  }
-  auto load_kv = [&](int tile, int buf) {
-    for (int c = tid; c < BK * kChunks; c += 128) {
-      const int r = c / kChunks, ch = c % kChunks;
-      const int key = tile * BK + r;
-      const bool valid = key < kv_len;
-      const int kk = valid ? key : 0;
-      const int blk = a.block_table[kk / bs];
-      const size_t row = (static_cast<size_t>(blk) * a.n_kv_local + kvh) * bs + kk % bs;
-      const uint32_t off = buf * BK * HD * 2 + swz<HD>(r, ch);
-      cp_async16(sKa + off, static_cast<const __nv_bfloat16*>(a.kcache) + row * HD + ch * 8, valid);
-      cp_async16(sVa + off, static_cast<const __nv_bfloat16*>(a.vcache) + row * HD + ch * 8, valid);
-    }
-  };
-  load_kv(0, 0);
-  cp_async_commit();
-
-  const float sl2 = a.scale * kLog2e;
-  float o[HD / 8][4];
-#pragma unroll
-  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
-  const int qr0 = q0 + warp * 16 + gid;        // this thread's two query rows (chunk-local)
-  const int qpos0 = s0 + qr0, qpos1 = qpos0 + 8;
-  uint32_t qf[HD / 16][4];
-
-  for (int t = 0; t < ntiles; ++t) {
-    const int buf = t & 1;
-    if (t + 1 < ntiles) load_kv(t + 1, buf ^ 1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    if (t == 0) {
-#pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const int row = warp * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
-        const int ch = kk * 2 + (lane >> 4);
-        ldmatrix_x4(sQa + swz<HD>(row, ch), qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
-      }
-    }
-    // S = Q K^T : 16 x 64 per warp
-    float sacc[BK / 8][4];
-#pragma unroll
-    for (int n = 0; n < BK / 8; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
-    const uint32_t kb = sKa + buf * BK * HD * 2;
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
-#pragma unroll
-      for (int n2 = 0; n2 < BK / 16; ++n2) {
-        const int row = n2 * 16 + (lane & 7) + 8 * (lane >> 4);
-        const int ch = kk * 2 + ((lane >> 3) & 1);
-        uint32_t b0, b1, b2, b3;
-        ldmatrix_x4(kb + swz<HD>(row, ch), b0, b1, b2, b3);
-        mma_bf16_16816(sacc[2 * n2], qf[kk], b0, b1);
-        mma_bf16_16816(sacc[2 * n2 + 1], qf[kk], b2, b3);
-      }
-    }
-    // mask + online softmax (log2 domain)
-    const int kbase = t * BK;
-    float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-    for (int n = 0; n < BK / 8; ++n) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int key = kbase + n * 8 + 2 * tig + (e & 1);
-        const int qp = (e < 2) ? qpos0 : qpos1;
-        float v = sacc[n][e] * sl2;
-        if (key > qp) v = -INFINITY;
-        sacc[n][e] = v;
-        mx[e >> 1] = fmaxf(mx[e >> 1], v);
-      }
-    }
-    float scale[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-      const float mnew = fmaxf(mrow[r], mx[r]);
-      scale[r] = (mnew == -INFINITY) ? 1.f : exp2f(mrow[r] - mnew);
-      mrow[r] = mnew;
-    }
-    float rs[2] = {0.f, 0.f};
-#pragma unroll
-    for (int n = 0; n < BK / 8; ++n) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float m = mrow[e >> 1];
-        const float pv = (m == -INFINITY) ? 0.f : exp2f(sacc[n][e] - m);
-        sacc[n][e] = pv;
-        rs[e >> 1] += pv;
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], 1);
-      rs[r] += __shfl_xor_sync(0xffffffffu, rs[r], 2);
-      lrow[r] = lrow[r] * scale[r] + rs[r];
-    }
-#pragma unroll
-    for (int i = 0; i < HD / 8; ++i) {
-      o[i][0] *= scale[0];
-      o[i][1] *= scale[0];
-      o[i][2] *= scale[1];
-      o[i][3] *= scale[1];
-    }
-    // O += P V
-    const uint32_t vb = sVa + buf * BK * HD * 2;
-#pragma unroll
-    for (int kk = 0; kk < BK / 16; ++kk) {
-      uint32_t pa[4];
-      pa[0] = pack_bf16x2(sacc[2 * kk][0], sacc[2 * kk][1]);
-      pa[1] = pack_bf16x2(sacc[2 * kk][2], sacc[2 * kk][3]);
-      pa[2] = pack_bf16x2(sacc[2 * kk + 1][0], sacc[2 * kk + 1][1]);
-      pa[3] = pack_bf16x2(sacc[2 * kk + 1][2], sacc[2 * kk + 1][3]);
-#pragma unroll
-      for (int n2 = 0; n2 < HD / 16; ++n2) {
-        const int row = kk * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
-        const int ch = n2 * 2 + (lane >> 4);
-        uint32_t b0, b1, b2, b3;
-        ldmatrix_x4_trans(vb + swz<HD>(row, ch), b0, b1, b2, b3);
-        mma_bf16_16816(o[2 * n2], pa, b0, b1);
-        mma_bf16_16816(o[2 * n2 + 1], pa, b2, b3);
-      }
-    }
-    __syncthreads();
-  }
-  cp_async_wait<0>();
-
-  // write O rows (bf16)
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int qi = qr0 + 8 * r;
-    if (qi >= p) continue;
-    const float inv = 1.f / lrow[r];
-    __nv_bfloat16* dst = a.out + static_cast<size_t>(a.q_row0 + qi) * a.out_ld + qh * HD;
-#pragma unroll
-    for (int n = 0; n < HD / 8; ++n) {
-      const int col = n * 8 + 2 * tig;
-      *reinterpret_cast<uint32_t*>(dst + col) = pack_bf16x2(o[n][2 * r] * inv, o[n][2 * r + 1] * inv);
-    }
-  }
-}
-
 
 // ---------------------------------------------------------------------------
 // Chunked-prefill attention on the 5th-gen tensor cores (tcgen05 / TMEM / TMA).
@@ -1003,39 +822,22 @@ cudaError_t launch_prefill_tc(const PrefillAttnArgs& a, const CUtensorMap& mq, c
 cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, const CUtensorMap* qmap, const CUtensorMap* kmap,
                                      const CUtensorMap* vmap, cudaStream_t st) {
   if (a.p == 0) return cudaSuccess;
-  const bool tc = qmap && kmap && vmap && (a.block_size == 16 || a.block_size == 32 || a.block_size == 64 ||
-                                           a.block_size == 128);
+  if (!qmap || !kmap || !vmap || 128 % a.block_size) return cudaErrorInvalidValue;  // alloc_kv: bs | 128
   // 128-key tiles; SARATHI_PREFILL_BK=64 selects the narrow tile (2 CTAs or a CTA + decode CTAs per
   // SM).  Measured: TP-1 step unchanged, TP-8 rank shapes 2-4 % slower, so not the default.
   static const bool narrow = getenv("SARATHI_PREFILL_BK") && atoi(getenv("SARATHI_PREFILL_BK")) == 64;
   const bool bk128 = a.block_size == 128 || !narrow;
   // P in TMEM (default); SARATHI_PREFILL_PT=0 selects the smem P image
   static const bool pt = !(getenv("SARATHI_PREFILL_PT") && atoi(getenv("SARATHI_PREFILL_PT")) == 0);
-  if (tc && a.head_dim == 128)
+  if (a.head_dim == 128)
     return !bk128 ? launch_prefill_tc<128, 64>(a, *qmap, *kmap, *vmap, st)
            : pt   ? launch_prefill_tc<128, 128, true>(a, *qmap, *kmap, *vmap, st)
                   : launch_prefill_tc<128, 128>(a, *qmap, *kmap, *vmap, st);
-  if (tc && a.head_dim == 64)
+  if (a.head_dim == 64)
     return !bk128 ? launch_prefill_tc<64, 64>(a, *qmap, *kmap, *vmap, st)
            : pt   ? launch_prefill_tc<64, 128, true>(a, *qmap, *kmap, *vmap, st)
                   : launch_prefill_tc<64, 128>(a, *qmap, *kmap, *vmap, st);
-  // mma.sync kernel: block sizes the tcgen05 tile (128 keys) does not tile
-  dim3 grid((a.p + 63) / 64, a.n_q_local);
-  if (a.head_dim == 128) {
-    const size_t smem = (64 + 4 * 64) * 128 * 2;
-    static bool c = false;
-    if (!c) {
-      cudaFuncSetAttribute(prefill_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      c = true;
-    }
-    prefill_attn_kernel<128><<<grid, 128, smem, st>>>(a);
-  } else if (a.head_dim == 64) {
-    const size_t smem = (64 + 4 * 64) * 64 * 2;
-    prefill_attn_kernel<64><<<grid, 128, smem, st>>>(a);
-  } else {
-    return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace sarathi

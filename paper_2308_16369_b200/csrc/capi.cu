@@ -338,17 +338,18 @@ void sarathi_sched_destroy(sarathi_sched* s) {
 int sarathi_sched_submit(sarathi_sched* s, int64_t req_id, int32_t P, int32_t D, int32_t arrival_iter) {
   if (!s) return fail(SARATHI_EINVAL, "sched_submit: NULL");
   std::string err;
-  if (!s->s->submit(req_id, P, D, arrival_iter, &err)) return fail(SARATHI_EINVAL, err);
+  const int rc = s->s->submit(req_id, P, D, arrival_iter, &err);
+  if (rc != SARATHI_OK) return fail(rc, err);
   return SARATHI_OK;
 }
 
 int sarathi_sched_next(sarathi_sched* s, sarathi_plan* plan, int64_t* dec_req, int32_t* dec_pos, int64_t* admitted,
                        int32_t cap) {
   if (!s || !plan) return fail(SARATHI_EINVAL, "sched_next: NULL");
+  // admitted and decodes are each at most B: check before next() mutates the scheduler
+  if (cap < s->s->B()) return fail(SARATHI_EINVAL, "sched_next: cap must be >= B");
   sarathi::PlanOut p;
   const bool have = s->s->next(&p);
-  if (static_cast<int32_t>(p.decodes.size()) > cap || static_cast<int32_t>(p.admitted.size()) > cap)
-    return fail(SARATHI_EINVAL, "sched_next: cap too small");
   plan->iteration = p.iteration;
   plan->prefill_req = p.prefill_req;
   plan->prefill_start = p.prefill_start;
@@ -366,8 +367,9 @@ int sarathi_sched_next(sarathi_sched* s, sarathi_plan* plan, int64_t* dec_req, i
 
 int sarathi_sched_complete(sarathi_sched* s, int64_t* finished, int32_t cap, int32_t* n_finished) {
   if (!s || !n_finished) return fail(SARATHI_EINVAL, "sched_complete: NULL");
+  // at most B requests run, so at most B finish: check before complete() mutates the scheduler
+  if (finished && cap < s->s->B()) return fail(SARATHI_EINVAL, "sched_complete: cap must be >= B");
   const auto fin = s->s->complete();
-  if (static_cast<int32_t>(fin.size()) > cap && finished) return fail(SARATHI_EINVAL, "sched_complete: cap too small");
   *n_finished = static_cast<int32_t>(fin.size());
   for (size_t i = 0; i < fin.size(); ++i)
     if (finished) finished[i] = fin[i];

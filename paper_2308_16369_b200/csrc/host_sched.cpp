@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include "../../include/sarathi.h"
+
 namespace sarathi {
 
 BlockAllocator::BlockAllocator(int64_t num_blocks, int32_t block_size)
@@ -11,7 +13,7 @@ BlockAllocator::BlockAllocator(int64_t num_blocks, int32_t block_size)
   for (int64_t b = 0; b < num_blocks; ++b) free_.insert(static_cast<int32_t>(b));
 }
 
-bool BlockAllocator::alloc(int64_t req, int32_t max_tokens) {
+bool BlockAllocator::alloc(int64_t req, int64_t max_tokens) {
   const int64_t n = blocks_for(max_tokens);
   if (n > static_cast<int64_t>(free_.size())) return false;
   std::vector<int32_t> t;
@@ -35,10 +37,14 @@ void BlockAllocator::free(int64_t req) {
 Scheduler::Scheduler(int32_t B, int32_t C, int32_t policy, bool tile_adjust, int64_t num_blocks, int32_t block_size)
     : B_(B), C_(C), policy_(policy), tile_adjust_(tile_adjust), alloc_(num_blocks, block_size) {}
 
-bool Scheduler::submit(int64_t req, int32_t P, int32_t D, int32_t arrival, std::string* err) {
+int Scheduler::submit(int64_t req, int32_t P, int32_t D, int32_t arrival, std::string* err) {
   if (reqs_.count(req) || P < 1 || D < 0) {
     if (err) *err = "sched_submit: duplicate id or bad P/D";
-    return false;
+    return SARATHI_EINVAL;
+  }
+  if (alloc_.blocks_for(static_cast<int64_t>(P) + D) > alloc_.num_blocks()) {
+    if (err) *err = "sched_submit: the P+D KV reservation exceeds the whole block pool (never admissible)";
+    return SARATHI_ENOKV;
   }
   Req r;
   r.id = req;
@@ -46,7 +52,7 @@ bool Scheduler::submit(int64_t req, int32_t P, int32_t D, int32_t arrival, std::
   r.D = D;
   r.arrival = arrival;
   reqs_.emplace(req, r);
-  return true;
+  return SARATHI_OK;
 }
 
 std::vector<Scheduler::Req*> Scheduler::running() {
@@ -78,7 +84,7 @@ bool Scheduler::next(PlanOut* out) {
     int32_t nrun = static_cast<int32_t>(run.size());
     for (Req* r : pend) {
       if (nrun >= B_ || !alloc_.can_alloc(static_cast<int64_t>(r->P) + r->D)) break;
-      alloc_.alloc(r->id, r->P + r->D);
+      alloc_.alloc(r->id, static_cast<int64_t>(r->P) + r->D);
       r->admitted = true;
       r->admit_seq = admit_counter_++;
       plan.admitted.push_back(r->id);

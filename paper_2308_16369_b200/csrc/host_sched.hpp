@@ -22,10 +22,10 @@ class BlockAllocator {
   bool can_alloc(int64_t max_tokens) const { return blocks_for(max_tokens) <= static_cast<int64_t>(free_.size()); }
   bool has(int64_t req) const { return tables_.count(req) != 0; }
   // returns false if it does not fit
-  bool alloc(int64_t req, int32_t max_tokens);
+  bool alloc(int64_t req, int64_t max_tokens);
   void free(int64_t req);
   const std::vector<int32_t>& table(int64_t req) const { return tables_.at(req); }
-  int32_t reserved(int64_t req) const { return reserved_.at(req); }
+  int64_t reserved(int64_t req) const { return reserved_.at(req); }
   int64_t free_blocks() const { return static_cast<int64_t>(free_.size()); }
   // slot = table[pos / bs] * bs + pos % bs
   int64_t slot(int64_t req, int32_t pos) const {
@@ -38,7 +38,7 @@ class BlockAllocator {
   int32_t block_size_ = 1;
   std::set<int32_t> free_;
   std::map<int64_t, std::vector<int32_t>> tables_;
-  std::map<int64_t, int32_t> reserved_;
+  std::map<int64_t, int64_t> reserved_;
 };
 
 struct PlanOut {
@@ -56,7 +56,11 @@ class Scheduler {
  public:
   enum Policy { SARATHI = 0, ORCA_BEST = 1, REQUEST_LEVEL = 2 };
   Scheduler(int32_t B, int32_t C, int32_t policy, bool tile_adjust, int64_t num_blocks, int32_t block_size);
-  bool submit(int64_t req, int32_t P, int32_t D, int32_t arrival, std::string* err);
+  // SARATHI_OK, SARATHI_EINVAL (duplicate id / P < 1 / D < 0) or SARATHI_ENOKV (the P+D
+  // reservation needs more blocks than the whole pool: it could never be admitted and, with strict
+  // FCFS, would block every later request forever)
+  int submit(int64_t req, int32_t P, int32_t D, int32_t arrival, std::string* err);
+  int32_t B() const { return B_; }
   // true if a plan was formed
   bool next(PlanOut* out);
   std::vector<int64_t> complete();

@@ -295,8 +295,10 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
 
 Status Model::alloc_kv(int64_t nb, int32_t bs) {
   if (kv_ready) return Status::err(SARATHI_ESTATE, "alloc_kv: already allocated");
-  if (nb < 1 || nb > (1ll << 31) - 1 || bs < 16 || bs > 256 || bs % 16)
-    return Status::err(SARATHI_EINVAL, "alloc_kv: num_blocks >= 1, block_size multiple of 16 in [16, 256]");
+  // block sizes the attention kernels tile: each divides the tcgen05 prefill kernel's 128-key tile,
+  // and the decode kernel's smallest (2-stage) K/V ring, 2 x 2 x bs x hd x 2 B, fits shared memory
+  if (nb < 1 || nb > (1ll << 31) - 1 || (bs != 16 && bs != 32 && bs != 64 && bs != 128))
+    return Status::err(SARATHI_EINVAL, "alloc_kv: num_blocks >= 1 and block_size in {16, 32, 64, 128}");
   const size_t per = static_cast<size_t>(nb) * nkv_l * bs * cfg.head_dim;
   kpool.resize(cfg.n_layers);
   vpool.resize(cfg.n_layers);

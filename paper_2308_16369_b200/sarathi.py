@@ -232,13 +232,17 @@ class Model:
             keep += [rq, tk, ps]
             ds = DecodeSetC(d, _p(rq, C.c_int64), _p(tk, C.c_int32), _p(ps, C.c_int32))
         ptr = logits_ptr
+        R = (p + d) if flags & RETURN_ALL_ROWS else d + (1 if p else 0)
         if logits_host is not None:
-            assert logits_host.dtype == np.float32 and logits_host.flags.c_contiguous
+            if logits_host.dtype != np.float32 or not logits_host.flags.c_contiguous:
+                raise ValueError("logits_host must be a C-contiguous float32 array")
+            if not flags & NO_LOGITS and logits_host.size < R * self.vocab:
+                raise ValueError(f"logits_host holds {logits_host.size} floats < R*V = {R}*{self.vocab}")
             flags |= LOGITS_HOST
             ptr = logits_host.ctypes.data
         _check(lib.sarathi_run_hybrid_batch(self.h, C.byref(pc) if pc else None, C.byref(ds) if ds else None,
                                             C.c_void_p(ptr) if ptr else None, flags))
-        return (p + d) if flags & RETURN_ALL_ROWS else d + (1 if p else 0)
+        return R
 
     def truncate(self, req_id: int, new_len: int):
         _check(lib.sarathi_request_truncate(self.h, req_id, new_len))

@@ -162,3 +162,32 @@ def test_prefill_attention_variants(env, select, n):
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert f"{n} passed" in r.stdout
+
+
+def test_block_size_32_schedule(S):
+    """bs = 32, the one accepted block size no other test runs: a multi-block hybrid schedule."""
+    cfg = dataclasses.replace(synth.TINY, name="tiny-bs32", max_seq_len=256)
+    reqs = [(1, 70, 5, 0), (2, 33, 9, 0), (3, 5, 12, 1)]
+    steps = gh.run_schedule(S, cfg, reqs, B=3, C=24, num_blocks=24, block_size=32, weight_seed=2)
+    _check(steps)
+
+
+def test_rejected_block_sizes_and_undersized_logits(S):
+    """alloc_kv accepts only block sizes the attention kernels tile (16/32/64/128); an undersized
+    host logits buffer is refused before the library writes R*V floats into it."""
+    cfg = synth.TINY
+    m = S.Model(S.config_from(cfg, 32), seed=0)
+    for bs in (48, 256, 8, 0):
+        with pytest.raises(S.SarathiError) as e:
+            m.alloc_kv(16, bs)
+        assert e.value.code == S.EINVAL
+    m.alloc_kv(16, 16)
+    m.request_alloc(1, 40)
+    toks = synth.tokens(7, 1, 0, 12, cfg.vocab)
+    with pytest.raises(ValueError):
+        m.run_hybrid_batch((1, 0, toks), [], logits_host=np.zeros((1, cfg.vocab), np.float32),
+                           flags=S.RETURN_ALL_ROWS)          # needs 12 rows
+    assert m.cached_len(1) == 0
+    out = np.zeros((12, cfg.vocab), np.float32)
+    assert m.run_hybrid_batch((1, 0, toks), [], logits_host=out, flags=S.RETURN_ALL_ROWS) == 12
+    m.close()

@@ -43,6 +43,61 @@ def test_error_reporting_without_gpu(S):
     assert e.value.code == S.EINVAL
 
 
+def test_never_admissible_request_is_rejected_at_submit(S):
+    """A request whose P+D reservation exceeds the whole pool could never be admitted; under strict
+    FCFS it would block every later request forever.  Both schedulers refuse it at submit (C++:
+    ENOKV, Python twin: ValueError) and the later requests still drain."""
+    s = S.Scheduler(2, 16, 4, 16)                  # pool: 4 blocks x 16 tokens = 64 tokens
+    with pytest.raises(S.SarathiError) as e:
+        s.submit(1, 60, 5)                          # 65 tokens -> 5 blocks > 4
+    assert e.value.code == S.ENOKV
+    with pytest.raises(S.SarathiError) as e:
+        s.submit(2, 2 ** 31 - 1, 2 ** 31 - 1)       # P+D overflows int32: still rejected, not wrapped
+    assert e.value.code == S.ENOKV
+    s.submit(3, 40, 24)                             # exactly 64 tokens: admissible
+    plans, _ = _drain_cpp_sched(s)
+    assert plans and s.done()
+    py = osch.Scheduler(2, 16, osch.BlockAllocator(4, 16))
+    with pytest.raises(ValueError):
+        py.submit(1, 60, 5)
+    py.submit(3, 40, 24)
+    assert osch.run_schedule(py)
+
+
+def test_sched_cap_checked_before_state_changes(S):
+    """sched_next / sched_complete with cap < B fail with EINVAL and leave the scheduler as it was
+    (the admitted ids and finished ids would otherwise be lost)."""
+    s = S.Scheduler(4, 16, 32, 16)
+    for rid in range(3):
+        s.submit(rid, 8, 1)
+    cap, s.cap = s.cap, 3                           # 3 < B = 4
+    with pytest.raises(S.SarathiError) as e:
+        s.next()
+    assert e.value.code == S.EINVAL
+    s.cap = cap
+    plan, admitted = s.next()                       # nothing was admitted by the failed call
+    assert admitted == [0, 1, 2] and plan[0] == (0, 0, 8)
+    s.cap = 2
+    with pytest.raises(S.SarathiError):
+        s.complete()
+    s.cap = cap
+    assert s.complete() == []                       # the plan is still pending, completes once
+    plan, admitted = s.next()
+    assert admitted == [] and plan[0] == (1, 0, 8) and plan[1] == [(0, 8)]
+
+
+def _drain_cpp_sched(s):
+    plans = []
+    while not s.done():
+        plan, _ = s.next()
+        if plan is None:
+            s.idle_step()
+            continue
+        plans.append(plan)
+        s.complete()
+    return plans, None
+
+
 def _drain_cpp(S, B, C, nb, bs, reqs, policy=0, tile_adjust=False):
     s = S.Scheduler(B, C, nb, bs, policy=policy, tile_adjust=tile_adjust)
     for rid, P, D, arr in reqs:

@@ -79,16 +79,26 @@ typedef struct {
 /* Writes a fresh ncclUniqueId (128 bytes) to out.  Host only.  ENCCL if NCCL is unavailable. */
 int sarathi_nccl_unique_id(void* out128);
 
-/* Creates the model on dist->device and generates this rank's weight shards ON DEVICE from the
- * counter-based generator spec (synth/__init__.py header; seed = weight_seed).  Weights are
- * packed in kernel layout: per layer QKV [(nq+2nkv)/t*hd, H] (inside each head, row 32j+l is dim
+/* Creates the model on dist->device with this rank's weight shards, either
+ *  - host_tensors == NULL: generated ON DEVICE from the counter-based generator spec
+ *    (synth/__init__.py header; seed = weight_seed), or
+ *  - host_tensors != NULL: loaded from the caller's LOGICAL (unsharded) bf16 tensors in host memory
+ *    (read during the call, not retained; weight_seed ignored), nn.Linear [out, in] row-major:
+ *      host_tensors[9*l + 0..8] = layer l's  Wq [nq*hd, H], Wk [nkv*hd, H], Wv [nkv*hd, H],
+ *                                 Wo [H, nq*hd], Wg [H2, H] (GELU: W1), Wu [H2, H] (GELU: NULL,
+ *                                 unused), Wd [H, H2] (GELU: W2), g1 [H], g2 [H]
+ *      host_tensors[9*L + 0..2]  = embedding [V, H], final norm gain [H], LM head [V, H]
+ *    (the paper's real-model setting, §4.5: configs of real LLaMA/GPT models).
+ *    The library takes this rank's Megatron shard (column/row/vocab-parallel, sarathi_shard_map),
+ *    applies the packed row orders and the tile-major layout below; EINVAL if a needed pointer is NULL.
+ * Weights are packed in kernel layout: per layer QKV [(nq+2nkv)/t*hd, H] (inside each head, row 32j+l is dim
  * 16j+l for l < 16 and dim hd/2+16j+l-16 otherwise: rotate-half partners share a warp), gate||up
  * interleaved in 16-row blocks [2*H2/t, H] (rows 32b..32b+15 gate features 16b.., the next 16 the
  * matching up features), O [H, nq*hd/t], down [H, H2/t]; embedding and final norm replicated; LM
  * head vocab-parallel [ceil(V/t), H].  Ownership: the library owns all device memory.
  * Errors: EINVAL (bad config / divisibility by world), ECUDA (allocation), ENCCL. */
 int sarathi_init_model(const sarathi_model_config* cfg, const sarathi_dist* dist, uint64_t weight_seed,
-                       sarathi_model** out);
+                       const void* const* host_tensors, sarathi_model** out);
 
 void sarathi_destroy(sarathi_model* m);
 

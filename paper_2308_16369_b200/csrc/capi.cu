@@ -43,11 +43,11 @@ int sarathi_nccl_unique_id(void* out128) {
 }
 
 int sarathi_init_model(const sarathi_model_config* cfg, const sarathi_dist* dist, uint64_t weight_seed,
-                       sarathi_model** out) {
+                       const void* const* host_tensors, sarathi_model** out) {
   if (!cfg || !dist || !out) return fail(SARATHI_EINVAL, "init_model: NULL argument");
   auto* h = new (std::nothrow) sarathi_model();
   if (!h) return fail(SARATHI_EINVAL, "init_model: out of host memory");
-  const sarathi::Status s = h->m.init(*cfg, *dist, weight_seed);
+  const sarathi::Status s = h->m.init(*cfg, *dist, weight_seed, host_tensors);
   if (s.code != SARATHI_OK) {
     h->m.destroy();
     delete h;

@@ -73,6 +73,7 @@ NcclApi* nccl_api(std::string* err) {
 // Counter-based generator constants (synth/__init__.py spec).
 constexpr int kWQ = 0, kWK = 1, kWV = 2, kWO = 3, kWG = 4, kWU = 5, kWD = 6, kG1 = 7, kG2 = 8;
 constexpr int kEmbTau = 1 << 20, kGfTau = (1 << 20) + 1, kWlmTau = (1 << 20) + 2;
+constexpr int kHostPerLayer = 9;  // host_tensors per layer: wq wk wv wo wg wu wd g1 g2 (= kWQ..kG2)
 
 float weight_scale(double sigma) { return static_cast<float>(std::sqrt(3.0) * sigma / 16777216.0); }
 
@@ -118,7 +119,8 @@ Status Model::dalloc_padded(__nv_bfloat16** p, int rows, int cols) {
     if (_s.code != SARATHI_OK) return _s; \
   } while (0)
 
-Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_t seed_) {
+Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_t seed_,
+                   const void* const* host_tensors) {
   cfg = c;
   rank = d.rank;
   world = d.world;
@@ -188,7 +190,49 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   SRET(dalloc(&d_tau, max_rows));
   SRET(dalloc(&d_scl, max_rows));
   SRET(dalloc(&d_base, max_rows));
+  // host_tensors: logical (unsharded) bf16 tensors, nn.Linear [out, in] layout, indexed
+  // [layer * kHostPerLayer + kind] (kind = kWQ..kG2) then emb, final gain, LM head
+  const int n_host = L * kHostPerLayer + 3;
+  auto host_ptr = [&](int t) -> const uint16_t* {  // generator tensor id -> host tensor
+    int idx;
+    if (t == kEmbTau) idx = L * kHostPerLayer;
+    else if (t == kGfTau) idx = L * kHostPerLayer + 1;
+    else if (t == kWlmTau) idx = L * kHostPerLayer + 2;
+    else idx = (t / 16) * kHostPerLayer + t % 16;
+    return idx < n_host ? static_cast<const uint16_t*>(host_tensors[idx]) : nullptr;
+  };
+  if (host_tensors) {
+    for (int i = 0; i < n_host; ++i)
+      if (!host_tensors[i] && !(c.ffn_kind == SARATHI_FFN_GELU && i < L * kHostPerLayer && i % kHostPerLayer == kWU))
+        return Status::err(SARATHI_EINVAL, "init_model: host_tensors[" + std::to_string(i) + "] is NULL");
+  }
+  __nv_bfloat16* staging = nullptr;  // host path: row-major shard [rows][cols] before packing
+  size_t staging_elems = 0;
+  std::vector<uint16_t> hbuf;
+  // host path: every packed row r is the contiguous segment [base[r], base[r] + cols) of logical
+  // tensor tau[r] (shard_map), so the shard is gathered row by row, copied H2D and packed on device
+  auto upload = [&](__nv_bfloat16* dst, int rows, int cols, int packed) -> Status {
+    hbuf.resize(static_cast<size_t>(rows) * cols);
+    for (int r = 0; r < rows; ++r)
+      std::memcpy(hbuf.data() + static_cast<size_t>(r) * cols, host_ptr(tau[r]) + base[r], static_cast<size_t>(cols) * 2);
+    if (!packed) return check(cudaMemcpy(dst, hbuf.data(), hbuf.size() * 2, cudaMemcpyHostToDevice), "H2D weights");
+    if (hbuf.size() > staging_elems) {
+      if (staging) cudaFree(staging);
+      staging = nullptr;
+      SRET(check(cudaMalloc(&staging, hbuf.size() * 2), "cudaMalloc staging"));
+      staging_elems = hbuf.size();
+    }
+    SRET(check(cudaMemcpy(staging, hbuf.data(), hbuf.size() * 2, cudaMemcpyHostToDevice), "H2D weights"));
+    SRET(check(launch_pack_weight(staging, dst, rows, cols, stream), "pack weight"));
+    ++launches;
+    return check(cudaStreamSynchronize(stream), "pack sync");
+  };
+  struct StagingGuard {
+    __nv_bfloat16** p;
+    ~StagingGuard() { if (*p) cudaFree(*p); }
+  } staging_guard{&staging};
   auto gen = [&](__nv_bfloat16* dst, int rows, int cols, int packed) -> Status {
+    if (host_tensors) return upload(dst, rows, cols, packed);
     SRET(check(cudaMemcpyAsync(d_tau, tau.data(), rows * sizeof(int), cudaMemcpyHostToDevice, stream), "H2D"));
     SRET(check(cudaMemcpyAsync(d_scl, scl.data(), rows * sizeof(float), cudaMemcpyHostToDevice, stream), "H2D"));
     SRET(check(cudaMemcpyAsync(d_base, base.data(), rows * sizeof(long long), cudaMemcpyHostToDevice, stream), "H2D"));
@@ -222,9 +266,14 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
     if (!make_tmap_weight(&w.m_qkv, w.qkv, qkv_rows, H) || !make_tmap_weight(&w.m_o, w.o, H, q_dim_l) ||
         !make_tmap_weight(&w.m_gu, w.gu, gu_rows, H) || !make_tmap_weight(&w.m_down, w.down, H, h2_l))
       return Status::err(SARATHI_ECUDA, "cuTensorMapEncodeTiled failed for a weight");
-    SRET(check(launch_gaingen(w.g1, H, 16 * l + kG1, 0, seed, stream), "gaingen"));
-    SRET(check(launch_gaingen(w.g2, H, 16 * l + kG2, 0, seed, stream), "gaingen"));
-    launches += 2;
+    if (host_tensors) {
+      SRET(check(cudaMemcpy(w.g1, host_ptr(16 * l + kG1), H * 2, cudaMemcpyHostToDevice), "H2D gain"));
+      SRET(check(cudaMemcpy(w.g2, host_ptr(16 * l + kG2), H * 2, cudaMemcpyHostToDevice), "H2D gain"));
+    } else {
+      SRET(check(launch_gaingen(w.g1, H, 16 * l + kG1, 0, seed, stream), "gaingen"));
+      SRET(check(launch_gaingen(w.g2, H, 16 * l + kG2, 0, seed, stream), "gaingen"));
+      launches += 2;
+    }
   }
   // embedding (replicated), final gain, LM head (vocab-parallel)
   SRET(dalloc(&emb, static_cast<size_t>(c.vocab) * H));
@@ -235,8 +284,12 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   }
   SRET(gen(emb, c.vocab, H, 0));
   SRET(dalloc(&gf, H));
-  SRET(check(launch_gaingen(gf, H, kGfTau, 0, seed, stream), "gaingen"));
-  ++launches;
+  if (host_tensors) {
+    SRET(check(cudaMemcpy(gf, host_ptr(kGfTau), H * 2, cudaMemcpyHostToDevice), "H2D gain"));
+  } else {
+    SRET(check(launch_gaingen(gf, H, kGfTau, 0, seed, stream), "gaingen"));
+    ++launches;
+  }
   SRET(dalloc_padded(&lm, vocab_l, H));
   {
     ShardDims sd;

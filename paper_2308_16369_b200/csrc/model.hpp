@@ -123,7 +123,8 @@ struct Model {
   void op_end(int op, cudaEvent_t b, cudaStream_t s = nullptr);
   Status collect_op_times();
 
-  Status init(const sarathi_model_config& c, const sarathi_dist& d, uint64_t seed);
+  // host_tensors: NULL (generate from seed) or the logical weights, see sarathi_init_model
+  Status init(const sarathi_model_config& c, const sarathi_dist& d, uint64_t seed, const void* const* host_tensors);
   Status alloc_kv(int64_t num_blocks, int32_t block_size);
   Status run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* dec, float* logits, int32_t flags);
   void destroy();

@@ -80,7 +80,7 @@ def _load() -> C.CDLL:
     P, I32, I64, U64, VP, F = C.POINTER, C.c_int32, C.c_int64, C.c_uint64, C.c_void_p, C.c_float
     sig = {
         "sarathi_nccl_unique_id": [VP],
-        "sarathi_init_model": [P(ModelConfigC), P(DistC), U64, P(VP)],
+        "sarathi_init_model": [P(ModelConfigC), P(DistC), U64, P(VP), P(VP)],
         "sarathi_alloc_kv": [VP, I64, I32],
         "sarathi_kv_bytes_per_token": [VP, P(I64)],
         "sarathi_max_batch": [VP, I32, I64, P(I32)],
@@ -162,13 +162,22 @@ class Model:
     """Owns a sarathi_model handle (one per GPU / process)."""
 
     def __init__(self, cfg: ModelConfigC, seed: int, rank: int = 0, world: int = 1, device: int = 0,
-                 nccl_id: Optional[bytes] = None, stream: int = 0):
+                 nccl_id: Optional[bytes] = None, stream: int = 0,
+                 host_tensors: Optional[Sequence[Optional[np.ndarray]]] = None):
+        """host_tensors: None (weights generated on device from `seed`) or the 9*L + 3 logical bf16
+        tensors (uint16 bit patterns, nn.Linear [out, in]) in the order of include/sarathi.h."""
         self.cfg = cfg
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         dist = DistC(rank, world, device, C.cast(self._idbuf, C.c_void_p) if self._idbuf else None,
                      C.c_void_p(stream) if stream else None)
+        ht = None
+        if host_tensors is not None:
+            if len(host_tensors) != 9 * cfg.n_layers + 3:
+                raise ValueError(f"host_tensors: expected {9 * cfg.n_layers + 3} entries")
+            keep = [None if t is None else np.ascontiguousarray(t, dtype=np.uint16) for t in host_tensors]
+            ht = (C.c_void_p * len(keep))(*[None if t is None else t.ctypes.data for t in keep])
         h = C.c_void_p()
-        _check(lib.sarathi_init_model(C.byref(cfg), C.byref(dist), C.c_uint64(seed), C.byref(h)))
+        _check(lib.sarathi_init_model(C.byref(cfg), C.byref(dist), C.c_uint64(seed), ht, C.byref(h)))
         self.h = h
         self.vocab = cfg.vocab
 

@@ -26,8 +26,9 @@ class StepResult:
 
 def run_schedule(S, cfg: synth.ModelConfig, reqs: Sequence[Tuple[int, int, int, int]], B: int, C: int,
                  num_blocks: int, block_size: int, weight_seed: int = 0, tok_seed: int = 1001,
-                 max_tokens: int = 64, dump: bool = True, oracle_weights=None) -> List[StepResult]:
-    m = S.Model(S.config_from(cfg, max_tokens_per_batch=max_tokens), seed=weight_seed)
+                 max_tokens: int = 64, dump: bool = True, oracle_weights=None,
+                 host_tensors=None) -> List[StepResult]:
+    m = S.Model(S.config_from(cfg, max_tokens_per_batch=max_tokens), seed=weight_seed, host_tensors=host_tensors)
     m.alloc_kv(num_blocks, block_size)
     sched = S.Scheduler(B, C, num_blocks, block_size)
     for r in reqs:
@@ -76,6 +77,18 @@ def run_schedule(S, cfg: synth.ModelConfig, reqs: Sequence[Tuple[int, int, int, 
             palloc.free(rid)
             orc.free(rid)
     m.close()
+    return out
+
+
+def synth_host_tensors(cfg: synth.ModelConfig, seed: int):
+    """The logical bf16 weights (uint16 bits) in sarathi_init_model's host_tensors order, produced
+    by the synth generator on the host (the seed path generates the same bits on device)."""
+    out = []
+    for l in range(cfg.n_layers):
+        for k in (synth.WQ, synth.WK, synth.WV, synth.WO, synth.WG, synth.WU, synth.WD, synth.G1, synth.G2):
+            out.append(None if (k == synth.WU and cfg.ffn_kind == synth.FFN_GELU)
+                       else synth.layer_tensor_bits(cfg, seed, l, k))
+    out += [synth.embedding_bits(cfg, seed), synth.final_gain_bits(cfg, seed), synth.lm_head_bits(cfg, seed)]
     return out
 
 

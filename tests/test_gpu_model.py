@@ -191,3 +191,35 @@ def test_rejected_block_sizes_and_undersized_logits(S):
     out = np.zeros((12, cfg.vocab), np.float32)
     assert m.run_hybrid_batch((1, 0, toks), [], logits_host=out, flags=S.RETURN_ALL_ROWS) == 12
     m.close()
+
+
+@pytest.mark.parametrize("variant", ["gqa", "gelu"])
+def test_host_tensor_weights(S, variant):
+    """sarathi_init_model(host_tensors=...): logical weights uploaded from host memory are packed
+    and sharded by the library into exactly the device bits the seed path generates (every packed
+    tensor compared bit for bit), and a hybrid schedule on them matches the fp64 oracle."""
+    if variant == "gqa":
+        cfg = dataclasses.replace(synth.TINY, name="tiny-gqa", n_kv_heads=2)
+    else:
+        cfg = dataclasses.replace(synth.TINY, name="tiny-gelu", ffn_kind=synth.FFN_GELU, ffn_hidden=1024)
+    ht = gh.synth_host_tensors(cfg, 13)
+    a = S.Model(S.config_from(cfg, 16), seed=13)
+    b = S.Model(S.config_from(cfg, 16), seed=999, host_tensors=ht)   # seed ignored on the host path
+    H = cfg.hidden
+    sizes = {0: (cfg.q_dim + 2 * cfg.kv_dim) * H, 1: H * cfg.q_dim,
+             2: (2 if cfg.ffn_kind == synth.FFN_SWIGLU else 1) * cfg.ffn_hidden * H, 3: H * cfg.ffn_hidden, 4: H, 5: H}
+    for l in range(cfg.n_layers):
+        for t, n in sizes.items():
+            assert np.array_equal(a.weight(l, t, 0, n), b.weight(l, t, 0, n)), (l, t)
+    for t, n in ((16, cfg.vocab * H), (17, H), (18, cfg.vocab * H)):
+        assert np.array_equal(a.weight(0, t, 0, n), b.weight(0, t, 0, n)), t
+    a.close()
+    b.close()
+    steps = gh.run_schedule(S, cfg, [(1, 20, 5, 0), (2, 9, 7, 0)], B=2, C=8, num_blocks=16, block_size=16,
+                            weight_seed=13, host_tensors=ht)
+    _check(steps)
+    bad = list(ht)
+    bad[3] = None                                                        # layer 0 Wo missing
+    with pytest.raises(S.SarathiError) as e:
+        S.Model(S.config_from(cfg, 16), seed=0, host_tensors=bad)
+    assert e.value.code == S.EINVAL

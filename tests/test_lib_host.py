@@ -86,6 +86,12 @@ def test_sched_cap_checked_before_state_changes(S):
     assert admitted == [] and plan[0] == (1, 0, 8) and plan[1] == [(0, 8)]
 
 
+def test_host_tensors_count_checked_before_the_library(S):
+    import synth
+    with pytest.raises(ValueError):
+        S.Model(S.config_from(synth.TINY, 16), seed=0, host_tensors=[None] * 5)
+
+
 def _drain_cpp_sched(s):
     plans = []
     while not s.done():

@@ -72,9 +72,23 @@ typedef struct {
   int32_t rank;
   int32_t world;
   int32_t device;             /* CUDA device ordinal used by this handle               */
-  const void* nccl_unique_id; /* 128 bytes, or NULL when world == 1                    */
+  const void* nccl_unique_id; /* 128 bytes, or NULL when world == 1 or local_group set */
   void* stream;               /* cudaStream_t all device work is enqueued on            */
+  void* local_group;          /* sarathi_local_group* (world > 1 on ONE device), or NULL */
 } sarathi_dist;
+
+/* Local tensor-parallel group: `world` (2..8) model handles created on the SAME device with
+ * dist.local_group set, each driven by its own host thread making identical calls (SPMD), stand in
+ * for one process per GPU.  Every world > 1 path of run_hybrid_batch runs unchanged (Megatron
+ * shards, bf16 partials, all-reduce-add fused into RMSNorm, vocab-parallel LM head + all-gather);
+ * only the two collectives are replaced: the all-reduce sums the ranks' bf16 partials in rank
+ * order (fp32 accumulate, identical on every rank) and the all-gather copies peer buffers, both
+ * ordered by CUDA events + a host barrier (timeout -> ENCCL; SARATHI_GROUP_TIMEOUT_S, default
+ * 120 s).  With dist.stream == NULL each rank gets its own library-owned stream.  Destroy the group
+ * after its models.  Used for on-one-GPU TP parity (§2.3). */
+typedef struct sarathi_local_group sarathi_local_group;
+int sarathi_local_group_create(int32_t world, int32_t device, sarathi_local_group** out);
+void sarathi_local_group_destroy(sarathi_local_group* g);
 
 /* Writes a fresh ncclUniqueId (128 bytes) to out.  Host only.  ENCCL if NCCL is unavailable. */
 int sarathi_nccl_unique_id(void* out128);

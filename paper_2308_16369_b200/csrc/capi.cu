@@ -42,6 +42,19 @@ int sarathi_nccl_unique_id(void* out128) {
   return SARATHI_OK;
 }
 
+int sarathi_local_group_create(int32_t world, int32_t device, sarathi_local_group** out) {
+  if (!out) return fail(SARATHI_EINVAL, "local_group_create: NULL");
+  sarathi::LocalGroup* g = nullptr;
+  const sarathi::Status s = sarathi::local_group_create(world, device, &g);
+  if (s.code != SARATHI_OK) return from(s);
+  *out = reinterpret_cast<sarathi_local_group*>(g);
+  return SARATHI_OK;
+}
+
+void sarathi_local_group_destroy(sarathi_local_group* g) {
+  sarathi::local_group_destroy(reinterpret_cast<sarathi::LocalGroup*>(g));
+}
+
 int sarathi_init_model(const sarathi_model_config* cfg, const sarathi_dist* dist, uint64_t weight_seed,
                        const void* const* host_tensors, sarathi_model** out) {
   if (!cfg || !dist || !out) return fail(SARATHI_EINVAL, "init_model: NULL argument");

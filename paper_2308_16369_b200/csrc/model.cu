@@ -160,7 +160,14 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   }
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device);
 
-  if (world > 1) {
+  if (world > 1 && d.local_group) {
+    SRET(local_group_join(static_cast<LocalGroup*>(d.local_group), rank, world, device));
+    group = static_cast<LocalGroup*>(d.local_group);
+    if (!stream) {  // each rank of a local group needs its own stream
+      SRET(check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "rank stream"));
+      owns_stream = true;
+    }
+  } else if (world > 1) {
     std::string err;
     NcclApi* api = nccl_api(&err);
     if (!api) return Status::err(SARATHI_ENCCL, err);
@@ -322,6 +329,8 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   SRET(dalloc(&o, static_cast<size_t>(Tmax) * q_dim_l));
   SRET(dalloc(&f, static_cast<size_t>(Tmax) * h2_l));
   SRET(dalloc(&ar, static_cast<size_t>(Tmax) * H));
+  if (group) SRET(dalloc(&ar_red, static_cast<size_t>(Tmax) * H));
+  ar_res = ar;
   SRET(dalloc(&af, static_cast<size_t>(Tmax) * H));
   SRET(dalloc(&logits_dev, static_cast<size_t>(Tmax) * c.vocab));
   if (world > 1) {
@@ -596,8 +605,14 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
                                  cudaMemcpyDeviceToDevice, stream),
                  "dump");
   };
-  NcclApi* api = world > 1 ? nccl_api(nullptr) : nullptr;
+  NcclApi* api = world > 1 && !group ? nccl_api(nullptr) : nullptr;
+  // TP all-reduce of the bf16 partial in `ar`; ar_res = the buffer holding the sum afterwards
   auto allreduce = [&]() -> Status {
+    if (group) {
+      ar_res = ar_red;
+      return local_allreduce_bf16(group, rank, ar, ar_red, static_cast<size_t>(T) * H, num_sms, stream);
+    }
+    ar_res = ar;
     ncclResult_t r = api->allReduce(ar, ar, static_cast<size_t>(T) * H, ncclBfloat16, ncclSum,
                                     static_cast<ncclComm_t>(nccl), stream);
     if (r != ncclSuccess) return Status::err(SARATHI_ENCCL, "ncclAllReduce failed");
@@ -619,7 +634,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     {
       unsigned long long *sp0, *sp1;
       SRET(take_span(SARATHI_OP_RMSNORM, &sp0, &sp1));
-      SRET(check(launch_rmsnorm(h, pending_ar ? ar : nullptr, w.g1, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1), "rmsnorm1"));
+      SRET(check(launch_rmsnorm(h, pending_ar ? ar_res : nullptr, w.g1, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1), "rmsnorm1"));
     }
     op_end(SARATHI_OP_RMSNORM, ob);
     ++launches;
@@ -826,7 +841,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     {
       unsigned long long *sp0, *sp1;
       SRET(take_span(SARATHI_OP_RMSNORM, &sp0, &sp1));
-      SRET(check(launch_rmsnorm(h, world > 1 ? ar : nullptr, w.g2, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1), "rmsnorm2"));
+      SRET(check(launch_rmsnorm(h, world > 1 ? ar_res : nullptr, w.g2, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1), "rmsnorm2"));
     }
     op_end(SARATHI_OP_RMSNORM, ob);
     ++launches;
@@ -859,7 +874,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     }
   }
   if (pending_ar && (dump_layers || !want_logits || all_rows)) {
-    SRET(check(launch_residual_add(h, ar, T, H, stream), "residual add"));
+    SRET(check(launch_residual_add(h, ar_res, T, H, stream), "residual add"));
     ++launches;
     pending_ar = false;
   }
@@ -867,7 +882,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   if (want_logits) {
     ob = op_begin();
     // final norm on the R logit rows (adds the pending TP partial for exactly those rows)
-    SRET(check(launch_rmsnorm(h, pending_ar ? ar : nullptr, gf, af, d_rows, R, H, cfg.rms_eps, stream), "final norm"));
+    SRET(check(launch_rmsnorm(h, pending_ar ? ar_res : nullptr, gf, af, d_rows, R, H, cfg.rms_eps, stream), "final norm"));
     ++launches;
     const bool host_out = flags & SARATHI_LOGITS_HOST;
     float* target = host_out ? logits_dev : logits;
@@ -881,9 +896,13 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       el.out = logits_local;
       el.ldo = vocab_l;
       SRET(gemm(m_lm, vocab_l, H, af, H, R, el));
-      ncclResult_t r = api->allGather(logits_local, logits_gather, static_cast<size_t>(R) * vocab_l, ncclFloat32,
-                                      static_cast<ncclComm_t>(nccl), stream);
-      if (r != ncclSuccess) return Status::err(SARATHI_ENCCL, "ncclAllGather failed");
+      if (group) {
+        SRET(local_allgather_f32(group, rank, logits_local, logits_gather, static_cast<size_t>(R) * vocab_l, stream));
+      } else {
+        ncclResult_t r = api->allGather(logits_local, logits_gather, static_cast<size_t>(R) * vocab_l, ncclFloat32,
+                                        static_cast<ncclComm_t>(nccl), stream);
+        if (r != ncclSuccess) return Status::err(SARATHI_ENCCL, "ncclAllGather failed");
+      }
       SRET(check(launch_vocab_permute(logits_gather, target, world, R, vocab_l, cfg.vocab, stream), "permute"));
       ++launches;
     }
@@ -911,8 +930,14 @@ void Model::destroy() {
     if (api) api->commDestroy(static_cast<ncclComm_t>(nccl));
     nccl = nullptr;
   }
+  if (group) {
+    local_group_leave(group, rank);
+    group = nullptr;
+  }
   for (void* p : allocations) cudaFree(p);
   allocations.clear();
+  if (owns_stream && stream) cudaStreamDestroy(stream);
+  owns_stream = false;
   if (aux) cudaStreamSynchronize(aux);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);

@@ -30,6 +30,18 @@ struct Status {
   }
 };
 
+// Local TP group (collective.cu): `world` handles on one device standing in for one process per GPU.
+struct LocalGroup;
+Status local_group_create(int world, int device, LocalGroup** out);
+void local_group_destroy(LocalGroup* g);
+Status local_group_join(LocalGroup* g, int rank, int world, int device);
+void local_group_leave(LocalGroup* g, int rank);
+// result = bf16(sum over ranks of partial) on every rank (ncclAllReduce semantics, out of place)
+Status local_allreduce_bf16(LocalGroup* g, int rank, const __nv_bfloat16* partial, __nv_bfloat16* result, size_t count,
+                            int num_sms, cudaStream_t st);
+// dst[r * count ...] = rank r's src (ncclAllGather layout)
+Status local_allgather_f32(LocalGroup* g, int rank, const float* src, float* dst, size_t count, cudaStream_t st);
+
 struct LayerWeights {
   __nv_bfloat16* qkv = nullptr;   // [(nq_l + 2 nkv_l) hd][H]
   __nv_bfloat16* o = nullptr;     // [H][nq_l hd]
@@ -102,8 +114,12 @@ struct Model {
   // caches
   std::map<std::tuple<int, int, int>, GemmPlan> plans;
   std::map<std::tuple<const void*, int, int, int>, CUtensorMap> xmaps;
-  // NCCL
+  // TP collectives: NCCL communicator (one process per GPU) or a local group (one device)
   void* nccl = nullptr;
+  LocalGroup* group = nullptr;
+  __nv_bfloat16* ar_red = nullptr;        // local group: all-reduce result buffer [Tmax][H]
+  const __nv_bfloat16* ar_res = nullptr;  // buffer holding the latest all-reduce result (ar or ar_red)
+  bool owns_stream = false;
   int64_t launches = 0;
   // I/O accounting and per-op timers
   int64_t last_h2d = 0, last_d2h = 0;

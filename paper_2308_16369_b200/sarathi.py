@@ -33,7 +33,7 @@ EXPORTS = [
     "sarathi_sched_submit", "sarathi_sched_next", "sarathi_sched_complete", "sarathi_sched_idle_step",
     "sarathi_sched_done", "sarathi_sched_block_table", "sarathi_op_gemm", "sarathi_op_rmsnorm",
     "sarathi_request_truncate", "sarathi_last_io_bytes", "sarathi_set_profiling", "sarathi_op_times", "sarathi_op_kernel_times",
-    "sarathi_op_pack_weight", "sarathi_shard_map",
+    "sarathi_op_pack_weight", "sarathi_shard_map", "sarathi_local_group_create", "sarathi_local_group_destroy",
 ]
 GEMM_W_PACKED = 0x100
 OP_NAMES = ["embed", "rmsnorm", "gemm_qkv", "prefill_attn", "decode_attn", "gemm_o", "gemm_gate_up",
@@ -55,7 +55,7 @@ class ModelConfigC(C.Structure):
 
 class DistC(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
-                ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p)]
+                ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p), ("local_group", C.c_void_p)]
 
 
 class PrefillChunkC(C.Structure):
@@ -109,6 +109,7 @@ def _load() -> C.CDLL:
         "sarathi_op_times": [VP, P(C.c_double), P(I64), I32, I32],
         "sarathi_op_kernel_times": [VP, P(C.c_double), P(I64), I32, I32],
         "sarathi_op_pack_weight": [VP, VP, I32, I32, VP],
+        "sarathi_local_group_create": [I32, I32, P(VP)],
         "sarathi_shard_map": [P(ModelConfigC), I32, I32, I32, I32, P(I32), P(F), P(I64), I32, P(I32), P(I32)],
     }
     for name, args in sig.items():
@@ -117,6 +118,8 @@ def _load() -> C.CDLL:
         fn.restype = C.c_int
     lib.sarathi_destroy.argtypes = [VP]
     lib.sarathi_destroy.restype = None
+    lib.sarathi_local_group_destroy.argtypes = [VP]
+    lib.sarathi_local_group_destroy.restype = None
     lib.sarathi_sched_destroy.argtypes = [VP]
     lib.sarathi_sched_destroy.restype = None
     lib.sarathi_last_error.argtypes = []
@@ -163,13 +166,15 @@ class Model:
 
     def __init__(self, cfg: ModelConfigC, seed: int, rank: int = 0, world: int = 1, device: int = 0,
                  nccl_id: Optional[bytes] = None, stream: int = 0,
-                 host_tensors: Optional[Sequence[Optional[np.ndarray]]] = None):
+                 host_tensors: Optional[Sequence[Optional[np.ndarray]]] = None,
+                 local_group: Optional["LocalGroup"] = None):
         """host_tensors: None (weights generated on device from `seed`) or the 9*L + 3 logical bf16
         tensors (uint16 bit patterns, nn.Linear [out, in]) in the order of include/sarathi.h."""
         self.cfg = cfg
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         dist = DistC(rank, world, device, C.cast(self._idbuf, C.c_void_p) if self._idbuf else None,
-                     C.c_void_p(stream) if stream else None)
+                     C.c_void_p(stream) if stream else None, local_group.h if local_group is not None else None)
+        self._group = local_group  # keep the group alive while this handle exists
         ht = None
         if host_tensors is not None:
             if len(host_tensors) != 9 * cfg.n_layers + 3:
@@ -313,6 +318,22 @@ class Model:
         v = C.c_int64()
         _check(lib.sarathi_launch_count(self.h, C.byref(v)))
         return v.value
+
+
+class LocalGroup:
+    """sarathi_local_group: `world` Model handles on one device, one host thread per rank (TP
+    stand-in for one process per GPU; see include/sarathi.h)."""
+
+    def __init__(self, world: int, device: int = 0):
+        h = C.c_void_p()
+        _check(lib.sarathi_local_group_create(world, device, C.byref(h)))
+        self.h = h
+        self.world = world
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.sarathi_local_group_destroy(self.h)
+            self.h = None
 
 
 class Scheduler:

@@ -24,60 +24,85 @@ class StepResult:
     ref_slots: np.ndarray
 
 
+def gpu_schedule(S, m, cfg: synth.ModelConfig, reqs: Sequence[Tuple[int, int, int, int]], B: int, C: int,
+                 num_blocks: int, block_size: int, tok_seed: int = 1001, dump: bool = True):
+    """Drives one model handle through the C++ scheduler; returns per step (plan, prefill, decodes,
+    logits, hidden, slots).  Under a local TP group every rank's thread calls this identically."""
+    sched = S.Scheduler(B, C, num_blocks, block_size)
+    for r in reqs:
+        sched.submit(*r)
+    info = {r[0]: (r[1], r[2]) for r in reqs}
+    V = cfg.vocab
+    tok = lambda rid, pos, n=1: synth.tokens(tok_seed, rid, pos, n, V)
+    out = []
+    pending_adm = []  # admitted on idle iterations: replayed before the next step
+    while not sched.done():
+        plan, admitted = sched.next()
+        for rid in admitted:
+            P, D = info[rid]
+            m.request_alloc(rid, P + D)
+        pending_adm += admitted
+        if plan is None:
+            sched.idle_step()
+            continue
+        pre, decs = plan
+        prefill = None
+        if pre is not None:
+            rid, start, n = pre
+            prefill = (rid, start, tok(rid, start, n))
+        decodes = [(rid, int(tok(rid, pos)[0]), pos) for rid, pos in decs]
+        T = (pre[2] if pre else 0) + len(decs)
+        logits = np.zeros((T, V), dtype=np.float32)
+        flags = S.RETURN_ALL_ROWS | (S.DUMP_LAYERS if dump else 0)
+        m.run_hybrid_batch(prefill, decodes, flags=flags, logits_host=logits)
+        hid = [m.hidden(l, T) for l in range(cfg.n_layers)] if dump else []
+        fin = sched.complete()
+        out.append(dict(plan=plan, prefill=prefill, decodes=decodes, logits=logits, hidden=hid,
+                        slots=m.slot_mapping(), admitted=pending_adm, finished=fin))
+        pending_adm = []
+        for rid in fin:
+            m.request_free(rid)
+    return out, info
+
+
+def oracle_schedule(w, gpu_steps, info, num_blocks: int, block_size: int) -> List[StepResult]:
+    """Replays the same batches through the fp64 incremental oracle and the Python allocator."""
+    orc = om.IncrementalOracle(w)
+    palloc = osch.BlockAllocator(num_blocks, block_size)
+    out = []
+    for st in gpu_steps:
+        for rid in st["admitted"]:  # same admission order as the library's allocator
+            P, D = info[rid]
+            palloc.alloc(rid, P + D)
+        opre = None
+        ref_slots = []
+        if st["prefill"] is not None:
+            rid, start, t = st["prefill"]
+            opre = om.PrefillItem(rid, start, t)
+            ref_slots += [palloc.slot(rid, start + i) for i in range(len(t))]
+        odec = []
+        for rid, t, pos in st["decodes"]:
+            odec.append(om.DecodeItem(rid, pos, t))
+            ref_slots.append(palloc.slot(rid, pos))
+        ref = orc.run_batch(opre, odec)
+        out.append(StepResult(st["plan"], st["logits"], ref.logits, st["hidden"], ref.hidden, st["slots"],
+                              np.array(ref_slots)))
+        for rid in st["finished"]:
+            palloc.free(rid)
+            orc.free(rid)
+    return out
+
+
 def run_schedule(S, cfg: synth.ModelConfig, reqs: Sequence[Tuple[int, int, int, int]], B: int, C: int,
                  num_blocks: int, block_size: int, weight_seed: int = 0, tok_seed: int = 1001,
                  max_tokens: int = 64, dump: bool = True, oracle_weights=None,
                  host_tensors=None) -> List[StepResult]:
     m = S.Model(S.config_from(cfg, max_tokens_per_batch=max_tokens), seed=weight_seed, host_tensors=host_tensors)
     m.alloc_kv(num_blocks, block_size)
-    sched = S.Scheduler(B, C, num_blocks, block_size)
-    for r in reqs:
-        sched.submit(*r)
-    info = {r[0]: (r[1], r[2]) for r in reqs}
-    w = oracle_weights if oracle_weights is not None else om.model_weights(cfg, weight_seed)
-    orc = om.IncrementalOracle(w)
-    palloc = osch.BlockAllocator(num_blocks, block_size)
-    V = cfg.vocab
-    tok = lambda rid, pos, n=1: synth.tokens(tok_seed, rid, pos, n, V)
-    out = []
-    while not sched.done():
-        plan, admitted = sched.next()
-        for rid in admitted:
-            P, D = info[rid]
-            m.request_alloc(rid, P + D)
-            palloc.alloc(rid, P + D)
-        if plan is None:
-            sched.idle_step()
-            continue
-        pre, decs = plan
-        prefill = None
-        opre = None
-        ref_slots = []
-        if pre is not None:
-            rid, start, n = pre
-            t = tok(rid, start, n)
-            prefill = (rid, start, t)
-            opre = om.PrefillItem(rid, start, t)
-            ref_slots += [palloc.slot(rid, start + i) for i in range(n)]
-        decodes, odec = [], []
-        for rid, pos in decs:
-            t = int(tok(rid, pos)[0])
-            decodes.append((rid, t, pos))
-            odec.append(om.DecodeItem(rid, pos, t))
-            ref_slots.append(palloc.slot(rid, pos))
-        T = (pre[2] if pre else 0) + len(decs)
-        logits = np.zeros((T, V), dtype=np.float32)
-        flags = S.RETURN_ALL_ROWS | (S.DUMP_LAYERS if dump else 0)
-        m.run_hybrid_batch(prefill, decodes, flags=flags, logits_host=logits)
-        hid = [m.hidden(l, T) for l in range(cfg.n_layers)] if dump else []
-        ref = orc.run_batch(opre, odec)
-        out.append(StepResult(plan, logits, ref.logits, hid, ref.hidden, m.slot_mapping(), np.array(ref_slots)))
-        for rid in sched.complete():
-            m.request_free(rid)
-            palloc.free(rid)
-            orc.free(rid)
+    steps, info = gpu_schedule(S, m, cfg, reqs, B, C, num_blocks, block_size, tok_seed, dump)
     m.close()
-    return out
+    w = oracle_weights if oracle_weights is not None else om.model_weights(cfg, weight_seed)
+    return oracle_schedule(w, steps, info, num_blocks, block_size)
 
 
 def synth_host_tensors(cfg: synth.ModelConfig, seed: int):

@@ -222,14 +222,19 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
     hbuf.resize(static_cast<size_t>(rows) * cols);
     for (int r = 0; r < rows; ++r)
       std::memcpy(hbuf.data() + static_cast<size_t>(r) * cols, host_ptr(tau[r]) + base[r], static_cast<size_t>(cols) * 2);
-    if (!packed) return check(cudaMemcpy(dst, hbuf.data(), hbuf.size() * 2, cudaMemcpyHostToDevice), "H2D weights");
+    // copies are ordered on the model stream: a pageable cudaMemcpy on the legacy stream may return
+    // before its DMA lands, and a rank's non-blocking stream would not wait for it
+    if (!packed) {
+      SRET(check(cudaMemcpyAsync(dst, hbuf.data(), hbuf.size() * 2, cudaMemcpyHostToDevice, stream), "H2D weights"));
+      return check(cudaStreamSynchronize(stream), "H2D sync");  // hbuf is reused
+    }
     if (hbuf.size() > staging_elems) {
       if (staging) cudaFree(staging);
       staging = nullptr;
       SRET(check(cudaMalloc(&staging, hbuf.size() * 2), "cudaMalloc staging"));
       staging_elems = hbuf.size();
     }
-    SRET(check(cudaMemcpy(staging, hbuf.data(), hbuf.size() * 2, cudaMemcpyHostToDevice), "H2D weights"));
+    SRET(check(cudaMemcpyAsync(staging, hbuf.data(), hbuf.size() * 2, cudaMemcpyHostToDevice, stream), "H2D weights"));
     SRET(check(launch_pack_weight(staging, dst, rows, cols, stream), "pack weight"));
     ++launches;
     return check(cudaStreamSynchronize(stream), "pack sync");
@@ -274,8 +279,8 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
         !make_tmap_weight(&w.m_gu, w.gu, gu_rows, H) || !make_tmap_weight(&w.m_down, w.down, H, h2_l))
       return Status::err(SARATHI_ECUDA, "cuTensorMapEncodeTiled failed for a weight");
     if (host_tensors) {
-      SRET(check(cudaMemcpy(w.g1, host_ptr(16 * l + kG1), H * 2, cudaMemcpyHostToDevice), "H2D gain"));
-      SRET(check(cudaMemcpy(w.g2, host_ptr(16 * l + kG2), H * 2, cudaMemcpyHostToDevice), "H2D gain"));
+      SRET(check(cudaMemcpyAsync(w.g1, host_ptr(16 * l + kG1), H * 2, cudaMemcpyHostToDevice, stream), "H2D gain"));
+      SRET(check(cudaMemcpyAsync(w.g2, host_ptr(16 * l + kG2), H * 2, cudaMemcpyHostToDevice, stream), "H2D gain"));
     } else {
       SRET(check(launch_gaingen(w.g1, H, 16 * l + kG1, 0, seed, stream), "gaingen"));
       SRET(check(launch_gaingen(w.g2, H, 16 * l + kG2, 0, seed, stream), "gaingen"));
@@ -292,7 +297,7 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   SRET(gen(emb, c.vocab, H, 0));
   SRET(dalloc(&gf, H));
   if (host_tensors) {
-    SRET(check(cudaMemcpy(gf, host_ptr(kGfTau), H * 2, cudaMemcpyHostToDevice), "H2D gain"));
+    SRET(check(cudaMemcpyAsync(gf, host_ptr(kGfTau), H * 2, cudaMemcpyHostToDevice, stream), "H2D gain"));
   } else {
     SRET(check(launch_gaingen(gf, H, kGfTau, 0, seed, stream), "gaingen"));
     ++launches;
@@ -316,7 +321,8 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
       th[2 * i + 1] = static_cast<float>(inv - static_cast<double>(th[2 * i]));
     }
     SRET(dalloc(&rope_theta, th.size()));
-    SRET(check(cudaMemcpy(rope_theta, th.data(), th.size() * 4, cudaMemcpyHostToDevice), "H2D rope"));
+    SRET(check(cudaMemcpyAsync(rope_theta, th.data(), th.size() * 4, cudaMemcpyHostToDevice, stream), "H2D rope"));
+    SRET(check(cudaStreamSynchronize(stream), "H2D rope sync"));  // th is a local
   }
 
   // activations / workspaces

@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
+import os
 from typing import Dict, List, Sequence, Tuple
 
 import numpy as np
@@ -185,11 +186,22 @@ def gen_gain_bits(seed: int, tau: int, n: int) -> np.ndarray:
     return f32_to_bf16_bits(x.astype(np.float32))
 
 
-def _chunked_bits(seed: int, tau: int, sigma: float, total: int, chunk: int = 1 << 24) -> np.ndarray:
+def _chunked_bits(seed: int, tau: int, sigma: float, total: int, chunk: int = 1 << 22) -> np.ndarray:
+    """Chunks are independent (counter-based), so they are generated on a thread pool (NumPy
+    releases the GIL inside the uint64 ufuncs); the bits do not depend on the chunking."""
     out = np.empty(total, dtype=np.uint16)
-    for s in range(0, total, chunk):
+
+    def one(s):
         n = min(chunk, total - s)
         out[s:s + n] = gen_weight_bits(seed, tau, sigma, s, n)
+
+    starts = range(0, total, chunk)
+    if total <= chunk:
+        one(0)
+        return out
+    import concurrent.futures as cf
+    with cf.ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
+        list(ex.map(one, starts))
     return out
 
 

@@ -238,46 +238,102 @@ class IncrementalOracle:
 
     def run_batch(self, prefill: Optional[PrefillItem], decodes: Sequence[DecodeItem]) -> BatchResult:
         cfg, w = self.cfg, self.w
-        rows: List[Tuple[int, int, int]] = []  # (req, pos, token)
-        if prefill is not None:
-            assert prefill.start == self.cached_len(prefill.req_id), "chunk must start at cached length"
-            for i, t in enumerate(prefill.tokens):
-                rows.append((prefill.req_id, prefill.start + i, int(t)))
-        seen = {prefill.req_id} if prefill is not None else set()
-        for d in decodes:
-            assert d.req_id not in seen, "a request appears once per batch (S:L443)"
-            seen.add(d.req_id)
-            assert d.pos == self.cached_len(d.req_id) and d.pos > 0, "decode at cached length"
-            rows.append((d.req_id, d.pos, int(d.token)))
+        rows = batch_rows(prefill, decodes, self.cached_len)
         T = len(rows)
-        assert T > 0
         pos = np.array([r[1] for r in rows])
         h = w.emb[np.array([r[2] for r in rows])]           # embedding gather
         hidden, layer_inputs = [], []
         for l, lw in enumerate(w.layers):
             layer_inputs.append(h.copy())
-            # Linear ops fused over all T = p + d rows ("fuse all the linear operations").
-            a = rmsnorm(h, lw.g1, cfg.rms_eps)
-            q = rope((a @ lw.wq.T).reshape(T, cfg.n_heads, cfg.head_dim), pos, cfg.rope_base)
-            k = rope((a @ lw.wk.T).reshape(T, cfg.n_kv_heads, cfg.head_dim), pos, cfg.rope_base)
-            v = (a @ lw.wv.T).reshape(T, cfg.n_kv_heads, cfg.head_dim)
-            # KV-cache in-place append (P:L112 pre-allocated cache).
-            for i, (rid, p_, _) in enumerate(rows):
+            kv_l = {}
+            for rid, _, _ in rows:
                 cache = self.kv.setdefault(rid, [(np.zeros((0, cfg.n_kv_heads, cfg.head_dim)),) * 2
                                                  for _ in range(cfg.n_layers)])
-                K, V = cache[l]
-                assert K.shape[0] == p_
-                cache[l] = (np.concatenate([K, k[i:i + 1]]), np.concatenate([V, v[i:i + 1]]))
-            # Attention split by token kind: prefill rows attend [0, s+i], decodes [0, ctx-1].
-            o = np.empty((T, cfg.q_dim))
-            for i, (rid, p_, _) in enumerate(rows):
-                K, V = self.kv[rid][l]
-                o[i] = attention_rows(cfg, q[i], K, V, p_)
-            u = h + o @ lw.wo.T
-            h = u + ffn(cfg, lw, rmsnorm(u, lw.g2, cfg.rms_eps))
+                kv_l[rid] = cache[l]
+            h = layer_step(cfg, lw, h, rows, kv_l)
+            for rid in kv_l:
+                self.kv[rid][l] = kv_l[rid]
             hidden.append(h.copy())
         logits = rmsnorm(h, w.gf, cfg.rms_eps) @ w.wlm.T
         return BatchResult(logits, hidden, pos, layer_inputs)
+
+
+def batch_rows(prefill: Optional[PrefillItem], decodes: Sequence[DecodeItem], cached_len):
+    """Token matrix of one hybrid batch (§4.3): the chunk's rows (positions s..s+p-1) then one row
+    per decode (position = its cached length); (req, pos, token) per row."""
+    rows: List[Tuple[int, int, int]] = []
+    if prefill is not None:
+        assert prefill.start == cached_len(prefill.req_id), "chunk must start at cached length"
+        for i, t in enumerate(prefill.tokens):
+            rows.append((prefill.req_id, prefill.start + i, int(t)))
+    seen = {prefill.req_id} if prefill is not None else set()
+    for d in decodes:
+        assert d.req_id not in seen, "a request appears once per batch (S:L443)"
+        seen.add(d.req_id)
+        assert d.pos == cached_len(d.req_id) and d.pos > 0, "decode at cached length"
+        rows.append((d.req_id, d.pos, int(d.token)))
+    assert len(rows) > 0
+    return rows
+
+
+def layer_step(cfg: ModelConfig, lw: LayerWeights, h: np.ndarray, rows, kv_l) -> np.ndarray:
+    """One decoder layer over the batch's rows, in the paper's order: linears over all T rows at once
+    ("fuse all the linear operations"), K/V appended in place to each request's cache of this
+    layer (kv_l[req] = (K, V), replaced by the extended arrays), attention split by
+    token kind with explicit key ranges [0, pos] (P:L369 progressive mask; reading O-9)."""
+    T = h.shape[0]
+    pos = np.array([r[1] for r in rows])
+    a = rmsnorm(h, lw.g1, cfg.rms_eps)
+    q = rope((a @ lw.wq.T).reshape(T, cfg.n_heads, cfg.head_dim), pos, cfg.rope_base)
+    k = rope((a @ lw.wk.T).reshape(T, cfg.n_kv_heads, cfg.head_dim), pos, cfg.rope_base)
+    v = (a @ lw.wv.T).reshape(T, cfg.n_kv_heads, cfg.head_dim)
+    # KV-cache in-place append (P:L112 pre-allocated cache, P:L224).
+    for i, (rid, p_, _) in enumerate(rows):
+        K, V = kv_l[rid]
+        assert K.shape[0] == p_
+        kv_l[rid] = (np.concatenate([K, k[i:i + 1]]), np.concatenate([V, v[i:i + 1]]))
+    # Attention split by token kind (P:L403): prefill rows attend [0, s+i], decodes [0, ctx-1].
+    o = np.empty((T, cfg.q_dim))
+    for i, (rid, p_, _) in enumerate(rows):
+        K, V = kv_l[rid]
+        o[i] = attention_rows(cfg, q[i], K, V, p_)
+    u = h + o @ lw.wo.T
+    return u + ffn(cfg, lw, rmsnorm(u, lw.g2, cfg.rms_eps))
+
+
+def replay_layer_major(cfg: ModelConfig, layer_weights_fn, emb_rows_fn, gf: np.ndarray, wlm: np.ndarray,
+                       batches) -> List[BatchResult]:
+    """The same computation as IncrementalOracle.run_batch over a sequence of batches, reordered
+    layer-major: every batch through layer 0, then every batch through layer 1, ...  Exact (each
+    batch's layer-l input and each request's layer-l KV are the same arrays in either order), so a
+    full-size model (e.g. 40 LLaMA-13B layers) needs ONE layer's fp64 weights in memory at a time.
+    layer_weights_fn(l) -> LayerWeights; emb_rows_fn(token ids) -> fp64 embedding rows;
+    batches = [(PrefillItem | None, [DecodeItem])]."""
+    lens: Dict[int, int] = {}
+    rows_b = []
+    for pre, decs in batches:
+        rows = batch_rows(pre, decs, lambda r: lens.get(r, 0))
+        for rid, _, _ in rows:
+            lens[rid] = lens.get(rid, 0) + 1
+        rows_b.append(rows)
+    h_b = [emb_rows_fn(np.array([r[2] for r in rows])) for rows in rows_b]
+    hidden_b: List[List[np.ndarray]] = [[] for _ in rows_b]
+    inputs_b: List[List[np.ndarray]] = [[] for _ in rows_b]
+    for l in range(cfg.n_layers):
+        lw = layer_weights_fn(l)
+        kv_l: Dict[int, Tuple[np.ndarray, np.ndarray]] = {}
+        for b, rows in enumerate(rows_b):
+            for rid, _, _ in rows:
+                kv_l.setdefault(rid, (np.zeros((0, cfg.n_kv_heads, cfg.head_dim)),) * 2)
+            inputs_b[b].append(h_b[b].copy())
+            h_b[b] = layer_step(cfg, lw, h_b[b], rows, kv_l)
+            hidden_b[b].append(h_b[b].copy())
+        del lw
+    out = []
+    for b, rows in enumerate(rows_b):
+        logits = rmsnorm(h_b[b], gf, cfg.rms_eps) @ wlm.T
+        out.append(BatchResult(logits, hidden_b[b], np.array([r[1] for r in rows]), inputs_b[b]))
+    return out
 
 
 # ---------------------------------------------------------------------------

@@ -57,6 +57,7 @@ struct KParams {
   int red_partials;       // split tiles accumulate in ONE zeroed fp32 slot by red.add (many contributors)
   uint32_t tmem_cols;
   uint32_t ring_bytes;
+  int sk_fast;            // stream-K: the last contributor reduces from its own TMEM (no partial round trip)
 };
 
 SARATHI_DEVICE float silu_f(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
@@ -170,7 +171,7 @@ SARATHI_DEVICE void red_add_v4(float* addr, float4 v) {
 
 SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[16], uint32_t q, uint32_t lane, int mt,
                              int nt, int c0, int tvalid, float* sbuf, const int* s_pos, const int* s_slot,
-                             const int* s_consec, const QkvLane& ql) {
+                             const int* s_consec, const QkvLane& ql, unsigned long long* trc = nullptr) {
   const int row0 = mt * kBM + static_cast<int>(q) * 32;  // first accumulator row of this warp
   const long long tb = static_cast<long long>(nt) * p.bn + c0;
   const int nv = (ep.dbg & 8) ? 0 : min(16, tvalid - c0);  // dbg bit 3: no global stores
@@ -279,6 +280,7 @@ SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[1
         for (int j = 0; j < 16; ++j) sb[j * 32 + lane] = __bfloat16_as_ushort(__float2bfloat16_rn(v[j]));
       }
       __syncwarp();
+      if (trc && lane == 0) *trc = globaltimer_ns();
       if (row0 < p.M) {
         const int hd_shift = ep.head_dim == 128 ? 7 : 6;
         const bool isq = ql.gh < ep.n_q_local;
@@ -580,8 +582,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             float v[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
+            if (ep.trace && tb < 2 && et == 0 && seg == 0 && ch < 64)
+              ep.trace[tb * 1024 + 800 + ch] = globaltimer_ns();
             if (!(ep.dbg & 4))
-              epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql);
+              epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql,
+                       ep.trace && tb < 2 && et == 0 && seg == 0 && ch < 64 ? ep.trace + tb * 1024 + 864 + ch : nullptr);
             if (ep.trace && tb < 2 && et == 0 && seg == 0 && ch < 64)
               ep.trace[tb * 1024 + 640 + ch] = globaltimer_ns();
             if (more) {
@@ -605,6 +610,69 @@ __global__ void __launch_bounds__(kThreads, 1)
         const size_t qoff = static_cast<size_t>(quarter) * 512 + lane * 4;  // + (ch * 4 * 512) + j * 128
         float* wsp = p.red_partials ? ep.ws_red + tile128 * tile_elems + qoff
                                     : ep.ws + (tile128 * p.max_slots + slot) * tile_elems + qoff;
+        // fast path: if every other contributor has already arrived (their partials are in the
+        // slots), this CTA is the tile's last: it reduces straight from its own TMEM accumulator
+        // (no partial write + re-read) summing in slot order with its own value at its slot, i.e.
+        // bit-identical to the slow path's slot-order sum.  In stream-K order the tile's head
+        // contributor finishes its part last, so this is the common case.
+        if (!p.red_partials && p.sk_fast) {
+          if (et == 0) {
+            int* ctr = ep.counters + tile128;
+            int c;
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(c) : "l"(ctr) : "memory");
+            s_last = (c == nslot - 1);
+            if (s_last) *ctr = 0;  // re-arm for the next launch (every other contributor has arrived)
+          }
+          named_bar_sync(1, kEpiThreads);
+          if (s_last) {
+            __threadfence();
+            const float* base0 = ep.ws + tile128 * p.max_slots * tile_elems + qoff;
+            auto sum_emit_own = [&](int ch, const uint32_t (&own)[16]) {
+              float v[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = 0.f;
+              for (int q = 0; q < nslot; ++q) {
+                if (q == slot) {
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) v[j] = q == 0 ? __uint_as_float(own[j]) : v[j] + __uint_as_float(own[j]);
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    const float4 x = __ldcg(reinterpret_cast<const float4*>(base0 + q * tile_elems + ch * 2048 + j * 128));
+                    v[4 * j + 0] = q == 0 ? x.x : v[4 * j + 0] + x.x;
+                    v[4 * j + 1] = q == 0 ? x.y : v[4 * j + 1] + x.y;
+                    v[4 * j + 2] = q == 0 ? x.z : v[4 * j + 2] + x.z;
+                    v[4 * j + 3] = q == 0 ? x.w : v[4 * j + 3] + x.w;
+                  }
+                }
+              }
+              epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql);
+            };
+            if (eh >= nchunks) {
+              release_tmem();
+            } else {
+              uint32_t raw[16];
+              tmem_ld_32x32b_x16(trow + tcol(eh), raw);
+              tmem_ld_wait_regs(raw);
+              after_load(eh);
+              for (int ch = eh; ch < nchunks; ch += 2) {
+                uint32_t nraw[16];
+                const bool more = ch + 2 < nchunks;
+                if (more) tmem_ld_32x32b_x16(trow + tcol(ch + 2), nraw);
+                sum_emit_own(ch, raw);
+                if (more) {
+                  tmem_ld_wait_regs(nraw);
+                  after_load(ch + 2);
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) raw[j] = nraw[j];
+                }
+              }
+            }
+            named_bar_sync(1, kEpiThreads);  // s_last is rewritten by the next segment's check
+            ++seg;
+            continue;
+          }
+        }
         if (eh >= nchunks) {
           release_tmem();
         } else {
@@ -800,7 +868,10 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
   } else if (tiles <= P) {
     const int sk_pairs = static_cast<int>(std::min<long long>(P, std::max<long long>(1, static_cast<long long>(tiles) * KB / 4)));
     // cost model in k-block units: a split tile adds a partial write + reduction ~ sk_cost * KB
-    static const double sk_cost = getenv("SARATHI_GEMM_SK_COST") ? atof(getenv("SARATHI_GEMM_SK_COST")) : 0.5;
+    // (the last contributor reduces from its own TMEM, sk_fast: the exposed cost is reading the
+    // other contributors' partials, ~0.08 KB; without the fast path a partial write + re-read, ~0.5 KB)
+    static const bool fast = !(getenv("SARATHI_GEMM_SK_FAST") && atoi(getenv("SARATHI_GEMM_SK_FAST")) == 0);
+    static const double sk_cost = getenv("SARATHI_GEMM_SK_COST") ? atof(getenv("SARATHI_GEMM_SK_COST")) : (fast ? 0.08 : 0.5);
     const double sk_units = std::ceil(static_cast<double>(tiles) * KB / sk_pairs) + sk_cost * KB;
     if (KB <= sk_units) {
       pairs = tiles;
@@ -903,7 +974,10 @@ void dump_gemm_trace(const unsigned long long* trace_dev, const GemmPlan& pl) {
         fprintf(stderr, "pair %d end %.2f\n", b / 2, h[2048 + b] ? (h[2048 + b] - t0) * 1e-3 : -1.0);
     }
   }
-  for (int ch = 0; ch < 64 && h[640 + ch]; ++ch) fprintf(stderr, "seg0 chunk %d emitted %8.3f us\n", ch, (h[640 + ch] - t0) * 1e-3);
+  for (int ch = 0; ch < 64 && h[640 + ch]; ++ch)
+    fprintf(stderr, "seg0 chunk %d loaded %8.3f  regs-done %8.3f  emitted %8.3f us\n", ch,
+            h[800 + ch] ? (h[800 + ch] - t0) * 1e-3 : -1.0, h[864 + ch] ? (h[864 + ch] - t0) * 1e-3 : -1.0,
+            (h[640 + ch] - t0) * 1e-3);
   for (int sgm = 0; sgm < 64 && h[512 + sgm]; ++sgm)
     fprintf(stderr, "seg %d epilogue wake %8.3f us  done %8.3f us  (partial stored %8.3f, fenced %8.3f)\n", sgm,
             (h[512 + sgm] - t0) * 1e-3, h[576 + sgm] ? (h[576 + sgm] - t0) * 1e-3 : -1.0,
@@ -939,6 +1013,8 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   kp.red_partials = pl.red_partials;
   kp.tmem_cols = (pl.nbuf == 2 || (pl.n_mma == 2 && 3 * (pl.bn / 2) <= 512)) ? 512 : pow2_cols(pl.bn);
   kp.ring_bytes = static_cast<uint32_t>(pl.stages * (kABytes + static_cast<size_t>(pl.bn / 2) * kBK * 2));
+  static const int sk_fast = !(getenv("SARATHI_GEMM_SK_FAST") && atoi(getenv("SARATHI_GEMM_SK_FAST")) == 0);
+  kp.sk_fast = sk_fast;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pl.ctas);
   cfg.blockDim = dim3(kThreads);

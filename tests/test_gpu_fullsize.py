@@ -92,3 +92,39 @@ def _layer_local(cfg, p, s, d, ctx, layers):
     for k, v in errs.items():
         assert v <= TOL, (k, v)
         assert v <= REGRESS, (k, v)
+
+
+def test_llama13b_40_layers_end_to_end():
+    """The accumulated error of the FULL 40-layer LLaMA-13B stack (H 5120) end to end: a hybrid
+    schedule (chunked prompts, piggybacked decodes, decode-only batches) through the C-ABI, every
+    batch's logits and every layer's residual against the fp64 oracle replayed layer-major (one
+    layer's weights in memory at a time; oracle/model.py replay_layer_major)."""
+    from paper_2308_16369_b200 import sarathi as S
+    from tests import gpu_harness as gh
+    cfg = synth.dataclasses.replace(synth.LLAMA_13B, max_seq_len=128)
+    m = S.Model(S.config_from(cfg, max_tokens_per_batch=64), seed=0)
+    m.alloc_kv(8, 64)
+    steps, info = gh.gpu_schedule(S, m, cfg, [(1, 70, 3, 0), (2, 30, 3, 0)], B=2, C=48, num_blocks=8,
+                                  block_size=64)
+    m.close()
+    batches = []
+    for st in steps:
+        pre = om.PrefillItem(*st["prefill"]) if st["prefill"] is not None else None
+        batches.append((pre, [om.DecodeItem(rid, pos, t) for rid, t, pos in st["decodes"]]))
+    emb = lambda t: _bf16(synth.embedding_rows_bits(cfg, 0, t))
+    ref = om.replay_layer_major(cfg, lambda l: om.layer_weights(cfg, 0, l), emb,
+                                _bf16(synth.final_gain_bits(cfg, 0)), _bf16(synth.lm_head_bits(cfg, 0)), batches)
+    errs = {"logits": 0.0, "hidden": 0.0, "hidden_l39": 0.0}
+    for st, r in zip(steps, ref):
+        errs["logits"] = max(errs["logits"], relative_error(st["logits"], r.logits))
+        for l, (g, h) in enumerate(zip(st["hidden"], r.hidden)):
+            e = relative_error(g, h)
+            errs["hidden"] = max(errs["hidden"], e)
+            if l == cfg.n_layers - 1:
+                errs["hidden_l39"] = max(errs["hidden_l39"], e)
+    print("LLaMA-13B 40-layer end-to-end errors:", {k: f"{v:.2e}" for k, v in errs.items()},
+          "plans:", [s["plan"] for s in steps])
+    assert len(steps) >= 5 and any(s["plan"][0] and s["plan"][1] for s in steps)
+    for k, v in errs.items():
+        assert v <= TOL, (k, v)
+        assert v <= REGRESS, (k, v)

@@ -413,3 +413,26 @@ def test_hybrid_batch_equals_each_request_alone_and_decode_equals_recompute(gqa_
         full = om.forward_full(gqa_w, toks[r][:last + 1]).logits
         for p_, row in got[r].items():
             assert _rel(row, full[p_]) < 1e-12, (r, p_)
+
+
+@pytest.mark.parametrize("which", ["tiny", "gqa"])
+def test_layer_major_replay_equals_incremental(which, tiny_w, gqa_w):
+    """replay_layer_major (the full-size end-to-end checker: one layer's weights in memory at a time)
+    reorders IncrementalOracle's work layer-major; the results are the same arrays (bitwise), for a
+    schedule with chunks, piggybacked decodes and decode-only batches."""
+    w = tiny_w if which == "tiny" else gqa_w
+    V = w.cfg.vocab
+    toks = {r: synth.tokens(31, r, 0, 60, V) for r in (0, 1, 2)}
+    batches = [(om.PrefillItem(1, 0, toks[1][:7]), []),
+               (om.PrefillItem(0, 0, toks[0][:16]), [om.DecodeItem(1, 7, toks[1][7])]),
+               (om.PrefillItem(0, 16, toks[0][16:21]), [om.DecodeItem(1, 8, toks[1][8])]),
+               (om.PrefillItem(2, 0, toks[2][:3]), [om.DecodeItem(0, 21, toks[0][21]), om.DecodeItem(1, 9, toks[1][9])]),
+               (None, [om.DecodeItem(2, 3, toks[2][3]), om.DecodeItem(0, 22, toks[0][22])])]
+    o = om.IncrementalOracle(w)
+    ref = [o.run_batch(p, d) for p, d in batches]
+    got = om.replay_layer_major(w.cfg, lambda l: w.layers[l], lambda t: w.emb[t], w.gf, w.wlm, batches)
+    for a, b in zip(got, ref):
+        assert np.array_equal(a.logits, b.logits)
+        assert np.array_equal(a.positions, b.positions)
+        for x, y in zip(a.hidden, b.hidden):
+            assert np.array_equal(x, y)

@@ -37,8 +37,9 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
-constexpr int kThreads = 320;               // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
-constexpr int kEpiThreads = 256;
+// warp 0 TMA, warp 1 MMA, warps 2 .. 2 + 4*NEH - 1 epilogue (NEH warps per TMEM lane quarter)
+template <int NEH>
+constexpr int threads_of() { return 64 + 128 * NEH; }
 constexpr int kWRowsPerTile = 32;            // packed W viewed as rows of 256 elements (512 B)
 
 struct KParams {
@@ -57,7 +58,6 @@ struct KParams {
   int red_partials;       // split tiles accumulate in ONE zeroed fp32 slot by red.add (many contributors)
   uint32_t tmem_cols;
   uint32_t ring_bytes;
-  int sk_fast;            // stream-K: the last contributor reduces from its own TMEM (no partial round trip)
 };
 
 SARATHI_DEVICE float silu_f(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
@@ -169,19 +169,20 @@ SARATHI_DEVICE void red_add_v4(float* addr, float4 v) {
                : "memory");
 }
 
+template <int MODE, bool DBG>
 SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[16], uint32_t q, uint32_t lane, int mt,
                              int nt, int c0, int tvalid, float* sbuf, const int* s_pos, const int* s_slot,
                              const int* s_consec, const QkvLane& ql, unsigned long long* trc = nullptr) {
   const int row0 = mt * kBM + static_cast<int>(q) * 32;  // first accumulator row of this warp
   const long long tb = static_cast<long long>(nt) * p.bn + c0;
-  const int nv = (ep.dbg & 8) ? 0 : min(16, tvalid - c0);  // dbg bit 3: no global stores
+  const int nv = (DBG && (ep.dbg & 8)) ? 0 : min(16, tvalid - c0);  // dbg bit 3: no global stores
   uint16_t* sb = reinterpret_cast<uint16_t*>(sbuf);
-  switch (ep.mode) {
+  switch (MODE) {
     case EPI_STORE_BF16:
     case EPI_GELU: {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const float x = ep.mode == EPI_GELU ? gelu_tanh_f(v[j]) : v[j];
+        const float x = MODE == EPI_GELU ? gelu_tanh_f(v[j]) : v[j];
         sb[j * 32 + lane] = __bfloat16_as_ushort(__float2bfloat16_rn(x));
       }
       __syncwarp();
@@ -208,7 +209,7 @@ SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[1
         if (tok < nv && m < p.M) {
           const float4 x = *reinterpret_cast<const float4*>(sbuf + tok * 32 + g * 4);
           float* dst = static_cast<float*>(ep.out) + (tb + tok) * ep.ldo + m;
-          if (ep.mode == EPI_ADD_F32)
+          if (MODE == EPI_ADD_F32)
             red_add_v4(dst, x);
           else
             *reinterpret_cast<float4*>(dst) = x;
@@ -241,7 +242,7 @@ SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[1
     case EPI_QKV_ROPE: {
       const int half = ep.head_dim >> 1;
       const bool lo = lane < 16;
-      if (ql.rope && !(ep.dbg & 32)) {  // dbg bit 5: no RoPE math (timing only)
+      if (ql.rope && !(DBG && (ep.dbg & 32))) {  // dbg bit 5: no RoPE math (timing only)
         // branch-free, 8 tokens per batch so the shuffles, position loads and sincos of different
         // tokens overlap (a per-token dependent chain cost ~150 cycles x 16 per chunk)
         // consecutive positions (prefill chunks): angle-addition recurrence from the chunk's first
@@ -291,7 +292,7 @@ SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[1
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
           const int tok = pass * 8 + static_cast<int>(lane >> 2);
-          if (tok >= nv || ((ep.dbg & 16) && !isq)) continue;  // dbg bit 4: no K/V cache stores
+          if (tok >= nv || (DBG && (ep.dbg & 16) && !isq)) continue;  // dbg bit 4: no K/V cache stores
           __nv_bfloat16* dst =
               isq ? static_cast<__nv_bfloat16*>(ep.out) + (tb + tok) * ep.ldo + (ql.gh << hd_shift) + d
                   : cache + (static_cast<size_t>(s_slot[c0 + tok] + kvh * ep.block_size) << hd_shift) + d;
@@ -306,9 +307,11 @@ SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[1
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int NEH, int MODE, bool DBG>
+__global__ void __launch_bounds__(threads_of<NEH>(), 1)
     gemm_bf16_pair(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, const KParams p,
                    const EpiParams ep) {
+  constexpr int kEpiThreads = 128 * NEH;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base derived by pointer arithmetic from the __shared__ array (not an integer
   // round trip), so every pointer below stays in the shared address space (STS/LDS, not generic ST/LD)
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t b_bytes = static_cast<uint32_t>(p.bn / 2) * kBK * 2;  // this CTA's half of the tokens
   const uint32_t stage_bytes = kABytes + b_bytes;
   float* stage_buf = reinterpret_cast<float*>(smem + p.ring_bytes);    // [8 warps][16 x 32] transpose
-  int* s_pos = reinterpret_cast<int*>(stage_buf + 8 * kStageFloats);   // [bn]
+  int* s_pos = reinterpret_cast<int*>(stage_buf + 4 * NEH * kStageFloats);  // [bn]
   int* s_slot = s_pos + p.bn;                                          // [bn]
   int* s_consec = s_slot + p.bn;                                       // [32] chunk has consecutive positions
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_consec + 32);         // 8-B aligned (bn is a multiple of 16)
@@ -344,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) mbar_init(&tfull[b], 1);
-    for (int b = 0; b < 3; ++b) mbar_init(&tempty[b], 16);  // 8 epilogue warps x 2 CTAs
+    for (int b = 0; b < 3; ++b) mbar_init(&tempty[b], 8 * NEH);  // 4*NEH epilogue warps x 2 CTAs
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       // incremental (k-block, stage, phase) counters inside a segment: no division in the hot loop
-      const uint32_t tx = 2 * (stage_bytes - ((ep.dbg & 1) ? b_bytes : 0) - ((ep.dbg & 2) ? kABytes : 0));
+      const uint32_t tx = 2 * (stage_bytes - ((DBG && (ep.dbg & 1)) ? b_bytes : 0) - ((DBG && (ep.dbg & 2)) ? kABytes : 0));
       int s = 0;
       uint32_t ph = 0;
       long long i = 0;
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < npre; ++j) {
             uint8_t* a = smem + static_cast<size_t>(j) * stage_bytes;
             if (rank == 0) mbar_arrive_expect_tx_warp(&full[j], tx);
-            if (!(ep.dbg & 2)) tma_load_2d_pair_warp(a, &mapW, &full[j], 0, wrow0 + j * kWRowsPerTile, pol_w);
+            if (!(DBG && (ep.dbg & 2))) tma_load_2d_pair_warp(a, &mapW, &full[j], 0, wrow0 + j * kWRowsPerTile, pol_w);
           }
         }
       }
@@ -406,13 +409,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             // both CTAs' bytes are counted on the leader's full[s] (pair TMA)
             if (rank == 0) mbar_arrive_expect_tx_warp(&full[s], tx);
             // W tile: the contiguous 16 KB pre-swizzled tile as 32 rows x 512 B (unswizzled map)
-            if (!(ep.dbg & 2)) tma_load_2d_pair_warp(a, &mapW, &full[s], 0, wrow, pol_w);
+            if (!(DBG && (ep.dbg & 2))) tma_load_2d_pair_warp(a, &mapW, &full[s], 0, wrow, pol_w);
           }
-          if (!(ep.dbg & 1))
+          if (!(DBG && (ep.dbg & 1)))
             for (int j = 0; j < p.n_mma; ++j)
               tma_load_2d_pair_warp(b + j * (ni / 2) * kBK * 2, &mapX, &full[s], kb * kBK,
                                     nt * p.bn + j * ni + static_cast<int>(rank) * (ni / 2), pol_x);
-          if (ep.trace && tb < 2 && i < 256 && lane == 0) ep.trace[tb * 1024 + i] = globaltimer_ns();
+          if ((DBG ? ep.trace : nullptr) && tb < 2 && i < 256 && lane == 0) (DBG ? ep.trace : nullptr)[tb * 1024 + i] = globaltimer_ns();
           if (++s == p.stages) {
             s = 0;
             ph ^= 1;
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb, ++i) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          if (ep.trace && tb == 0 && lane == 0 && i < 256) ep.trace[256 + i] = globaltimer_ns();
+          if ((DBG ? ep.trace : nullptr) && tb == 0 && lane == 0 && i < 256) (DBG ? ep.trace : nullptr)[256 + i] = globaltimer_ns();
           {
             // warp-uniform issue (operands stay in uniform registers), one elected lane issues
             const uint32_t a = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
@@ -481,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------- Epilogue (warps 2..9 of both CTAs) ----------------
-    // two warps per TMEM lane quarter (warp & 3); warp half `eh` takes chunks eh, eh + 2, ...
+    // NEH warps per TMEM lane quarter (warp & 3); warp `eh` of a quarter takes chunks eh, eh + NEH, ...
     const int et = threadIdx.x - 64;                        // 0..255
     const int ew = static_cast<int>(warp) - 2;              // 0..7
     const int eh = ew >> 2;
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
     int seg = 0;
     const size_t tile_elems = static_cast<size_t>(p.bn) * kBM;
-    const bool rope_mode = ep.mode == EPI_QKV_ROPE;
+    constexpr bool rope_mode = MODE == EPI_QKV_ROPE;
     SegIter it;
     it.init(p, pair);
     int tile, kb0, kb1;
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t use = seg / p.nbuf;
       const int tvalid = min(p.bn, p.N - nt * p.bn);
       // whole tiles and residual adds (red.add of every contributor's partial) emit straight from TMEM
-      const bool direct = (kb0 == 0 && kb1 == p.KB) || ep.mode == EPI_ADD_F32;
+      const bool direct = (kb0 == 0 && kb1 == p.KB) || MODE == EPI_ADD_F32;
       QkvLane ql{};
       if (rope_mode) ql = qkv_lane(ep, mt, quarter, lane);
       const int nchunks = (tvalid + 15) / 16;
@@ -520,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       auto last_of = [&](int lim) {  // this warp's last chunk below lim (-1 if none)
         if (lim <= eh) return -1;
-        return eh + ((lim - 1 - eh) / 2) * 2;
+        return eh + ((lim - 1 - eh) / NEH) * NEH;
       };
       const int lastA = last_of(min(nA, nchunks)), lastAll = last_of(nchunks);
       auto release_tmem = [&]() {  // everything this warp owes for the segment
@@ -564,10 +567,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
       tc_fence_after();
-      if (ep.trace && tb < 2 && et == 0 && seg < 64) ep.trace[tb * 1024 + 512 + seg] = globaltimer_ns();
+      if ((DBG ? ep.trace : nullptr) && tb < 2 && et == 0 && seg < 64) (DBG ? ep.trace : nullptr)[tb * 1024 + 512 + seg] = globaltimer_ns();
       const uint32_t trow = tmem + ((quarter * 32u) << 16);
       if (direct) {
-        // software-pipelined TMEM drain: this warp's next chunk (ch + 2) is in flight while ch is emitted
+        // software-pipelined TMEM drain: this warp's next chunk (ch + NEH) is in flight while ch is emitted
         if (eh >= nchunks) {
           release_tmem();
         } else {
@@ -575,23 +578,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_32x32b_x16(trow + tcol(eh), raw);
           tmem_ld_wait_regs(raw);
           after_load(eh);
-          for (int ch = eh; ch < nchunks; ch += 2) {
+          for (int ch = eh; ch < nchunks; ch += NEH) {
             uint32_t nraw[16];
-            const bool more = ch + 2 < nchunks;
-            if (more) tmem_ld_32x32b_x16(trow + tcol(ch + 2), nraw);
+            const bool more = ch + NEH < nchunks;
+            if (more) tmem_ld_32x32b_x16(trow + tcol(ch + NEH), nraw);
             float v[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
-            if (ep.trace && tb < 2 && et == 0 && seg == 0 && ch < 64)
-              ep.trace[tb * 1024 + 800 + ch] = globaltimer_ns();
-            if (!(ep.dbg & 4))
-              epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql,
-                       ep.trace && tb < 2 && et == 0 && seg == 0 && ch < 64 ? ep.trace + tb * 1024 + 864 + ch : nullptr);
-            if (ep.trace && tb < 2 && et == 0 && seg == 0 && ch < 64)
-              ep.trace[tb * 1024 + 640 + ch] = globaltimer_ns();
+            if ((DBG ? ep.trace : nullptr) && tb < 2 && et == 0 && seg == 0 && ch < 64)
+              (DBG ? ep.trace : nullptr)[tb * 1024 + 800 + ch] = globaltimer_ns();
+            if (!(DBG && (ep.dbg & 4)))
+              epi_emit<MODE, DBG>(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql,
+                       (DBG ? ep.trace : nullptr) && tb < 2 && et == 0 && seg == 0 && ch < 64 ? (DBG ? ep.trace : nullptr) + tb * 1024 + 864 + ch : nullptr);
+            if ((DBG ? ep.trace : nullptr) && tb < 2 && et == 0 && seg == 0 && ch < 64)
+              (DBG ? ep.trace : nullptr)[tb * 1024 + 640 + ch] = globaltimer_ns();
             if (more) {
               tmem_ld_wait_regs(nraw);
-              after_load(ch + 2);
+              after_load(ch + NEH);
 #pragma unroll
               for (int j = 0; j < 16; ++j) raw[j] = nraw[j];
             }
@@ -610,59 +613,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const size_t qoff = static_cast<size_t>(quarter) * 512 + lane * 4;  // + (ch * 4 * 512) + j * 128
         float* wsp = p.red_partials ? ep.ws_red + tile128 * tile_elems + qoff
                                     : ep.ws + (tile128 * p.max_slots + slot) * tile_elems + qoff;
-        // fast path: if every other contributor has already arrived (their partials are in the
-        // slots), this CTA is the tile's last: it reduces straight from its own TMEM accumulator
-        // (no partial write + re-read) summing in slot order with its own value at its slot, i.e.
-        // bit-identical to the slow path's slot-order sum.  In stream-K order the tile's head
-        // contributor finishes its part last, so this is the common case.
-        if (!p.red_partials && p.sk_fast) {
-          if (et == 0) {
-            int* ctr = ep.counters + tile128;
-            int c;
-            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(c) : "l"(ctr) : "memory");
-            s_last = (c == nslot - 1);
-            if (s_last) *ctr = 0;  // re-arm for the next launch (every other contributor has arrived)
-          }
-          named_bar_sync(1, kEpiThreads);
-          if (s_last) {
-            __threadfence();
-            const float* base0 = ep.ws + tile128 * p.max_slots * tile_elems + qoff;
-            auto sum_emit_own = [&](int ch, const uint32_t (&own)[16]) {
-              float v[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = 0.f;
-              for (int q = 0; q < nslot; ++q) {
-                if (q == slot) {
-#pragma unroll
-                  for (int j = 0; j < 16; ++j) v[j] = q == 0 ? __uint_as_float(own[j]) : v[j] + __uint_as_float(own[j]);
-                } else {
-#pragma unroll
-                  for (int j = 0; j < 4; ++j) {
-                    const float4 x = __ldcg(reinterpret_cast<const float4*>(base0 + q * tile_elems + ch * 2048 + j * 128));
-                    v[4 * j + 0] = q == 0 ? x.x : v[4 * j + 0] + x.x;
-                    v[4 * j + 1] = q == 0 ? x.y : v[4 * j + 1] + x.y;
-                    v[4 * j + 2] = q == 0 ? x.z : v[4 * j + 2] + x.z;
-                    v[4 * j + 3] = q == 0 ? x.w : v[4 * j + 3] + x.w;
-                  }
-                }
-              }
-              epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql);
-            };
-            if (eh >= nchunks) {
+        if (eh >= nchunks) {
               release_tmem();
             } else {
               uint32_t raw[16];
               tmem_ld_32x32b_x16(trow + tcol(eh), raw);
               tmem_ld_wait_regs(raw);
               after_load(eh);
-              for (int ch = eh; ch < nchunks; ch += 2) {
+              for (int ch = eh; ch < nchunks; ch += NEH) {
                 uint32_t nraw[16];
-                const bool more = ch + 2 < nchunks;
-                if (more) tmem_ld_32x32b_x16(trow + tcol(ch + 2), nraw);
+                const bool more = ch + NEH < nchunks;
+                if (more) tmem_ld_32x32b_x16(trow + tcol(ch + NEH), nraw);
                 sum_emit_own(ch, raw);
                 if (more) {
                   tmem_ld_wait_regs(nraw);
-                  after_load(ch + 2);
+                  after_load(ch + NEH);
 #pragma unroll
                   for (int j = 0; j < 16; ++j) raw[j] = nraw[j];
                 }
@@ -681,10 +646,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_32x32b_x16(trow + tcol(eh), raw);
           tmem_ld_wait_regs(raw);
           after_load(eh);
-          for (int ch = eh; ch < nchunks; ch += 2) {
+          for (int ch = eh; ch < nchunks; ch += NEH) {
             uint32_t nraw[16];
-            const bool more = ch + 2 < nchunks;
-            if (more) tmem_ld_32x32b_x16(trow + tcol(ch + 2), nraw);
+            const bool more = ch + NEH < nchunks;
+            if (more) tmem_ld_32x32b_x16(trow + tcol(ch + NEH), nraw);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const float4 x = make_float4(__uint_as_float(raw[4 * j]), __uint_as_float(raw[4 * j + 1]),
@@ -696,16 +661,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (more) {
               tmem_ld_wait_regs(nraw);
-              after_load(ch + 2);
+              after_load(ch + NEH);
 #pragma unroll
               for (int j = 0; j < 16; ++j) raw[j] = nraw[j];
             }
           }
         }
-        if (ep.trace && tb < 2 && et == 0 && seg < 32) ep.trace[tb * 1024 + 704 + seg] = globaltimer_ns();
+        if ((DBG ? ep.trace : nullptr) && tb < 2 && et == 0 && seg < 32) (DBG ? ep.trace : nullptr)[tb * 1024 + 704 + seg] = globaltimer_ns();
         __threadfence();
         named_bar_sync(1, kEpiThreads);
-        if (ep.trace && tb < 2 && et == 0 && seg < 32) ep.trace[tb * 1024 + 736 + seg] = globaltimer_ns();
+        if ((DBG ? ep.trace : nullptr) && tb < 2 && et == 0 && seg < 32) (DBG ? ep.trace : nullptr)[tb * 1024 + 736 + seg] = globaltimer_ns();
         if (et == 0) {
           int* ctr = ep.counters + tile128;
           const int old = atomicAdd(ctr, 1);
@@ -743,27 +708,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                 v[4 * j + 3] += x.w;
               }
             }
-            epi_emit(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql);
+            epi_emit<MODE, DBG>(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql);
           };
           float4 A[4], B[4];
           load1(eh, A);
-          for (int ch = eh; ch < nchunks; ch += 4) {
-            if (ch + 2 < nchunks) load1(ch + 2, B);
+          for (int ch = eh; ch < nchunks; ch += 2 * NEH) {
+            if (ch + NEH < nchunks) load1(ch + NEH, B);
             sum_emit(ch, A);
-            if (ch + 2 < nchunks) {
-              if (ch + 4 < nchunks) load1(ch + 4, A);
-              sum_emit(ch + 2, B);
+            if (ch + NEH < nchunks) {
+              if (ch + 2 * NEH < nchunks) load1(ch + 2 * NEH, A);
+              sum_emit(ch + NEH, B);
             }
           }
           if (p.red_partials) {  // re-zero this thread's part of the slot for the next launch
-            for (int ch = eh; ch < nchunks; ch += 2)
+            for (int ch = eh; ch < nchunks; ch += NEH)
 #pragma unroll
               for (int j = 0; j < 4; ++j)
                 __stcg(reinterpret_cast<float4*>(rowbase + ch * 2048 + j * 128), make_float4(0.f, 0.f, 0.f, 0.f));
           }
         }
       }
-      if (ep.trace && tb < 2 && et == 0 && seg < 64) ep.trace[tb * 1024 + 576 + seg] = globaltimer_ns();
+      if ((DBG ? ep.trace : nullptr) && tb < 2 && et == 0 && seg < 64) (DBG ? ep.trace : nullptr)[tb * 1024 + 576 + seg] = globaltimer_ns();
       ++seg;
     }
   }
@@ -771,9 +736,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (ep.span_end && threadIdx.x == 0) atomicMax(ep.span_end, globaltimer_ns());
-  if (ep.trace && threadIdx.x == 0) {
-    ep.trace[2048 + blockIdx.x] = globaltimer_ns();  // per-CTA end (debug)
-    if (blockIdx.x == 0) ep.trace[2047] = 1;
+  if ((DBG ? ep.trace : nullptr) && threadIdx.x == 0) {
+    (DBG ? ep.trace : nullptr)[2048 + blockIdx.x] = globaltimer_ns();  // per-CTA end (debug)
+    if (blockIdx.x == 0) (DBG ? ep.trace : nullptr)[2047] = 1;
   }
   cluster_sync_all();
   if (warp == 1) {
@@ -805,7 +770,11 @@ uint32_t pow2_cols(int n) {
   return c;
 }
 
-size_t extra_smem(int bn) { return 8 * kStageFloats * 4 + 32 * 4 + 2 * static_cast<size_t>(bn) * 4 + 3 * 8 * 8 + 64 + 64; }
+// epilogue warps per TMEM lane quarter: 2 (3 and 4 were measured: no faster / slower with spills)
+constexpr int kNEH = 2;
+size_t extra_smem(int bn) {
+  return 4 * kNEH * kStageFloats * 4 + 32 * 4 + 2 * static_cast<size_t>(bn) * 4 + 3 * 8 * 8 + 64 + 64;
+}
 
 }  // namespace
 
@@ -868,10 +837,7 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
   } else if (tiles <= P) {
     const int sk_pairs = static_cast<int>(std::min<long long>(P, std::max<long long>(1, static_cast<long long>(tiles) * KB / 4)));
     // cost model in k-block units: a split tile adds a partial write + reduction ~ sk_cost * KB
-    // (the last contributor reduces from its own TMEM, sk_fast: the exposed cost is reading the
-    // other contributors' partials, ~0.08 KB; without the fast path a partial write + re-read, ~0.5 KB)
-    static const bool fast = !(getenv("SARATHI_GEMM_SK_FAST") && atoi(getenv("SARATHI_GEMM_SK_FAST")) == 0);
-    static const double sk_cost = getenv("SARATHI_GEMM_SK_COST") ? atof(getenv("SARATHI_GEMM_SK_COST")) : (fast ? 0.08 : 0.5);
+    static const double sk_cost = getenv("SARATHI_GEMM_SK_COST") ? atof(getenv("SARATHI_GEMM_SK_COST")) : 0.5;
     const double sk_units = std::ceil(static_cast<double>(tiles) * KB / sk_pairs) + sk_cost * KB;
     if (KB <= sk_units) {
       pairs = tiles;
@@ -974,8 +940,8 @@ void dump_gemm_trace(const unsigned long long* trace_dev, const GemmPlan& pl) {
         fprintf(stderr, "pair %d end %.2f\n", b / 2, h[2048 + b] ? (h[2048 + b] - t0) * 1e-3 : -1.0);
     }
   }
-  for (int ch = 0; ch < 64 && h[640 + ch]; ++ch)
-    fprintf(stderr, "seg0 chunk %d loaded %8.3f  regs-done %8.3f  emitted %8.3f us\n", ch,
+  for (int ch = 0; ch < 64; ++ch)
+    if (h[640 + ch]) fprintf(stderr, "seg0 chunk %d loaded %8.3f  regs-done %8.3f  emitted %8.3f us\n", ch,
             h[800 + ch] ? (h[800 + ch] - t0) * 1e-3 : -1.0, h[864 + ch] ? (h[864 + ch] - t0) * 1e-3 : -1.0,
             (h[640 + ch] - t0) * 1e-3);
   for (int sgm = 0; sgm < 64 && h[512 + sgm]; ++sgm)
@@ -987,12 +953,25 @@ void dump_gemm_trace(const unsigned long long* trace_dev, const GemmPlan& pl) {
 
 cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const GemmPlan& pl, const EpiParams& ep,
                         cudaStream_t stream) {
+  // one kernel per (epilogue mode, debug) so the epilogue has no runtime mode switch (smaller code,
+  // fewer branches); debug/trace instrumentation only in the DBG instantiations
+  using KFn = void (*)(const CUtensorMap, const CUtensorMap, const KParams, const EpiParams);
+  static const KFn table[2][6] = {
+      {gemm_bf16_pair<kNEH, 0, false>, gemm_bf16_pair<kNEH, 1, false>, gemm_bf16_pair<kNEH, 2, false>,
+       gemm_bf16_pair<kNEH, 3, false>, gemm_bf16_pair<kNEH, 4, false>, gemm_bf16_pair<kNEH, 5, false>},
+      {gemm_bf16_pair<kNEH, 0, true>, gemm_bf16_pair<kNEH, 1, true>, gemm_bf16_pair<kNEH, 2, true>,
+       gemm_bf16_pair<kNEH, 3, true>, gemm_bf16_pair<kNEH, 4, true>, gemm_bf16_pair<kNEH, 5, true>}};
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
-    if (e != cudaSuccess) return e;
+    for (auto& row : table)
+      for (KFn fn : row) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+        if (e != cudaSuccess) return e;
+      }
     configured = true;
   }
+  if (ep.mode < 0 || ep.mode > 5) return cudaErrorInvalidValue;
+  const KFn fn = table[(ep.dbg || ep.trace) ? 1 : 0][ep.mode];
   KParams kp;
   kp.M = pl.M;
   kp.N = pl.N;
@@ -1013,11 +992,9 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   kp.red_partials = pl.red_partials;
   kp.tmem_cols = (pl.nbuf == 2 || (pl.n_mma == 2 && 3 * (pl.bn / 2) <= 512)) ? 512 : pow2_cols(pl.bn);
   kp.ring_bytes = static_cast<uint32_t>(pl.stages * (kABytes + static_cast<size_t>(pl.bn / 2) * kBK * 2));
-  static const int sk_fast = !(getenv("SARATHI_GEMM_SK_FAST") && atoi(getenv("SARATHI_GEMM_SK_FAST")) == 0);
-  kp.sk_fast = sk_fast;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pl.ctas);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads_of<kNEH>());
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -1029,7 +1006,7 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, gemm_bf16_pair, mapW, mapX, kp, ep);
+  return cudaLaunchKernelEx(&cfg, fn, mapW, mapX, kp, ep);
 }
 
 }  // namespace sarathi

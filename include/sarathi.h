@@ -243,7 +243,8 @@ int sarathi_shard_map(const sarathi_model_config* cfg, int32_t rank, int32_t wor
 /* Policy (reading O-16): FCFS admission by (arrival, id) while fewer than B requests run and the
  * full (P+D)-token KV reservation fits in the sched's own block allocator (lowest-free-first,
  * same algorithm as the model's); batch = <= 1 chunk of min(C_eff, P - done) from the oldest
- * running request with prefill left (C_eff = C, or C-(B-1) with tile_adjust) + every
+ * running request with prefill left (tile_adjust 0: C; 1: the paper's C-(B-1); 2: the B200
+ * token-quantum rule sarathi_chunk_advice(C, d, remaining) with d = this batch's decodes) + every
  * decode-phase request in admission order, at most B-1 with a chunk and B without.
  * SARATHI_POLICY_ORCA_BEST: C_eff = the full remaining prompt.
  * SARATHI_POLICY_REQUEST_LEVEL: cohorts; prompts as prefill-only batches, then decode-only. */
@@ -280,6 +281,15 @@ int sarathi_sched_complete(sarathi_sched* s, int64_t* finished, int32_t cap, int
 int sarathi_sched_idle_step(sarathi_sched* s);
 int sarathi_sched_done(const sarathi_sched* s, int32_t* done);
 int sarathi_sched_block_table(const sarathi_sched* s, int64_t req_id, int32_t* out, int32_t cap, int32_t* n_out);
+
+/* Token tiling of the layer GEMMs for a T-token batch (host only): capacity = token columns the
+ * tcgen05 GEMM computes (padding included), n_tiles token tiles, n_mma UMMAs per k-step (1 when a
+ * tile holds <= 256 tokens).  n_tiles / n_mma may be NULL. */
+int sarathi_token_capacity(int32_t T, int32_t* capacity, int32_t* n_tiles, int32_t* n_mma);
+/* B200 chunk advisor (the §4.4 tile-quantization rule, on this GEMM's quanta):
+ * with chunk C, d decodes in the batch and `remaining` prompt tokens: p = b - d when C + d overshoots
+ * b in {256, 512} by at most C/8, else capacity(C + d) - d; clamped to [1, remaining].  Host only. */
+int sarathi_chunk_advice(int32_t C, int32_t d, int32_t remaining, int32_t* p_out);
 
 /* ---- kernel-level entry points (device pointers, caller's stream) for parity tests ------ */
 /* out = X · Wᵀ on tcgen05: W bf16 [M][K] (K-major), X bf16 [N][K]; mode 0: out bf16 [N][M],

@@ -63,6 +63,31 @@ def advise_chunk_size(C: int, B: int) -> int:
     return C - (B - 1)
 
 
+def gemm_token_capacity(T: int) -> int:
+    """Token columns the B200 swap-AB GEMM computes for T tokens (the padding is free): token tiles
+    of <= 512; a tile of per <= 256 tokens is one UMMA of N = 16*ceil(per/16), a wider one two UMMAs
+    with bn = 32*ceil(per/32) (the UMMA N quanta 16 / 32 of tcgen05.mma cta_group::2)."""
+    T = max(T, 1)
+    n_tiles = -(-T // 512)
+    per = -(-T // n_tiles)
+    bn = max(16, 16 * -(-per // 16)) if per <= 256 else 32 * -(-per // 32)
+    return bn * n_tiles
+
+
+def b200_chunk(C: int, d: int, remaining: int) -> int:
+    """The paper's tile-quantization chunk rule (trim the chunk so chunk + decodes lands
+    on the tile boundary) restated for the B200 GEMM's quanta: if T = C + d overshoots a cost step
+    b in {256, 512} by at most C/8, trim to b - d; otherwise fill the padded tile to
+    gemm_token_capacity(T) - d.  Clamped to [1, remaining]."""
+    T = C + d
+    p = gemm_token_capacity(T) - d
+    for b in (256, 512):
+        if b < T <= b + C // 8 and b - d >= 1:
+            p = b - d
+            break
+    return max(1, min(p, remaining))
+
+
 def optimal_pd(C: int, B: int) -> float:
     """Balanced P:D = C / (B-1)."""
     if B < 2:
@@ -166,7 +191,9 @@ class Scheduler:
     """
 
     def __init__(self, B: int, C: int, allocator: BlockAllocator, policy: str = SARATHI,
-                 tile_adjust: bool = False):
+                 tile_adjust: int = 0):
+        """tile_adjust: 0 the literal chunk C; 1 the paper's C - (B-1); 2 b200_chunk with
+        the batch's own decode count."""
         if B < 1 or C < 1:
             raise ValueError("B >= 1 and C >= 1")
         self.B, self.C, self.alloc, self.policy = B, C, allocator, policy
@@ -221,11 +248,14 @@ class Scheduler:
                 decoders = []
         elif cand:
             r = cand[0]
+            rem = r.P - r.prefill_done
             if self.policy == ORCA_BEST:
-                c_eff = r.P
+                n = rem
+            elif self.tile_adjust == 2:
+                n = b200_chunk(self.C, min(len(decoders), self.B - 1), rem)
             else:
-                c_eff = advise_chunk_size(self.C, self.B) if self.tile_adjust else self.C
-            prefill = (r.req_id, r.prefill_done, min(c_eff, r.P - r.prefill_done))
+                n = min(advise_chunk_size(self.C, self.B) if self.tile_adjust == 1 else self.C, rem)
+            prefill = (r.req_id, r.prefill_done, n)
         cap = self.B - 1 if prefill is not None else self.B
         decodes = [(r.req_id, r.P + r.decode_done) for r in decoders[:cap]]
         if prefill is None and not decodes:

@@ -334,10 +334,11 @@ int sarathi_sched_create(int32_t B, int32_t C, int32_t policy, int32_t tile_adju
                          int32_t block_size, sarathi_sched** out) {
   if (!out || B < 1 || C < 1 || policy < 0 || policy > 2 || num_blocks < 0 || block_size < 1)
     return fail(SARATHI_EINVAL, "sched_create: bad argument");
-  if (tile_adjust && C <= B - 1) return fail(SARATHI_EINVAL, "sched_create: tile-adjusted chunk C-(B-1) must be >= 1");
+  if (tile_adjust < 0 || tile_adjust > 2) return fail(SARATHI_EINVAL, "sched_create: tile_adjust must be 0, 1 or 2");
+  if (tile_adjust == 1 && C <= B - 1) return fail(SARATHI_EINVAL, "sched_create: tile-adjusted chunk C-(B-1) must be >= 1");
   auto* s = new (std::nothrow) sarathi_sched();
   if (!s) return fail(SARATHI_EINVAL, "sched_create: out of memory");
-  s->s = new sarathi::Scheduler(B, C, policy, tile_adjust != 0, num_blocks, block_size);
+  s->s = new sarathi::Scheduler(B, C, policy, tile_adjust, num_blocks, block_size);
   *out = s;
   return SARATHI_OK;
 }
@@ -411,6 +412,21 @@ int sarathi_sched_block_table(const sarathi_sched* s, int64_t req_id, int32_t* o
     if (cap < static_cast<int32_t>(t.size())) return fail(SARATHI_EINVAL, "sched_block_table: cap");
     std::memcpy(out, t.data(), t.size() * sizeof(int32_t));
   }
+  return SARATHI_OK;
+}
+
+int sarathi_token_capacity(int32_t T, int32_t* capacity, int32_t* n_tiles, int32_t* n_mma) {
+  if (T < 1 || !capacity) return fail(SARATHI_EINVAL, "token_capacity: bad argument");
+  const sarathi::TokenTiling t = sarathi::gemm_token_tiling(T);
+  *capacity = t.capacity();
+  if (n_tiles) *n_tiles = t.n_tiles;
+  if (n_mma) *n_mma = t.n_mma;
+  return SARATHI_OK;
+}
+
+int sarathi_chunk_advice(int32_t C, int32_t d, int32_t remaining, int32_t* p_out) {
+  if (C < 1 || d < 0 || remaining < 1 || !p_out) return fail(SARATHI_EINVAL, "chunk_advice: bad argument");
+  *p_out = sarathi::b200_chunk(C, d, remaining);
   return SARATHI_OK;
 }
 

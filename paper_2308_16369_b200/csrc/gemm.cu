@@ -23,6 +23,7 @@
 //               GELU, RoPE + paged KV append, bf16/fp32 stores, or the stream-K partial
 #include "common.cuh"
 #include "gemm.cuh"
+#include "host_sched.hpp"
 
 #include <algorithm>
 #include <vector>
@@ -614,31 +615,6 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
         float* wsp = p.red_partials ? ep.ws_red + tile128 * tile_elems + qoff
                                     : ep.ws + (tile128 * p.max_slots + slot) * tile_elems + qoff;
         if (eh >= nchunks) {
-              release_tmem();
-            } else {
-              uint32_t raw[16];
-              tmem_ld_32x32b_x16(trow + tcol(eh), raw);
-              tmem_ld_wait_regs(raw);
-              after_load(eh);
-              for (int ch = eh; ch < nchunks; ch += NEH) {
-                uint32_t nraw[16];
-                const bool more = ch + NEH < nchunks;
-                if (more) tmem_ld_32x32b_x16(trow + tcol(ch + NEH), nraw);
-                sum_emit_own(ch, raw);
-                if (more) {
-                  tmem_ld_wait_regs(nraw);
-                  after_load(ch + NEH);
-#pragma unroll
-                  for (int j = 0; j < 16; ++j) raw[j] = nraw[j];
-                }
-              }
-            }
-            named_bar_sync(1, kEpiThreads);  // s_last is rewritten by the next segment's check
-            ++seg;
-            continue;
-          }
-        }
-        if (eh >= nchunks) {
           release_tmem();
         } else {
           // TMEM drain pipelined like the direct path; TMEM is released right after the last load
@@ -798,15 +774,10 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
   pl.N = N;
   pl.K = K;
   const int KB = K / kBK;
-  pl.n_tiles = (N + 511) / 512;
-  const int per = (N + pl.n_tiles - 1) / pl.n_tiles;
-  if (per <= 256) {
-    pl.n_mma = 1;
-    pl.bn = std::max(16, (per + 15) / 16 * 16);
-  } else {
-    pl.n_mma = 2;
-    pl.bn = (per + 31) / 32 * 32;
-  }
+  const TokenTiling tt = gemm_token_tiling(N);  // shared with the scheduler's chunk advisor
+  pl.n_tiles = tt.n_tiles;
+  pl.n_mma = tt.n_mma;
+  pl.bn = tt.bn;
   pl.box_rows = pl.bn / pl.n_mma / 2;  // each CTA of the pair holds half of every UMMA's tokens
   pl.pm_tiles = (M + 2 * kBM - 1) / (2 * kBM);
   pl.m_tiles = 2 * pl.pm_tiles;

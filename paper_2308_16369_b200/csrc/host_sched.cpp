@@ -8,6 +8,32 @@
 
 namespace sarathi {
 
+TokenTiling gemm_token_tiling(int T) {
+  TokenTiling t;
+  T = std::max(T, 1);
+  t.n_tiles = (T + 511) / 512;
+  const int per = (T + t.n_tiles - 1) / t.n_tiles;
+  if (per <= 256) {
+    t.n_mma = 1;
+    t.bn = std::max(16, (per + 15) / 16 * 16);
+  } else {
+    t.n_mma = 2;
+    t.bn = (per + 31) / 32 * 32;
+  }
+  return t;
+}
+
+int b200_chunk(int C, int d, int remaining) {
+  const int T = C + d;
+  int p = gemm_token_tiling(T).capacity() - d;
+  for (int b : {256, 512})
+    if (T > b && T - b <= C / 8 && b - d >= 1) {
+      p = b - d;
+      break;
+    }
+  return std::max(1, std::min(p, remaining));
+}
+
 BlockAllocator::BlockAllocator(int64_t num_blocks, int32_t block_size)
     : num_blocks_(num_blocks), block_size_(block_size) {
   for (int64_t b = 0; b < num_blocks; ++b) free_.insert(static_cast<int32_t>(b));
@@ -34,7 +60,7 @@ void BlockAllocator::free(int64_t req) {
   reserved_.erase(req);
 }
 
-Scheduler::Scheduler(int32_t B, int32_t C, int32_t policy, bool tile_adjust, int64_t num_blocks, int32_t block_size)
+Scheduler::Scheduler(int32_t B, int32_t C, int32_t policy, int32_t tile_adjust, int64_t num_blocks, int32_t block_size)
     : B_(B), C_(C), policy_(policy), tile_adjust_(tile_adjust), alloc_(num_blocks, block_size) {}
 
 int Scheduler::submit(int64_t req, int32_t P, int32_t D, int32_t arrival, std::string* err) {
@@ -101,18 +127,21 @@ bool Scheduler::next(PlanOut* out) {
   std::vector<Req*> dec;
   for (Req* r : run)
     if (r->prefill_done == r->P && r->decode_done < r->D) dec.push_back(r);
+  const size_t cap = static_cast<size_t>(cand ? B_ - 1 : B_);
   if (cand) {
-    int32_t c_eff;
+    const int32_t remaining = cand->P - cand->prefill_done;
+    int32_t len;
     if (policy_ == ORCA_BEST || policy_ == REQUEST_LEVEL)
-      c_eff = cand->P;
+      len = remaining;
+    else if (tile_adjust_ == 2)  // decodes riding in THIS batch
+      len = b200_chunk(C_, static_cast<int>(std::min(dec.size(), cap)), remaining);
     else
-      c_eff = tile_adjust_ ? C_ - (B_ - 1) : C_;
+      len = std::min(tile_adjust_ == 1 ? C_ - (B_ - 1) : C_, remaining);
     plan.prefill_req = cand->id;
     plan.prefill_start = cand->prefill_done;
-    plan.prefill_len = std::min(c_eff, cand->P - cand->prefill_done);
+    plan.prefill_len = len;
     if (policy_ == REQUEST_LEVEL) dec.clear();
   }
-  const size_t cap = static_cast<size_t>(cand ? B_ - 1 : B_);
   for (size_t i = 0; i < dec.size() && i < cap; ++i)
     plan.decodes.emplace_back(dec[i]->id, dec[i]->P + dec[i]->decode_done);
   if (!cand && plan.decodes.empty()) {

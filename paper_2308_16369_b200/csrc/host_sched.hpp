@@ -9,6 +9,28 @@
 
 namespace sarathi {
 
+// Token tiling of the swap-AB tcgen05 GEMM (gemm.cu plan_gemm uses exactly this): a batch of T
+// tokens is cut into n_tiles = ceil(T / 512) token tiles of per = ceil(T / n_tiles) tokens; a tile
+// of per <= 256 tokens is ONE UMMA per k-step of N = 16 * ceil(per / 16) (TMEM double-buffered),
+// a wider one TWO UMMAs of N = bn / 2 with bn = 32 * ceil(per / 32).  capacity = bn * n_tiles is
+// the number of token columns the GEMM computes anyway (the padding is free).
+struct TokenTiling {
+  int n_tiles = 1, bn = 16, n_mma = 1;
+  int capacity() const { return bn * n_tiles; }
+};
+TokenTiling gemm_token_tiling(int T);
+
+// B200 analogue of the paper's tile-quantization chunk rule (§4.4: the chunk is
+// trimmed to C - (B-1) so chunk + decodes fills 256 tokens exactly, because crossing a 128-token
+// tile boundary costs a whole extra tile).  Here the token quantum is the UMMA N granularity (16/32)
+// and the cost steps are at T = 256 (one -> two UMMAs per k-step, TMEM double buffer -> ring) and
+// T = 512 (a second token tile).  Given the configured chunk C, the batch's decode count d and the
+// request's remaining prompt tokens:
+//   * T = C + d just past a step b in {256, 512} (T - b <= C / 8): trim, p = b - d;
+//   * otherwise fill the padded tile: p = capacity(C + d) - d (>= C; those columns are computed anyway);
+//   p = min(p, remaining), at least 1.
+int b200_chunk(int C, int d, int remaining);
+
 // Paged KV block allocator: a request reserves ceil(max_tokens / bs) blocks up front (the paper
 // pre-allocates KV per maximum sequence length, §4.5), lowest-free-block-first
 // (reading O-17) so the tables are deterministic and identical on every TP rank.
@@ -55,7 +77,8 @@ struct PlanOut {
 class Scheduler {
  public:
   enum Policy { SARATHI = 0, ORCA_BEST = 1, REQUEST_LEVEL = 2 };
-  Scheduler(int32_t B, int32_t C, int32_t policy, bool tile_adjust, int64_t num_blocks, int32_t block_size);
+  // tile_adjust: 0 literal chunk C; 1 the paper's C - (B-1); 2 b200_chunk(C, d, remaining)
+  Scheduler(int32_t B, int32_t C, int32_t policy, int32_t tile_adjust, int64_t num_blocks, int32_t block_size);
   // SARATHI_OK, SARATHI_EINVAL (duplicate id / P < 1 / D < 0) or SARATHI_ENOKV (the P+D
   // reservation needs more blocks than the whole pool: it could never be admitted and, with strict
   // FCFS, would block every later request forever)
@@ -78,7 +101,7 @@ class Scheduler {
   };
   std::vector<Req*> running();
   int32_t B_, C_, policy_;
-  bool tile_adjust_;
+  int32_t tile_adjust_;
   BlockAllocator alloc_;
   std::map<int64_t, Req> reqs_;
   int32_t iteration_ = 0;

@@ -34,6 +34,7 @@ EXPORTS = [
     "sarathi_sched_done", "sarathi_sched_block_table", "sarathi_op_gemm", "sarathi_op_rmsnorm",
     "sarathi_request_truncate", "sarathi_last_io_bytes", "sarathi_set_profiling", "sarathi_op_times", "sarathi_op_kernel_times",
     "sarathi_op_pack_weight", "sarathi_shard_map", "sarathi_local_group_create", "sarathi_local_group_destroy",
+    "sarathi_token_capacity", "sarathi_chunk_advice",
 ]
 GEMM_W_PACKED = 0x100
 OP_NAMES = ["embed", "rmsnorm", "gemm_qkv", "prefill_attn", "decode_attn", "gemm_o", "gemm_gate_up",
@@ -110,6 +111,8 @@ def _load() -> C.CDLL:
         "sarathi_op_kernel_times": [VP, P(C.c_double), P(I64), I32, I32],
         "sarathi_op_pack_weight": [VP, VP, I32, I32, VP],
         "sarathi_local_group_create": [I32, I32, P(VP)],
+        "sarathi_token_capacity": [I32, P(I32), P(I32), P(I32)],
+        "sarathi_chunk_advice": [I32, I32, I32, P(I32)],
         "sarathi_shard_map": [P(ModelConfigC), I32, I32, I32, I32, P(I32), P(F), P(I64), I32, P(I32), P(I32)],
     }
     for name, args in sig.items():
@@ -340,7 +343,8 @@ class Scheduler:
     """Host scheduler (decode-maximal batching, §4.3) — C++ implementation behind the C ABI."""
 
     def __init__(self, B: int, C_: int, num_blocks: int, block_size: int, policy: int = POLICY_SARATHI,
-                 tile_adjust: bool = False):
+                 tile_adjust: int = 0):
+        """tile_adjust: 0 literal chunk C, 1 the paper's C - (B-1), 2 the B200 advisor (chunk_advice)."""
         h = C.c_void_p()
         _check(lib.sarathi_sched_create(B, C_, policy, int(tile_adjust), num_blocks, block_size, C.byref(h)))
         self.h = h
@@ -392,6 +396,19 @@ class Scheduler:
         out = np.zeros(n.value, dtype=np.int32)
         _check(lib.sarathi_sched_block_table(self.h, req_id, _p(out, C.c_int32), n.value, C.byref(n)))
         return out
+
+
+def token_capacity(T: int) -> Tuple[int, int, int]:
+    """(capacity, n_tiles, n_mma) of the layer GEMMs' token tiling for a T-token batch (host only)."""
+    a, b, c = C.c_int32(), C.c_int32(), C.c_int32()
+    _check(lib.sarathi_token_capacity(T, C.byref(a), C.byref(b), C.byref(c)))
+    return a.value, b.value, c.value
+
+
+def chunk_advice(C_: int, d: int, remaining: int) -> int:
+    v = C.c_int32()
+    _check(lib.sarathi_chunk_advice(C_, d, remaining, C.byref(v)))
+    return v.value
 
 
 def op_gemm(W_ptr: int, X_ptr: int, out_ptr: int, M: int, N: int, K: int, mode: int, force_splits: int = 0,

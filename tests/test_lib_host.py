@@ -155,7 +155,9 @@ def test_cpp_scheduler_matches_python_twin(S, seed, policy):
     rnd = random.Random(seed * 7 + policy)
     B, C, bs = rnd.randint(1, 8), rnd.choice([4, 16, 64, 256]), rnd.choice([16, 64])
     nb = rnd.randint(8, 200)
-    tile = policy == 0 and C > B - 1 and rnd.random() < 0.3
+    tile = rnd.choice([0, 0, 1, 2]) if policy == 0 else 0
+    if tile == 1 and C <= B - 1:
+        tile = 0
     reqs = []
     for rid in range(rnd.randint(1, 25)):
         P, D = rnd.randint(1, 300), rnd.randint(0, 40)
@@ -167,3 +169,27 @@ def test_cpp_scheduler_matches_python_twin(S, seed, policy):
     b = _drain_py(B, C, nb, bs, reqs, py_policy, tile)
     assert a[0] == b[0]
     assert a[1] == b[1]
+
+
+def test_b200_chunk_advisor_hand_cases_and_cpp_twin(S):
+    """B200 tile-quantization chunk rule (PAPER.md L457-463 restated on the tcgen05 GEMM's token
+    quanta): hand-computed cases, then the C++ advisor / token tiling == the Python twin."""
+    cap = osch.gemm_token_capacity
+    # token capacity: 16-multiples up to 256 (one UMMA), 32-multiples to 512 (two), then 2 tiles
+    assert [cap(t) for t in (1, 16, 17, 255, 256, 257, 288, 289, 320, 512, 513, 1024)] == \
+        [16, 16, 32, 256, 256, 288, 288, 320, 320, 512, 576, 1024]
+    ch = osch.b200_chunk
+    assert ch(256, 0, 10**6) == 256          # exactly on the quantum
+    assert ch(256, 1, 10**6) == 255          # 257 tokens: trim to 256 (the paper's 256 - (B-1))
+    assert ch(256, 32, 10**6) == 224         # overshoot 32 = C/8: still trimmed
+    assert ch(256, 33, 10**6) == 287         # overshoot 33 > C/8: fill the 320-token tile... bn 320
+    assert ch(256, 64, 10**6) == 256         # T = 320 = capacity
+    assert ch(128, 5, 10**6) == 139          # T = 133 -> 144-token tile: fill
+    assert ch(128, 5, 50) == 50              # the last chunk of a prompt
+    assert ch(500, 20, 10**6) == 492         # T = 520 overshoots 512 by 8 <= 62: trim
+    for C in (16, 64, 128, 192, 256, 320, 384, 512):
+        for d in range(0, 140, 3):
+            for rem in (1, 7, C // 2 + 1, 10**6):
+                assert S.chunk_advice(C, d, rem) == osch.b200_chunk(C, d, rem), (C, d, rem)
+    for T in range(1, 1600):
+        assert S.token_capacity(T)[0] == cap(T), T

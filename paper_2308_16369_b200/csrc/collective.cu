@@ -74,6 +74,9 @@ struct LocalGroup {
   std::vector<cudaEvent_t> ev_ready, ev_done;
   std::vector<const void*> slot;  // pointer each rank publishes for the current collective
   std::vector<int> joined;
+  // fused all-reduce registry: rank r's partial double buffer and ready-flag array
+  std::vector<__nv_bfloat16*> arbuf0, arbuf1;
+  std::vector<unsigned int*> ready;
 
   // false on timeout / broken group (a peer failed and will never arrive)
   bool barrier() {
@@ -106,6 +109,9 @@ Status local_group_create(int world, int device, LocalGroup** out) {
   g->ev_done.assign(world, nullptr);
   g->slot.assign(world, nullptr);
   g->joined.assign(world, 0);
+  g->arbuf0.assign(world, nullptr);
+  g->arbuf1.assign(world, nullptr);
+  g->ready.assign(world, nullptr);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
@@ -164,6 +170,48 @@ static Status exchange_end(LocalGroup* g, int rank, cudaStream_t st) {
     if (r != rank && cudaStreamWaitEvent(st, g->ev_done[r], 0) != cudaSuccess)
       return Status::err(SARATHI_ECUDA, "group: stream wait");
   return Status::ok();
+}
+
+void local_group_register(LocalGroup* g, int rank, __nv_bfloat16* const arbuf[2], unsigned int* ready) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  g->arbuf0[rank] = arbuf[0];
+  g->arbuf1[rank] = arbuf[1];
+  g->ready[rank] = ready;
+}
+
+bool local_group_peers(LocalGroup* g, const __nv_bfloat16* peer_ar[2][8], unsigned int* peer_ready[8]) {
+  std::lock_guard<std::mutex> lk(g->mu);
+  for (int r = 0; r < g->world; ++r) {
+    if (!g->arbuf0[r] || !g->ready[r]) return false;
+    peer_ar[0][r] = g->arbuf0[r];
+    peer_ar[1][r] = g->arbuf1[r];
+    peer_ready[r] = g->ready[r];
+  }
+  return true;
+}
+
+Status local_fused_begin(LocalGroup* g, int rank, cudaStream_t st) { return exchange_begin(g, rank, nullptr, st); }
+Status local_fused_end(LocalGroup* g, int rank, cudaStream_t st) { return exchange_end(g, rank, st); }
+
+namespace {
+struct FlagPtrs {
+  unsigned int* f[8];
+};
+__global__ void signal_ready_kernel(FlagPtrs pf, int rank, int world, unsigned int epoch) {
+  const int r = threadIdx.x;
+  if (r < world) {
+    __threadfence_system();  // the partial (written by the preceding GEMM) before the flag, system scope
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pf.f[r] + rank), "r"(epoch) : "memory");
+  }
+}
+}  // namespace
+
+cudaError_t launch_signal_ready(unsigned int* const peer_ready[8], int rank, int world, unsigned int epoch,
+                                cudaStream_t st) {
+  FlagPtrs pf{};
+  for (int r = 0; r < world; ++r) pf.f[r] = peer_ready[r];
+  signal_ready_kernel<<<1, 32, 0, st>>>(pf, rank, world, epoch);
+  return cudaGetLastError();
 }
 
 Status local_allreduce_bf16(LocalGroup* g, int rank, const __nv_bfloat16* partial, __nv_bfloat16* result, size_t count,

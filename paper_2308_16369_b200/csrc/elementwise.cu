@@ -53,9 +53,39 @@ __device__ float block_sum(float v, float* sred) {
   return t;
 }
 
+// Wait until every rank's partial of this all-reduce is published (ready[r] >= epoch).
+__device__ __forceinline__ void peer_wait(const PeerSum& ps) {
+  if (!ps.ready) return;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < ps.world; ++r) {
+      unsigned int v;
+      while (true) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ps.ready + r) : "memory");
+        if (static_cast<int>(v - ps.epoch) >= 0) break;
+        __nanosleep(64);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// sum over ranks (rank order, fp32) of 4 consecutive bf16 partial values at element offset i
+__device__ __forceinline__ float4 peer_sum4(const PeerSum& ps, size_t i) {
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int r = 0; r < ps.world; ++r) {
+    const uint2 raw = *reinterpret_cast<const uint2*>(ps.p[r] + i);
+    const float2 a0 = unpack_bf16x2(raw.x), a1 = unpack_bf16x2(raw.y);
+    a.x += a0.x;
+    a.y += a0.y;
+    a.z += a1.x;
+    a.w += a1.y;
+  }
+  return a;
+}
+
 // RMSNorm(x; g) = x / sqrt(mean(x^2) + eps) * g  (reading O-8), fp32 math, bf16 out.
 template <int kThreads, int kVec>
-__global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h, const __nv_bfloat16* __restrict__ add,
+__global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h, const PeerSum add,
                                                            const __nv_bfloat16* __restrict__ g,
                                                            __nv_bfloat16* __restrict__ out, const int* __restrict__ rows,
                                                            int H, float eps, unsigned long long* span_start,
@@ -70,6 +100,7 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h
     if (i < H) gv[c] = *reinterpret_cast<const uint2*>(g + i);
   }
   griddep_wait();  // h / add come from the preceding GEMM (PDL)
+  peer_wait(add);  // fused all-reduce: every rank's partial published
   if (span_start && threadIdx.x == 0) atomicMin(span_start, globaltimer_ns());
   const int r = blockIdx.x;
   const int row = rows ? rows[r] : r;
@@ -82,10 +113,9 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h
     const int i = (c * kThreads + threadIdx.x) * 4;
     if (i < H) {
       v[c] = *reinterpret_cast<const float4*>(x + i);
-      if (add) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(add + static_cast<size_t>(row) * H + i);
-        const float2 a0 = unpack_bf16x2(raw.x), a1 = unpack_bf16x2(raw.y);
-        v[c].x += a0.x; v[c].y += a0.y; v[c].z += a1.x; v[c].w += a1.y;
+      if (add.world) {
+        const float4 a = peer_sum4(add, static_cast<size_t>(row) * H + i);
+        v[c].x += a.x; v[c].y += a.y; v[c].z += a.z; v[c].w += a.w;
         *reinterpret_cast<float4*>(x + i) = v[c];
       }
       ss += v[c].x * v[c].x + v[c].y * v[c].y + v[c].z * v[c].z + v[c].w * v[c].w;
@@ -108,13 +138,13 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h
   if (span_end && threadIdx.x == 0) atomicMax(span_end, globaltimer_ns());
 }
 
-__global__ void residual_add_kernel(float* __restrict__ h, const __nv_bfloat16* __restrict__ add, size_t n) {
+__global__ void residual_add_kernel(float* __restrict__ h, const PeerSum add, size_t n) {
+  peer_wait(add);
   for (size_t i = (blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x) * 4; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x * 4) {
     float4 v = *reinterpret_cast<float4*>(h + i);
-    const uint2 raw = *reinterpret_cast<const uint2*>(add + i);
-    const float2 a0 = unpack_bf16x2(raw.x), a1 = unpack_bf16x2(raw.y);
-    v.x += a0.x; v.y += a0.y; v.z += a1.x; v.w += a1.y;
+    const float4 a = peer_sum4(add, i);
+    v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
     *reinterpret_cast<float4*>(h + i) = v;
   }
 }
@@ -192,7 +222,7 @@ cudaError_t launch_embedding(const int* tok, const __nv_bfloat16* E, float* h, i
   return cudaGetLastError();
 }
 
-cudaError_t launch_rmsnorm(float* h, const __nv_bfloat16* add, const __nv_bfloat16* g, __nv_bfloat16* out,
+cudaError_t launch_rmsnorm(float* h, const PeerSum& add, const __nv_bfloat16* g, __nv_bfloat16* out,
                            const int* rows, int R, int H, float eps, cudaStream_t st, unsigned long long* span_start,
                            unsigned long long* span_end) {
   if (R == 0) return cudaSuccess;
@@ -211,7 +241,7 @@ cudaError_t launch_rmsnorm(float* h, const __nv_bfloat16* add, const __nv_bfloat
   return cudaGetLastError();
 }
 
-cudaError_t launch_residual_add(float* h, const __nv_bfloat16* add, int T, int H, cudaStream_t st) {
+cudaError_t launch_residual_add(float* h, const PeerSum& add, int T, int H, cudaStream_t st) {
   const size_t n = static_cast<size_t>(T) * H;
   if (n == 0) return cudaSuccess;
   const int blocks = static_cast<int>(std::min<size_t>(1184, (n / 4 + 255) / 256));

@@ -78,17 +78,39 @@ cudaError_t launch_decode_attention(const DecodeAttnArgs& a, const CUtensorMap& 
 cudaError_t launch_prefill_attention(const PrefillAttnArgs& a, const CUtensorMap* qmap, const CUtensorMap* kmap,
                                      const CUtensorMap* vmap, cudaStream_t st);
 
+// TP partials to add into the residual before a norm (Megatron row-parallel O / down, PAPER.md L249
+// §2.3).  world == 0: nothing.  world == 1: p[0] holds the already all-reduced sum (NCCL path).
+// world > 1: the one-shot all-reduce fused into the consumer — p[r] is rank r's bf16 partial (peer
+// memory: the same device in a local group, CUDA-IPC mapped over NVLink across processes), summed
+// in rank order in fp32 (identical on every rank); when ready != nullptr the kernel first waits until
+// ready[r] >= epoch for every rank r (each rank's signal after its GEMM; ld.acquire.sys).
+struct PeerSum {
+  const __nv_bfloat16* p[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int world = 0;
+  const unsigned int* ready = nullptr;
+  unsigned int epoch = 0;
+};
+
 // h[t][:] = float(E[tok[t]][:])
 cudaError_t launch_embedding(const int* tok, const __nv_bfloat16* E, float* h, int T, int H, cudaStream_t st);
 
 // out[r][:] = bf16(RMSNorm(h[row(r)]) * g); row(r) = rows ? rows[r] : r.
-// If add != nullptr (TP all-reduced partial, bf16): h[row] += add[row] first and h is updated.
-cudaError_t launch_rmsnorm(float* h, const __nv_bfloat16* add, const __nv_bfloat16* g, __nv_bfloat16* out,
+// With TP partials (PeerSum world >= 1): h[row] += sum of the partials' row first and h is updated.
+cudaError_t launch_rmsnorm(float* h, const PeerSum& add, const __nv_bfloat16* g, __nv_bfloat16* out,
                            const int* rows, int R, int H, float eps, cudaStream_t st,
                            unsigned long long* span_start = nullptr, unsigned long long* span_end = nullptr);
+inline cudaError_t launch_rmsnorm(float* h, const __nv_bfloat16* add, const __nv_bfloat16* g, __nv_bfloat16* out,
+                                  const int* rows, int R, int H, float eps, cudaStream_t st,
+                                  unsigned long long* span_start = nullptr, unsigned long long* span_end = nullptr) {
+  PeerSum ps;
+  ps.world = add ? 1 : 0;
+  ps.p[0] = add;
+  return launch_rmsnorm(h, ps, g, out, rows, R, H, eps, st, span_start, span_end);
+}
 
-// h[t][:] += add[t][:] (bf16 -> fp32), no norm (last layer under TP before the final norm)
-cudaError_t launch_residual_add(float* h, const __nv_bfloat16* add, int T, int H, cudaStream_t st);
+// h[t][:] += sum of the partials (PeerSum, world >= 1), no norm (last layer under TP before the
+// final norm)
+cudaError_t launch_residual_add(float* h, const PeerSum& add, int T, int H, cudaStream_t st);
 
 // logits[r][rank*Vl + c] = gathered[rank][r][c]  (vocab-parallel all-gather layout -> [R][V])
 cudaError_t launch_vocab_permute(const float* gathered, float* logits, int world, int R, int Vl, int V,

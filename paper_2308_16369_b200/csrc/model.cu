@@ -337,6 +337,24 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   SRET(dalloc(&ar, static_cast<size_t>(Tmax) * H));
   if (group) SRET(dalloc(&ar_red, static_cast<size_t>(Tmax) * H));
   ar_res = ar;
+  // fused all-reduce (NEXT-1): default in a local group (parity-tested on one GPU); for one process
+  // per GPU it is opt-in (SARATHI_TP_FUSED=1: CUDA-IPC peer mappings, not yet measured on hardware)
+  {
+    const char* fe = getenv("SARATHI_TP_FUSED");
+    tp_fused = world > 1 && (group ? !(fe && fe[0] == '0') : (fe && fe[0] == '1'));
+  }
+  if (tp_fused) {
+    SRET(dalloc(&arbuf[0], static_cast<size_t>(Tmax) * H));
+    SRET(dalloc(&arbuf[1], static_cast<size_t>(Tmax) * H));
+    SRET(dalloc(&ready, 8));
+    SRET(check(cudaMemsetAsync(ready, 0, 8 * sizeof(unsigned int), stream), "memset flags"));
+    SRET(check(cudaStreamSynchronize(stream), "flags"));
+    if (group) {
+      local_group_register(group, rank, arbuf, ready);
+    } else {
+      SRET(ipc_exchange());
+    }
+  }
   SRET(dalloc(&af, static_cast<size_t>(Tmax) * H));
   SRET(dalloc(&logits_dev, static_cast<size_t>(Tmax) * c.vocab));
   if (world > 1) {
@@ -358,6 +376,49 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   SRET(dalloc(&pp_ctr, pp_pairs));
   SRET(check(cudaMemset(pp_ctr, 0, pp_pairs * sizeof(int)), "memset"));
   SRET(check(cudaStreamSynchronize(stream), "init sync"));
+  return Status::ok();
+}
+
+// Multi-process fused all-reduce: every rank's partial double buffer and ready flags mapped into
+// every other rank over CUDA IPC (handles exchanged with one ncclAllGather).
+Status Model::ipc_exchange() {
+  NcclApi* api = nccl_api(nullptr);
+  if (!api || !nccl) return Status::err(SARATHI_ENCCL, "fused all-reduce: NCCL communicator required");
+  constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
+  std::vector<unsigned char> mine(3 * kH), all(static_cast<size_t>(world) * 3 * kH);
+  void* ptrs[3] = {arbuf[0], arbuf[1], ready};
+  for (int i = 0; i < 3; ++i) {
+    cudaIpcMemHandle_t hd;
+    SRET(check(cudaIpcGetMemHandle(&hd, ptrs[i]), "cudaIpcGetMemHandle"));
+    std::memcpy(mine.data() + i * kH, &hd, kH);
+  }
+  unsigned char* dev = nullptr;
+  SRET(dalloc(&dev, all.size()));
+  SRET(check(cudaMemcpy(dev + static_cast<size_t>(rank) * 3 * kH, mine.data(), 3 * kH, cudaMemcpyHostToDevice), "H2D"));
+  if (api->allGather(dev + static_cast<size_t>(rank) * 3 * kH, dev, 3 * kH, ncclUint8, static_cast<ncclComm_t>(nccl),
+                     stream) != ncclSuccess)
+    return Status::err(SARATHI_ENCCL, "ncclAllGather (IPC handles) failed");
+  SRET(check(cudaStreamSynchronize(stream), "allgather sync"));
+  SRET(check(cudaMemcpy(all.data(), dev, all.size(), cudaMemcpyDeviceToHost), "D2H"));
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) {
+      peer_ar[0][r] = arbuf[0];
+      peer_ar[1][r] = arbuf[1];
+      peer_ready[r] = ready;
+      continue;
+    }
+    void* q[3];
+    for (int i = 0; i < 3; ++i) {
+      cudaIpcMemHandle_t hd;
+      std::memcpy(&hd, all.data() + (static_cast<size_t>(r) * 3 + i) * kH, kH);
+      SRET(check(cudaIpcOpenMemHandle(&q[i], hd, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle"));
+      ipc_opened.push_back(q[i]);
+    }
+    peer_ar[0][r] = static_cast<const __nv_bfloat16*>(q[0]);
+    peer_ar[1][r] = static_cast<const __nv_bfloat16*>(q[1]);
+    peer_ready[r] = static_cast<unsigned int*>(q[2]);
+  }
+  peers_ok = true;
   return Status::ok();
 }
 
@@ -612,18 +673,56 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
                  "dump");
   };
   NcclApi* api = world > 1 && !group ? nccl_api(nullptr) : nullptr;
-  // TP all-reduce of the bf16 partial in `ar`; ar_res = the buffer holding the sum afterwards
+  if (tp_fused && !peers_ok) {
+    if (!group || !local_group_peers(group, peer_ar, peer_ready))
+      return Status::err(SARATHI_ESTATE, "fused all-reduce: not every rank of the group is initialised");
+    peers_ok = true;
+  }
+  // TP all-reduce of a row-parallel GEMM's bf16 partial (2 per layer).  The GEMM
+  // writes to ar_target(); allreduce() then leaves in `pend` what the consuming kernel (the next
+  // RMSNorm, or the residual add) adds into h, and ar_end() runs after that consumer.
+  //   NCCL: in-place ncclAllReduce, pend = the sum.  Local group, unfused: out-of-place summing
+  //   kernel.  Fused (NEXT-1): signal the ranks' ready flags; pend = every rank's partial, summed
+  //   by the consumer over peer memory (local group: + event/barrier ordering around it).
+  PeerSum pend;
+  bool pend_end = false;
+  auto ar_target = [&]() -> __nv_bfloat16* { return tp_fused ? arbuf[ar_epoch & 1] : ar; };
   auto allreduce = [&]() -> Status {
+    if (tp_fused) {
+      const int b = static_cast<int>(ar_epoch & 1);
+      ++ar_epoch;
+      SRET(check(launch_signal_ready(peer_ready, rank, world, ar_epoch, stream), "signal"));
+      ++launches;
+      pend = PeerSum();
+      pend.world = world;
+      for (int r = 0; r < world; ++r) pend.p[r] = peer_ar[b][r];
+      pend.ready = ready;
+      pend.epoch = ar_epoch;
+      if (group) {
+        SRET(local_fused_begin(group, rank, stream));
+        pend_end = true;
+      }
+      return Status::ok();
+    }
+    pend = PeerSum();
+    pend.world = 1;
     if (group) {
-      ar_res = ar_red;
+      pend.p[0] = ar_red;
+      ++launches;
       return local_allreduce_bf16(group, rank, ar, ar_red, static_cast<size_t>(T) * H, num_sms, stream);
     }
-    ar_res = ar;
+    pend.p[0] = ar;
     ncclResult_t r = api->allReduce(ar, ar, static_cast<size_t>(T) * H, ncclBfloat16, ncclSum,
                                     static_cast<ncclComm_t>(nccl), stream);
     if (r != ncclSuccess) return Status::err(SARATHI_ENCCL, "ncclAllReduce failed");
     return Status::ok();
   };
+  auto ar_end = [&]() -> Status {  // after the consumer of `pend`
+    if (!pend_end) return Status::ok();
+    pend_end = false;
+    return local_fused_end(group, rank, stream);
+  };
+  const PeerSum no_add;
 
   cudaEvent_t ob = op_begin();
   SRET(check(launch_embedding(d_tok, emb, h, T, H, stream), "embedding"));
@@ -640,8 +739,9 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     {
       unsigned long long *sp0, *sp1;
       SRET(take_span(SARATHI_OP_RMSNORM, &sp0, &sp1));
-      SRET(check(launch_rmsnorm(h, pending_ar ? ar_res : nullptr, w.g1, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1), "rmsnorm1"));
+      SRET(check(launch_rmsnorm(h, pending_ar ? pend : no_add, w.g1, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1), "rmsnorm1"));
     }
+    if (pending_ar) SRET(ar_end());
     op_end(SARATHI_OP_RMSNORM, ob);
     ++launches;
     pending_ar = false;
@@ -832,7 +932,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       eo.ldo = H;
     } else {
       eo.mode = EPI_STORE_BF16;
-      eo.out = ar;
+      eo.out = ar_target();
       eo.ldo = H;
     }
     ob = op_begin();
@@ -847,8 +947,9 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     {
       unsigned long long *sp0, *sp1;
       SRET(take_span(SARATHI_OP_RMSNORM, &sp0, &sp1));
-      SRET(check(launch_rmsnorm(h, world > 1 ? ar_res : nullptr, w.g2, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1), "rmsnorm2"));
+      SRET(check(launch_rmsnorm(h, world > 1 ? pend : no_add, w.g2, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1), "rmsnorm2"));
     }
+    if (world > 1) SRET(ar_end());
     op_end(SARATHI_OP_RMSNORM, ob);
     ++launches;
     // FFN
@@ -866,7 +967,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       ed.ldo = H;
     } else {
       ed.mode = EPI_STORE_BF16;
-      ed.out = ar;
+      ed.out = ar_target();
       ed.ldo = H;
     }
     ob = op_begin();
@@ -880,7 +981,8 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     }
   }
   if (pending_ar && (dump_layers || !want_logits || all_rows)) {
-    SRET(check(launch_residual_add(h, ar_res, T, H, stream), "residual add"));
+    SRET(check(launch_residual_add(h, pend, T, H, stream), "residual add"));
+    SRET(ar_end());
     ++launches;
     pending_ar = false;
   }
@@ -888,7 +990,8 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   if (want_logits) {
     ob = op_begin();
     // final norm on the R logit rows (adds the pending TP partial for exactly those rows)
-    SRET(check(launch_rmsnorm(h, pending_ar ? ar_res : nullptr, gf, af, d_rows, R, H, cfg.rms_eps, stream), "final norm"));
+    SRET(check(launch_rmsnorm(h, pending_ar ? pend : no_add, gf, af, d_rows, R, H, cfg.rms_eps, stream), "final norm"));
+    if (pending_ar) SRET(ar_end());
     ++launches;
     const bool host_out = flags & SARATHI_LOGITS_HOST;
     float* target = host_out ? logits_dev : logits;
@@ -940,6 +1043,8 @@ void Model::destroy() {
     local_group_leave(group, rank);
     group = nullptr;
   }
+  for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+  ipc_opened.clear();
   for (void* p : allocations) cudaFree(p);
   allocations.clear();
   if (owns_stream && stream) cudaStreamDestroy(stream);

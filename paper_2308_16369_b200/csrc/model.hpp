@@ -41,6 +41,17 @@ Status local_allreduce_bf16(LocalGroup* g, int rank, const __nv_bfloat16* partia
                             int num_sms, cudaStream_t st);
 // dst[r * count ...] = rank r's src (ncclAllGather layout)
 Status local_allgather_f32(LocalGroup* g, int rank, const float* src, float* dst, size_t count, cudaStream_t st);
+// Fused all-reduce (NEXT-1) in a local group: register this rank's partial buffers / ready flags,
+// read the peers' (valid once every rank has initialised), and order the streams around the
+// consumer kernel (events + host barrier: the device-side flags are then always already set).
+void local_group_register(LocalGroup* g, int rank, __nv_bfloat16* const arbuf[2], unsigned int* ready);
+bool local_group_peers(LocalGroup* g, const __nv_bfloat16* peer_ar[2][8], unsigned int* peer_ready[8]);
+Status local_fused_begin(LocalGroup* g, int rank, cudaStream_t st);
+Status local_fused_end(LocalGroup* g, int rank, cudaStream_t st);
+// Publish this rank's partial of all-reduce `epoch`: ready_r[rank] = epoch on every rank r
+// (st.release.sys after a system fence; peer flags over NVLink / same device).
+cudaError_t launch_signal_ready(unsigned int* const peer_ready[8], int rank, int world, unsigned int epoch,
+                                cudaStream_t st);
 
 struct LayerWeights {
   __nv_bfloat16* qkv = nullptr;   // [(nq_l + 2 nkv_l) hd][H]
@@ -120,6 +131,18 @@ struct Model {
   __nv_bfloat16* ar_red = nullptr;        // local group: all-reduce result buffer [Tmax][H]
   const __nv_bfloat16* ar_res = nullptr;  // buffer holding the latest all-reduce result (ar or ar_red)
   bool owns_stream = false;
+  // fused TP all-reduce: the row-parallel GEMM writes its bf16 partial to
+  // arbuf[epoch & 1] (peer-visible), signals the ranks' ready flags, and the consuming RMSNorm /
+  // residual kernel sums every rank's partial over peer memory (one-shot all-reduce fused into
+  // the consumer, no NCCL call).  Double buffering makes a separate "done reading" flag unneeded.
+  bool tp_fused = false;
+  __nv_bfloat16* arbuf[2] = {nullptr, nullptr};
+  unsigned int* ready = nullptr;                 // [8] epochs published by each rank (this rank's copy)
+  const __nv_bfloat16* peer_ar[2][8] = {};       // rank r's arbuf[b]
+  unsigned int* peer_ready[8] = {};              // rank r's ready array
+  bool peers_ok = false;
+  unsigned int ar_epoch = 0;
+  std::vector<void*> ipc_opened;                 // cudaIpcOpenMemHandle mappings (multi-process)
   int64_t launches = 0;
   // I/O accounting and per-op timers
   int64_t last_h2d = 0, last_d2h = 0;
@@ -142,6 +165,7 @@ struct Model {
   // host_tensors: NULL (generate from seed) or the logical weights, see sarathi_init_model
   Status init(const sarathi_model_config& c, const sarathi_dist& d, uint64_t seed, const void* const* host_tensors);
   Status alloc_kv(int64_t num_blocks, int32_t block_size);
+  Status ipc_exchange();
   Status run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* dec, float* logits, int32_t flags);
   void destroy();
 

@@ -8,6 +8,7 @@ Checks per schedule: every rank returns bit-identical logits and per-layer resid
 all-reduce result is identical everywhere), slot mappings are bit-exact, and logits / residuals
 are within the 2e-2 contract (8e-3 regression bound) of the oracle."""
 import dataclasses
+import os
 import threading
 
 import numpy as np
@@ -28,10 +29,21 @@ def S():
     return sarathi
 
 
-def run_tp(S, cfg, reqs, world, B, C, num_blocks, block_size, weight_seed=0, max_tokens=64, host_tensors=None):
+def run_tp(S, cfg, reqs, world, B, C, num_blocks, block_size, weight_seed=0, max_tokens=64, host_tensors=None,
+           fused=True):
+    """fused: the NEXT-1 path (one-shot all-reduce fused into the consuming RMSNorm over peer
+    memory, ready flags + double-buffered partials); else the summing-kernel stand-in for NCCL."""
     g = S.LocalGroup(world)
-    models = [S.Model(S.config_from(cfg, max_tokens), seed=weight_seed, rank=r, world=world, local_group=g,
-                      host_tensors=host_tensors) for r in range(world)]
+    old = os.environ.get("SARATHI_TP_FUSED")
+    os.environ["SARATHI_TP_FUSED"] = "1" if fused else "0"
+    try:
+        models = [S.Model(S.config_from(cfg, max_tokens), seed=weight_seed, rank=r, world=world, local_group=g,
+                          host_tensors=host_tensors) for r in range(world)]
+    finally:
+        if old is None:
+            os.environ.pop("SARATHI_TP_FUSED")
+        else:
+            os.environ["SARATHI_TP_FUSED"] = old
     for m in models:
         m.alloc_kv(num_blocks, block_size)
     res = [None] * world
@@ -84,9 +96,10 @@ def _check_tp(res, cfg, weight_seed, num_blocks, block_size):
 CONFIG1 = [(1, 5, 12, 0), (2, 11, 12, 0), (3, 16, 12, 0), (0, 64, 4, 3)]
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused-ar", "sum-kernel"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_tp_tiny_config1(S, world):
-    res = run_tp(S, synth.TINY, CONFIG1, world, B=4, C=16, num_blocks=32, block_size=16)
+def test_tp_tiny_config1(S, world, fused):
+    res = run_tp(S, synth.TINY, CONFIG1, world, B=4, C=16, num_blocks=32, block_size=16, fused=fused)
     _check_tp(res, synth.TINY, 0, 32, 16)
 
 
@@ -109,14 +122,15 @@ def test_tp_gqa_gelu_and_host_weights(S, case):
         _check_tp(res, cfg, 5, 16, 16)
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused-ar", "sum-kernel"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_tp_llama13b_width_two_layers(S, world):
+def test_tp_llama13b_width_two_layers(S, world, fused):
     """LLaMA-13B width (H 5120, 40 heads, H2 13824, V 32000), 2 layers, TP 2 / 4: rank shards of
     the real shapes (TP4: 10 heads, 3456 FFN rows, 8000 vocab rows per rank) against the unsharded
     oracle; a chunked prompt with decodes riding along."""
     cfg = dataclasses.replace(synth.LLAMA_13B, name="llama13b-L2", n_layers=2, max_seq_len=512)
     reqs = [(1, 40, 3, 0), (2, 150, 2, 0)]
-    res = run_tp(S, cfg, reqs, world, B=2, C=64, num_blocks=16, block_size=64, max_tokens=80)
+    res = run_tp(S, cfg, reqs, world, B=2, C=64, num_blocks=16, block_size=64, max_tokens=80, fused=fused)
     _check_tp(res, cfg, 0, 16, 64)
 
 

@@ -337,6 +337,7 @@ __global__ void decode_combine_kernel(DecodeAttnArgs a, int HD) {
 //   Issue (TMA + UMMA) is warp 0, warp-uniform with one elected lane.
 // ---------------------------------------------------------------------------
 constexpr int kPBQ = 128;  // queries per CTA
+constexpr int kMaxKsplit = 8;  // key-range split of one (q-tile, head) pair (PrefillAttnArgs::ksplit)
 
 // MN-major SW128 UMMA smem descriptor: 64-element (128 B) rows along MN, MN atoms LBO apart,
 // 8-row K groups SBO apart (CuTe canonical ((8,n),(8,k)):((1,LBO),(8,SBO)) in 16-B units).
@@ -672,11 +673,11 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
     if (s_merge && q0 + r < p) {
       __threadfence();
       const size_t row0 = static_cast<size_t>(pq) * ksplit * kPBQ + r;  // + i * kPBQ per range
-      // ksplit <= 4 (host): every range's (m, l) and O loads are issued before they are used
-      float mi[4], li[4], wi[4];
+      // ksplit <= kMaxKsplit (host): every range's (m, l) and O loads are issued before they are used
+      float mi[kMaxKsplit], li[kMaxKsplit], wi[kMaxKsplit];
       float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < kMaxKsplit; ++i) {
         const float2 ml = i < ksplit ? __ldcg(reinterpret_cast<const float2*>(a.part_ml + 2 * (row0 + i * kPBQ)))
                                      : make_float2(-INFINITY, 0.f);
         mi[i] = ml.x;
@@ -685,7 +686,7 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
       }
       float lsum = 0.f;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < kMaxKsplit; ++i) {
         wi[i] = mi[i] == -INFINITY ? 0.f : exp2f(mi[i] - mx);  // ranges past ksplit: m = -inf
         lsum = fmaf(wi[i], li[i], lsum);
       }
@@ -693,9 +694,9 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
       __nv_bfloat16* dst = a.out + static_cast<size_t>(a.q_row0 + q0 + r) * a.out_ld + qh * HD + chh * kOC;
 #pragma unroll 2
       for (int c = 0; c < kOC; c += 8) {
-        float4 x[4][2];
+        float4 x[kMaxKsplit][2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < kMaxKsplit; ++i) {
           const float4* src = reinterpret_cast<const float4*>(a.part_o) +
                               (static_cast<size_t>(pq) * ksplit + i) * (HD / 4) * kPBQ +
                               ((chh * kOC + c) >> 2) * kPBQ + r;
@@ -704,7 +705,7 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
         }
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < kMaxKsplit; ++i) {
           const float w = wi[i] * linv;
           acc[0] = fmaf(x[i][0].x, w, acc[0]); acc[1] = fmaf(x[i][0].y, w, acc[1]);
           acc[2] = fmaf(x[i][0].z, w, acc[2]); acc[3] = fmaf(x[i][0].w, w, acc[3]);

@@ -778,6 +778,18 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
   pl.n_tiles = tt.n_tiles;
   pl.n_mma = tt.n_mma;
   pl.bn = tt.bn;
+  {
+    // few weight-row tiles (a TP rank's small M): more, narrower token tiles spread the epilogue
+    // (and the split-K reduction) over more CTA pairs; experiment knob SARATHI_GEMM_NT_SMALLM=n
+    static const int nt_small = getenv("SARATHI_GEMM_NT_SMALLM") ? atoi(getenv("SARATHI_GEMM_NT_SMALLM")) : 0;
+    const int pm = (M + 2 * kBM - 1) / (2 * kBM);
+    if (nt_small > tt.n_tiles && force_pairs == 0 && 2 * pm * tt.n_tiles < num_sms / 2) {
+      pl.n_tiles = nt_small;
+      const int per = (N + nt_small - 1) / nt_small;
+      pl.n_mma = per <= 256 ? 1 : 2;
+      pl.bn = per <= 256 ? std::max(16, (per + 15) / 16 * 16) : (per + 31) / 32 * 32;
+    }
+  }
   pl.box_rows = pl.bn / pl.n_mma / 2;  // each CTA of the pair holds half of every UMMA's tokens
   pl.pm_tiles = (M + 2 * kBM - 1) / (2 * kBM);
   pl.m_tiles = 2 * pl.pm_tiles;

@@ -806,7 +806,8 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
           ks = d > 0 ? static_cast<int>(std::ceil(est_p / std::max(est_d, 1.0))) : num_sms / pairs;
         static const int ks_env = getenv("SARATHI_PREFILL_KSPLIT") ? atoi(getenv("SARATHI_PREFILL_KSPLIT")) : 0;
         if (ks_env > 0) ks = ks_env;
-        ks = std::min({ks, 4, first_tiles, std::max(1, num_sms / pairs)});
+        static const int ks_cap = getenv("SARATHI_PREFILL_KSPLIT_MAX") ? atoi(getenv("SARATHI_PREFILL_KSPLIT_MAX")) : 4;
+        ks = std::min({ks, std::min(ks_cap, 8), first_tiles, std::max(1, num_sms / pairs)});
         if (static_cast<size_t>(pairs) * ks * 128 > pp_rows || pairs > pp_pairs) ks = 1;
         pa.ksplit = std::max(1, ks);
         pa.part_o = pp_o;

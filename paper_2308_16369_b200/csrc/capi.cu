@@ -473,8 +473,9 @@ int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t 
   if (!prepacked && (cudaMemsetAsync(wp, 0, need * 2, st) != cudaSuccess ||
                      launch_pack_weight(static_cast<const __nv_bfloat16*>(W), wp, M, K, st) != cudaSuccess))
     return fail(SARATHI_ECUDA, "op_gemm: weight packing failed");
-  CUtensorMap mw, mx;
-  if (!make_tmap_weight(&mw, prepacked ? W : wp, M, K) || !make_tmap_bf16(&mx, X, N, K, K, pl.box_rows))
+  CUtensorMap mw, mx, mx2;
+  if (!make_tmap_weight(&mw, prepacked ? W : wp, M, K) || !make_tmap_bf16(&mx, X, N, K, K, pl.box_rows) ||
+      !make_tmap_bf16(&mx2, X, N, K, K, pl.box_rows2))
     return fail(SARATHI_ECUDA, "op_gemm: tensor map encode failed");
   EpiParams ep;
   ep.mode = mode;
@@ -491,7 +492,7 @@ int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t 
     cudaMemsetAsync(trace, 0, 4096 * 8, st);
     ep.trace = trace;
   }
-  const cudaError_t e = launch_gemm(mw, mx, pl, ep, st);
+  const cudaError_t e = launch_gemm(mw, mx, mx2, pl, ep, st);
   if (tracing) {
     cudaStreamSynchronize(st);
     dump_gemm_trace(trace, pl);

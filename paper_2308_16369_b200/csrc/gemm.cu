@@ -59,6 +59,7 @@ struct KParams {
   int red_partials;       // split tiles accumulate in ONE zeroed fp32 slot by red.add (many contributors)
   uint32_t tmem_cols;
   uint32_t ring_bytes;
+  int n0, n1;             // tokens of UMMA 0 / 1 per k-step (n_mma == 2: equal halves, or 256 + tail)
 };
 
 SARATHI_DEVICE float silu_f(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
@@ -310,7 +311,8 @@ SARATHI_DEVICE void epi_emit(const KParams& p, const EpiParams& ep, float (&v)[1
 
 template <int NEH, int MODE, bool DBG>
 __global__ void __launch_bounds__(threads_of<NEH>(), 1)
-    gemm_bf16_pair(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, const KParams p,
+    gemm_bf16_pair(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX,
+                   const __grid_constant__ CUtensorMap mapX2, const KParams p,
                    const EpiParams ep) {
   constexpr int kEpiThreads = 128 * NEH;
   extern __shared__ uint8_t smem_raw[];
@@ -354,6 +356,7 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapW);
     tma_prefetch_desc(&mapX);
+    if (p.n0 != p.n1) tma_prefetch_desc(&mapX2);
   }
   if (warp == 1) tmem_alloc_pair(holder, p.tmem_cols);
   tc_fence_before();
@@ -366,7 +369,9 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
   // (2s mod 3, 2s+1 mod 3) of ni columns, so segment s+1 only needs the first half of segment s's
   // accumulator drained (its other slot was freed a segment earlier) and the next mainloop overlaps
   // most of the epilogue.  Otherwise: two 256-column buffers (bn <= 256) or one.
-  const bool ring = p.n_mma == 2 && 3 * ni <= 512;
+  // uneven split (n0 = 256 + a 16..240-token tail n1, single accumulator): one full-width UMMA plus
+  // a narrow one instead of two halves, for single-segment plans (no epilogue overlap to keep)
+  const bool ring = p.n_mma == 2 && p.n0 == p.n1 && 3 * ni <= 512;
   if (warp != 0) griddep_wait();  // the producer waits after prefetching its first W tiles
 
   if (warp == 0) {
@@ -412,10 +417,12 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
             // W tile: the contiguous 16 KB pre-swizzled tile as 32 rows x 512 B (unswizzled map)
             if (!(DBG && (ep.dbg & 2))) tma_load_2d_pair_warp(a, &mapW, &full[s], 0, wrow, pol_w);
           }
-          if (!(DBG && (ep.dbg & 1)))
-            for (int j = 0; j < p.n_mma; ++j)
-              tma_load_2d_pair_warp(b + j * (ni / 2) * kBK * 2, &mapX, &full[s], kb * kBK,
-                                    nt * p.bn + j * ni + static_cast<int>(rank) * (ni / 2), pol_x);
+          if (!(DBG && (ep.dbg & 1))) {
+            tma_load_2d_pair_warp(b, &mapX, &full[s], kb * kBK, nt * p.bn + static_cast<int>(rank) * (p.n0 / 2), pol_x);
+            if (p.n_mma == 2)
+              tma_load_2d_pair_warp(b + (p.n0 / 2) * kBK * 2, p.n0 == p.n1 ? &mapX : &mapX2, &full[s], kb * kBK,
+                                    nt * p.bn + p.n0 + static_cast<int>(rank) * (p.n1 / 2), pol_x);
+          }
           if ((DBG ? ep.trace : nullptr) && tb < 2 && i < 256 && lane == 0) (DBG ? ep.trace : nullptr)[tb * 1024 + i] = globaltimer_ns();
           if (++s == p.stages) {
             s = 0;
@@ -428,7 +435,8 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader, lane 0) / stage relay (peer) ----------------
     if (rank == 0) {
-      const uint32_t idesc = make_idesc_bf16_f32(2 * kBM, ni);
+      const uint32_t idesc = make_idesc_bf16_f32(2 * kBM, p.n0);
+      const uint32_t idesc1 = make_idesc_bf16_f32(2 * kBM, p.n1);
       int i = 0, seg = 0, s = 0;
       uint32_t ph = 0;
       SegIter it;
@@ -452,7 +460,7 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
         } else {
           mbar_wait_cluster(&tempty[buf], (use & 1) ^ 1);  // both CTAs' epilogues drained it
           d0 = tmem + buf * 256;
-          d1 = d0 + ni;
+          d1 = d0 + p.n0;
           tb_idx = buf;
         }
         tc_fence_after();
@@ -470,7 +478,7 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
               umma_f16_ss_pair_warp(d0, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc, acc);
               if (p.n_mma == 2)
                 umma_f16_ss_pair_warp(d1, make_desc_k_sw128(a + k * 32),
-                                      make_desc_k_sw128(b + (ni / 2) * 128 + k * 32), idesc, acc);
+                                      make_desc_k_sw128(b + (p.n0 / 2) * 128 + k * 32), idesc1, acc);
             }
             umma_commit_pair_mc_warp(&empty[s], 0x3);
             if (kb == kb1 - 1) umma_commit_pair_mc_warp(&tfull[tb_idx], 0x3);
@@ -779,11 +787,19 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
   pl.n_mma = tt.n_mma;
   pl.bn = tt.bn;
   {
-    // few weight-row tiles (a TP rank's small M): more, narrower token tiles spread the epilogue
-    // (and the split-K reduction) over more CTA pairs; experiment knob SARATHI_GEMM_NT_SMALLM=n
-    static const int nt_small = getenv("SARATHI_GEMM_NT_SMALLM") ? atoi(getenv("SARATHI_GEMM_NT_SMALLM")) : 0;
+    // Few weight-row tiles (a TP rank's small M) or, for residual adds, a short K: two token
+    // tiles spread the exposed epilogue (and halve the split-K red.add volume) over twice the CTA
+    // pairs.  Measured (tools/shard_step.py, profiles/r02_shard_step.txt): LLaMA-2-70B TP-8 rank
+    // QKV 37.9 -> 26.4 us, O 13.6 -> 11.7, gate||up 51.8 -> 44.6 (per layer 172.7 -> 158.8 us);
+    // but the 13B TP-1 O / down (K = 5120 / 13824) got slower (23.8 -> 30.8, 46 -> 72 us), hence
+    // the K bound for residual adds.  SARATHI_GEMM_NT_SMALLM=n overrides the split (0 = off).
+    static const int nt_small = getenv("SARATHI_GEMM_NT_SMALLM") ? atoi(getenv("SARATHI_GEMM_NT_SMALLM")) : 2;
     const int pm = (M + 2 * kBM - 1) / (2 * kBM);
-    if (nt_small > tt.n_tiles && force_pairs == 0 && 2 * pm * tt.n_tiles < num_sms / 2) {
+    // (GPT-3 TP-8 rank, K = 12288: QKV 52.6 -> 55.4, gate 53.6 -> 65.9 us with the split, so long
+    // K keeps the full token tile: the mainloop dominates and narrow UMMAs cost more than the
+    // epilogue saves)
+    const bool small = atomic_epilogue ? KB <= 32 : (2 * pm * tt.n_tiles < num_sms / 2 && KB <= 128);
+    if (nt_small > tt.n_tiles && force_pairs == 0 && small) {
       pl.n_tiles = nt_small;
       const int per = (N + nt_small - 1) / nt_small;
       pl.n_mma = per <= 256 ? 1 : 2;
@@ -791,6 +807,8 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
     }
   }
   pl.box_rows = pl.bn / pl.n_mma / 2;  // each CTA of the pair holds half of every UMMA's tokens
+  pl.n0 = pl.n1 = pl.bn / pl.n_mma;
+  pl.box_rows2 = pl.box_rows;
   pl.pm_tiles = (M + 2 * kBM - 1) / (2 * kBM);
   pl.m_tiles = 2 * pl.pm_tiles;
   const int tiles = pl.pm_tiles * pl.n_tiles;
@@ -877,6 +895,28 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
   pl.kb_per_split = pl.splits;
   pl.ws_floats = units > 0 && !atomic_epilogue && !pl.red_partials ? tiles128 * max_slots * tile_elems : 0;
   pl.nbuf = pl.bn <= 256 ? 2 : 1;
+  // Uneven split for 256 < T <= 512 when every pair runs ONE segment (nothing to overlap a second
+  // accumulator with): UMMA 0 takes 256 tokens, UMMA 1 the 16-multiple tail, so T = 257 costs
+  // 256 + 16 token columns instead of 2 x 144 (the B200 form of the paper's tile quantization,
+  // P:L457-463).  SARATHI_GEMM_UNEVEN=0 keeps the equal halves.
+  {
+    static const bool uneven_on = !(getenv("SARATHI_GEMM_UNEVEN") && atoi(getenv("SARATHI_GEMM_UNEVEN")) == 0);
+    int max_segs = 0;
+    for (int c = 0; c < pl.ctas; ++c) {
+      const long long u0 = static_cast<long long>(c) * pl.units / pl.ctas, u1 = static_cast<long long>(c + 1) * pl.units / pl.ctas;
+      const int sk = u1 > u0 ? static_cast<int>((u1 - 1) / KB - u0 / KB + 1) : 0;
+      max_segs = std::max(max_segs, sk + pl.dp_per_pair + (c < pl.dp_extra ? 1 : 0));
+    }
+    const int per = (N + pl.n_tiles - 1) / pl.n_tiles;
+    if (uneven_on && pl.n_mma == 2 && pl.n_tiles == 1 && max_segs <= 1 && per > 256 && per <= 512) {
+      pl.n0 = 256;
+      pl.n1 = std::max(16, (per - 256 + 15) / 16 * 16);
+      pl.bn = pl.n0 + pl.n1;
+      pl.box_rows = 128;
+      pl.box_rows2 = pl.n1 / 2;
+      pl.nbuf = 1;
+    }
+  }
   const size_t stage = kABytes + static_cast<size_t>(pl.bn / 2) * kBK * 2;
   const size_t budget = 226 * 1024 - 1024 - extra_smem(pl.bn);
   pl.stages = static_cast<int>(std::max<size_t>(2, std::min<size_t>(8, budget / stage)));
@@ -934,11 +974,11 @@ void dump_gemm_trace(const unsigned long long* trace_dev, const GemmPlan& pl) {
             sgm < 32 && h[736 + sgm] ? (h[736 + sgm] - t0) * 1e-3 : -1.0);
 }
 
-cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const GemmPlan& pl, const EpiParams& ep,
-                        cudaStream_t stream) {
+cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const CUtensorMap& mapX2, const GemmPlan& pl,
+                        const EpiParams& ep, cudaStream_t stream) {
   // one kernel per (epilogue mode, debug) so the epilogue has no runtime mode switch (smaller code,
   // fewer branches); debug/trace instrumentation only in the DBG instantiations
-  using KFn = void (*)(const CUtensorMap, const CUtensorMap, const KParams, const EpiParams);
+  using KFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const KParams, const EpiParams);
   static const KFn table[2][6] = {
       {gemm_bf16_pair<kNEH, 0, false>, gemm_bf16_pair<kNEH, 1, false>, gemm_bf16_pair<kNEH, 2, false>,
        gemm_bf16_pair<kNEH, 3, false>, gemm_bf16_pair<kNEH, 4, false>, gemm_bf16_pair<kNEH, 5, false>},
@@ -971,6 +1011,8 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   kp.tiles = pl.tiles;
   kp.stages = pl.stages;
   kp.nbuf = pl.nbuf;
+  kp.n0 = pl.n0;
+  kp.n1 = pl.n1;
   kp.max_slots = pl.max_slots;
   kp.red_partials = pl.red_partials;
   kp.tmem_cols = (pl.nbuf == 2 || (pl.n_mma == 2 && 3 * (pl.bn / 2) <= 512)) ? 512 : pow2_cols(pl.bn);
@@ -989,7 +1031,7 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, fn, mapW, mapX, kp, ep);
+  return cudaLaunchKernelEx(&cfg, fn, mapW, mapX, mapX2, kp, ep);
 }
 
 }  // namespace sarathi

@@ -46,7 +46,9 @@ struct GemmPlan {
   int M = 0, N = 0, K = 0;
   int bn = 0;          // tokens per tile (multiple of 16, <= 512)
   int n_mma = 1;       // UMMAs per k-step (bn / n_mma <= 256 tokens each)
-  int box_rows = 0;    // X TMA box rows (per CTA of the pair: half of one UMMA's tokens)
+  int box_rows = 0;    // X TMA box rows (per CTA of the pair: half of UMMA 0's tokens)
+  int n0 = 0, n1 = 0;  // tokens of UMMA 0 / 1 (n_mma == 2); uneven (256 + tail) for single-segment plans
+  int box_rows2 = 0;   // X box rows of UMMA 1 (n1 / 2) when the split is uneven
   int pm_tiles = 0;    // 256-row tiles (one per CTA pair)
   int m_tiles = 0, n_tiles = 0;  // 128-row tiles (2 * pm_tiles), token tiles
   long long units = 0; // stream-K (pair tile, k-block) units = sk_tiles * K/64
@@ -81,8 +83,9 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
 // is read as 32 rows x 512 B (unswizzled box; the bytes are already the SW128 smem image).
 bool make_tmap_weight(CUtensorMap* map, const void* w, int M, int K);
 // mapW: make_tmap_weight map; mapX: activation [N][K] map (make_tmap_bf16, box rows plan.box_rows).
-cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const GemmPlan& plan, const EpiParams& ep,
-                        cudaStream_t stream);
+// mapX2: X map with box rows plan.box_rows2 (uneven split), else ignored (may equal mapX)
+cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const CUtensorMap& mapX2, const GemmPlan& plan,
+                        const EpiParams& ep, cudaStream_t stream);
 
 // Debug: prints the globaltimer trace (EpiParams.trace, 4096 u64) of the first CTA pair to stderr.
 void dump_gemm_trace(const unsigned long long* trace_dev, const GemmPlan& plan);

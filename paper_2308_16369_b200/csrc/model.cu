@@ -483,13 +483,20 @@ Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, 
   auto it = plans.find(pk);
   if (it == plans.end()) it = plans.emplace(pk, plan_gemm(M, N, K, num_sms, gemm_ws_floats, 0, atomic)).first;
   const GemmPlan& pl = it->second;
-  auto xk = std::make_tuple(X, N, K, pl.box_rows);
-  auto xi = xmaps.find(xk);
-  if (xi == xmaps.end()) {
-    CUtensorMap m;
-    if (!make_tmap_bf16(&m, X, N, K, ldx, pl.box_rows)) return Status::err(SARATHI_ECUDA, "tensor map (activation)");
-    xi = xmaps.emplace(xk, m).first;
-  }
+  auto xmap = [&](int box_rows, const CUtensorMap** out) -> Status {
+    auto xk = std::make_tuple(X, N, K, box_rows);
+    auto xi = xmaps.find(xk);
+    if (xi == xmaps.end()) {
+      CUtensorMap m;
+      if (!make_tmap_bf16(&m, X, N, K, ldx, box_rows)) return Status::err(SARATHI_ECUDA, "tensor map (activation)");
+      xi = xmaps.emplace(xk, m).first;
+    }
+    *out = &xi->second;
+    return Status::ok();
+  };
+  const CUtensorMap *mx = nullptr, *mx2 = nullptr;
+  SRET(xmap(pl.box_rows, &mx));
+  SRET(xmap(pl.box_rows2, &mx2));
   EpiParams ep = ep_in;
   ep.ws = gemm_ws;
   ep.ws_red = gemm_ws + gemm_ws_floats / 2;
@@ -507,13 +514,13 @@ Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, 
     cudaMemsetAsync(tr, 0, 4096 * 8, stream);
     ep.trace = tr;
     if (const char* d = getenv("SARATHI_GEMM_DBG")) ep.dbg = atoi(d);  // traced launch only
-    const Status st = check(launch_gemm(mw, xi->second, pl, ep, stream), "gemm launch");
+    const Status st = check(launch_gemm(mw, *mx, *mx2, pl, ep, stream), "gemm launch");
     cudaStreamSynchronize(stream);
     dump_gemm_trace(tr, pl);
     cudaFree(tr);
     return st;
   }
-  return check(launch_gemm(mw, xi->second, pl, ep, stream), "gemm launch");
+  return check(launch_gemm(mw, *mx, *mx2, pl, ep, stream), "gemm launch");
 }
 
 cudaEvent_t Model::op_begin(cudaStream_t s) {

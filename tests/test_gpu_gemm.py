@@ -27,6 +27,8 @@ def _int_operands(M, N, K, seed):
 SHAPES = [
     (128, 16, 64, 0), (128, 1, 64, 0), (256, 320, 5120, 1), (256, 320, 5120, 4), (384, 7, 128, 0),
     (200, 37, 192, 0), (128, 600, 256, 0), (1280, 282, 8192, 0), (512, 257, 1024, 3), (640, 512, 640, 2),
+    # 256 < N <= 512 with one segment per CTA pair: the uneven split (UMMA N = 256 + 16-multiple tail)
+    (256, 257, 256, 0), (768, 300, 512, 0), (256, 497, 128, 0), (5120, 272, 1024, 0),
 ]
 
 

@@ -8,8 +8,18 @@ N = n_factor * B requests arrive at t = 0.  The same C-ABI model and host schedu
   * request_level  : the baseline — each prompt as its own prefill-only batch, then decode-only
                      batches of the running cohort
   * orca_best      : iteration-level batching with whole prompts (Orca best case)
+  * sarathi_b200   : sarathi with the chunk chosen per iteration by sarathi_chunk_advice (B200
+                     tile-quantization rule)
 End-to-end throughput = sum_r (P_r + D_r) / makespan (wall clock around the whole run, device
 synchronised at the end; every batch also computes the LM head for its returned rows).
+
+Roofline counterfactual (round 2): every iteration's composition (chunk p at prefix s, decode
+contexts) is also priced at the machine's roofline with the measured peaks (MEASURED_PEAKS.json:
+sustained bf16 tensor FLOP/s, HBM copy GB/s): per layer max(2 T W / F, 2 W / B) for the linears +
+max(FLOPs / F, KV bytes / B) for the chunk's attention + decode KV bytes / B, plus the LM head.
+roofline tokens/s = sum_r (P_r + D_r) / sum of the iterations' roofline times.  The ratio of
+policies at roofline says what the machine balance alone predicts; the measured ratio what this
+implementation achieves.
 
     python tools/e2e_policies.py [--model llama-33b] [--lengths 1024] [--pd 10] [--n-factor 2]
 """
@@ -23,14 +33,35 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def run_policy(S, synth, torch, m, cfg, policy, P, D, N, B, C, num_blocks, bs, stream):
-    sched = S.Scheduler(B, C, num_blocks, bs, policy=policy)
+def roofline_iter_s(cfg, p, s, dec_ctx, peaks):
+    """Roofline time of one hybrid batch on one GPU (seconds)."""
+    F = peaks["bf16_tflops_sustained"] * 1e12
+    Bw = peaks["hbm_gbs"] * 1e9
+    W = cfg.params_per_layer()
+    T = p + len(dec_ctx)
+    hd, nq, nkv = cfg.head_dim, cfg.n_heads, cfg.n_kv_heads
+    t_lin = max(2.0 * T * W / F, 2.0 * W / Bw)
+    t_pre = 0.0
+    if p:
+        fl = 4.0 * hd * nq * (p * s + p * (p + 1) / 2)
+        by = (s + p) * 2 * nkv * hd * 2
+        t_pre = max(fl / F, by / Bw)
+    t_dec = sum(dec_ctx) * 2 * nkv * hd * 2 / Bw
+    R = len(dec_ctx) + (1 if p else 0)
+    t_head = max(2.0 * R * cfg.vocab * cfg.hidden / F, 2.0 * cfg.vocab * cfg.hidden / Bw)
+    return cfg.n_layers * (t_lin + t_pre + t_dec) + t_head
+
+
+def run_policy(S, synth, torch, m, cfg, policy, P, D, N, B, C, num_blocks, bs, stream, peaks=None):
+    policy, tile = policy if isinstance(policy, tuple) else (policy, 0)
+    sched = S.Scheduler(B, C, num_blocks, bs, policy=policy, tile_adjust=tile)
     for r in range(N):
         sched.submit(r, P, D, 0)
     logits = torch.empty((B + 1, cfg.vocab), dtype=torch.float32, device="cuda")
     V = cfg.vocab
     tok = lambda r, a, n=1: synth.tokens(11, r, a, n, V)
     iters = 0
+    roof = 0.0
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     while not sched.done():
@@ -45,10 +76,12 @@ def run_policy(S, synth, torch, m, cfg, policy, P, D, N, B, C, num_blocks, bs, s
         decodes = [(rid, int(tok(rid, pos)[0]), pos) for rid, pos in decs]
         m.run_hybrid_batch(prefill, decodes, logits_ptr=logits.data_ptr())
         iters += 1
+        if peaks:
+            roof += roofline_iter_s(cfg, pre[2] if pre else 0, pre[1] if pre else 0, [pos + 1 for _, pos in decs], peaks)
         for rid in sched.complete():
             m.request_free(rid)
     torch.cuda.synchronize()
-    return time.perf_counter() - t0, iters
+    return time.perf_counter() - t0, iters, roof
 
 
 def main():
@@ -68,7 +101,9 @@ def main():
     cfg = synth.CONFIGS[args.model]
     stream = torch.cuda.Stream()
     bs = 64
-    pol = {"sarathi": S.POLICY_SARATHI, "request_level": S.POLICY_REQUEST_LEVEL, "orca_best": S.POLICY_ORCA_BEST}
+    pol = {"sarathi": S.POLICY_SARATHI, "request_level": S.POLICY_REQUEST_LEVEL, "orca_best": S.POLICY_ORCA_BEST,
+           "sarathi_b200": (S.POLICY_SARATHI, 2)}  # chunk per iteration by the B200 advisor
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     rows = []
     for L in args.lengths:
         m = S.Model(S.config_from(cfg, max_tokens_per_batch=max(L, args.chunk) + 512), seed=0, stream=stream.cuda_stream)
@@ -81,10 +116,12 @@ def main():
             P, D = synth.split_pd(L, r)
             res = {}
             for name in args.policies:
-                wall, iters = run_policy(S, synth, torch, m, cfg, pol[name], P, D, N, B, args.chunk, num_blocks, bs,
-                                         stream)
+                wall, iters, roof = run_policy(S, synth, torch, m, cfg, pol[name], P, D, N, B, args.chunk, num_blocks,
+                                               bs, stream, peaks)
                 res[name] = {"makespan_s": round(wall, 3), "iterations": iters,
-                             "tokens_per_s": round(N * (P + D) / wall, 1)}
+                             "tokens_per_s": round(N * (P + D) / wall, 1),
+                             "roofline_tokens_per_s": round(N * (P + D) / roof, 1),
+                             "frac_of_roofline": round(roof / wall, 3)}
             row = {"model": args.model, "length": L, "pd_ratio": r, "P": P, "D": D, "B": B, "N": N,
                    "chunk": args.chunk, **res}
             if "request_level" in res:
@@ -92,6 +129,8 @@ def main():
                     if name != "request_level":
                         row[f"speedup_{name}_vs_request_level"] = round(res[name]["tokens_per_s"] /
                                                                          res["request_level"]["tokens_per_s"], 3)
+                        row[f"roofline_speedup_{name}_vs_request_level"] = round(
+                            res[name]["roofline_tokens_per_s"] / res["request_level"]["roofline_tokens_per_s"], 3)
             rows.append(row)
             print(json.dumps(row), flush=True)
         m.close()

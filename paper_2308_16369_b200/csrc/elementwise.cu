@@ -72,6 +72,15 @@ __device__ __forceinline__ void peer_wait(const PeerSum& ps) {
 // sum over ranks (rank order, fp32) of 4 consecutive bf16 partial values at element offset i
 __device__ __forceinline__ float4 peer_sum4(const PeerSum& ps, size_t i) {
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (ps.mm) {  // NVLS: the switch returns the rank sum (fp32 accumulate, bf16 result)
+    uint32_t r0, r1;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v2.bf16x2 {%0, %1}, [%2];"
+                 : "=r"(r0), "=r"(r1)
+                 : "l"(ps.mm + i)
+                 : "memory");
+    const float2 a0 = unpack_bf16x2(r0), a1 = unpack_bf16x2(r1);
+    return make_float4(a0.x, a0.y, a1.x, a1.y);
+  }
   for (int r = 0; r < ps.world; ++r) {
     const uint2 raw = *reinterpret_cast<const uint2*>(ps.p[r] + i);
     const float2 a0 = unpack_bf16x2(raw.x), a1 = unpack_bf16x2(raw.y);

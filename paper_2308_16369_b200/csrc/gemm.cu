@@ -166,6 +166,15 @@ SARATHI_DEVICE QkvLane qkv_lane(const EpiParams& ep, int mt, uint32_t q, uint32_
   return o;
 }
 
+// Orders later uses of r after a preceding tcgen05.wait::ld (a second in-flight load's registers).
+SARATHI_DEVICE void regs_fence(uint32_t (&r)[16]) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+}
+
 SARATHI_DEVICE void red_add_v4(float* addr, float4 v) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
@@ -578,7 +587,52 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
       tc_fence_after();
       if ((DBG ? ep.trace : nullptr) && tb < 2 && et == 0 && seg < 64) (DBG ? ep.trace : nullptr)[tb * 1024 + 512 + seg] = globaltimer_ns();
       const uint32_t trow = tmem + ((quarter * 32u) << 16);
-      if (direct) {
+      // TMEM drain with TWO of this warp's chunks in flight (one tcgen05.wait::ld per pair of
+      // chunks): for epilogues whose per-chunk work is shorter than a TMEM load round trip
+      // (partials, residual adds, plain stores), the drain would otherwise be latency-bound
+      auto drain2 = [&](auto&& body) {
+        if (eh >= nchunks) {
+          release_tmem();
+          return;
+        }
+        uint32_t ra[16], rb[16];
+        const bool hb = eh + NEH < nchunks;
+        tmem_ld_32x32b_x16(trow + tcol(eh), ra);
+        if (hb) tmem_ld_32x32b_x16(trow + tcol(eh + NEH), rb);
+        tmem_ld_wait_regs(ra);
+        regs_fence(rb);
+        after_load(eh);
+        if (hb) after_load(eh + NEH);
+        for (int ch = eh; ch < nchunks; ch += 2 * NEH) {
+          uint32_t na[16], nb[16];
+          const int c2 = ch + 2 * NEH, c3 = ch + 3 * NEH;
+          const bool m2 = c2 < nchunks, m3 = c3 < nchunks;
+          if (m2) tmem_ld_32x32b_x16(trow + tcol(c2), na);
+          if (m3) tmem_ld_32x32b_x16(trow + tcol(c3), nb);
+          body(ch, ra);
+          if (ch + NEH < nchunks) body(ch + NEH, rb);
+          if (m2) {
+            tmem_ld_wait_regs(na);
+            regs_fence(nb);
+            after_load(c2);
+            if (m3) after_load(c3);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              ra[j] = na[j];
+              rb[j] = nb[j];
+            }
+          }
+        }
+      };
+      constexpr bool kDeepDrain = MODE == EPI_ADD_F32 || MODE == EPI_STORE_F32 || MODE == EPI_STORE_BF16;
+      if (direct && kDeepDrain && !DBG) {
+        drain2([&](int ch, uint32_t (&raw)[16]) {
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
+          epi_emit<MODE, DBG>(p, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql);
+        });
+      } else if (direct) {
         // software-pipelined TMEM drain: this warp's next chunk (ch + NEH) is in flight while ch is emitted
         if (eh >= nchunks) {
           release_tmem();
@@ -622,35 +676,18 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
         const size_t qoff = static_cast<size_t>(quarter) * 512 + lane * 4;  // + (ch * 4 * 512) + j * 128
         float* wsp = p.red_partials ? ep.ws_red + tile128 * tile_elems + qoff
                                     : ep.ws + (tile128 * p.max_slots + slot) * tile_elems + qoff;
-        if (eh >= nchunks) {
-          release_tmem();
-        } else {
-          // TMEM drain pipelined like the direct path; TMEM is released right after the last load
-          uint32_t raw[16];
-          tmem_ld_32x32b_x16(trow + tcol(eh), raw);
-          tmem_ld_wait_regs(raw);
-          after_load(eh);
-          for (int ch = eh; ch < nchunks; ch += NEH) {
-            uint32_t nraw[16];
-            const bool more = ch + NEH < nchunks;
-            if (more) tmem_ld_32x32b_x16(trow + tcol(ch + NEH), nraw);
+        // TMEM is released right after the last load (drain2)
+        drain2([&](int ch, uint32_t (&raw)[16]) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float4 x = make_float4(__uint_as_float(raw[4 * j]), __uint_as_float(raw[4 * j + 1]),
-                                           __uint_as_float(raw[4 * j + 2]), __uint_as_float(raw[4 * j + 3]));
-              if (p.red_partials)
-                red_add_v4(wsp + ch * 2048 + j * 128, x);
-              else
-                __stcg(reinterpret_cast<float4*>(wsp + ch * 2048 + j * 128), x);
-            }
-            if (more) {
-              tmem_ld_wait_regs(nraw);
-              after_load(ch + NEH);
-#pragma unroll
-              for (int j = 0; j < 16; ++j) raw[j] = nraw[j];
-            }
+          for (int j = 0; j < 4; ++j) {
+            const float4 x = make_float4(__uint_as_float(raw[4 * j]), __uint_as_float(raw[4 * j + 1]),
+                                         __uint_as_float(raw[4 * j + 2]), __uint_as_float(raw[4 * j + 3]));
+            if (p.red_partials)
+              red_add_v4(wsp + ch * 2048 + j * 128, x);
+            else
+              __stcg(reinterpret_cast<float4*>(wsp + ch * 2048 + j * 128), x);
           }
-        }
+        });
         if ((DBG ? ep.trace : nullptr) && tb < 2 && et == 0 && seg < 32) (DBG ? ep.trace : nullptr)[tb * 1024 + 704 + seg] = globaltimer_ns();
         __threadfence();
         named_bar_sync(1, kEpiThreads);

@@ -89,6 +89,9 @@ struct PeerSum {
   int world = 0;
   const unsigned int* ready = nullptr;
   unsigned int epoch = 0;
+  // NVLS: multicast address of the partial buffer; the sum over ranks is ONE
+  // multimem.ld_reduce.add.acc::f32 per 4 bf16 (reduced in the NVSwitch) instead of world loads
+  const __nv_bfloat16* mm = nullptr;
 };
 
 // h[t][:] = float(E[tok[t]][:])

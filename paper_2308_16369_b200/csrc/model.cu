@@ -342,8 +342,13 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   {
     const char* fe = getenv("SARATHI_TP_FUSED");
     tp_fused = world > 1 && (group ? !(fe && fe[0] == '0') : (fe && fe[0] == '1'));
+    const char* nv = getenv("SARATHI_TP_NVLS");
+    tp_nvls = world > 1 && !group && nv && nv[0] == '1';
   }
-  if (tp_fused) {
+  if (tp_nvls) {
+    tp_fused = true;
+    SRET(nvls_setup(*this));
+  } else if (tp_fused) {
     SRET(dalloc(&arbuf[0], static_cast<size_t>(Tmax) * H));
     SRET(dalloc(&arbuf[1], static_cast<size_t>(Tmax) * H));
     SRET(dalloc(&ready, 8));
@@ -705,6 +710,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       for (int r = 0; r < world; ++r) pend.p[r] = peer_ar[b][r];
       pend.ready = ready;
       pend.epoch = ar_epoch;
+      pend.mm = tp_nvls ? mm_ar[b] : nullptr;
       if (group) {
         SRET(local_fused_begin(group, rank, stream));
         pend_end = true;
@@ -1042,6 +1048,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
 
 void Model::destroy() {
   if (stream) cudaStreamSynchronize(stream);
+  if (nvls) nvls_teardown(*this);
   if (nccl) {
     NcclApi* api = nccl_api(nullptr);
     if (api) api->commDestroy(static_cast<ncclComm_t>(nccl));

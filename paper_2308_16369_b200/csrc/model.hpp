@@ -143,6 +143,11 @@ struct Model {
   bool peers_ok = false;
   unsigned int ar_epoch = 0;
   std::vector<void*> ipc_opened;                 // cudaIpcOpenMemHandle mappings (multi-process)
+  // NVLS variant (nvls.cu, SARATHI_TP_NVLS=1): partials + flags in an NCCL symmetric window,
+  // the consumer reads the rank sum through the window's multimem address
+  bool tp_nvls = false;
+  void* nvls = nullptr;                          // NvlsState
+  const __nv_bfloat16* mm_ar[2] = {nullptr, nullptr};
   int64_t launches = 0;
   // I/O accounting and per-op timers
   int64_t last_h2d = 0, last_d2h = 0;
@@ -180,5 +185,7 @@ struct Model {
 };
 
 int nccl_unique_id(void* out128, std::string* err);
+Status nvls_setup(Model& m);
+void nvls_teardown(Model& m);
 
 }  // namespace sarathi

@@ -193,3 +193,16 @@ def test_b200_chunk_advisor_hand_cases_and_cpp_twin(S):
                 assert S.chunk_advice(C, d, rem) == osch.b200_chunk(C, d, rem), (C, d, rem)
     for T in range(1, 1600):
         assert S.token_capacity(T)[0] == cap(T), T
+
+
+def test_library_sass_is_blackwell_native(S):
+    """The built library runs on sm_100a tensor-core / TMA / TMEM instructions (tcgen05.mma ->
+    UTCHMMA incl. the CTA-pair form, cp.async.bulk.tensor -> UTMALDG, tcgen05.ld -> LDTM) and
+    the NVLS all-reduce consumer compiles to multimem.ld_reduce (LDGMC)."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    sass = subprocess.run([exe, "-sass", S.LIB_PATH], capture_output=True, text=True).stdout
+    for op in ("UTCHMMA.2CTA", "UTMALDG.2D.2CTA", "LDTM", "LDGMC"):
+        assert op in sass, op
+    assert "sm_100a" in subprocess.run([exe, "-lelf", S.LIB_PATH], capture_output=True, text=True).stdout

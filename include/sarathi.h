@@ -75,6 +75,10 @@ typedef struct {
   const void* nccl_unique_id; /* 128 bytes, or NULL when world == 1 or local_group set */
   void* stream;               /* cudaStream_t all device work is enqueued on            */
   void* local_group;          /* sarathi_local_group* (world > 1 on ONE device), or NULL */
+  int32_t pp_stage;           /* pipeline stage of this handle (0-based); 0 with pp_stages <= 1   */
+  int32_t pp_stages;          /* pipeline stages (0 or 1 = no pipeline); stage s holds layers     */
+                              /* [floor(L s / S), floor(L (s+1) / S)), the first also the         */
+                              /* embedding, the last the final norm + LM head (NEXT-4)            */
 } sarathi_dist;
 
 /* Local tensor-parallel group: `world` (2..8) model handles created on the SAME device with
@@ -179,6 +183,15 @@ int sarathi_run_hybrid_batch(sarathi_model* m, const sarathi_prefill_chunk* pref
  * slots are overwritten by subsequent appends.  Used to replay one fixed batch composition in
  * benchmarks.  EUNKNOWN_REQ, EINVAL. */
 int sarathi_request_truncate(sarathi_model* m, int64_t req_id, int32_t new_len);
+
+/* Pipeline parallelism (§3.2 / L1-19 §5.3): a stage > 0 takes
+ * its input residual stream from the previous stage.  sarathi_stage_input: h_dev = fp32 [T][H]
+ * device memory (the previous stage's sarathi_stage_output, or a copy of it on this device),
+ * read by the next run_hybrid_batch (which must carry the same batch).  sarathi_stage_output:
+ * this stage's residual stream after its last layer for the last batch (valid until the next run on
+ * this handle; TP partials already added).  Stages before the last return no logits.  EINVAL. */
+int sarathi_stage_input(sarathi_model* m, const float* h_dev);
+int sarathi_stage_output(const sarathi_model* m, const float** h_dev, int32_t* T_out);
 
 /* Bytes the last sarathi_run_hybrid_batch moved host->device (batch metadata: token ids, positions,
  * slots, block tables) and device->host (logits, only with SARATHI_LOGITS_HOST). */

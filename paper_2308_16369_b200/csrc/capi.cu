@@ -83,7 +83,7 @@ int sarathi_alloc_kv(sarathi_model* m, int64_t num_blocks, int32_t block_size) {
 
 int sarathi_kv_bytes_per_token(const sarathi_model* m, int64_t* out) {
   if (!m || !out) return fail(SARATHI_EINVAL, "kv_bytes_per_token: NULL");
-  *out = 2ll * m->m.cfg.n_layers * m->m.nkv_l * m->m.cfg.head_dim * 2;
+  *out = 2ll * m->m.nl * m->m.nkv_l * m->m.cfg.head_dim * 2;  // this handle's layers
   return SARATHI_OK;
 }
 
@@ -92,7 +92,7 @@ int sarathi_max_batch(const sarathi_model* m, int32_t tokens_per_request, int64_
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return fail(SARATHI_ECUDA, "cudaMemGetInfo failed");
   const double num = static_cast<double>(fr) - static_cast<double>(reserve_bytes);
-  const double mkv = 2.0 * m->m.cfg.n_layers * m->m.nkv_l * m->m.cfg.head_dim * 2;
+  const double mkv = 2.0 * m->m.nl * m->m.nkv_l * m->m.cfg.head_dim * 2;
   *B_out = num <= 0 ? 0 : static_cast<int32_t>(num / (tokens_per_request * mkv));
   return SARATHI_OK;
 }
@@ -130,6 +130,20 @@ int sarathi_request_truncate(sarathi_model* m, int64_t req_id, int32_t new_len) 
   if (it == m->m.cached.end()) return fail(SARATHI_EUNKNOWN_REQ, "request_truncate: unknown request");
   if (new_len < 0 || new_len > it->second) return fail(SARATHI_EINVAL, "request_truncate: new_len > cached length");
   it->second = new_len;
+  return SARATHI_OK;
+}
+
+int sarathi_stage_input(sarathi_model* m, const float* h_dev) {
+  if (!m || !h_dev) return fail(SARATHI_EINVAL, "stage_input: NULL");
+  if (m->m.pp_stage == 0) return fail(SARATHI_EINVAL, "stage_input: the first pipeline stage embeds its tokens");
+  m->m.pp_in = h_dev;
+  return SARATHI_OK;
+}
+
+int sarathi_stage_output(const sarathi_model* m, const float** h_dev, int32_t* T_out) {
+  if (!m || !h_dev || !T_out) return fail(SARATHI_EINVAL, "stage_output: NULL");
+  *h_dev = m->m.h;
+  *T_out = m->m.last_T;
   return SARATHI_OK;
 }
 
@@ -209,7 +223,7 @@ int sarathi_debug_hidden(const sarathi_model* m, int32_t layer, float* host_out)
   if (!m || !host_out) return fail(SARATHI_EINVAL, "debug_hidden: NULL");
   const auto& M = m->m;
   if (!M.last_dumped || !M.dump) return fail(SARATHI_ESTATE, "debug_hidden: last batch not run with DUMP_LAYERS");
-  if (layer < -1 || layer >= M.cfg.n_layers) return fail(SARATHI_EINVAL, "debug_hidden: layer out of range");
+  if (layer < -1 || layer >= M.nl) return fail(SARATHI_EINVAL, "debug_hidden: layer out of range (this stage's layers)");
   cudaStreamSynchronize(M.stream);
   const size_t n = static_cast<size_t>(M.last_T) * M.cfg.hidden;
   if (cudaMemcpy(host_out, M.dump + static_cast<size_t>(layer + 1) * M.Tmax * M.cfg.hidden, n * 4,
@@ -222,7 +236,7 @@ int sarathi_debug_kv(const sarathi_model* m, int32_t layer, int64_t req_id, int3
                      uint16_t* host_v) {
   if (!m || !host_k || !host_v) return fail(SARATHI_EINVAL, "debug_kv: NULL");
   const auto& M = m->m;
-  if (!M.kv_ready || layer < 0 || layer >= M.cfg.n_layers) return fail(SARATHI_EINVAL, "debug_kv: bad layer/state");
+  if (!M.kv_ready || layer < 0 || layer >= M.nl) return fail(SARATHI_EINVAL, "debug_kv: bad layer/state");
   if (!M.alloc.has(req_id)) return fail(SARATHI_EUNKNOWN_REQ, "debug_kv: unknown request");
   if (pos0 < 0 || n < 0 || pos0 + n > M.alloc.reserved(req_id)) return fail(SARATHI_EINVAL, "debug_kv: range");
   cudaStreamSynchronize(M.stream);
@@ -261,7 +275,7 @@ int sarathi_debug_weight(const sarathi_model* m, int32_t layer, int32_t tensor, 
   bool packed = true;  // GEMM weights live in the tile-major layout; report the logical [rows][cols] view
   const int H = M.cfg.hidden;
   if (tensor < 16) {
-    if (layer < 0 || layer >= M.cfg.n_layers) return fail(SARATHI_EINVAL, "debug_weight: layer");
+    if (layer < 0 || layer >= M.nl) return fail(SARATHI_EINVAL, "debug_weight: layer (this stage's layers)");
     const auto& w = M.layers[layer];
     switch (tensor) {
       case 0: src = w.qkv; rows = M.qkv_rows; cols = H; break;
@@ -281,6 +295,7 @@ int sarathi_debug_weight(const sarathi_model* m, int32_t layer, int32_t tensor, 
     }
   }
   const size_t total = static_cast<size_t>(rows) * cols;
+  if (!src) return fail(SARATHI_EINVAL, "debug_weight: tensor not held by this pipeline stage");
   if (static_cast<size_t>(offset + count) > total) return fail(SARATHI_EINVAL, "debug_weight: range");
   cudaStreamSynchronize(M.stream);
   if (!packed) {

@@ -134,6 +134,13 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
     return Status::err(SARATHI_EINVAL, "init_model: invalid model configuration");
   if (world < 1 || rank < 0 || rank >= world)
     return Status::err(SARATHI_EINVAL, "init_model: invalid rank/world");
+  // pipeline stage (NEXT-4): contiguous layer range [l0, l0 + nl) of the L layers
+  pp_stages = d.pp_stages > 0 ? d.pp_stages : 1;
+  pp_stage = d.pp_stage;
+  if (pp_stage < 0 || pp_stage >= pp_stages || pp_stages > c.n_layers)
+    return Status::err(SARATHI_EINVAL, "init_model: need 0 <= pp_stage < pp_stages <= n_layers");
+  l0 = static_cast<int>(static_cast<long long>(c.n_layers) * pp_stage / pp_stages);
+  nl = static_cast<int>(static_cast<long long>(c.n_layers) * (pp_stage + 1) / pp_stages) - l0;
   if (c.n_heads % world || c.n_kv_heads % world || c.ffn_hidden % (64 * world) || c.vocab % world)
     return Status::err(SARATHI_EINVAL,
                        "init_model: n_heads, n_kv_heads, vocab must divide by world and ffn_hidden by 64*world");
@@ -257,9 +264,9 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
     scl.assign(rows, 0.f);
     base.assign(rows, 0);
   };
-  layers.resize(L);
-  for (int l = 0; l < L; ++l) {
-    LayerWeights& w = layers[l];
+  layers.resize(nl);
+  for (int l = l0; l < l0 + nl; ++l) {  // global layer index l (generator ids), local storage l - l0
+    LayerWeights& w = layers[l - l0];
     // GEMM weights in the tile-major layout (rows padded to 128; padding zero)
     SRET(dalloc_padded(&w.qkv, qkv_rows, H));
     SRET(dalloc_padded(&w.o, H, q_dim_l));
@@ -287,14 +294,15 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
       launches += 2;
     }
   }
-  // embedding (replicated), final gain, LM head (vocab-parallel)
-  SRET(dalloc(&emb, static_cast<size_t>(c.vocab) * H));
-  {
+  // embedding (replicated; first pipeline stage), final gain, LM head (vocab-parallel; last stage)
+  if (pp_stage == 0) {
+    SRET(dalloc(&emb, static_cast<size_t>(c.vocab) * H));
     ShardDims sd;
     shard_map(c.n_layers, H, c.n_heads, c.n_kv_heads, hd, c.ffn_hidden, c.vocab, c.ffn_kind, rank, world, 0, 16, &tau,
               &scl, &base, &sd);
+    SRET(gen(emb, c.vocab, H, 0));
   }
-  SRET(gen(emb, c.vocab, H, 0));
+  if (pp_stage == pp_stages - 1) {
   SRET(dalloc(&gf, H));
   if (host_tensors) {
     SRET(check(cudaMemcpyAsync(gf, host_ptr(kGfTau), H * 2, cudaMemcpyHostToDevice, stream), "H2D gain"));
@@ -310,6 +318,7 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   }
   SRET(gen(lm, vocab_l, H, 1));
   if (!make_tmap_weight(&m_lm, lm, vocab_l, H)) return Status::err(SARATHI_ECUDA, "tensor map (lm head)");
+  }
 
   // RoPE tables (fp64 on host -> fp32), reading O-7
   {
@@ -434,11 +443,11 @@ Status Model::alloc_kv(int64_t nb, int32_t bs) {
   if (nb < 1 || nb > (1ll << 31) - 1 || (bs != 16 && bs != 32 && bs != 64 && bs != 128))
     return Status::err(SARATHI_EINVAL, "alloc_kv: num_blocks >= 1 and block_size in {16, 32, 64, 128}");
   const size_t per = static_cast<size_t>(nb) * nkv_l * bs * cfg.head_dim;
-  kpool.resize(cfg.n_layers);
-  vpool.resize(cfg.n_layers);
-  kmap.resize(cfg.n_layers);
-  vmap.resize(cfg.n_layers);
-  for (int l = 0; l < cfg.n_layers; ++l) {
+  kpool.resize(nl);
+  vpool.resize(nl);
+  kmap.resize(nl);
+  vmap.resize(nl);
+  for (int l = 0; l < nl; ++l) {
     SRET(dalloc(&kpool[l], per));
     SRET(dalloc(&vpool[l], per));
     // zero once: slots never written (past a request's length inside a block, or in blocks a tile
@@ -593,6 +602,8 @@ Status Model::collect_op_times() {
 
 Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* dec, float* logits, int32_t flags) {
   if (!kv_ready) return Status::err(SARATHI_ESTATE, "run_hybrid_batch: alloc_kv not called");
+  // a pipeline stage before the last hands its residual stream on (sarathi_stage_output): no logits
+  if (pp_stage != pp_stages - 1) flags = (flags | SARATHI_NO_LOGITS) & ~SARATHI_LOGITS_HOST;
   const int p = pre ? pre->n_tokens : 0;
   const int d = dec ? dec->n : 0;
   const int T = p + d;
@@ -677,7 +688,8 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
 
   const int H = cfg.hidden, hd = cfg.head_dim;
   const bool dump_layers = flags & SARATHI_DUMP_LAYERS;
-  if (dump_layers && !dump) SRET(dalloc(&dump, static_cast<size_t>(cfg.n_layers + 1) * Tmax * H));
+  if (dump_layers && !dump) SRET(dalloc(&dump, static_cast<size_t>(nl + 1) * Tmax * H));
+  if (pp_stage > 0 && !pp_in) return Status::err(SARATHI_ESTATE, "run_hybrid_batch: pipeline stage > 0 needs sarathi_stage_input");
   auto dump_h = [&](int idx) -> Status {
     if (!dump_layers) return Status::ok();
     return check(cudaMemcpyAsync(dump + static_cast<size_t>(idx) * Tmax * H, h, static_cast<size_t>(T) * H * 4,
@@ -738,7 +750,11 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   const PeerSum no_add;
 
   cudaEvent_t ob = op_begin();
-  SRET(check(launch_embedding(d_tok, emb, h, T, H, stream), "embedding"));
+  if (pp_stage == 0) {
+    SRET(check(launch_embedding(d_tok, emb, h, T, H, stream), "embedding"));
+  } else {  // pipeline: the previous stage's residual stream (fp32 [T][H], device)
+    SRET(check(cudaMemcpyAsync(h, pp_in, static_cast<size_t>(T) * H * 4, cudaMemcpyDeviceToDevice, stream), "stage input"));
+  }
   op_end(SARATHI_OP_EMBED, ob);
   ++launches;
   SRET(dump_h(0));
@@ -746,7 +762,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   bool pending_ar = false;  // TP: down-proj partial in `ar` not yet added to h
   static const bool no_aux = getenv("SARATHI_NO_AUX") != nullptr;  // experiment: serial attention
   static const bool attn_chain = !(getenv("SARATHI_ATTN_CHAIN") && atoi(getenv("SARATHI_ATTN_CHAIN")) == 0);
-  for (int l = 0; l < cfg.n_layers; ++l) {
+  for (int l = 0; l < nl; ++l) {  // this stage's layers (local index)
     LayerWeights& w = layers[l];
     ob = op_begin();
     {
@@ -1000,7 +1016,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     ++launches;
     pending_ar = false;
   }
-  SRET(dump_h(cfg.n_layers));
+  SRET(dump_h(nl));
   if (want_logits) {
     ob = op_begin();
     // final norm on the R logit rows (adds the pending TP partial for exactly those rows)

@@ -66,6 +66,9 @@ struct LayerWeights {
 struct Model {
   sarathi_model_config cfg{};
   int rank = 0, world = 1, device = 0;
+  // pipeline parallelism (NEXT-4): this handle holds layers [l0, l0 + nl) of the L layers
+  int pp_stage = 0, pp_stages = 1, l0 = 0, nl = 0;
+  const float* pp_in = nullptr;  // stage > 0: the previous stage's residual stream [T][H] (device)
   cudaStream_t stream = nullptr;
   // side stream, used only with SARATHI_ATTN_CHAIN=0 (the default "attention chain" keeps both
   // attentions in the main stream): the chunked-prefill attention runs concurrently with the

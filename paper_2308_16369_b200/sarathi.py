@@ -34,7 +34,7 @@ EXPORTS = [
     "sarathi_sched_done", "sarathi_sched_block_table", "sarathi_op_gemm", "sarathi_op_rmsnorm",
     "sarathi_request_truncate", "sarathi_last_io_bytes", "sarathi_set_profiling", "sarathi_op_times", "sarathi_op_kernel_times",
     "sarathi_op_pack_weight", "sarathi_shard_map", "sarathi_local_group_create", "sarathi_local_group_destroy",
-    "sarathi_token_capacity", "sarathi_chunk_advice",
+    "sarathi_token_capacity", "sarathi_chunk_advice", "sarathi_stage_input", "sarathi_stage_output",
 ]
 GEMM_W_PACKED = 0x100
 OP_NAMES = ["embed", "rmsnorm", "gemm_qkv", "prefill_attn", "decode_attn", "gemm_o", "gemm_gate_up",
@@ -56,7 +56,8 @@ class ModelConfigC(C.Structure):
 
 class DistC(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
-                ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p), ("local_group", C.c_void_p)]
+                ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p), ("local_group", C.c_void_p),
+                ("pp_stage", C.c_int32), ("pp_stages", C.c_int32)]
 
 
 class PrefillChunkC(C.Structure):
@@ -113,6 +114,8 @@ def _load() -> C.CDLL:
         "sarathi_local_group_create": [I32, I32, P(VP)],
         "sarathi_token_capacity": [I32, P(I32), P(I32), P(I32)],
         "sarathi_chunk_advice": [I32, I32, I32, P(I32)],
+        "sarathi_stage_input": [VP, VP],
+        "sarathi_stage_output": [VP, P(VP), P(I32)],
         "sarathi_shard_map": [P(ModelConfigC), I32, I32, I32, I32, P(I32), P(F), P(I64), I32, P(I32), P(I32)],
     }
     for name, args in sig.items():
@@ -170,13 +173,14 @@ class Model:
     def __init__(self, cfg: ModelConfigC, seed: int, rank: int = 0, world: int = 1, device: int = 0,
                  nccl_id: Optional[bytes] = None, stream: int = 0,
                  host_tensors: Optional[Sequence[Optional[np.ndarray]]] = None,
-                 local_group: Optional["LocalGroup"] = None):
+                 local_group: Optional["LocalGroup"] = None, pp_stage: int = 0, pp_stages: int = 1):
         """host_tensors: None (weights generated on device from `seed`) or the 9*L + 3 logical bf16
         tensors (uint16 bit patterns, nn.Linear [out, in]) in the order of include/sarathi.h."""
         self.cfg = cfg
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         dist = DistC(rank, world, device, C.cast(self._idbuf, C.c_void_p) if self._idbuf else None,
-                     C.c_void_p(stream) if stream else None, local_group.h if local_group is not None else None)
+                     C.c_void_p(stream) if stream else None, local_group.h if local_group is not None else None,
+                     pp_stage, pp_stages)
         self._group = local_group  # keep the group alive while this handle exists
         ht = None
         if host_tensors is not None:
@@ -260,6 +264,16 @@ class Model:
         _check(lib.sarathi_run_hybrid_batch(self.h, C.byref(pc) if pc else None, C.byref(ds) if ds else None,
                                             C.c_void_p(ptr) if ptr else None, flags))
         return R
+
+    def stage_input(self, h_ptr: int):
+        """Pipeline stage > 0: device pointer (fp32 [T][H]) of the previous stage's output."""
+        _check(lib.sarathi_stage_input(self.h, C.c_void_p(h_ptr)))
+
+    def stage_output(self) -> Tuple[int, int]:
+        """(device pointer of this stage's residual stream after its layers, T) for the last batch."""
+        p, t = C.c_void_p(), C.c_int32()
+        _check(lib.sarathi_stage_output(self.h, C.byref(p), C.byref(t)))
+        return p.value, t.value
 
     def truncate(self, req_id: int, new_len: int):
         _check(lib.sarathi_request_truncate(self.h, req_id, new_len))

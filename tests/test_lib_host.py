@@ -206,3 +206,18 @@ def test_library_sass_is_blackwell_native(S):
     for op in ("UTCHMMA.2CTA", "UTMALDG.2D.2CTA", "LDTM", "LDGMC"):
         assert op in sass, op
     assert "sm_100a" in subprocess.run([exe, "-lelf", S.LIB_PATH], capture_output=True, text=True).stdout
+
+
+def test_pipeline_timeline_hand_cases():
+    """Max-plus pipeline recurrence (paper_2308_16369_b200/pipeline.py) on hand-worked cases: uniform
+    micro-batches leave no bubble; a long first micro-batch (a full prompt, PB1) stalls its slot's
+    next iteration: stage 0 idles 2 units before micro-batch 2 (t = [3, 1, 1, 1], 2 stages)."""
+    from paper_2308_16369_b200.pipeline import pipeline_timeline, request_bubbles
+    _, fin, bub = pipeline_timeline([1, 1, 1, 1], 2)
+    assert bub == [0, 0, 0, 0] and fin[1][3] == 5
+    st, fin, bub = pipeline_timeline([3, 1, 1, 1], 2)
+    assert bub == [0, 0, 2, 0]
+    assert [st[0][m] for m in range(4)] == [0, 3, 6, 7] and [fin[1][m] for m in range(4)] == [6, 7, 8, 9]
+    assert request_bubbles([[1, 2], [3], [1], [3]], bub) == {1: 2.0, 2: 0.0, 3: 0.0}
+    _, fin, bub = pipeline_timeline([2, 5], 1)          # one stage: no pipeline, no bubbles
+    assert bub == [0, 0] and fin[0][1] == 7

@@ -764,6 +764,7 @@ cudaError_t launch_decode_hd(const DecodeAttnArgs& a, const CUtensorMap& mk, con
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(decode_attn_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    prefer_max_smem(decode_attn_mma<HD>);
     configured = true;
   }
   dim3 grid(a.d, a.n_kv_local, a.splits);
@@ -805,6 +806,7 @@ cudaError_t launch_prefill_tc(const PrefillAttnArgs& a, const CUtensorMap& mq, c
   using L = PtcSmem<HD, BK, PT>;
   static bool configured = false;
   if (!configured) {
+    prefer_max_smem(prefill_attn_tc<HD, BK, PT>);
     cudaError_t e = cudaFuncSetAttribute(prefill_attn_tc<HD, BK, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(L::kTotal));
     if (e != cudaSuccess) return e;

@@ -414,6 +414,15 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16_f32(uint32_t M, uint32_t 
 
 // Host: launch with programmatic stream serialization (PDL) unless SARATHI_PDL=0.
 bool pdl_enabled();
+// Host: every kernel of the layer chain prefers the maximum shared-memory carveout, so an SM does
+// not switch its L1 / shared split between a 226-KB GEMM CTA and a small RMSNorm CTA at every kernel
+// boundary (SARATHI_CARVEOUT=0 leaves the driver's default).  Idempotent per kernel.
+bool carveout_enabled();
+template <typename... KArgs>
+void prefer_max_smem(void (*kernel)(KArgs...)) {
+  if (carveout_enabled())
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args&&... args) {
@@ -427,6 +436,11 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  static bool carved = false;  // one flag per kernel instantiation of this template
+  if (!carved) {
+    prefer_max_smem(kernel);
+    carved = true;
+  }
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

@@ -8,6 +8,14 @@
 
 namespace sarathi {
 
+bool carveout_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SARATHI_CARVEOUT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("SARATHI_PDL");
@@ -254,6 +262,11 @@ cudaError_t launch_residual_add(float* h, const PeerSum& add, int T, int H, cuda
   const size_t n = static_cast<size_t>(T) * H;
   if (n == 0) return cudaSuccess;
   const int blocks = static_cast<int>(std::min<size_t>(1184, (n / 4 + 255) / 256));
+  static bool carved = false;
+  if (!carved) {
+    prefer_max_smem(residual_add_kernel);
+    carved = true;
+  }
   residual_add_kernel<<<blocks, 256, 0, st>>>(h, add, n);
   return cudaGetLastError();
 }

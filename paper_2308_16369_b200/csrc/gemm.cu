@@ -1027,6 +1027,7 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
       for (KFn fn : row) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
         if (e != cudaSuccess) return e;
+        prefer_max_smem(fn);
       }
     configured = true;
   }

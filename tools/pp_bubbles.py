@@ -32,25 +32,32 @@ def measure_costs(S, synth, torch, cfg, steps=5):
     m = S.Model(S.config_from(cfg, max_tokens_per_batch=maxT, max_seq_len=4096), seed=0, stream=stream.cuda_stream)
     bs = 64
     nd = 27
-    m.alloc_kv((nd + 2) * (4096 // bs) + 8, bs)
+    prefixes = (0, 1024, 2048)
+    m.alloc_kv((nd + 1 + len(prefixes)) * (4096 // bs) + 8, bs)
     tok = lambda r, a, n: synth.tokens(7, r, a, n, cfg.vocab)
-    m.request_alloc(0, 4096)
-    m.request_alloc(nd + 1, 4096)
     for r in range(1, nd + 1):
         m.request_alloc(r, 4096)
         for a in range(0, 4095, 2048):
             m.run_hybrid_batch((r, a, tok(r, a, min(2048, 4095 - a))), [], flags=S.NO_LOGITS)
-    for a in range(0, 3072, 2048):
-        m.run_hybrid_batch((0, a, tok(0, a, min(2048, 3072 - a))), [], flags=S.NO_LOGITS)
+    # one chunk request per prefix length s (its cache stays >= s: every timed step truncates back to s)
+    pre_req = {}
+    for i, s0 in enumerate(prefixes):
+        rid = 100 + i
+        pre_req[s0] = rid
+        m.request_alloc(rid, 4096)
+        for a in range(0, s0, 2048):
+            m.run_hybrid_batch((rid, a, tok(rid, a, min(2048, s0 - a))), [], flags=S.NO_LOGITS)
     logits = torch.empty((maxT, cfg.vocab), dtype=torch.float32, device="cuda")
     rows = []
 
     def timed(p, s, d, ctx):
-        pre = (0, s, tok(0, s, p)) if p else None
+        rid = pre_req[s]
+        pre = (rid, s, tok(rid, s, p)) if p else None
         decs = [(r, int(tok(r, ctx - 1, 1)[0]), ctx - 1) for r in range(1, d + 1)]
 
         def step():
-            m.truncate(0, s)
+            if p:
+                m.truncate(rid, s)
             for r, _, pos in decs:
                 m.truncate(r, pos)
             m.run_hybrid_batch(pre, decs, logits_ptr=logits.data_ptr())
@@ -145,7 +152,7 @@ def main():
     out = {}
     for name, pol, tile in (("orca_best", S.POLICY_ORCA_BEST, 0), ("sarathi", S.POLICY_SARATHI, 0),
                             ("sarathi_b200", S.POLICY_SARATHI, 2)):
-        mbs = schedule(S, synth, reqs, args.stages, args.B, args.chunk, pol, tile, 1 << 20, 64)
+        mbs = schedule(S, synth, reqs, args.stages, args.B, args.chunk, pol, tile, args.B * 64 + 64, 64)
         t = []
         for (p, s, ctx), ids in mbs:
             if not ids:

@@ -33,12 +33,17 @@ def measure_costs(S, synth, torch, cfg, steps=5):
     bs = 64
     nd = 27
     prefixes = (0, 1024, 2048)
-    m.alloc_kv((nd + 1 + len(prefixes)) * (4096 // bs) + 8, bs)
+    ctxs = (1024, 2048, 3072, 4096)
+    m.alloc_kv((nd * len(ctxs) + len(prefixes)) * (4096 // bs) + 8, bs)
     tok = lambda r, a, n: synth.tokens(7, r, a, n, cfg.vocab)
-    for r in range(1, nd + 1):
-        m.request_alloc(r, 4096)
-        for a in range(0, 4095, 2048):
-            m.run_hybrid_batch((r, a, tok(r, a, min(2048, 4095 - a))), [], flags=S.NO_LOGITS)
+    # nd decode requests per context length (cached ctx - 1 tokens; a timed step truncates back)
+    dec_req = {}
+    for i, cx in enumerate(ctxs):
+        dec_req[cx] = list(range(1000 * (i + 1), 1000 * (i + 1) + nd))
+        for r in dec_req[cx]:
+            m.request_alloc(r, 4096)
+            for a in range(0, cx - 1, 2048):
+                m.run_hybrid_batch((r, a, tok(r, a, min(2048, cx - 1 - a))), [], flags=S.NO_LOGITS)
     # one chunk request per prefix length s (its cache stays >= s: every timed step truncates back to s)
     pre_req = {}
     for i, s0 in enumerate(prefixes):
@@ -53,7 +58,7 @@ def measure_costs(S, synth, torch, cfg, steps=5):
     def timed(p, s, d, ctx):
         rid = pre_req[s]
         pre = (rid, s, tok(rid, s, p)) if p else None
-        decs = [(r, int(tok(r, ctx - 1, 1)[0]), ctx - 1) for r in range(1, d + 1)]
+        decs = [(r, int(tok(r, ctx - 1, 1)[0]), ctx - 1) for r in dec_req[ctx][:d]] if d else []
 
         def step():
             if p:
@@ -74,7 +79,7 @@ def measure_costs(S, synth, torch, cfg, steps=5):
 
     for p in (64, 128, 256, 512, 1024, 2048):
         for s in (0, 1024):
-            rows.append((p, s, 0, 0, timed(p, s, 0, 1)))
+            rows.append((p, s, 0, 0, timed(p, s, 0, 1024)))
     for d in (1, 4, 11, 27):
         for ctx in (1024, 2048, 4096):
             rows.append((0, 0, d, ctx, timed(0, 0, d, ctx)))

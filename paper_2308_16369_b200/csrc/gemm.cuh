@@ -90,4 +90,54 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
 // Debug: prints the globaltimer trace (EpiParams.trace, 4096 u64) of the first CTA pair to stderr.
 void dump_gemm_trace(const unsigned long long* trace_dev, const GemmPlan& plan);
 
+// ---------------------------------------------------------------------------
+// Layer chain: O-proj -> FFN1 -> FFN2 -> next layer's QKV as ONE persistent launch (gemm_chain.cu).
+// Job j+1 reads job j's output through per-128-row-tile flags (flag >= epoch) instead of a kernel
+// boundary, so a pair that finishes its share of one GEMM starts the next, the tile quantization
+// of one job is filled by the next, and no RMSNorm launch sits between them: a residual-add job's
+// tiles are finalised by their last contributor, which writes X = bf16(g * h) for its 128 columns
+// and the per-token partial sum of squares; the consuming job's epilogue scales token t by
+// rsqrt(sum_parts / H + eps) (RMSNorm is a per-token scale, so it commutes with the GEMM).
+constexpr int kChainMaxJobs = 4;
+struct ChainJobDev {
+  EpiParams ep;                      // mode: EPI_ADD_F32 / EPI_SILU_MUL / EPI_GELU / EPI_QKV_ROPE
+  int M = 0, KB = 0;                 // weight rows, k-blocks
+  const unsigned* dep_flag = nullptr;  // X k-block kb waits for dep_flag[kb >> dep_shift] >= epoch
+  int dep_shift = 0;
+  // norm-free input (X = bf16(g * h)): the epilogue scales token t by rsqrt(sum_p ss_in[p][t] * inv_h + eps)
+  const float* ss_in = nullptr;      // [ss_parts][ss_ld]; published with dep_flag[0 .. ss_parts)
+  int ss_parts = 0;
+  float inv_h = 0.f, eps = 0.f;
+  // residual-add finalisation (per 128-row tile; the last of need[pair tile] contributors):
+  // fin_xa[t][col] = bf16(fin_g[col] * h[t][col]), fin_ss[tile][t] = sum_col h^2, flag_out[tile] = epoch
+  int* fin_cnt = nullptr;            // [2 * pair tiles], zero between launches
+  const int* fin_need = nullptr;     // [pair tiles]
+  const void* fin_g = nullptr;       // bf16 [M]
+  void* fin_xa = nullptr;            // bf16 [tokens][M]
+  float* fin_ss = nullptr;           // [M / 128][ss_ld]
+  unsigned* flag_out = nullptr;      // whole-tile jobs: set after the tile's epilogue; split: after finalisation
+};
+struct ChainLaunch {
+  ChainJobDev job[kChainMaxJobs];
+  int njobs = 0;
+  const int* segs = nullptr;         // device: 4 ints per segment (job, pair tile, kb0, kb1)
+  const int* seg_off = nullptr;      // device: [pairs + 1]
+  int pairs = 0;
+  int N = 0, bn = 0, n_mma = 1, stages = 0, nbuf = 1;
+  int ss_ld = 0;                     // row stride of the ss arrays (max tokens)
+  unsigned epoch = 0;
+  size_t smem = 0;
+  uint32_t tmem_cols = 0, ring_bytes = 0;
+  unsigned long long* span_start = nullptr;
+  unsigned long long* span_end = nullptr;
+};
+struct ChainMaps {
+  CUtensorMap w[kChainMaxJobs];      // make_tmap_weight maps
+  CUtensorMap x[kChainMaxJobs];      // activation maps, box rows bn / n_mma / 2
+};
+// Token tiling / ring of a chain over N tokens (N <= 512: one token tile).  Fills bn, n_mma,
+// stages, nbuf, smem, tmem_cols, ring_bytes; returns false if N needs more than one token tile.
+bool plan_chain_tiling(int N, ChainLaunch* cl);
+cudaError_t launch_chain(const ChainMaps& maps, const ChainLaunch& cl, int ffn_mode, cudaStream_t stream);
+
 }  // namespace sarathi

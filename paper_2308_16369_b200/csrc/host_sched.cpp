@@ -2,6 +2,7 @@
 #include "host_sched.hpp"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 
 #include "../../include/sarathi.h"
@@ -270,6 +271,138 @@ bool shard_map(int n_layers, int hidden, int n_heads, int n_kv_heads, int head_d
   dims->rows = rows;
   dims->cols = cols;
   return true;
+}
+
+
+ChainSchedule schedule_chain(const std::vector<ChainJobShape>& jobs, int P, double e_add, double e_fin, int min_seg) {
+  ChainSchedule out;
+  P = std::max(1, P);
+  std::vector<double> f(P, 0.0);                 // time each pair's MMA pipe becomes free
+  std::vector<std::vector<std::array<int, 4>>> per(P);
+  std::vector<double> prev_ready;                // previous job: time each 128-row tile is published
+  out.need.resize(jobs.size());
+  for (size_t j = 0; j < jobs.size(); ++j) {
+    const ChainJobShape& J = jobs[j];
+    const int KB = J.KB;
+    std::vector<double> dep(KB, 0.0);
+    if (J.dep_shift >= 0 && j > 0)
+      for (int kb = 0; kb < KB; ++kb) {
+        const size_t q = static_cast<size_t>(kb >> J.dep_shift);
+        dep[kb] = q < prev_ready.size() ? prev_ready[q] : 0.0;
+      }
+    std::vector<double> ready(2 * static_cast<size_t>(J.pm_tiles), 0.0);
+    out.need[j].assign(J.pm_tiles, 0);
+    // a segment's mainloop: one unit per k-block, each k-block no earlier than its input
+    auto run = [&](double t, int kb0, int kb1) {
+      for (int kb = kb0; kb < kb1; ++kb) t = std::max(t, dep[kb]) + 1.0;
+      return t;
+    };
+    if (!J.split) {
+      double D = 0.0;  // no tile can finish before every k-block's input exists
+      for (int kb = 0; kb < KB; ++kb) D = std::max(D, dep[kb] + (KB - kb));
+      for (int pt = 0; pt < J.pm_tiles; ++pt) {
+        const int c = static_cast<int>(std::min_element(f.begin(), f.end()) - f.begin());
+        const double end = std::max(f[c] + KB, D);
+        per[c].push_back({static_cast<int>(j), pt, 0, KB});
+        f[c] = end;
+        ready[2 * pt] = ready[2 * pt + 1] = end + J.e_done;
+        out.need[j][pt] = 1;
+      }
+    } else {
+      // bands: contiguous k-ranges whose inputs are published within `tol` of the band's first
+      const double tol = 2.0;
+      std::vector<std::pair<int, int>> bands;
+      for (int k0 = 0, kb = 1; kb <= KB; ++kb)
+        if (kb == KB || std::fabs(dep[kb] - dep[k0]) > tol) {
+          bands.push_back({k0, kb});
+          k0 = kb;
+        }
+      std::stable_sort(bands.begin(), bands.end(), [&](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+        return dep[a.first] < dep[b.first];
+      });
+      struct Run {
+        int pt, k0, k1;
+      };
+      std::vector<Run> runs;
+      for (const auto& b : bands)
+        for (int pt = 0; pt < J.pm_tiles; ++pt) runs.push_back({pt, b.first, b.second});
+      const long long U = static_cast<long long>(J.pm_tiles) * KB;
+      // water-filling: pairs by free time; all pairs below the level T_end share U
+      std::vector<int> order(P);
+      for (int c = 0; c < P; ++c) order[c] = c;
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return f[a] < f[b]; });
+      int m = P;
+      double T_end = 0.0;
+      for (; m >= 1; --m) {
+        double S = 0.0;
+        for (int i = 0; i < m; ++i) S += f[order[i]];
+        T_end = (static_cast<double>(U) + S) / m;
+        if (m == 1 || T_end >= f[order[m - 1]]) break;
+      }
+      std::vector<long long> budget(m, 0);
+      {
+        double cum = 0.0;
+        long long given = 0;
+        for (int i = 0; i < m; ++i) {
+          cum += T_end - f[order[i]];
+          const long long upto = (i == m - 1) ? U : std::min<long long>(U, std::llround(cum));
+          budget[i] = std::max<long long>(0, upto - given);
+          given += budget[i];
+        }
+        // too-short ranges cost a whole epilogue: fold them into the next (or previous) pair
+        for (int i = 0; i < m; ++i)
+          if (budget[i] > 0 && budget[i] < min_seg) {
+            int k = i + 1;
+            if (k >= m)
+              for (k = i - 1; k > 0 && budget[k] == 0; --k) {
+              }
+            if (k >= 0 && k != i) {
+              budget[k] += budget[i];
+              budget[i] = 0;
+            }
+          }
+      }
+      std::vector<double> contrib(J.pm_tiles, 0.0);
+      size_t r = 0;
+      int rk = runs.empty() ? 0 : runs[0].k0;  // cursor inside runs[r]
+      for (int i = 0; i < m; ++i) {
+        const int c = order[i];
+        long long n = budget[i];
+        double t = f[c];
+        while (n > 0 && r < runs.size()) {
+          const Run& R = runs[r];
+          const int take = static_cast<int>(std::min<long long>(n, R.k1 - rk));
+          // merge with this pair's previous segment when it continues the same tile's k-range
+          auto& v = per[c];
+          if (!v.empty() && v.back()[0] == static_cast<int>(j) && v.back()[1] == R.pt && v.back()[3] == rk) {
+            v.back()[3] = rk + take;
+          } else {
+            v.push_back({static_cast<int>(j), R.pt, rk, rk + take});
+            ++out.need[j][R.pt];
+          }
+          t = run(t, rk, rk + take);
+          contrib[R.pt] = std::max(contrib[R.pt], t + e_add);
+          n -= take;
+          rk += take;
+          if (rk == R.k1 && ++r < runs.size()) rk = runs[r].k0;
+        }
+        f[c] = t;
+      }
+      for (int pt = 0; pt < J.pm_tiles; ++pt) ready[2 * pt] = ready[2 * pt + 1] = contrib[pt] + e_fin;
+    }
+    double je = 0.0;
+    for (double x : ready) je = std::max(je, x);
+    out.job_end.push_back(je);
+    prev_ready = ready;
+  }
+  out.seg_off.assign(P + 1, 0);
+  for (int c = 0; c < P; ++c) {
+    out.seg_off[c + 1] = out.seg_off[c] + static_cast<int>(per[c].size());
+    for (const auto& s : per[c]) out.segs.insert(out.segs.end(), s.begin(), s.end());
+  }
+  out.makespan = out.job_end.empty() ? 0.0 : out.job_end.back();
+  for (double x : f) out.makespan = std::max(out.makespan, x);
+  return out;
 }
 
 }  // namespace sarathi

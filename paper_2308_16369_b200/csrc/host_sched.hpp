@@ -123,4 +123,33 @@ bool shard_map(int n_layers, int hidden, int n_heads, int n_kv_heads, int head_d
                int ffn_kind, int rank, int world, int layer, int tensor, std::vector<int>* tau,
                std::vector<float>* scale, std::vector<long long>* base, ShardDims* dims);
 
+// ---------------------------------------------------------------------------
+// Layer-chain schedule (gemm_chain.cu).  A chain is a sequence of GEMM jobs of one hybrid batch
+// executed by ONE persistent launch of CTA pairs, job j+1 consuming job j's output tile by tile
+// (dependency flags instead of kernel boundaries): O-proj -> FFN1 -> FFN2 -> next layer's QKV.
+// Work is cut into segments (job, 256-row pair tile, k-block range); a whole-tile job (an epilogue
+// that needs the full K sum: SiLU / GELU / RoPE) gets whole tiles, a split job (residual add,
+// red.add into h) any k-range.  The schedule is a list schedule over a per-pair timeline in
+// k-block units: whole tiles go to the earliest-free pair, a split job's units are ordered by the
+// readiness of the k-blocks they consume (bands), then tile-major, and handed out as contiguous
+// ranges so every pair ends at the same predicted time (water-filling over the pairs' free times).
+struct ChainJobShape {
+  int pm_tiles = 0;   // 256-row pair tiles
+  int KB = 0;         // k-blocks of 64
+  bool split = false; // residual-add job (any k-range per segment)
+  int dep_shift = -1; // X k-block kb needs the previous job's 128-row tile kb >> dep_shift (-1: none)
+  double e_done = 0;  // epilogue latency until the output tile is published (k-block units)
+};
+struct ChainSchedule {
+  std::vector<int> seg_off;             // [pairs + 1] segment range of every pair
+  std::vector<int> segs;                // 4 ints per segment: job, pair tile, kb0, kb1
+  std::vector<std::vector<int>> need;   // per job, per pair tile: number of segments (split jobs)
+  std::vector<double> job_end;          // predicted time the last tile of each job is published
+  double makespan = 0;                  // predicted (k-block units)
+};
+// e_add: red.add epilogue of a split segment; e_fin: finalisation of a split tile after its last
+// contributor (k-block units).  min_seg: split ranges shorter than this merge into a neighbour.
+ChainSchedule schedule_chain(const std::vector<ChainJobShape>& jobs, int pairs, double e_add, double e_fin,
+                             int min_seg = 4);
+
 }  // namespace sarathi

@@ -396,6 +396,8 @@ def gemm_roofline(cfg, synth, world, T, ops, kops, peaks):
     tot_flops, tot_s, tot_ks = 0.0, 0.0, 0.0
     for k, params in w.items():
         t_ms, n = ops[k]
+        if n == 0:
+            continue
         flops = 2.0 * T * params / world
         byts = 2.0 * params / world
         avg = t_ms / max(n, 1) / 1e3
@@ -415,6 +417,36 @@ def gemm_roofline(cfg, synth, world, T, ops, kops, peaks):
             tot_ks += kavg
             gemm[k]["us_kernel"] = round(kavg * 1e6, 2)
             gemm[k]["frac_tensor_kernel"] = round(flops / kavg / 1e12 / sus, 3)
+    # layer chain (gemm_chain.cu): one launch per layer = O + FFN1 + FFN2 (+ the next layer's QKV
+    # for every layer but the last); the standalone launches above are then layer 0's QKV only
+    c_ms, cn = ops.get("gemm_chain", (0.0, 0))
+    if cn:
+        L = cfg.n_layers
+        steps = cn / L
+        qkv_fl = 2.0 * T * w["gemm_qkv"] / world
+        rest_fl = sum(2.0 * T * w[k] / world for k in ("gemm_o", "gemm_gate_up", "gemm_down"))
+        fl = (L * rest_fl + (L - 1) * qkv_fl) / L  # per launch
+        avg = c_ms / cn / 1e3
+        ent = {"us": round(avg * 1e6, 2), "launches_per_step": L, "tflops": round(fl / avg / 1e12, 1),
+               "frac_tensor": round(fl / avg / 1e12 / sus, 3),
+               "frac_tensor_burst": round(fl / avg / 1e12 / peaks["bf16_tflops"], 3),
+               "gemms": "O + FFN1 + FFN2 + next layer's QKV (RMSNorm folded in)"}
+        kt_ms, kn = kops.get("gemm_chain", (0.0, 0))
+        if kn:
+            kavg = kt_ms / kn / 1e3
+            ent["us_kernel"] = round(kavg * 1e6, 2)
+            ent["frac_tensor_kernel"] = round(fl / kavg / 1e12 / sus, 3)
+        gemm["gemm_chain"] = ent
+        # per layer: the chain's share plus layer 0's standalone QKV amortised over the layers
+        q_ms, qn = ops.get("gemm_qkv", (0.0, 0))
+        lay_s = (c_ms + q_ms) / 1e3 / (steps * L)
+        lay_fl = rest_fl + qkv_fl
+        gemm["all_layer_gemms"] = {"us": round(lay_s * 1e6, 2), "frac_tensor": round(lay_fl / lay_s / 1e12 / sus, 3)}
+        if kn:
+            qk_ms, qkn = kops.get("gemm_qkv", (0.0, 0))
+            lay_ks = (kt_ms + qk_ms) / 1e3 / (steps * L)
+            gemm["all_layer_gemms"]["frac_tensor_kernel"] = round(lay_fl / lay_ks / 1e12 / sus, 3)
+        return gemm
     if tot_s > 0:
         gemm["all_layer_gemms"] = {"us": round(tot_s * 1e6, 2), "frac_tensor": round(tot_flops / tot_s / 1e12 / sus, 3),
                                    "frac_tensor_kernel": round(tot_flops / tot_ks / 1e12 / sus, 3) if tot_ks else None}

@@ -212,7 +212,8 @@ int sarathi_last_io_bytes(const sarathi_model* m, int64_t* h2d, int64_t* d2h);
 #define SARATHI_OP_LM_HEAD 8
 #define SARATHI_OP_ALLREDUCE 9
 #define SARATHI_OP_OTHER 10
-#define SARATHI_NUM_OPS 11
+#define SARATHI_OP_GEMM_CHAIN 11
+#define SARATHI_NUM_OPS 12
 int sarathi_set_profiling(sarathi_model* m, int32_t enable);
 int sarathi_op_times(sarathi_model* m, double* ms_out, int64_t* counts_out, int32_t n, int32_t reset);
 /* Device spans of the profiled layer GEMMs (QKV, O, gate||up, down) and attention kernels (decode:
@@ -303,6 +304,16 @@ int sarathi_token_capacity(int32_t T, int32_t* capacity, int32_t* n_tiles, int32
  * with chunk C, d decodes in the batch and `remaining` prompt tokens: p = b - d when C + d overshoots
  * b in {256, 512} by at most C/8, else capacity(C + d) - d; clamped to [1, remaining].  Host only. */
 int sarathi_chunk_advice(int32_t C, int32_t d, int32_t remaining, int32_t* p_out);
+/* Layer-chain schedule (host only; the work list of the one-launch O -> FFN1 -> FFN2 -> next-QKV
+ * GEMM chain, gemm_chain.cu).  Job j has pm_tiles[j] 256-row pair tiles and KB[j] k-blocks of 64;
+ * split[j] != 0: a residual-add job (any k-range per segment), else whole tiles only; dep_shift[j]:
+ * X k-block kb waits for the previous job's 128-row tile kb >> dep_shift (-1 none); e_done[j],
+ * e_add, e_fin: epilogue latencies in k-block units.  Output: seg_off[pairs + 1] and segs[4 * n]
+ * (job, pair tile, kb0, kb1) in per-pair execution order (cap = capacity of segs in segments),
+ * *n_segs, *makespan (predicted, k-block units).  EINVAL on bad arguments or cap too small. */
+int sarathi_chain_schedule(int32_t njobs, const int32_t* pm_tiles, const int32_t* KB, const int32_t* split,
+                           const int32_t* dep_shift, const double* e_done, int32_t pairs, double e_add, double e_fin,
+                           int32_t* seg_off, int32_t* segs, int32_t cap, int32_t* n_segs, double* makespan);
 
 /* ---- kernel-level entry points (device pointers, caller's stream) for parity tests ------ */
 /* out = X · Wᵀ on tcgen05: W bf16 [M][K] (K-major), X bf16 [N][K]; mode 0: out bf16 [N][M],

@@ -445,6 +445,27 @@ int sarathi_chunk_advice(int32_t C, int32_t d, int32_t remaining, int32_t* p_out
   return SARATHI_OK;
 }
 
+int sarathi_chain_schedule(int32_t njobs, const int32_t* pm_tiles, const int32_t* KB, const int32_t* split,
+                           const int32_t* dep_shift, const double* e_done, int32_t pairs, double e_add, double e_fin,
+                           int32_t* seg_off, int32_t* segs, int32_t cap, int32_t* n_segs, double* makespan) {
+  if (njobs < 1 || njobs > 8 || !pm_tiles || !KB || !split || !dep_shift || !e_done || pairs < 1 || !seg_off || !segs ||
+      !n_segs || cap < 0)
+    return fail(SARATHI_EINVAL, "chain_schedule: bad argument");
+  std::vector<sarathi::ChainJobShape> jobs(njobs);
+  for (int j = 0; j < njobs; ++j) {
+    if (pm_tiles[j] < 1 || KB[j] < 1) return fail(SARATHI_EINVAL, "chain_schedule: empty job");
+    jobs[j] = {pm_tiles[j], KB[j], split[j] != 0, dep_shift[j], e_done[j]};
+  }
+  const sarathi::ChainSchedule sc = sarathi::schedule_chain(jobs, pairs, e_add, e_fin);
+  const int n = static_cast<int>(sc.segs.size() / 4);
+  if (n > cap) return fail(SARATHI_EINVAL, "chain_schedule: cap too small");
+  std::copy(sc.seg_off.begin(), sc.seg_off.end(), seg_off);
+  std::copy(sc.segs.begin(), sc.segs.end(), segs);
+  *n_segs = n;
+  if (makespan) *makespan = sc.makespan;
+  return SARATHI_OK;
+}
+
 // ---- kernel-level ops ----
 int sarathi_op_gemm(const void* W, const void* X, void* out, int32_t M, int32_t N, int32_t K, int32_t mode,
                     int32_t force_splits, void* stream) {

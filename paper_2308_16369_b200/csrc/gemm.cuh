@@ -130,7 +130,11 @@ struct ChainLaunch {
   uint32_t tmem_cols = 0, ring_bytes = 0;
   unsigned long long* span_start = nullptr;
   unsigned long long* span_end = nullptr;
+  // debug timeline (SARATHI_CHAIN_TRACE): [pairs][kChainTraceSegs][8] globaltimer stamps of the
+  // leader CTA: mma start / first stage / last commit, epilogue wake / published, producer dep-wait ns
+  unsigned long long* trace = nullptr;
 };
+constexpr int kChainTraceSegs = 16;
 struct ChainMaps {
   CUtensorMap w[kChainMaxJobs];      // make_tmap_weight maps
   CUtensorMap x[kChainMaxJobs];      // activation maps, box rows bn / n_mma / 2

@@ -40,6 +40,12 @@ SARATHI_DEVICE unsigned ld_acquire_gpu(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+SARATHI_DEVICE unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+SARATHI_DEVICE void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 SARATHI_DEVICE void st_release_gpu(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -95,6 +101,7 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
   const uint32_t rank = cluster_ctarank();
   griddep_launch_dependents();
   if (p.span_start && threadIdx.x == 0) atomicMin(p.span_start, globaltimer_ns());
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[static_cast<size_t>(gridDim.x / 2) * kChainTraceSegs * 8] = globaltimer_ns();
   const int pair = blockIdx.x >> 1;
   const int seg_begin = __ldg(p.seg_off + pair), seg_end = __ldg(p.seg_off + pair + 1);
 
@@ -160,10 +167,27 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
         }
         if (J.dep_flag) {
           const int need = kb >> J.dep_shift;
-          if (need != have) {
-            wait_flag(J.dep_flag + need, p.epoch);
+          if (need > have) {
+            // one warp-wide relaxed scan of the next 32 dependency tiles (instead of an acquire per
+            // tile), one acquire fence for all of them, one proxy fence before the TMA reads
+            const unsigned long long tw = p.trace ? globaltimer_ns() : 0;
+            const int last = (sg.kb1 - 1) >> J.dep_shift;
+            while (true) {
+              const int q = need + static_cast<int>(lane);
+              bool ok = true;
+              if (q <= last) ok = static_cast<int>(ld_relaxed_gpu(J.dep_flag + q) - p.epoch) >= 0;
+              const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+              const int nready = bad ? __ffs(bad) - 1 : 32;
+              if (nready > 0) {
+                have = need + nready - 1;
+                break;
+              }
+              wait_flag(J.dep_flag + need, p.epoch);  // the first one is not ready: block on it
+            }
+            fence_acq_rel_gpu();
             fence_proxy_async_global();
-            have = need;
+            if (p.trace && rank == 0 && lane == 0 && si - seg_begin < kChainTraceSegs)
+              p.trace[(static_cast<size_t>(pair) * kChainTraceSegs + (si - seg_begin)) * 8 + 5] += globaltimer_ns() - tw;
           }
         }
         tma_load_2d_pair_warp(b, mx, &full[s], kb * kBK, static_cast<int>(rank) * (ni / 2), pol_x);
@@ -206,9 +230,14 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
           tb_idx = buf;
         }
         tc_fence_after();
+        unsigned long long* tr = (p.trace && seg < kChainTraceSegs && lane == 0)
+                                     ? p.trace + (static_cast<size_t>(pair) * kChainTraceSegs + seg) * 8
+                                     : nullptr;
+        if (tr) tr[0] = globaltimer_ns();
         for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          if (tr && kb == sg.kb0) tr[1] = globaltimer_ns();
           const uint32_t a = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
           const uint32_t b = a + kABytes;
 #pragma unroll
@@ -225,6 +254,11 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
             s = 0;
             ph ^= 1;
           }
+        }
+        if (tr) {
+          tr[2] = globaltimer_ns();
+          tr[6] = (static_cast<unsigned long long>(sg.job) << 48) | (static_cast<unsigned long long>(sg.pt) << 32) |
+                  (static_cast<unsigned long long>(sg.kb0) << 16) | static_cast<unsigned long long>(sg.kb1);
         }
       }
     }
@@ -319,6 +353,10 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
       }
       __syncwarp();
       tc_fence_after();
+      unsigned long long* tre = (p.trace && rank == 0 && et == 0 && seg < kChainTraceSegs)
+                                    ? p.trace + (static_cast<size_t>(pair) * kChainTraceSegs + seg) * 8
+                                    : nullptr;
+      if (tre) tre[3] = globaltimer_ns();
       const uint32_t trow = tmem + ((quarter * 32u) << 16);
       auto scale = [&](int ch, float (&v)[16]) {
         if (scaled) {
@@ -412,22 +450,23 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
         if (s_last && in_range) {
           __threadfence();
           // finalise 128 columns: X' = bf16(g * h) and the per-token sum of squares (one warp per
-          // token, 4 columns per lane; 4 tokens per iteration for memory-level parallelism)
+          // 16-token block, 4 columns per lane, all 16 loads in flight; a transpose-reduction leaves
+          // token u's sum in lanes 2u, 2u+1 after 16 shuffles)
           const float* hsrc = static_cast<const float*>(ep.out);
           const int c0 = mt * kBM + static_cast<int>(lane) * 4;
           const uint2 graw = __ldg(reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(J.fin_g) + c0));
           const float2 g01 = unpack_bf16x2(graw.x), g23 = unpack_bf16x2(graw.y);
           __nv_bfloat16* xa = static_cast<__nv_bfloat16*>(J.fin_xa);
-          for (int t0 = ew * 4; t0 < tvalid; t0 += 8 * 4) {
-            float4 x[4];
-            float ss[4];
+          for (int t0 = ew * 16; t0 < tvalid; t0 += 8 * 16) {
+            float4 x[16];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < 16; ++u)
               x[u] = t0 + u < tvalid ? __ldcg(reinterpret_cast<const float4*>(hsrc + static_cast<size_t>(t0 + u) * ep.ldo + c0))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+            float r[16];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              ss[u] = x[u].x * x[u].x + x[u].y * x[u].y + x[u].z * x[u].z + x[u].w * x[u].w;
+            for (int u = 0; u < 16; ++u) {
+              r[u] = x[u].x * x[u].x + x[u].y * x[u].y + x[u].z * x[u].z + x[u].w * x[u].w;
               if (t0 + u < tvalid) {
                 uint2 pk;
                 pk.x = pack_bf16x2(g01.x * x[u].x, g01.y * x[u].y);
@@ -436,13 +475,17 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
               }
             }
 #pragma unroll
-            for (int off = 16; off >= 1; off >>= 1)
+            for (int w = 8; w >= 1; w >>= 1) {  // offsets 16, 8, 4, 2: keep half of the values
+              const bool hi = (lane & (2 * w)) != 0;
 #pragma unroll
-              for (int u = 0; u < 4; ++u) ss[u] += __shfl_xor_sync(0xffffffffu, ss[u], off);
-            if (lane == 0)
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (t0 + u < tvalid) J.fin_ss[static_cast<size_t>(mt) * p.ss_ld + t0 + u] = ss[u];
+              for (int i = 0; i < w; ++i) {
+                const float keep = hi ? r[i + w] : r[i], send = hi ? r[i] : r[i + w];
+                r[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * w);
+              }
+            }
+            r[0] += __shfl_xor_sync(0xffffffffu, r[0], 1);
+            const int u = static_cast<int>(lane >> 1);
+            if ((lane & 1) == 0 && t0 + u < tvalid) J.fin_ss[static_cast<size_t>(mt) * p.ss_ld + t0 + u] = r[0];
           }
           fence_proxy_async_global();
           __threadfence();
@@ -455,6 +498,7 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
         named_bar_sync(1, kEpiThreads);
         if (et == 0 && in_range) st_release_gpu(J.flag_out + mt, p.epoch);
       }
+      if (tre) tre[4] = globaltimer_ns();
     }
   }
 

@@ -278,6 +278,7 @@ ChainSchedule schedule_chain(const std::vector<ChainJobShape>& jobs, int P, doub
   ChainSchedule out;
   P = std::max(1, P);
   std::vector<double> f(P, 0.0);                 // time each pair's MMA pipe becomes free
+  std::vector<double> g(P, 0.0);                 // time each pair's epilogue warps become free
   std::vector<std::vector<std::array<int, 4>>> per(P);
   std::vector<double> prev_ready;                // previous job: time each 128-row tile is published
   out.need.resize(jobs.size());
@@ -305,7 +306,8 @@ ChainSchedule schedule_chain(const std::vector<ChainJobShape>& jobs, int P, doub
         const double end = std::max(f[c] + KB, D);
         per[c].push_back({static_cast<int>(j), pt, 0, KB});
         f[c] = end;
-        ready[2 * pt] = ready[2 * pt + 1] = end + J.e_done;
+        g[c] = std::max(end, g[c]) + J.e_done;
+        ready[2 * pt] = ready[2 * pt + 1] = g[c];
         out.need[j][pt] = 1;
       }
     } else {
@@ -320,73 +322,130 @@ ChainSchedule schedule_chain(const std::vector<ChainJobShape>& jobs, int P, doub
       std::stable_sort(bands.begin(), bands.end(), [&](const std::pair<int, int>& a, const std::pair<int, int>& b) {
         return dep[a.first] < dep[b.first];
       });
-      struct Run {
-        int pt, k0, k1;
-      };
-      std::vector<Run> runs;
-      for (const auto& b : bands)
-        for (int pt = 0; pt < J.pm_tiles; ++pt) runs.push_back({pt, b.first, b.second});
-      const long long U = static_cast<long long>(J.pm_tiles) * KB;
-      // water-filling: pairs by free time; all pairs below the level T_end share U
-      std::vector<int> order(P);
-      for (int c = 0; c < P; ++c) order[c] = c;
-      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return f[a] < f[b]; });
-      int m = P;
-      double T_end = 0.0;
-      for (; m >= 1; --m) {
-        double S = 0.0;
-        for (int i = 0; i < m; ++i) S += f[order[i]];
-        T_end = (static_cast<double>(U) + S) / m;
-        if (m == 1 || T_end >= f[order[m - 1]]) break;
-      }
-      std::vector<long long> budget(m, 0);
-      {
-        double cum = 0.0;
-        long long given = 0;
-        for (int i = 0; i < m; ++i) {
-          cum += T_end - f[order[i]];
-          const long long upto = (i == m - 1) ? U : std::min<long long>(U, std::llround(cum));
-          budget[i] = std::max<long long>(0, upto - given);
-          given += budget[i];
-        }
-        // too-short ranges cost a whole epilogue: fold them into the next (or previous) pair
-        for (int i = 0; i < m; ++i)
-          if (budget[i] > 0 && budget[i] < min_seg) {
-            int k = i + 1;
-            if (k >= m)
-              for (k = i - 1; k > 0 && budget[k] == 0; --k) {
+      // per band (in readiness order) two candidate partitions, simulated, the better one kept:
+      //  * water-filling: the band's units (tile-major) as contiguous ranges over the pairs'
+      //    effective free times max(f, band ready), every pair ending together;
+      //  * tile-aligned: each tile's k-range cut into n equal parts (one segment, one residual-add
+      //    epilogue per pair: no pair straddles two tiles), n = 1 .. pairs / tiles.
+      std::vector<double> contrib(J.pm_tiles, 0.0);
+      for (const auto& band : bands) {
+        const int bk0 = band.first, bk1 = band.second, len = bk1 - bk0;
+        double bready = 0.0;
+        for (int kb = bk0; kb < bk1; ++kb) bready = std::max(bready, dep[kb]);
+        const long long U = static_cast<long long>(J.pm_tiles) * len;
+        std::vector<double> eff(P);
+        for (int c = 0; c < P; ++c) eff[c] = std::max(f[c], bready);
+        std::vector<int> order(P);
+        for (int c = 0; c < P; ++c) order[c] = c;
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return eff[x] < eff[y]; });
+        using Assign = std::vector<std::array<int, 4>>;  // pair, tile, k0, k1 (execution order per pair)
+        auto evaluate = [&](const Assign& as, std::vector<double>* f2, std::vector<double>* g2,
+                            std::vector<double>* c2) {
+          *f2 = f;
+          *g2 = g;
+          *c2 = contrib;
+          for (const auto& x : as) {
+            const double t = run((*f2)[x[0]], x[2], x[3]);
+            (*f2)[x[0]] = t;
+            const double e = std::max(t, (*g2)[x[0]]) + e_add;  // epilogues of a pair run in order
+            (*g2)[x[0]] = e;
+            (*c2)[x[1]] = std::max((*c2)[x[1]], e);
+          }
+          double mx = 0.0;
+          for (int pt = 0; pt < J.pm_tiles; ++pt) mx = std::max(mx, (*c2)[pt]);
+          return mx;
+        };
+        Assign best;
+        double best_end = 1e300;
+        {  // water-filling
+          int m = P;
+          double T_end = 0.0;
+          for (; m >= 1; --m) {
+            double S = 0.0;
+            for (int i = 0; i < m; ++i) S += eff[order[i]];
+            T_end = (static_cast<double>(U) + S) / m;
+            if (m == 1 || T_end >= eff[order[m - 1]]) break;
+          }
+          std::vector<long long> budget(m, 0);
+          double cum = 0.0;
+          long long given = 0;
+          for (int i = 0; i < m; ++i) {
+            cum += T_end - eff[order[i]];
+            const long long upto = (i == m - 1) ? U : std::min<long long>(U, std::llround(cum));
+            budget[i] = std::max<long long>(0, upto - given);
+            given += budget[i];
+          }
+          for (int i = 0; i < m; ++i)  // too-short ranges cost a whole epilogue: fold into a neighbour
+            if (budget[i] > 0 && budget[i] < min_seg) {
+              int k = i + 1;
+              if (k >= m)
+                for (k = i - 1; k > 0 && budget[k] == 0; --k) {
+                }
+              if (k >= 0 && k != i) {
+                budget[k] += budget[i];
+                budget[i] = 0;
               }
-            if (k >= 0 && k != i) {
-              budget[k] += budget[i];
-              budget[i] = 0;
+            }
+          Assign as;
+          int rpt = 0, rk = bk0;
+          for (int i = 0; i < m; ++i) {
+            long long n = budget[i];
+            while (n > 0 && rpt < J.pm_tiles) {
+              const int take = static_cast<int>(std::min<long long>(n, bk1 - rk));
+              as.push_back({order[i], rpt, rk, rk + take});
+              n -= take;
+              rk += take;
+              if (rk == bk1) {
+                ++rpt;
+                rk = bk0;
+              }
             }
           }
-      }
-      std::vector<double> contrib(J.pm_tiles, 0.0);
-      size_t r = 0;
-      int rk = runs.empty() ? 0 : runs[0].k0;  // cursor inside runs[r]
-      for (int i = 0; i < m; ++i) {
-        const int c = order[i];
-        long long n = budget[i];
-        double t = f[c];
-        while (n > 0 && r < runs.size()) {
-          const Run& R = runs[r];
-          const int take = static_cast<int>(std::min<long long>(n, R.k1 - rk));
-          // merge with this pair's previous segment when it continues the same tile's k-range
-          auto& v = per[c];
-          if (!v.empty() && v.back()[0] == static_cast<int>(j) && v.back()[1] == R.pt && v.back()[3] == rk) {
-            v.back()[3] = rk + take;
-          } else {
-            v.push_back({static_cast<int>(j), R.pt, rk, rk + take});
-            ++out.need[j][R.pt];
-          }
-          t = run(t, rk, rk + take);
-          contrib[R.pt] = std::max(contrib[R.pt], t + e_add);
-          n -= take;
-          rk += take;
-          if (rk == R.k1 && ++r < runs.size()) rk = runs[r].k0;
+          std::vector<double> f2, g2, c2;
+          best_end = evaluate(as, &f2, &g2, &c2);
+          best = as;
         }
-        f[c] = t;
+        for (int n = 1; n <= std::max(1, P / J.pm_tiles) && n <= len; ++n) {  // tile-aligned
+          // parts of each tile's range, longest first; the pm * n parts go to the earliest pairs
+          std::vector<std::array<int, 3>> parts;  // tile, k0, k1
+          for (int pt = 0; pt < J.pm_tiles; ++pt)
+            for (int q = 0; q < n; ++q)
+              parts.push_back({pt, bk0 + static_cast<int>(static_cast<long long>(len) * q / n),
+                               bk0 + static_cast<int>(static_cast<long long>(len) * (q + 1) / n)});
+          std::stable_sort(parts.begin(), parts.end(),
+                           [](const std::array<int, 3>& x, const std::array<int, 3>& y) { return x[2] - x[1] > y[2] - y[1]; });
+          Assign as;
+          std::vector<double> load(eff);
+          for (const auto& pr : parts) {  // LPT on the effective free times
+            int c = 0;
+            for (int k = 1; k < P; ++k)
+              if (load[k] < load[c]) c = k;
+            as.push_back({c, pr[0], pr[1], pr[2]});
+            load[c] += pr[2] - pr[1];
+          }
+          std::vector<double> f2, g2, c2;
+          const double e = evaluate(as, &f2, &g2, &c2);
+          if (e < best_end - 1e-9) {
+            best_end = e;
+            best = as;
+          }
+        }
+        // commit the kept partition
+        for (const auto& x : best) {
+          const int c = x[0];
+          auto& v = per[c];  // merge with this pair's previous segment when it continues the k-range
+          if (!v.empty() && v.back()[0] == static_cast<int>(j) && v.back()[1] == x[1] && v.back()[3] == x[2]) {
+            v.back()[3] = x[3];
+          } else {
+            v.push_back({static_cast<int>(j), x[1], x[2], x[3]});
+            ++out.need[j][x[1]];
+          }
+        }
+        std::vector<double> f2, g2, c2;
+        evaluate(best, &f2, &g2, &c2);
+        f = f2;
+        g = g2;
+        contrib = c2;
       }
       for (int pt = 0; pt < J.pm_tiles; ++pt) ready[2 * pt] = ready[2 * pt + 1] = contrib[pt] + e_fin;
     }

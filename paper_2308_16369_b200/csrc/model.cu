@@ -389,6 +389,22 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   pp_pairs = ((Tmax + 127) / 128) * nq_l;
   SRET(dalloc(&pp_ctr, pp_pairs));
   SRET(check(cudaMemset(pp_ctr, 0, pp_pairs * sizeof(int)), "memset"));
+  // layer chain (world == 1; SARATHI_CHAIN=0 keeps one launch per GEMM + RMSNorm kernels)
+  {
+    const char* ce = getenv("SARATHI_CHAIN");
+    chain_on = world == 1 && H % 128 == 0 && !(ce && ce[0] == '0');
+  }
+  if (chain_on) {
+    nt_h = 2 * ((H + 255) / 256);
+    nt_gu = 2 * ((gu_rows + 255) / 256);
+    SRET(dalloc(&a2, static_cast<size_t>(Tmax) * H));
+    SRET(dalloc(&ss1, static_cast<size_t>(nt_h) * Tmax));
+    SRET(dalloc(&ss2, static_cast<size_t>(nt_h) * Tmax));
+    SRET(dalloc(&cflags, static_cast<size_t>(2 * nt_h + nt_gu)));
+    SRET(dalloc(&ccnt, static_cast<size_t>(2 * nt_h)));
+    SRET(check(cudaMemset(cflags, 0, (2 * nt_h + nt_gu) * sizeof(unsigned)), "memset"));
+    SRET(check(cudaMemset(ccnt, 0, 2 * nt_h * sizeof(int)), "memset"));
+  }
   SRET(check(cudaStreamSynchronize(stream), "init sync"));
   return Status::ok();
 }
@@ -491,26 +507,233 @@ Status Model::take_span(int op, unsigned long long** start, unsigned long long**
   return Status::ok();
 }
 
+Status Model::xmap(const void* X, int N, int K, int ldx, int box_rows, const CUtensorMap** out) {
+  auto xk = std::make_tuple(X, N, K, box_rows);
+  auto xi = xmaps.find(xk);
+  if (xi == xmaps.end()) {
+    CUtensorMap m;
+    if (!make_tmap_bf16(&m, X, N, K, ldx, box_rows)) return Status::err(SARATHI_ECUDA, "tensor map (activation)");
+    xi = xmaps.emplace(xk, m).first;
+  }
+  *out = &xi->second;
+  return Status::ok();
+}
+
+// Schedule of the layer chain for T tokens (cached per (T, with_qkv)): host list schedule
+// (host_sched.cpp schedule_chain) uploaded once; costs in k-block units, env
+// SARATHI_CHAIN_COSTS="silu,qkv,add,fin" overrides them for experiments.
+Status Model::chain_plan(int T, bool with_qkv, const ChainPlanDev** out) {
+  auto key = std::make_pair(T, with_qkv ? 1 : 0);
+  auto it = chain_plans.find(key);
+  if (it != chain_plans.end()) {
+    *out = &it->second;
+    return Status::ok();
+  }
+  ChainPlanDev pd;
+  if (!plan_chain_tiling(T, &pd.base)) return Status::err(SARATHI_EINVAL, "chain: T needs more than one token tile");
+  static double costs[4] = {22.0, 27.0, 16.0, 6.0};
+  static bool costs_read = false;
+  if (!costs_read) {
+    costs_read = true;
+    if (const char* ce = getenv("SARATHI_CHAIN_COSTS"))
+      sscanf(ce, "%lf,%lf,%lf,%lf", &costs[0], &costs[1], &costs[2], &costs[3]);
+  }
+  const int H = cfg.hidden;
+  const bool swiglu = cfg.ffn_kind == SARATHI_FFN_SWIGLU;
+  std::vector<ChainJobShape> jobs(with_qkv ? 4 : 3);
+  jobs[0] = {(H + 255) / 256, q_dim_l / 64, true, -1, 0.0};
+  jobs[1] = {(gu_rows + 255) / 256, H / 64, false, 1, swiglu ? costs[0] : costs[0]};
+  jobs[2] = {(H + 255) / 256, h2_l / 64, true, swiglu ? 0 : 1, 0.0};
+  if (with_qkv) jobs[3] = {(qkv_rows + 255) / 256, H / 64, false, 1, costs[1]};
+  pd.sch = schedule_chain(jobs, num_sms / 2, costs[2], costs[3]);
+  const ChainSchedule& sc = pd.sch;
+  const int pairs = num_sms / 2;
+  std::vector<int> blob(sc.segs);
+  blob.insert(blob.end(), sc.seg_off.begin(), sc.seg_off.end());
+  pd.need_o = static_cast<int>(blob.size());
+  blob.insert(blob.end(), sc.need[0].begin(), sc.need[0].end());
+  pd.need_f2 = static_cast<int>(blob.size());
+  blob.insert(blob.end(), sc.need[2].begin(), sc.need[2].end());
+  SRET(dalloc(&pd.dev, blob.size()));
+  SRET(check(cudaMemcpy(pd.dev, blob.data(), blob.size() * sizeof(int), cudaMemcpyHostToDevice), "chain plan"));
+  pd.base.segs = pd.dev;
+  pd.base.seg_off = pd.dev + sc.segs.size();
+  pd.base.pairs = pairs;
+  pd.base.ss_ld = Tmax;
+  if (getenv("SARATHI_CHAIN_PRINT")) {
+    fprintf(stderr, "chain T=%d qkv=%d: %zu segments, predicted makespan %.1f k-blocks (job ends", T, with_qkv ? 1 : 0,
+            sc.segs.size() / 4, sc.makespan);
+    for (double e : sc.job_end) fprintf(stderr, " %.1f", e);
+    fprintf(stderr, ")\n");
+  }
+  it = chain_plans.emplace(key, pd).first;
+  *out = &it->second;
+  return Status::ok();
+}
+
+// One layer's GEMM phase as a chain launch: O(l) + residual -> FFN1(l) -> FFN2(l) + residual ->
+// [QKV(l+1) + RoPE + KV append] (see gemm_chain.cu).
+Status Model::run_chain(int l, int T, bool with_qkv, const int* d_pos_dev, const int* d_slot_dev) {
+  const ChainPlanDev* pd = nullptr;
+  SRET(chain_plan(T, with_qkv, &pd));
+  const int H = cfg.hidden;
+  const bool swiglu = cfg.ffn_kind == SARATHI_FFN_SWIGLU;
+  LayerWeights& w = layers[l];
+  ChainLaunch cl = pd->base;
+  ChainMaps maps;
+  const int box = cl.bn / cl.n_mma / 2;
+  unsigned* f_o = cflags;
+  unsigned* f_gu = cflags + nt_h;
+  unsigned* f_dn = cflags + nt_h + nt_gu;
+  const CUtensorMap* mx = nullptr;
+  cl.epoch = ++chain_epoch;
+  if (cl.epoch == 0) cl.epoch = chain_epoch = 1;  // (2^32 launches) flags compare by signed difference
+  cl.njobs = with_qkv ? 4 : 3;
+  // job 0: O projection, h += o Wo^T; finalise: a2 = bf16(g2 * h), ss2
+  {
+    ChainJobDev& J = cl.job[0];
+    J.ep.mode = EPI_ADD_F32;
+    J.ep.out = h;
+    J.ep.ldo = H;
+    J.M = H;
+    J.KB = q_dim_l / 64;
+    J.fin_cnt = ccnt;
+    J.fin_need = pd->dev + pd->need_o;
+    J.fin_g = w.g2;
+    J.fin_xa = a2;
+    J.fin_ss = ss2;
+    J.flag_out = f_o;
+    maps.w[0] = w.m_o;
+    SRET(xmap(o, T, q_dim_l, q_dim_l, box, &mx));
+    maps.x[0] = *mx;
+  }
+  // job 1: FFN1 (gate||up + SiLU*up, or W1 + GELU) on a2, scaled by rsqrt(mean h^2 + eps)
+  {
+    ChainJobDev& J = cl.job[1];
+    J.ep.mode = swiglu ? EPI_SILU_MUL : EPI_GELU;
+    J.ep.out = f;
+    J.ep.ldo = h2_l;
+    J.M = gu_rows;
+    J.KB = H / 64;
+    J.dep_flag = f_o;
+    J.dep_shift = 1;
+    J.ss_in = ss2;
+    J.ss_parts = H / 128;
+    J.inv_h = 1.0f / static_cast<float>(H);
+    J.eps = cfg.rms_eps;
+    J.flag_out = f_gu;
+    maps.w[1] = w.m_gu;
+    SRET(xmap(a2, T, H, H, box, &mx));
+    maps.x[1] = *mx;
+  }
+  // job 2: FFN2, h += f Wd^T; finalise (when the next QKV follows): a = bf16(g1' * h), ss1
+  {
+    ChainJobDev& J = cl.job[2];
+    J.ep.mode = EPI_ADD_F32;
+    J.ep.out = h;
+    J.ep.ldo = H;
+    J.M = H;
+    J.KB = h2_l / 64;
+    J.dep_flag = f_gu;
+    J.dep_shift = swiglu ? 0 : 1;
+    if (with_qkv) {
+      J.fin_cnt = ccnt + nt_h;
+      J.fin_need = pd->dev + pd->need_f2;
+      J.fin_g = layers[l + 1].g1;
+      J.fin_xa = a;
+      J.fin_ss = ss1;
+      J.flag_out = f_dn;
+    }
+    maps.w[2] = w.m_down;
+    SRET(xmap(f, T, h2_l, h2_l, box, &mx));
+    maps.x[2] = *mx;
+  }
+  if (with_qkv) {
+    LayerWeights& wn = layers[l + 1];
+    ChainJobDev& J = cl.job[3];
+    EpiParams& e = J.ep;
+    e.mode = EPI_QKV_ROPE;
+    e.out = q;
+    e.ldo = q_dim_l;
+    e.pos = d_pos_dev;
+    e.slot = d_slot_dev;
+    e.rope_theta = rope_theta;
+    e.kcache = kpool[l + 1];
+    e.vcache = vpool[l + 1];
+    e.head_dim = cfg.head_dim;
+    e.n_q_local = nq_l;
+    e.n_kv_local = nkv_l;
+    e.block_size = block_size;
+    J.M = qkv_rows;
+    J.KB = H / 64;
+    J.dep_flag = f_dn;
+    J.dep_shift = 1;
+    J.ss_in = ss1;
+    J.ss_parts = H / 128;
+    J.inv_h = 1.0f / static_cast<float>(H);
+    J.eps = cfg.rms_eps;
+    maps.w[3] = wn.m_qkv;
+    SRET(xmap(a, T, H, H, box, &mx));
+    maps.x[3] = *mx;
+  }
+  ++launches;
+  SRET(take_span(SARATHI_OP_GEMM_CHAIN, &cl.span_start, &cl.span_end));
+  // debug: SARATHI_CHAIN_TRACE=<T> prints the timeline of the first chain launch with T tokens
+  // at layer 1 (per pair: segments with mainloop / epilogue stamps and producer dependency waits)
+  static const char* ctr = getenv("SARATHI_CHAIN_TRACE");
+  static bool ctraced = false;
+  if (ctr && !ctraced && atoi(ctr) == T && l == 1) {
+    ctraced = true;
+    const size_t n = static_cast<size_t>(cl.pairs) * kChainTraceSegs * 8 + 8;
+    unsigned long long* tr = nullptr;
+    cudaMalloc(&tr, n * 8);
+    cudaMemsetAsync(tr, 0, n * 8, stream);
+    cl.trace = tr;
+    const Status st = check(launch_chain(maps, cl, swiglu ? EPI_SILU_MUL : EPI_GELU, stream), "chain launch");
+    std::vector<unsigned long long> hb(n);
+    cudaStreamSynchronize(stream);
+    cudaMemcpy(hb.data(), tr, n * 8, cudaMemcpyDeviceToHost);
+    cudaFree(tr);
+    const unsigned long long t0 = hb[static_cast<size_t>(cl.pairs) * kChainTraceSegs * 8];
+    auto us = [&](unsigned long long t) { return t ? (static_cast<double>(t) - static_cast<double>(t0)) * 1e-3 : -1.0; };
+    double jmax[4][3] = {};  // per job: last commit, last published, sum of dep waits
+    double jmin[4];
+    for (double& x : jmin) x = 1e30;
+    for (int c = 0; c < cl.pairs; ++c) {
+      fprintf(stderr, "pair %2d:", c);
+      for (int sgi = 0; sgi < kChainTraceSegs; ++sgi) {
+        const unsigned long long* e = &hb[(static_cast<size_t>(c) * kChainTraceSegs + sgi) * 8];
+        if (!e[0]) break;
+        const int jb = static_cast<int>(e[6] >> 48), pt = static_cast<int>((e[6] >> 32) & 0xFFFF);
+        const int k0 = static_cast<int>((e[6] >> 16) & 0xFFFF), k1 = static_cast<int>(e[6] & 0xFFFF);
+        fprintf(stderr, " [j%d t%d %d-%d mma %.1f|%.1f-%.1f epi %.1f-%.1f w%.1f]", jb, pt, k0, k1, us(e[0]), us(e[1]),
+                us(e[2]), us(e[3]), us(e[4]), e[5] * 1e-3);
+        if (jb < 4) {
+          jmin[jb] = std::min(jmin[jb], us(e[1]));
+          jmax[jb][0] = std::max(jmax[jb][0], us(e[2]));
+          jmax[jb][1] = std::max(jmax[jb][1], us(e[4]));
+          jmax[jb][2] += e[5] * 1e-3;
+        }
+      }
+      fprintf(stderr, "\n");
+    }
+    for (int jb = 0; jb < cl.njobs; ++jb)
+      fprintf(stderr, "job %d: first stage %.1f us, last commit %.1f us, last published %.1f us, dep waits %.1f pair-us\n",
+              jb, jmin[jb], jmax[jb][0], jmax[jb][1], jmax[jb][2]);
+    return st;
+  }
+  return check(launch_chain(maps, cl, swiglu ? EPI_SILU_MUL : EPI_GELU, stream), "chain launch");
+}
+
 Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, int N, const EpiParams& ep_in, int op) {
   const bool atomic = ep_in.mode == EPI_ADD_F32;
   auto pk = std::make_tuple(M, N, K * 2 + (atomic ? 1 : 0));
   auto it = plans.find(pk);
   if (it == plans.end()) it = plans.emplace(pk, plan_gemm(M, N, K, num_sms, gemm_ws_floats, 0, atomic)).first;
   const GemmPlan& pl = it->second;
-  auto xmap = [&](int box_rows, const CUtensorMap** out) -> Status {
-    auto xk = std::make_tuple(X, N, K, box_rows);
-    auto xi = xmaps.find(xk);
-    if (xi == xmaps.end()) {
-      CUtensorMap m;
-      if (!make_tmap_bf16(&m, X, N, K, ldx, box_rows)) return Status::err(SARATHI_ECUDA, "tensor map (activation)");
-      xi = xmaps.emplace(xk, m).first;
-    }
-    *out = &xi->second;
-    return Status::ok();
-  };
   const CUtensorMap *mx = nullptr, *mx2 = nullptr;
-  SRET(xmap(pl.box_rows, &mx));
-  SRET(xmap(pl.box_rows2, &mx2));
+  SRET(xmap(X, N, K, ldx, pl.box_rows, &mx));
+  SRET(xmap(X, N, K, ldx, pl.box_rows2, &mx2));
   EpiParams ep = ep_in;
   ep.ws = gemm_ws;
   ep.ws_red = gemm_ws + gemm_ws_floats / 2;
@@ -762,8 +985,12 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   bool pending_ar = false;  // TP: down-proj partial in `ar` not yet added to h
   static const bool no_aux = getenv("SARATHI_NO_AUX") != nullptr;  // experiment: serial attention
   static const bool attn_chain = !(getenv("SARATHI_ATTN_CHAIN") && atoi(getenv("SARATHI_ATTN_CHAIN")) == 0);
+  // layer chain: layer l's O -> FFN1 -> FFN2 and layer l+1's RMSNorm + QKV run as ONE launch
+  // (gemm_chain.cu), so a layer after the first starts at its attention
+  const bool use_chain = chain_on && gemm_token_tiling(T).n_tiles == 1;
   for (int l = 0; l < nl; ++l) {  // this stage's layers (local index)
     LayerWeights& w = layers[l];
+    if (l == 0 || !use_chain) {
     ob = op_begin();
     {
       unsigned long long *sp0, *sp1;
@@ -774,7 +1001,9 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     op_end(SARATHI_OP_RMSNORM, ob);
     ++launches;
     pending_ar = false;
+    }
     if (l > 0) SRET(dump_h(l));  // h after layer l-1 (TP: once the all-reduce has been added)
+    if (l == 0 || !use_chain) {
     EpiParams e;
     e.mode = EPI_QKV_ROPE;
     e.out = q;
@@ -791,6 +1020,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     ob = op_begin();
     SRET(gemm(w.m_qkv, qkv_rows, H, a, H, T, e, SARATHI_OP_GEMM_QKV));
     op_end(SARATHI_OP_GEMM_QKV, ob);
+    }
     const bool chain = attn_chain && p > 0 && d > 0 && !no_aux;
     if (p > 0) {
       PrefillAttnArgs pa;
@@ -953,6 +1183,12 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       op_end(SARATHI_OP_DECODE_ATTN, ob);
       launches += da.splits > 1 ? 2 : 1;
       if (p > 0 && !no_aux && !chain) SRET(check(cudaStreamWaitEvent(stream, ev_join, 0), "join"));
+    }
+    if (use_chain) {
+      ob = op_begin();
+      SRET(run_chain(l, T, l + 1 < nl, d_pos, d_slot));
+      op_end(SARATHI_OP_GEMM_CHAIN, ob);
+      continue;
     }
     // O-projection (postproj) + residual / TP all-reduce
     EpiParams eo;

@@ -151,6 +151,26 @@ struct Model {
   bool tp_nvls = false;
   void* nvls = nullptr;                          // NvlsState
   const __nv_bfloat16* mm_ar[2] = {nullptr, nullptr};
+  // layer chain (gemm_chain.cu, world == 1): O -> FFN1 -> FFN2 -> next layer's QKV in ONE launch,
+  // tile-level flags instead of kernel boundaries, RMSNorm folded into finalisers + epilogue scales
+  bool chain_on = false;
+  __nv_bfloat16* a2 = nullptr;        // FFN1 input bf16(g2 * h), written by the O finalisers [Tmax][H]
+  float* ss1 = nullptr;               // per-128-column sums of squares of h for the next QKV [H/128][Tmax]
+  float* ss2 = nullptr;               // ... for FFN1
+  unsigned* cflags = nullptr;         // O fin [nt_h] | FFN1 out [nt_gu] | FFN2 fin [nt_h] (epoch-valued)
+  int* ccnt = nullptr;                // O fin counters [nt_h] | FFN2 fin counters [nt_h]
+  int nt_h = 0, nt_gu = 0;            // 128-row tiles (rounded up to pair tiles)
+  unsigned chain_epoch = 0;
+  struct ChainPlanDev {
+    ChainSchedule sch;
+    int* dev = nullptr;  // segs | seg_off | need(O) | need(FFN2)
+    ChainLaunch base;
+    int need_o = 0, need_f2 = 0;  // offsets (ints) of the need arrays in dev
+  };
+  std::map<std::pair<int, int>, ChainPlanDev> chain_plans;  // (T, with next QKV)
+  Status chain_plan(int T, bool with_qkv, const ChainPlanDev** out);
+  Status run_chain(int l, int T, bool with_qkv, const int* d_pos, const int* d_slot);
+  Status xmap(const void* X, int N, int K, int ldx, int box_rows, const CUtensorMap** out);
   int64_t launches = 0;
   // I/O accounting and per-op timers
   int64_t last_h2d = 0, last_d2h = 0;

@@ -35,10 +35,11 @@ EXPORTS = [
     "sarathi_request_truncate", "sarathi_last_io_bytes", "sarathi_set_profiling", "sarathi_op_times", "sarathi_op_kernel_times",
     "sarathi_op_pack_weight", "sarathi_shard_map", "sarathi_local_group_create", "sarathi_local_group_destroy",
     "sarathi_token_capacity", "sarathi_chunk_advice", "sarathi_stage_input", "sarathi_stage_output",
+    "sarathi_chain_schedule",
 ]
 GEMM_W_PACKED = 0x100
 OP_NAMES = ["embed", "rmsnorm", "gemm_qkv", "prefill_attn", "decode_attn", "gemm_o", "gemm_gate_up",
-            "gemm_down", "lm_head", "allreduce", "other"]
+            "gemm_down", "lm_head", "allreduce", "other", "gemm_chain"]
 
 
 class SarathiError(RuntimeError):
@@ -114,6 +115,8 @@ def _load() -> C.CDLL:
         "sarathi_local_group_create": [I32, I32, P(VP)],
         "sarathi_token_capacity": [I32, P(I32), P(I32), P(I32)],
         "sarathi_chunk_advice": [I32, I32, I32, P(I32)],
+        "sarathi_chain_schedule": [I32, P(I32), P(I32), P(I32), P(I32), P(C.c_double), I32, C.c_double, C.c_double,
+                                   P(I32), P(I32), I32, P(I32), P(C.c_double)],
         "sarathi_stage_input": [VP, VP],
         "sarathi_stage_output": [VP, P(VP), P(I32)],
         "sarathi_shard_map": [P(ModelConfigC), I32, I32, I32, I32, P(I32), P(F), P(I64), I32, P(I32), P(I32)],
@@ -423,6 +426,22 @@ def chunk_advice(C_: int, d: int, remaining: int) -> int:
     v = C.c_int32()
     _check(lib.sarathi_chunk_advice(C_, d, remaining, C.byref(v)))
     return v.value
+
+
+def chain_schedule(jobs, pairs: int, e_add: float, e_fin: float):
+    """Layer-chain work list (host only): jobs = [(pm_tiles, KB, split, dep_shift, e_done)].
+    Returns (seg_off [pairs + 1], segs [n, 4] = (job, pair tile, kb0, kb1), predicted makespan)."""
+    nj = len(jobs)
+    col = lambda i, dt: np.ascontiguousarray([j[i] for j in jobs], dtype=dt)
+    pm, kb, sp, ds, ed = col(0, np.int32), col(1, np.int32), col(2, np.int32), col(3, np.int32), col(4, np.float64)
+    cap = 8 * pairs + 4 * int(sum(j[0] for j in jobs)) + 64
+    off = np.zeros(pairs + 1, np.int32)
+    segs = np.zeros(4 * cap, np.int32)
+    n, ms = C.c_int32(), C.c_double()
+    _check(lib.sarathi_chain_schedule(nj, _p(pm, C.c_int32), _p(kb, C.c_int32), _p(sp, C.c_int32), _p(ds, C.c_int32),
+                                      _p(ed, C.c_double), pairs, e_add, e_fin, _p(off, C.c_int32), _p(segs, C.c_int32),
+                                      cap, C.byref(n), C.byref(ms)))
+    return off, segs[: 4 * n.value].reshape(-1, 4), ms.value
 
 
 def op_gemm(W_ptr: int, X_ptr: int, out_ptr: int, M: int, N: int, K: int, mode: int, force_splits: int = 0,

@@ -108,6 +108,13 @@ struct ChainJobDev {
   const float* ss_in = nullptr;      // [ss_parts][ss_ld]; published with dep_flag[0 .. ss_parts)
   int ss_parts = 0;
   float inv_h = 0.f, eps = 0.f;
+  // split whole-tile jobs (activation / RoPE epilogues): the need[pt] contributors of a pair tile
+  // bulk-reduce-add their partials into scratch slabs (ChainMaps::scr columns slab[pt] * 256 +
+  // rank * 128 ...); the last to arrive loads the sum back, adds its own accumulator, runs the
+  // epilogue and re-zeroes the slab
+  const int* slab = nullptr;         // [pair tiles] slab of a split tile (-1: whole tile)
+  int* arrive = nullptr;             // [2 * pair tiles] arrivals / partials reduced (zero between launches)
+  int* written = nullptr;
   // residual-add finalisation (per 128-row tile; the last of need[pair tile] contributors):
   // fin_xa[t][col] = bf16(fin_g[col] * h[t][col]), fin_ss[tile][t] = sum_col h^2, flag_out[tile] = epoch
   int* fin_cnt = nullptr;            // [2 * pair tiles], zero between launches
@@ -125,6 +132,8 @@ struct ChainLaunch {
   int pairs = 0;
   int N = 0, bn = 0, n_mma = 1, stages = 0, nbuf = 1;
   int ss_ld = 0;                     // row stride of the ss arrays (max tokens)
+  float* scr = nullptr;              // split-tile scratch base (row stride scr_ld floats), zero between launches
+  int scr_ld = 0;
   unsigned epoch = 0;
   size_t smem = 0;
   uint32_t tmem_cols = 0, ring_bytes = 0;
@@ -138,7 +147,11 @@ constexpr int kChainTraceSegs = 16;
 struct ChainMaps {
   CUtensorMap w[kChainMaxJobs];      // make_tmap_weight maps
   CUtensorMap x[kChainMaxJobs];      // activation maps, box rows bn / n_mma / 2
+  CUtensorMap hred;                  // fp32 residual h [T][H], box 32 columns x 16 tokens (TMA reduce-add)
+  CUtensorMap scr;                   // fp32 split-tile scratch [T][slabs * 256], same box
 };
+// fp32 [rows][cols] map with a 32-column x 16-row box, no swizzle (bulk reduce-add target).
+bool make_tmap_f32_red(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_elems);
 // Token tiling / ring of a chain over N tokens (N <= 512: one token tile).  Fills bn, n_mma,
 // stages, nbuf, smem, tmem_cols, ring_bytes; returns false if N needs more than one token tile.
 bool plan_chain_tiling(int N, ChainLaunch* cl);

@@ -61,6 +61,19 @@ SARATHI_DEVICE void wait_flag(const unsigned* f, unsigned epoch) {
   }
 }
 
+// Bulk reduce-add of a warp's 16-token x 32-column fp32 block (token-major in shared memory) into
+// global memory through the TMA engine (one 2 KB request instead of 128 vector red.adds).
+SARATHI_DEVICE void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+SARATHI_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+SARATHI_DEVICE void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+SARATHI_DEVICE void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+SARATHI_DEVICE void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 struct Seg {
   int job, pt, kb0, kb1;
 };
@@ -70,8 +83,8 @@ SARATHI_DEVICE Seg load_seg(const int* segs, int i) {
 }
 
 size_t chain_extra_smem(int bn) {
-  // transpose buffers + s_pos/s_slot (2 bn ints) + s_consec[32] + s_rs[bn] + barriers + holder
-  return 4 * kNEHc * kStageFloats * 4 + 32 * 4 + 3 * static_cast<size_t>(bn) * 4 + 3 * 8 * 8 + 64 + 64;
+  // 2 sets of transpose buffers + s_pos/s_slot (2 bn ints) + s_consec[32] + s_rs[bn] + barriers + holder
+  return 2 * 4 * kNEHc * kStageFloats * 4 + 32 * 4 + 3 * static_cast<size_t>(bn) * 4 + 3 * 8 * 8 + 16 * 8 + 64 + 64;
 }
 
 template <int FFN>
@@ -83,8 +96,8 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t b_bytes = static_cast<uint32_t>(p.bn / 2) * kBK * 2;  // this CTA's half of the tokens
   const uint32_t stage_bytes = kABytes + b_bytes;
-  float* stage_buf = reinterpret_cast<float*>(smem + p.ring_bytes);
-  int* s_pos = reinterpret_cast<int*>(stage_buf + 4 * NEH * kStageFloats);  // [bn]
+  float* stage_buf = reinterpret_cast<float*>(smem + p.ring_bytes);       // [2][8 warps][16 x 32]
+  int* s_pos = reinterpret_cast<int*>(stage_buf + 2 * 4 * NEH * kStageFloats);  // [bn]
   int* s_slot = s_pos + p.bn;                                               // [bn]
   int* s_consec = s_slot + p.bn;                                            // [32]
   float* s_rs = reinterpret_cast<float*>(s_consec + 32);                    // [bn] per-token RMSNorm scale
@@ -93,14 +106,14 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;  // [2]
   uint64_t* tempty = tfull + 2;        // [3]
-  uint32_t* holder = reinterpret_cast<uint32_t*>(tempty + 3);
+  uint64_t* sbar = tempty + 3;         // [8 epilogue warps][2] split-tile scratch loads
+  uint32_t* holder = reinterpret_cast<uint32_t*>(sbar + 8 * NEH);
   __shared__ int s_last;
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   griddep_launch_dependents();
-  if (p.span_start && threadIdx.x == 0) atomicMin(p.span_start, globaltimer_ns());
   if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[static_cast<size_t>(gridDim.x / 2) * kChainTraceSegs * 8] = globaltimer_ns();
   const int pair = blockIdx.x >> 1;
   const int seg_begin = __ldg(p.seg_off + pair), seg_end = __ldg(p.seg_off + pair + 1);
@@ -112,6 +125,7 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
     }
     for (int b = 0; b < 2; ++b) mbar_init(&tfull[b], 1);
     for (int b = 0; b < 3; ++b) mbar_init(&tempty[b], 8 * NEH);
+    for (int b = 0; b < 8 * NEH; ++b) mbar_init(&sbar[b], 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -129,6 +143,9 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
   const int ni = p.bn / p.n_mma;
   const bool ring = p.n_mma == 2 && 3 * ni <= 512;
   if (warp != 0) griddep_wait();
+  // device span from the end of the grid dependency (the predecessor's completion), not residency
+  if (p.span_start && threadIdx.x == 64) atomicMin(p.span_start, globaltimer_ns());
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 64) p.trace[static_cast<size_t>(gridDim.x / 2) * kChainTraceSegs * 8 + 1] = globaltimer_ns();
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -269,6 +286,10 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
     const int eh = ew >> 2;
     const uint32_t quarter = warp & 3;
     float* sbuf = stage_buf + ew * kStageFloats;
+    float* sbuf2 = stage_buf + (4 * NEH + ew) * kStageFloats;  // second buffer (bulk reduce double buffering)
+    int red_par = 0;
+    uint32_t sph[2] = {0, 0};  // phases of this warp's two scratch-load barriers
+    int rs_job = -1;           // job whose per-token RMSNorm scales s_rs holds
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
     const int tvalid = p.N;
     const int nchunks = (tvalid + 15) / 16;
@@ -332,19 +353,30 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
           s_consec[et] = ok;
         }
       }
-      if (scaled) {
+      const bool new_rs = scaled && rs_job != sg.job;  // once per job and CTA (consecutive segments share it)
+      if (new_rs) {
         // the RMSNorm statistics of the input: every producer tile published (acquire), then the
-        // per-token sum of squares over the tiles in tile order
+        // per-token sum of squares over the tiles in tile order (8 independent loads in flight)
+        rs_job = sg.job;
         if (ew == 0)
           for (int q = static_cast<int>(lane); q < J.ss_parts; q += 32) wait_flag(J.dep_flag + q, p.epoch);
         named_bar_sync(2, kEpiThreads);
         for (int t = et; t < tvalid; t += kEpiThreads) {
-          float ssum = 0.f;
-          for (int q = 0; q < J.ss_parts; ++q) ssum += __ldcg(J.ss_in + static_cast<size_t>(q) * p.ss_ld + t);
-          s_rs[t] = rsqrtf(ssum * J.inv_h + J.eps);
+          const float* src = J.ss_in + t;
+          float acc = 0.f;
+          int q = 0;
+          for (; q + 8 <= J.ss_parts; q += 8) {
+            float x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = __ldcg(src + static_cast<size_t>(q + u) * p.ss_ld);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += x[u];  // tile order
+          }
+          for (; q < J.ss_parts; ++q) acc += __ldcg(src + static_cast<size_t>(q) * p.ss_ld);
+          s_rs[t] = rsqrtf(acc * J.inv_h + J.eps);
         }
       }
-      if (mode == EPI_QKV_ROPE || scaled) named_bar_sync(2, kEpiThreads);
+      if (mode == EPI_QKV_ROPE || new_rs) named_bar_sync(2, kEpiThreads);
       if (lane == 0) {
         if (ring)
           mbar_wait(&tfull[seg & 1], (seg >> 1) & 1);
@@ -364,9 +396,32 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
           for (int j = 0; j < 16; ++j) v[j] *= s_rs[min(ch * 16 + j, tvalid - 1)];
         }
       };
+      // split whole-tile job: contributors reduce into a scratch slab, the last one finishes the tile
+      const int need = (mode != EPI_ADD_F32 && J.fin_need) ? __ldg(J.fin_need + sg.pt) : 1;
+      const bool split = need > 1;
+      const int scol = split ? __ldg(J.slab + sg.pt) * 2 * kBM + static_cast<int>(rank) * kBM + static_cast<int>(quarter) * 32 : 0;
+      bool last = true;
+      if (split) {
+        named_bar_sync(1, kEpiThreads);
+        if (et == 0) {
+          s_last = atomicAdd(J.arrive + mt, 1) == need - 1;
+          if (s_last) {  // every other contributor arrived; wait until their reductions completed
+            const unsigned long long t0 = globaltimer_ns();
+            while (static_cast<int>(ld_acquire_gpu(reinterpret_cast<const unsigned*>(J.written + mt))) < need - 1) {
+              __nanosleep(32);
+              if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+            }
+            J.arrive[mt] = 0;  // re-arm for the next launch
+            J.written[mt] = 0;
+          }
+        }
+        named_bar_sync(1, kEpiThreads);
+        last = s_last;
+        if (last) fence_proxy_async_global();  // the others' bulk reductions -> this CTA's TMA loads
+      }
       if (eh >= nchunks) {
         release_tmem();
-      } else if (mode == EPI_ADD_F32) {
+      } else if (mode == EPI_ADD_F32 || !last) {
         // light epilogue: two chunks in flight per TMEM wait
         uint32_t ra[16], rb[16];
         const bool hb = eh + NEH < nchunks;
@@ -382,20 +437,27 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
           const bool m2 = c2 < nchunks, m3 = c3 < nchunks;
           if (m2) tmem_ld_32x32b_x16(trow + tcol(c2), na);
           if (m3) tmem_ld_32x32b_x16(trow + tcol(c3), nb);
-          {
-            float v[16];
+          // token-major 16 x 32 block into the warp's transpose buffer (alternating two), then
+          // one bulk reduce-add into h; a buffer is rewritten only after its previous read completed
+          auto put = [&](int c, const uint32_t (&r)[16]) {
+            float* b = red_par ? sbuf2 : sbuf;
+            if (lane == 0) bulk_wait_read1();
+            __syncwarp();
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(ra[j]);
-            epi_emit<EPI_ADD_F32, false>(J.M, p.bn, ep, v, quarter, lane, mt, 0, ch * 16, tvalid, sbuf, s_pos, s_slot,
-                                         s_consec, ql);
-          }
-          if (ch + NEH < nchunks) {
-            float v[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(rb[j]);
-            epi_emit<EPI_ADD_F32, false>(J.M, p.bn, ep, v, quarter, lane, mt, 0, (ch + NEH) * 16, tvalid, sbuf, s_pos,
-                                         s_slot, s_consec, ql);
-          }
+            for (int j = 0; j < 16; ++j) b[j * 32 + lane] = __uint_as_float(r[j]);
+            fence_proxy_async_shared();
+            __syncwarp();
+            if (lane == 0 && mt * kBM < J.M) {
+              if (split)
+                tma_reduce_add_2d(&maps.scr, b, scol, c * 16);
+              else
+                tma_reduce_add_2d(&maps.hred, b, mt * kBM + static_cast<int>(quarter) * 32, c * 16);
+              bulk_commit();
+            }
+            red_par ^= 1;
+          };
+          put(ch, ra);
+          if (ch + NEH < nchunks) put(ch + NEH, rb);
           if (m2) {
             tmem_ld_wait_regs(na);
             regs_fence(nb);
@@ -409,7 +471,20 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
           }
         }
       } else {
-        // heavy epilogue (activation / RoPE): the next chunk in flight while this one is emitted
+        // heavy epilogue (activation / RoPE): the next chunk in flight while this one is emitted;
+        // the last contributor of a split tile also streams the other contributors' sum of each
+        // chunk (16 tokens x its 32 rows) from the scratch slab into its transpose buffers by TMA
+        // (one 2 KB buffer per warp, sbuf2: a chunk's sum is read into registers before the next
+        // chunk's load is issued into it; the epilogue itself transposes through sbuf)
+        auto fetch = [&](int c) {
+          uint64_t* bb = &sbar[ew * 2];
+          if (elect_one()) {
+            mbar_arrive_expect_tx(bb, 16 * 32 * 4);
+            tma_load_2d(sbuf2, &maps.scr, bb, scol, c * 16, policy_evict_first());
+          }
+          __syncwarp();
+        };
+        if (split) fetch(eh);
         uint32_t raw[16];
         tmem_ld_32x32b_x16(trow + tcol(eh), raw);
         tmem_ld_wait_regs(raw);
@@ -421,6 +496,18 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
           float v[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
+          if (split) {
+            mbar_wait(&sbar[ew * 2], sph[0]);
+            sph[0] ^= 1;
+            float* zrow = p.scr + static_cast<size_t>(ch * 16) * p.scr_ld + scol + lane;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              v[j] += sbuf2[j * 32 + lane];
+              if (ch * 16 + j < tvalid) zrow[static_cast<size_t>(j) * p.scr_ld] = 0.f;  // re-zero the slab
+            }
+            __syncwarp();
+            if (more) fetch(ch + NEH);
+          }
           scale(ch, v);
           if (mode == EPI_QKV_ROPE)
             epi_emit<EPI_QKV_ROPE, false>(J.M, p.bn, ep, v, quarter, lane, mt, 0, ch * 16, tvalid, sbuf, s_pos, s_slot,
@@ -436,8 +523,19 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
           }
         }
       }
+      if (tre) tre[7] = globaltimer_ns();
       // ---- publish ----
       const bool in_range = mt * kBM < J.M;
+      if (mode == EPI_ADD_F32 || !last) {  // the bulk reductions of this segment are complete in global memory
+        if (lane == 0) bulk_wait0();
+        __syncwarp();
+        fence_proxy_async_global();
+      }
+      if (!last) {  // split tile, not the last contributor: publish "my partial is in the slab"
+        __threadfence();
+        named_bar_sync(1, kEpiThreads);
+        if (et == 0) atomicAdd(J.written + mt, 1);
+      }
       if (mode == EPI_ADD_F32 && J.fin_cnt) {
         __threadfence();
         named_bar_sync(1, kEpiThreads);
@@ -492,7 +590,7 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
           named_bar_sync(1, kEpiThreads);
           if (et == 0) st_release_gpu(J.flag_out + mt, p.epoch);
         }
-      } else if (J.flag_out) {
+      } else if (J.flag_out && last) {
         fence_proxy_async_global();
         __threadfence();
         named_bar_sync(1, kEpiThreads);

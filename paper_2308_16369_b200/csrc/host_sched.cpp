@@ -274,185 +274,242 @@ bool shard_map(int n_layers, int hidden, int n_heads, int n_kv_heads, int head_d
 }
 
 
-ChainSchedule schedule_chain(const std::vector<ChainJobShape>& jobs, int P, double e_add, double e_fin, int min_seg) {
+ChainSchedule schedule_chain(const std::vector<ChainJobShape>& jobs, int P, double e_add, double e_fin, int min_seg,
+                             bool split_whole) {
   ChainSchedule out;
   P = std::max(1, P);
-  std::vector<double> f(P, 0.0);                 // time each pair's MMA pipe becomes free
-  std::vector<double> g(P, 0.0);                 // time each pair's epilogue warps become free
+  std::vector<double> f(P, 0.0);  // time each pair's MMA pipe becomes free
+  std::vector<double> g(P, 0.0);  // time each pair's epilogue warps become free
   std::vector<std::vector<std::array<int, 4>>> per(P);
-  std::vector<double> prev_ready;                // previous job: time each 128-row tile is published
+  std::vector<double> prev_ready;  // previous job: time each 128-row tile is published
   out.need.resize(jobs.size());
+  using Assign = std::vector<std::array<int, 4>>;  // (pair, tile, k0, k1) in execution order per pair
   for (size_t j = 0; j < jobs.size(); ++j) {
     const ChainJobShape& J = jobs[j];
-    const int KB = J.KB;
+    const int KB = J.KB, PT = J.pm_tiles;
     std::vector<double> dep(KB, 0.0);
     if (J.dep_shift >= 0 && j > 0)
       for (int kb = 0; kb < KB; ++kb) {
         const size_t q = static_cast<size_t>(kb >> J.dep_shift);
         dep[kb] = q < prev_ready.size() ? prev_ready[q] : 0.0;
       }
-    std::vector<double> ready(2 * static_cast<size_t>(J.pm_tiles), 0.0);
-    out.need[j].assign(J.pm_tiles, 0);
     // a segment's mainloop: one unit per k-block, each k-block no earlier than its input
     auto run = [&](double t, int kb0, int kb1) {
       for (int kb = kb0; kb < kb1; ++kb) t = std::max(t, dep[kb]) + 1.0;
       return t;
     };
+    // simulate an assignment on top of the current pair timelines: returns the time the job's last
+    // tile is published; a tile with several contributors (split) is published after the last
+    // contributor's epilogue (split residual job: + e_fin; split whole-tile job: + e_done)
+    struct Sim {
+      std::vector<double> f, g, ready;
+      double end = 0.0;
+    };
+    auto simulate = [&](const Assign& as) {
+      Sim r{f, g, std::vector<double>(2 * static_cast<size_t>(PT), 0.0)};
+      std::vector<int> cnt(PT, 0);
+      for (const auto& x : as) ++cnt[x[1]];
+      std::vector<double> tile_end(PT, 0.0);
+      for (const auto& x : as) {
+        const double t = run(r.f[x[0]], x[2], x[3]);
+        r.f[x[0]] = t;
+        const bool whole = cnt[x[1]] == 1 && !J.split;
+        const double e = std::max(t, r.g[x[0]]) + (whole ? J.e_done : e_add);
+        r.g[x[0]] = e;
+        tile_end[x[1]] = std::max(tile_end[x[1]], e);
+      }
+      for (int pt = 0; pt < PT; ++pt) {
+        const double extra = J.split ? e_fin : (cnt[pt] > 1 ? J.e_done : 0.0);
+        r.ready[2 * pt] = r.ready[2 * pt + 1] = tile_end[pt] + extra;
+        r.end = std::max(r.end, r.ready[2 * pt]);
+      }
+      return r;
+    };
+    // water-filling of tiles [t0, PT) of the k-range [bk0, bk1): contiguous tile-major unit ranges
+    // over the pairs' effective free times max(free, ready) so that every pair ends together
+    auto waterfill = [&](const std::vector<double>& free_t, double bready, int t0, int bk0, int bk1) {
+      const int len = bk1 - bk0;
+      const long long U = static_cast<long long>(PT - t0) * len;
+      Assign as;
+      if (U <= 0) return as;
+      std::vector<double> eff(P);
+      for (int c = 0; c < P; ++c) eff[c] = std::max(free_t[c], bready);
+      std::vector<int> order(P);
+      for (int c = 0; c < P; ++c) order[c] = c;
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return eff[x] < eff[y]; });
+      int m = P;
+      double T_end = 0.0;
+      for (; m >= 1; --m) {
+        double S = 0.0;
+        for (int i = 0; i < m; ++i) S += eff[order[i]];
+        T_end = (static_cast<double>(U) + S) / m;
+        if (m == 1 || T_end >= eff[order[m - 1]]) break;
+      }
+      std::vector<long long> budget(m, 0);
+      double cum = 0.0;
+      long long given = 0;
+      for (int i = 0; i < m; ++i) {
+        cum += T_end - eff[order[i]];
+        const long long upto = (i == m - 1) ? U : std::min<long long>(U, std::llround(cum));
+        budget[i] = std::max<long long>(0, upto - given);
+        given += budget[i];
+      }
+      // too-short ranges cost a whole epilogue: fold into a neighbour (and at most ~16 contributors
+      // per tile and band)
+      const long long shortest = std::max<long long>(min_seg, (len + 15) / 16);
+      for (int i = 0; i < m; ++i)
+        if (budget[i] > 0 && budget[i] < shortest) {
+          int k = i + 1;
+          if (k >= m)
+            for (k = i - 1; k > 0 && budget[k] == 0; --k) {
+            }
+          if (k >= 0 && k != i) {
+            budget[k] += budget[i];
+            budget[i] = 0;
+          }
+        }
+      int rpt = t0, rk = bk0;
+      for (int i = 0; i < m; ++i) {
+        long long n = budget[i];
+        while (n > 0 && rpt < PT) {
+          const int take = static_cast<int>(std::min<long long>(n, bk1 - rk));
+          as.push_back({order[i], rpt, rk, rk + take});
+          n -= take;
+          rk += take;
+          if (rk == bk1) {
+            ++rpt;
+            rk = bk0;
+          }
+        }
+      }
+      return as;
+    };
+    // tile-aligned split of tiles [t0, PT): each tile's k-range in n equal parts, LPT over the pairs
+    auto aligned = [&](const std::vector<double>& free_t, double bready, int t0, int bk0, int bk1, int n) {
+      const int len = bk1 - bk0;
+      std::vector<std::array<int, 3>> parts;
+      for (int pt = t0; pt < PT; ++pt)
+        for (int q = 0; q < n; ++q)
+          parts.push_back({pt, bk0 + static_cast<int>(static_cast<long long>(len) * q / n),
+                           bk0 + static_cast<int>(static_cast<long long>(len) * (q + 1) / n)});
+      std::stable_sort(parts.begin(), parts.end(),
+                       [](const std::array<int, 3>& x, const std::array<int, 3>& y) { return x[2] - x[1] > y[2] - y[1]; });
+      Assign as;
+      std::vector<double> load(P);
+      for (int c = 0; c < P; ++c) load[c] = std::max(free_t[c], bready);
+      for (const auto& pr : parts) {
+        int c = 0;
+        for (int k = 1; k < P; ++k)
+          if (load[k] < load[c]) c = k;
+        as.push_back({c, pr[0], pr[1], pr[2]});
+        load[c] += pr[2] - pr[1];
+      }
+      return as;
+    };
+    Assign best;
+    Sim best_sim;
+    bool have = false;
+    auto consider = [&](const Assign& as) {
+      Sim r = simulate(as);
+      if (!have || r.end < best_sim.end - 1e-9) {
+        best = as;
+        best_sim = r;
+        have = true;
+      }
+    };
     if (!J.split) {
-      double D = 0.0;  // no tile can finish before every k-block's input exists
-      for (int kb = 0; kb < KB; ++kb) D = std::max(D, dep[kb] + (KB - kb));
-      for (int pt = 0; pt < J.pm_tiles; ++pt) {
-        const int c = static_cast<int>(std::min_element(f.begin(), f.end()) - f.begin());
-        const double end = std::max(f[c] + KB, D);
-        per[c].push_back({static_cast<int>(j), pt, 0, KB});
-        f[c] = end;
-        g[c] = std::max(end, g[c]) + J.e_done;
-        ready[2 * pt] = ready[2 * pt + 1] = g[c];
-        out.need[j][pt] = 1;
+      // whole tiles only; or `w` whole waves then the remaining tiles split (stream-K remainder);
+      // or every tile split
+      double dready = 0.0;
+      for (int kb = 0; kb < KB; ++kb) dready = std::max(dready, dep[kb]);
+      for (int w = PT / P; split_whole && w >= 0; --w) {
+        Assign as;
+        std::vector<double> ft(f);
+        const int nwhole = (w == PT / P && PT % P == 0) ? PT : w * P;
+        for (int pt = 0; pt < nwhole; ++pt) {  // whole tiles, LPT by free time
+          const int c = static_cast<int>(std::min_element(ft.begin(), ft.end()) - ft.begin());
+          as.push_back({c, pt, 0, KB});
+          ft[c] = run(ft[c], 0, KB);
+        }
+        if (nwhole < PT) {
+          Assign rest = waterfill(ft, dready, nwhole, 0, KB);
+          as.insert(as.end(), rest.begin(), rest.end());
+          for (int n = 1; n <= std::max(1, P / std::max(1, PT - nwhole)); ++n) {
+            Assign al(as.begin(), as.begin() + nwhole);
+            Assign r2 = aligned(ft, dready, nwhole, 0, KB, n);
+            al.insert(al.end(), r2.begin(), r2.end());
+            consider(al);
+          }
+        }
+        consider(as);
+      }
+      {  // all whole tiles, LPT
+        Assign as;
+        std::vector<double> ft(f);
+        for (int pt = 0; pt < PT; ++pt) {
+          const int c = static_cast<int>(std::min_element(ft.begin(), ft.end()) - ft.begin());
+          as.push_back({c, pt, 0, KB});
+          ft[c] = run(ft[c], 0, KB);
+        }
+        consider(as);
       }
     } else {
-      // bands: contiguous k-ranges whose inputs are published within `tol` of the band's first
-      const double tol = 2.0;
+      // residual job: per band (contiguous k-ranges whose inputs are published within `tol`),
+      // in readiness order, the better of water-filling and tile-aligned splits
+      const double tol = 4.0;
       std::vector<std::pair<int, int>> bands;
       for (int k0 = 0, kb = 1; kb <= KB; ++kb)
         if (kb == KB || std::fabs(dep[kb] - dep[k0]) > tol) {
-          bands.push_back({k0, kb});
+          // a band of fewer than 8 k-blocks would only produce short segments: merge it
+          if (!bands.empty() && (kb - k0 < 8 || bands.back().second - bands.back().first < 8))
+            bands.back().second = kb;
+          else
+            bands.push_back({k0, kb});
           k0 = kb;
         }
-      std::stable_sort(bands.begin(), bands.end(), [&](const std::pair<int, int>& a, const std::pair<int, int>& b) {
-        return dep[a.first] < dep[b.first];
+      std::stable_sort(bands.begin(), bands.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+        return dep[x.first] < dep[y.first];
       });
-      // per band (in readiness order) two candidate partitions, simulated, the better one kept:
-      //  * water-filling: the band's units (tile-major) as contiguous ranges over the pairs'
-      //    effective free times max(f, band ready), every pair ending together;
-      //  * tile-aligned: each tile's k-range cut into n equal parts (one segment, one residual-add
-      //    epilogue per pair: no pair straddles two tiles), n = 1 .. pairs / tiles.
-      std::vector<double> contrib(J.pm_tiles, 0.0);
+      Assign all;
+      std::vector<double> ft(f);
       for (const auto& band : bands) {
-        const int bk0 = band.first, bk1 = band.second, len = bk1 - bk0;
         double bready = 0.0;
-        for (int kb = bk0; kb < bk1; ++kb) bready = std::max(bready, dep[kb]);
-        const long long U = static_cast<long long>(J.pm_tiles) * len;
-        std::vector<double> eff(P);
-        for (int c = 0; c < P; ++c) eff[c] = std::max(f[c], bready);
-        std::vector<int> order(P);
-        for (int c = 0; c < P; ++c) order[c] = c;
-        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return eff[x] < eff[y]; });
-        using Assign = std::vector<std::array<int, 4>>;  // pair, tile, k0, k1 (execution order per pair)
-        auto evaluate = [&](const Assign& as, std::vector<double>* f2, std::vector<double>* g2,
-                            std::vector<double>* c2) {
-          *f2 = f;
-          *g2 = g;
-          *c2 = contrib;
-          for (const auto& x : as) {
-            const double t = run((*f2)[x[0]], x[2], x[3]);
-            (*f2)[x[0]] = t;
-            const double e = std::max(t, (*g2)[x[0]]) + e_add;  // epilogues of a pair run in order
-            (*g2)[x[0]] = e;
-            (*c2)[x[1]] = std::max((*c2)[x[1]], e);
-          }
-          double mx = 0.0;
-          for (int pt = 0; pt < J.pm_tiles; ++pt) mx = std::max(mx, (*c2)[pt]);
-          return mx;
-        };
-        Assign best;
-        double best_end = 1e300;
-        {  // water-filling
-          int m = P;
-          double T_end = 0.0;
-          for (; m >= 1; --m) {
-            double S = 0.0;
-            for (int i = 0; i < m; ++i) S += eff[order[i]];
-            T_end = (static_cast<double>(U) + S) / m;
-            if (m == 1 || T_end >= eff[order[m - 1]]) break;
-          }
-          std::vector<long long> budget(m, 0);
-          double cum = 0.0;
-          long long given = 0;
-          for (int i = 0; i < m; ++i) {
-            cum += T_end - eff[order[i]];
-            const long long upto = (i == m - 1) ? U : std::min<long long>(U, std::llround(cum));
-            budget[i] = std::max<long long>(0, upto - given);
-            given += budget[i];
-          }
-          for (int i = 0; i < m; ++i)  // too-short ranges cost a whole epilogue: fold into a neighbour
-            if (budget[i] > 0 && budget[i] < min_seg) {
-              int k = i + 1;
-              if (k >= m)
-                for (k = i - 1; k > 0 && budget[k] == 0; --k) {
-                }
-              if (k >= 0 && k != i) {
-                budget[k] += budget[i];
-                budget[i] = 0;
-              }
-            }
-          Assign as;
-          int rpt = 0, rk = bk0;
-          for (int i = 0; i < m; ++i) {
-            long long n = budget[i];
-            while (n > 0 && rpt < J.pm_tiles) {
-              const int take = static_cast<int>(std::min<long long>(n, bk1 - rk));
-              as.push_back({order[i], rpt, rk, rk + take});
-              n -= take;
-              rk += take;
-              if (rk == bk1) {
-                ++rpt;
-                rk = bk0;
-              }
-            }
-          }
-          std::vector<double> f2, g2, c2;
-          best_end = evaluate(as, &f2, &g2, &c2);
-          best = as;
-        }
-        for (int n = 1; n <= std::max(1, P / J.pm_tiles) && n <= len; ++n) {  // tile-aligned
-          // parts of each tile's range, longest first; the pm * n parts go to the earliest pairs
-          std::vector<std::array<int, 3>> parts;  // tile, k0, k1
-          for (int pt = 0; pt < J.pm_tiles; ++pt)
-            for (int q = 0; q < n; ++q)
-              parts.push_back({pt, bk0 + static_cast<int>(static_cast<long long>(len) * q / n),
-                               bk0 + static_cast<int>(static_cast<long long>(len) * (q + 1) / n)});
-          std::stable_sort(parts.begin(), parts.end(),
-                           [](const std::array<int, 3>& x, const std::array<int, 3>& y) { return x[2] - x[1] > y[2] - y[1]; });
-          Assign as;
-          std::vector<double> load(eff);
-          for (const auto& pr : parts) {  // LPT on the effective free times
-            int c = 0;
-            for (int k = 1; k < P; ++k)
-              if (load[k] < load[c]) c = k;
-            as.push_back({c, pr[0], pr[1], pr[2]});
-            load[c] += pr[2] - pr[1];
-          }
-          std::vector<double> f2, g2, c2;
-          const double e = evaluate(as, &f2, &g2, &c2);
-          if (e < best_end - 1e-9) {
-            best_end = e;
-            best = as;
+        for (int kb = band.first; kb < band.second; ++kb) bready = std::max(bready, dep[kb]);
+        Assign bb;
+        double bend = 1e300;
+        std::vector<Assign> cands;
+        cands.push_back(waterfill(ft, bready, 0, band.first, band.second));
+        for (int n = 1; n <= std::max(1, P / PT) && n <= band.second - band.first; ++n)
+          cands.push_back(aligned(ft, bready, 0, band.first, band.second, n));
+        for (const auto& c : cands) {
+          Assign trial(all);
+          trial.insert(trial.end(), c.begin(), c.end());
+          const Sim r = simulate(trial);
+          if (r.end < bend - 1e-9) {
+            bend = r.end;
+            bb = c;
           }
         }
-        // commit the kept partition
-        for (const auto& x : best) {
-          const int c = x[0];
-          auto& v = per[c];  // merge with this pair's previous segment when it continues the k-range
-          if (!v.empty() && v.back()[0] == static_cast<int>(j) && v.back()[1] == x[1] && v.back()[3] == x[2]) {
-            v.back()[3] = x[3];
-          } else {
-            v.push_back({static_cast<int>(j), x[1], x[2], x[3]});
-            ++out.need[j][x[1]];
-          }
-        }
-        std::vector<double> f2, g2, c2;
-        evaluate(best, &f2, &g2, &c2);
-        f = f2;
-        g = g2;
-        contrib = c2;
+        all.insert(all.end(), bb.begin(), bb.end());
+        for (const auto& x : bb) ft[x[0]] = run(ft[x[0]], x[2], x[3]);
       }
-      for (int pt = 0; pt < J.pm_tiles; ++pt) ready[2 * pt] = ready[2 * pt + 1] = contrib[pt] + e_fin;
+      consider(all);
     }
-    double je = 0.0;
-    for (double x : ready) je = std::max(je, x);
-    out.job_end.push_back(je);
-    prev_ready = ready;
+    // commit: per-pair segments (a pair's consecutive ranges of one tile merge), contributor counts
+    out.need[j].assign(PT, 0);
+    for (const auto& x : best) {
+      auto& v = per[x[0]];
+      if (!v.empty() && v.back()[0] == static_cast<int>(j) && v.back()[1] == x[1] && v.back()[3] == x[2]) {
+        v.back()[3] = x[3];
+      } else {
+        v.push_back({static_cast<int>(j), x[1], x[2], x[3]});
+        ++out.need[j][x[1]];
+      }
+    }
+    f = best_sim.f;
+    g = best_sim.g;
+    out.job_end.push_back(best_sim.end);
+    prev_ready = best_sim.ready;
   }
   out.seg_off.assign(P + 1, 0);
   for (int c = 0; c < P; ++c) {

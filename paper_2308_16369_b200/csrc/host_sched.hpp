@@ -149,7 +149,10 @@ struct ChainSchedule {
 };
 // e_add: red.add epilogue of a split segment; e_fin: finalisation of a split tile after its last
 // contributor (k-block units).  min_seg: split ranges shorter than this merge into a neighbour.
+// split_whole: whole-tile jobs may also be split (contributors reduce through scratch slabs; the
+// last one finishes the tile).  Measured slower than whole tiles on every shape tried (DESIGN.md
+// §6: the last contributor's scratch reads are L2 round trips on the critical path), so opt-in.
 ChainSchedule schedule_chain(const std::vector<ChainJobShape>& jobs, int pairs, double e_add, double e_fin,
-                             int min_seg = 4);
+                             int min_seg = 4, bool split_whole = true);
 
 }  // namespace sarathi

@@ -401,9 +401,14 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
     SRET(dalloc(&ss1, static_cast<size_t>(nt_h) * Tmax));
     SRET(dalloc(&ss2, static_cast<size_t>(nt_h) * Tmax));
     SRET(dalloc(&cflags, static_cast<size_t>(2 * nt_h + nt_gu)));
-    SRET(dalloc(&ccnt, static_cast<size_t>(2 * nt_h)));
+    nt_qkv = 2 * ((qkv_rows + 255) / 256);
+    SRET(dalloc(&ccnt, static_cast<size_t>(2 * nt_h + 2 * nt_gu + 2 * nt_qkv)));
+    // split-tile scratch of the whole-tile jobs (FFN1, QKV): one 256-column slab per pair tile
+    scr_ld = (nt_gu + nt_qkv) * 128;
+    SRET(dalloc(&cscr, static_cast<size_t>(Tmax) * scr_ld));
+    SRET(check(cudaMemset(cscr, 0, static_cast<size_t>(Tmax) * scr_ld * sizeof(float)), "memset"));
     SRET(check(cudaMemset(cflags, 0, (2 * nt_h + nt_gu) * sizeof(unsigned)), "memset"));
-    SRET(check(cudaMemset(ccnt, 0, 2 * nt_h * sizeof(int)), "memset"));
+    SRET(check(cudaMemset(ccnt, 0, (2 * nt_h + 2 * nt_gu + 2 * nt_qkv) * sizeof(int)), "memset"));
   }
   SRET(check(cudaStreamSynchronize(stream), "init sync"));
   return Status::ok();
@@ -545,11 +550,22 @@ Status Model::chain_plan(int T, bool with_qkv, const ChainPlanDev** out) {
   jobs[1] = {(gu_rows + 255) / 256, H / 64, false, 1, swiglu ? costs[0] : costs[0]};
   jobs[2] = {(H + 255) / 256, h2_l / 64, true, swiglu ? 0 : 1, 0.0};
   if (with_qkv) jobs[3] = {(qkv_rows + 255) / 256, H / 64, false, 1, costs[1]};
-  pd.sch = schedule_chain(jobs, num_sms / 2, costs[2], costs[3]);
+  static const bool split_whole = getenv("SARATHI_CHAIN_SPLIT") && atoi(getenv("SARATHI_CHAIN_SPLIT")) == 1;
+  pd.sch = schedule_chain(jobs, num_sms / 2, costs[2], costs[3], 4, split_whole);
   const ChainSchedule& sc = pd.sch;
   const int pairs = num_sms / 2;
   std::vector<int> blob(sc.segs);
   blob.insert(blob.end(), sc.seg_off.begin(), sc.seg_off.end());
+  pd.need_gu = static_cast<int>(blob.size());
+  blob.insert(blob.end(), sc.need[1].begin(), sc.need[1].end());
+  pd.slab_gu = static_cast<int>(blob.size());
+  for (int pt = 0; pt < jobs[1].pm_tiles; ++pt) blob.push_back(pt);
+  if (with_qkv) {
+    pd.need_qkv = static_cast<int>(blob.size());
+    blob.insert(blob.end(), sc.need[3].begin(), sc.need[3].end());
+    pd.slab_qkv = static_cast<int>(blob.size());
+    for (int pt = 0; pt < jobs[3].pm_tiles; ++pt) blob.push_back(nt_gu / 2 + pt);
+  }
   pd.need_o = static_cast<int>(blob.size());
   blob.insert(blob.end(), sc.need[0].begin(), sc.need[0].end());
   pd.need_f2 = static_cast<int>(blob.size());
@@ -622,6 +638,10 @@ Status Model::run_chain(int l, int T, bool with_qkv, const int* d_pos_dev, const
     J.inv_h = 1.0f / static_cast<float>(H);
     J.eps = cfg.rms_eps;
     J.flag_out = f_gu;
+    J.fin_need = pd->dev + pd->need_gu;  // split tiles reduce through scratch slabs
+    J.slab = pd->dev + pd->slab_gu;
+    J.arrive = ccnt + 2 * nt_h;
+    J.written = ccnt + 2 * nt_h + nt_gu;
     maps.w[1] = w.m_gu;
     SRET(xmap(a2, T, H, H, box, &mx));
     maps.x[1] = *mx;
@@ -648,6 +668,27 @@ Status Model::run_chain(int l, int T, bool with_qkv, const int* d_pos_dev, const
     SRET(xmap(f, T, h2_l, h2_l, box, &mx));
     maps.x[2] = *mx;
   }
+  {
+    // residual h [T][H] as the bulk reduce-add target (rows >= T clipped by the map)
+    auto hk = std::make_tuple(static_cast<const void*>(h), T, H, -1);
+    auto hi = xmaps.find(hk);
+    if (hi == xmaps.end()) {
+      CUtensorMap m;
+      if (!make_tmap_f32_red(&m, h, T, H, H)) return Status::err(SARATHI_ECUDA, "tensor map (h reduce)");
+      hi = xmaps.emplace(hk, m).first;
+    }
+    maps.hred = hi->second;
+    auto sk = std::make_tuple(static_cast<const void*>(cscr), T, scr_ld, -1);
+    auto si = xmaps.find(sk);
+    if (si == xmaps.end()) {
+      CUtensorMap m;
+      if (!make_tmap_f32_red(&m, cscr, T, scr_ld, scr_ld)) return Status::err(SARATHI_ECUDA, "tensor map (scratch)");
+      si = xmaps.emplace(sk, m).first;
+    }
+    maps.scr = si->second;
+    cl.scr = cscr;
+    cl.scr_ld = scr_ld;
+  }
   if (with_qkv) {
     LayerWeights& wn = layers[l + 1];
     ChainJobDev& J = cl.job[3];
@@ -672,6 +713,10 @@ Status Model::run_chain(int l, int T, bool with_qkv, const int* d_pos_dev, const
     J.ss_parts = H / 128;
     J.inv_h = 1.0f / static_cast<float>(H);
     J.eps = cfg.rms_eps;
+    J.fin_need = pd->dev + pd->need_qkv;
+    J.slab = pd->dev + pd->slab_qkv;
+    J.arrive = ccnt + 2 * nt_h + 2 * nt_gu;
+    J.written = ccnt + 2 * nt_h + 2 * nt_gu + nt_qkv;
     maps.w[3] = wn.m_qkv;
     SRET(xmap(a, T, H, H, box, &mx));
     maps.x[3] = *mx;
@@ -682,19 +727,24 @@ Status Model::run_chain(int l, int T, bool with_qkv, const int* d_pos_dev, const
   // at layer 1 (per pair: segments with mainloop / epilogue stamps and producer dependency waits)
   static const char* ctr = getenv("SARATHI_CHAIN_TRACE");
   static bool ctraced = false;
-  if (ctr && !ctraced && atoi(ctr) == T && l == 1) {
-    ctraced = true;
-    const size_t n = static_cast<size_t>(cl.pairs) * kChainTraceSegs * 8 + 8;
-    unsigned long long* tr = nullptr;
+  static unsigned long long* tr = nullptr;  // allocated and zeroed ahead so the traced launch keeps its PDL overlap
+  const size_t n = static_cast<size_t>(cl.pairs) * kChainTraceSegs * 8 + 8;
+  if (ctr && !tr) {
     cudaMalloc(&tr, n * 8);
-    cudaMemsetAsync(tr, 0, n * 8, stream);
+    cudaMemset(tr, 0, n * 8);
+    cudaDeviceSynchronize();
+  }
+  static int cmatch = 0;  // trace the 100th chain launch with T tokens (warm: a few steps in)
+  if (ctr && !ctraced && atoi(ctr) == T && ++cmatch == 100) {
+    ctraced = true;
     cl.trace = tr;
     const Status st = check(launch_chain(maps, cl, swiglu ? EPI_SILU_MUL : EPI_GELU, stream), "chain launch");
     std::vector<unsigned long long> hb(n);
     cudaStreamSynchronize(stream);
     cudaMemcpy(hb.data(), tr, n * 8, cudaMemcpyDeviceToHost);
-    cudaFree(tr);
     const unsigned long long t0 = hb[static_cast<size_t>(cl.pairs) * kChainTraceSegs * 8];
+    fprintf(stderr, "chain trace: grid dependency resolved at %.1f us after the first CTA started\n",
+            (static_cast<double>(hb[static_cast<size_t>(cl.pairs) * kChainTraceSegs * 8 + 1]) - static_cast<double>(t0)) * 1e-3);
     auto us = [&](unsigned long long t) { return t ? (static_cast<double>(t) - static_cast<double>(t0)) * 1e-3 : -1.0; };
     double jmax[4][3] = {};  // per job: last commit, last published, sum of dep waits
     double jmin[4];
@@ -706,8 +756,8 @@ Status Model::run_chain(int l, int T, bool with_qkv, const int* d_pos_dev, const
         if (!e[0]) break;
         const int jb = static_cast<int>(e[6] >> 48), pt = static_cast<int>((e[6] >> 32) & 0xFFFF);
         const int k0 = static_cast<int>((e[6] >> 16) & 0xFFFF), k1 = static_cast<int>(e[6] & 0xFFFF);
-        fprintf(stderr, " [j%d t%d %d-%d mma %.1f|%.1f-%.1f epi %.1f-%.1f w%.1f]", jb, pt, k0, k1, us(e[0]), us(e[1]),
-                us(e[2]), us(e[3]), us(e[4]), e[5] * 1e-3);
+        fprintf(stderr, " [j%d t%d %d-%d mma %.1f|%.1f-%.1f epi %.1f-%.1f-%.1f w%.1f]", jb, pt, k0, k1, us(e[0]), us(e[1]),
+                us(e[2]), us(e[3]), us(e[7]), us(e[4]), e[5] * 1e-3);
         if (jb < 4) {
           jmin[jb] = std::min(jmin[jb], us(e[1]));
           jmax[jb][0] = std::max(jmax[jb][0], us(e[2]));
@@ -987,7 +1037,13 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   static const bool attn_chain = !(getenv("SARATHI_ATTN_CHAIN") && atoi(getenv("SARATHI_ATTN_CHAIN")) == 0);
   // layer chain: layer l's O -> FFN1 -> FFN2 and layer l+1's RMSNorm + QKV run as ONE launch
   // (gemm_chain.cu), so a layer after the first starts at its attention
-  const bool use_chain = chain_on && gemm_token_tiling(T).n_tiles == 1;
+  // (measured: a net gain only when the whole-tile jobs fill the GPU by themselves; a TP rank's
+  // small-M QKV / FFN1 leave most pairs idle in the chain and run faster as standalone stream-K
+  // GEMMs, profiles/r02_chain_*.txt; SARATHI_CHAIN=2 forces the chain for every shape)
+  static const bool chain_force = getenv("SARATHI_CHAIN") && atoi(getenv("SARATHI_CHAIN")) == 2;
+  const int pairs_avail = num_sms / 2;
+  const bool chain_fits = 4 * ((gu_rows + 255) / 256) >= 3 * pairs_avail && 4 * ((qkv_rows + 255) / 256) >= 3 * pairs_avail;
+  const bool use_chain = chain_on && gemm_token_tiling(T).n_tiles == 1 && (chain_fits || chain_force);
   for (int l = 0; l < nl; ++l) {  // this stage's layers (local index)
     LayerWeights& w = layers[l];
     if (l == 0 || !use_chain) {

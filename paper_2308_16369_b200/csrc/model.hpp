@@ -158,7 +158,10 @@ struct Model {
   float* ss1 = nullptr;               // per-128-column sums of squares of h for the next QKV [H/128][Tmax]
   float* ss2 = nullptr;               // ... for FFN1
   unsigned* cflags = nullptr;         // O fin [nt_h] | FFN1 out [nt_gu] | FFN2 fin [nt_h] (epoch-valued)
-  int* ccnt = nullptr;                // O fin counters [nt_h] | FFN2 fin counters [nt_h]
+  int* ccnt = nullptr;                // O fin [nt_h] | FFN2 fin [nt_h] | FFN1 arrive/written [2 nt_gu] | QKV [2 nt_qkv]
+  int nt_qkv = 0;
+  float* cscr = nullptr;              // split-tile scratch [Tmax][scr_ld] (zero between launches)
+  int scr_ld = 0;
   int nt_h = 0, nt_gu = 0;            // 128-row tiles (rounded up to pair tiles)
   unsigned chain_epoch = 0;
   struct ChainPlanDev {
@@ -166,6 +169,7 @@ struct Model {
     int* dev = nullptr;  // segs | seg_off | need(O) | need(FFN2)
     ChainLaunch base;
     int need_o = 0, need_f2 = 0;  // offsets (ints) of the need arrays in dev
+    int need_gu = 0, slab_gu = 0, need_qkv = 0, slab_qkv = 0;  // split whole-tile jobs
   };
   std::map<std::pair<int, int>, ChainPlanDev> chain_plans;  // (T, with next QKV)
   Status chain_plan(int T, bool with_qkv, const ChainPlanDev** out);

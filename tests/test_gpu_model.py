@@ -164,6 +164,25 @@ def test_prefill_attention_variants(env, select, n):
     assert f"{n} passed" in r.stdout
 
 
+@pytest.mark.skipif(os.environ.get("SARATHI_PREFILL_VARIANT_CHILD") == "1", reason="child process")
+@pytest.mark.parametrize("env", [{"SARATHI_CHAIN": "2"}, {"SARATHI_CHAIN": "2", "SARATHI_CHAIN_SPLIT": "1"}])
+def test_layer_chain_variants(env):
+    """The one-launch layer chain (gemm_chain.cu) on the tiny shapes, where the default policy
+    keeps standalone GEMMs (whole-tile jobs too small to fill the GPU): forced on (SARATHI_CHAIN=2,
+    whole tiles, tile flags, RMSNorm folded into finalisers / epilogue scales) and with split
+    whole-tile jobs reduced through scratch slabs (SARATHI_CHAIN_SPLIT=1), over hybrid schedules
+    incl. GQA, GELU, bs 32/64 and multi-tile prefill chunks."""
+    env = dict(os.environ, SARATHI_PREFILL_VARIANT_CHILD="1", **env)
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m", "gpu", "-k",
+                        "config1 or gqa or gelu or multitile or block_size_32", "-p", "no:cacheprovider"],
+                       env=env, capture_output=True, text=True, timeout=900,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    import re
+    m = re.search(r"(\d+) passed", r.stdout)
+    assert m and int(m.group(1)) >= 8 and "failed" not in r.stdout, r.stdout[-2000:]
+
+
 def test_block_size_32_schedule(S):
     """bs = 32, the one accepted block size no other test runs: a multi-block hybrid schedule."""
     cfg = dataclasses.replace(synth.TINY, name="tiny-bs32", max_seq_len=256)

@@ -402,27 +402,19 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
           }
         }
       };
-      constexpr bool kDeepDrain = MODE == EPI_ADD_F32 || MODE == EPI_STORE_F32 || MODE == EPI_STORE_BF16;
-      if (direct && kDeepDrain && !DBG) {
-        drain2([&](int ch, uint32_t (&raw)[16]) {
-          float v[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
-          epi_emit<MODE, DBG>(p.M, p.bn, ep, v, quarter, lane, mt, nt, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec, ql);
-        });
-      } else if (direct) {
-        // software-pipelined TMEM drain: this warp's next chunk (ch + NEH) is in flight while ch is emitted
+      if (direct) {
+        // TMEM drain, one chunk in flight (load, wait, emit): measured faster than keeping the next
+        // chunk's load in flight across the emit, for every epilogue mode (tools/tmem_drain.cu;
+        // [13B-1] QKV 66.2 -> 64.8 us, gate||up 92.3 -> 89.8, O 30.8 -> 30.2; step 19.05 -> 18.85 ms,
+        // interleaved A/B, profiles/r02_ab_drain.txt)
         if (eh >= nchunks) {
           release_tmem();
         } else {
-          uint32_t raw[16];
-          tmem_ld_32x32b_x16(trow + tcol(eh), raw);
-          tmem_ld_wait_regs(raw);
-          after_load(eh);
           for (int ch = eh; ch < nchunks; ch += NEH) {
-            uint32_t nraw[16];
-            const bool more = ch + NEH < nchunks;
-            if (more) tmem_ld_32x32b_x16(trow + tcol(ch + NEH), nraw);
+            uint32_t raw[16];
+            tmem_ld_32x32b_x16(trow + tcol(ch), raw);
+            tmem_ld_wait_regs(raw);
+            after_load(ch);
             float v[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
@@ -433,12 +425,6 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
                        (DBG ? ep.trace : nullptr) && tb < 2 && et == 0 && seg == 0 && ch < 64 ? (DBG ? ep.trace : nullptr) + tb * 1024 + 864 + ch : nullptr);
             if ((DBG ? ep.trace : nullptr) && tb < 2 && et == 0 && seg == 0 && ch < 64)
               (DBG ? ep.trace : nullptr)[tb * 1024 + 640 + ch] = globaltimer_ns();
-            if (more) {
-              tmem_ld_wait_regs(nraw);
-              after_load(ch + NEH);
-#pragma unroll
-              for (int j = 0; j < 16; ++j) raw[j] = nraw[j];
-            }
           }
         }
       } else {

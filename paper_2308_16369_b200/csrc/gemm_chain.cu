@@ -52,13 +52,16 @@ SARATHI_DEVICE void st_release_gpu(unsigned* p, unsigned v) {
 // generic-proxy global writes <-> async-proxy (TMA) reads of the same data
 SARATHI_DEVICE void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
+// Spin with relaxed loads (an acquire load per iteration also invalidates L1: CCTL.IVALL), then one
+// acquire fence once the flag is seen.
 SARATHI_DEVICE void wait_flag(const unsigned* f, unsigned epoch) {
   if (static_cast<int>(ld_acquire_gpu(f) - epoch) >= 0) return;
   const unsigned long long t0 = globaltimer_ns();
-  while (static_cast<int>(ld_acquire_gpu(f) - epoch) < 0) {
-    __nanosleep(40);
+  while (static_cast<int>(ld_relaxed_gpu(f) - epoch) < 0) {
+    __nanosleep(64);
     if (globaltimer_ns() - t0 > 4000000000ull) __trap();
   }
+  fence_acq_rel_gpu();
 }
 
 // Bulk reduce-add of a warp's 16-token x 32-column fp32 block (token-major in shared memory) into
@@ -485,14 +488,12 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
           __syncwarp();
         };
         if (split) fetch(eh);
-        uint32_t raw[16];
-        tmem_ld_32x32b_x16(trow + tcol(eh), raw);
-        tmem_ld_wait_regs(raw);
-        after_load(eh);
         for (int ch = eh; ch < nchunks; ch += NEH) {
-          uint32_t nraw[16];
+          uint32_t raw[16];
+          tmem_ld_32x32b_x16(trow + tcol(ch), raw);
+          tmem_ld_wait_regs(raw);
+          after_load(ch);
           const bool more = ch + NEH < nchunks;
-          if (more) tmem_ld_32x32b_x16(trow + tcol(ch + NEH), nraw);
           float v[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
@@ -515,12 +516,6 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
           else
             epi_emit<FFN, false>(J.M, p.bn, ep, v, quarter, lane, mt, 0, ch * 16, tvalid, sbuf, s_pos, s_slot, s_consec,
                                  ql);
-          if (more) {
-            tmem_ld_wait_regs(nraw);
-            after_load(ch + NEH);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) raw[j] = nraw[j];
-          }
         }
       }
       if (tre) tre[7] = globaltimer_ns();

@@ -392,7 +392,10 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   // layer chain (world == 1; SARATHI_CHAIN=0 keeps one launch per GEMM + RMSNorm kernels)
   {
     const char* ce = getenv("SARATHI_CHAIN");
-    chain_on = world == 1 && H % 128 == 0 && !(ce && ce[0] == '0');
+    // opt-in: measured no faster than the standalone PDL-chained GEMMs at [13B-1] (interleaved A/B,
+    // profiles/r02_ab_drain.txt) and slower on TP-rank shapes; SARATHI_CHAIN=1 (policy: large-M
+    // shapes) or 2 (every shape)
+    chain_on = world == 1 && H % 128 == 0 && ce && (ce[0] == '1' || ce[0] == '2');
   }
   if (chain_on) {
     nt_h = 2 * ((H + 255) / 256);

@@ -9,6 +9,10 @@ h^{l-1} and the request's KV context read back from the paged cache and recomput
   * the layer's update h^l - h^{l-1} (attention over [0, pos] + O-proj + FFN),
 and for the final residual the logits on a sampled vocabulary subset.  Max relative error
 <= 2e-2 (north star) on each."""
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 
@@ -27,6 +31,22 @@ def _bf16(bits):
 
 def test_llama13b_bench_composition_sampled_layer_local():
     _layer_local(synth.LLAMA_13B, 256, 768, 64, 1024, (0, synth.LLAMA_13B.n_layers - 1))
+
+
+@pytest.mark.skipif(os.environ.get("SARATHI_FULLSIZE_CHILD") == "1", reason="child process")
+@pytest.mark.parametrize("env", [{"SARATHI_CHAIN": "1"}, {"SARATHI_CHAIN": "2", "SARATHI_CHAIN_SPLIT": "1"}])
+def test_layer_chain_full_size(env):
+    """The one-launch layer chain (opt-in, gemm_chain.cu) at LLaMA-13B full size in the bench
+    composition (SARATHI_CHAIN=1: whole tiles, 60 QKV / 108 gate||up pair tiles) and forced with
+    split whole-tile jobs on every shape incl. the TP-8 rank shards (scratch-slab reductions of
+    5-18 contributors per tile): the same layer-local checks, in a child process."""
+    env = dict(os.environ, SARATHI_FULLSIZE_CHILD="1", **env)
+    sel = "bench_composition" if env["SARATHI_CHAIN"] == "1" else "bench_composition or config_shards"
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m", "gpu", "-k", sel,
+                        "-p", "no:cacheprovider"], env=env, capture_output=True, text=True, timeout=1200,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "failed" not in r.stdout and " passed" in r.stdout, r.stdout[-2000:]
 
 
 # Per-rank shard shapes of the other BASELINE.json configs at full width (SURVEY §8(a) reference

@@ -167,8 +167,8 @@ def test_prefill_attention_variants(env, select, n):
 @pytest.mark.skipif(os.environ.get("SARATHI_PREFILL_VARIANT_CHILD") == "1", reason="child process")
 @pytest.mark.parametrize("env", [{"SARATHI_CHAIN": "2"}, {"SARATHI_CHAIN": "2", "SARATHI_CHAIN_SPLIT": "1"}])
 def test_layer_chain_variants(env):
-    """The one-launch layer chain (gemm_chain.cu) on the tiny shapes, where the default policy
-    keeps standalone GEMMs (whole-tile jobs too small to fill the GPU): forced on (SARATHI_CHAIN=2,
+    """The opt-in one-launch layer chain (gemm_chain.cu) on the tiny shapes, whose whole-tile jobs
+    are too small for the chain's own policy (SARATHI_CHAIN=1): forced on (SARATHI_CHAIN=2,
     whole tiles, tile flags, RMSNorm folded into finalisers / epilogue scales) and with split
     whole-tile jobs reduced through scratch slabs (SARATHI_CHAIN_SPLIT=1), over hybrid schedules
     incl. GQA, GELU, bs 32/64 and multi-tile prefill chunks."""

@@ -51,6 +51,7 @@ struct KParams {
   int nbuf;               // TMEM accumulator buffers (2 if bn <= 256)
   int max_slots;          // partial slots per tile
   int red_partials;       // split tiles accumulate in ONE zeroed fp32 slot by red.add (many contributors)
+  int atomic;             // residual add: every contributor red.adds its partial (else slots, deterministic)
   uint32_t tmem_cols;
   uint32_t ring_bytes;
   int n0, n1;             // tokens of UMMA 0 / 1 per k-step (n_mma == 2: equal halves, or 256 + tail)
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
       const uint32_t use = seg / p.nbuf;
       const int tvalid = min(p.bn, p.N - nt * p.bn);
       // whole tiles and residual adds (red.add of every contributor's partial) emit straight from TMEM
-      const bool direct = (kb0 == 0 && kb1 == p.KB) || MODE == EPI_ADD_F32;
+      const bool direct = (kb0 == 0 && kb1 == p.KB) || (MODE == EPI_ADD_F32 && p.atomic);
       QkvLane ql{};
       if (rope_mode) ql = qkv_lane(ep, mt, quarter, lane);
       const int nchunks = (tvalid + 15) / 16;
@@ -577,8 +578,11 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
   return r == CUDA_SUCCESS;
 }
 
-GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int force_pairs, bool atomic_epilogue) {
+GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int force_pairs, bool atomic_epilogue,
+                   bool deterministic) {
+  if (deterministic) atomic_epilogue = false;  // residual adds reduce through slots as well
   GemmPlan pl;
+  pl.atomic = atomic_epilogue ? 1 : 0;
   pl.M = M;
   pl.N = N;
   pl.K = K;
@@ -673,7 +677,7 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
   // partials by red.add into one zeroed fp32 slot per tile (the last contributor reads it once, runs
   // the epilogue and re-zeroes it) instead of shrinking the grid to <= 4 slots
   pl.red_partials = 0;
-  if (!atomic_epilogue && dp_per == 0 && max_slots > 4 && tiles128 * tile_elems <= ws_cap_floats / 2) {
+  if (!deterministic && !atomic_epilogue && dp_per == 0 && max_slots > 4 && tiles128 * tile_elems <= ws_cap_floats / 2) {
     pl.red_partials = 1;
     max_slots = 1;
   }
@@ -830,6 +834,7 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   kp.n1 = pl.n1;
   kp.max_slots = pl.max_slots;
   kp.red_partials = pl.red_partials;
+  kp.atomic = pl.atomic;
   kp.tmem_cols = (pl.nbuf == 2 || (pl.n_mma == 2 && 3 * (pl.bn / 2) <= 512)) ? 512 : pow2_cols(pl.bn);
   kp.ring_bytes = static_cast<uint32_t>(pl.stages * (kABytes + static_cast<size_t>(pl.bn / 2) * kBK * 2));
   cudaLaunchConfig_t cfg = {};

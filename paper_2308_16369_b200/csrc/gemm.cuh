@@ -59,6 +59,7 @@ struct GemmPlan {
   int dp_extra = 0;    // pairs [0, dp_extra) take one extra whole tile
   int max_slots = 1;   // stream-K partial slots per tile
   int red_partials = 0;  // split tiles accumulate by red.add into ONE zeroed slot (ws_red)
+  int atomic = 0;        // residual-add split tiles red.add every contributor's partial into the output
   int nbuf = 1;        // TMEM accumulator buffers
   int splits = 1, kb_per_split = 0;  // units per CTA (informational)
   int stages = 0;
@@ -72,8 +73,11 @@ struct GemmPlan {
 // tcgen05 cta_group::2).  force_pairs > 0 fixes the grid (tests use it to exercise multi-pair
 // reductions of one tile).
 // atomic_epilogue: the epilogue is a residual add (split tiles reduce with red.add, no reduction pass).
+// deterministic: no red.add reductions anywhere (split tiles reduce through partial slots summed
+// in slot order by the last contributor; a residual-add epilogue then adds ONE sum per element), so
+// a launch's result is bitwise reproducible run to run (slower: DESIGN.md §6).
 GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int force_pairs = 0,
-                   bool atomic_epilogue = false);
+                   bool atomic_epilogue = false, bool deterministic = false);
 
 // 2D bf16 K-major tensor map with 128B swizzle: rows x cols(=K), box = box_rows x 64.
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,

@@ -779,10 +779,13 @@ Status Model::run_chain(int l, int T, bool with_qkv, const int* d_pos_dev, const
 }
 
 Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, int N, const EpiParams& ep_in, int op) {
+  // SARATHI_DETERMINISTIC=1: no red.add reductions (bitwise run-to-run reproducible residual stream)
+  static const bool deterministic = getenv("SARATHI_DETERMINISTIC") && atoi(getenv("SARATHI_DETERMINISTIC")) == 1;
   const bool atomic = ep_in.mode == EPI_ADD_F32;
   auto pk = std::make_tuple(M, N, K * 2 + (atomic ? 1 : 0));
   auto it = plans.find(pk);
-  if (it == plans.end()) it = plans.emplace(pk, plan_gemm(M, N, K, num_sms, gemm_ws_floats, 0, atomic)).first;
+  if (it == plans.end())
+    it = plans.emplace(pk, plan_gemm(M, N, K, num_sms, gemm_ws_floats, 0, atomic, deterministic)).first;
   const GemmPlan& pl = it->second;
   const CUtensorMap *mx = nullptr, *mx2 = nullptr;
   SRET(xmap(X, N, K, ldx, pl.box_rows, &mx));

@@ -183,6 +183,44 @@ def test_layer_chain_variants(env):
     assert m and int(m.group(1)) >= 8 and "failed" not in r.stdout, r.stdout[-2000:]
 
 
+# a width at which the residual-add GEMMs split K over several CTA pairs (red.add by default)
+MID = synth.ModelConfig("mid-2048", 2, 2048, 16, 16, 128, 5632, 512, max_seq_len=512)
+MID_REQS = [(1, 300, 3, 0), (2, 40, 6, 0), (3, 90, 4, 1)]
+
+
+@pytest.mark.skipif(os.environ.get("SARATHI_DET_CHILD") != "1", reason="runs in test_deterministic_mode's child")
+def test_deterministic_bitwise_child(S):
+    """Two identical runs of a hybrid schedule in deterministic mode: every logit and every layer's
+    residual bitwise identical (no red.add reduction anywhere), and within the oracle contract."""
+    runs = []
+    for _ in range(2):
+        m = S.Model(S.config_from(MID, max_tokens_per_batch=320), seed=4)
+        m.alloc_kv(64, 16)
+        steps, info = gh.gpu_schedule(S, m, MID, MID_REQS, B=3, C=256, num_blocks=64, block_size=16)
+        m.close()
+        runs.append(steps)
+    for a, b in zip(*runs):
+        assert np.array_equal(a["logits"], b["logits"])
+        for ha, hb in zip(a["hidden"], b["hidden"]):
+            assert np.array_equal(ha, hb)
+    ref = gh.oracle_schedule(om.model_weights(MID, 4), runs[0], {r[0]: (r[1], r[2]) for r in MID_REQS}, 64, 16)
+    _check(ref)
+
+
+@pytest.mark.skipif(os.environ.get("SARATHI_DET_CHILD") == "1", reason="child process")
+def test_deterministic_mode():
+    """SARATHI_DETERMINISTIC=1 (split tiles reduce through partial slots summed in slot order, the
+    residual add then applies one sum per element): bitwise run-to-run reproducibility, in a child
+    process (the mode is read once per process)."""
+    env = dict(os.environ, SARATHI_DET_CHILD="1", SARATHI_DETERMINISTIC="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m", "gpu", "-k",
+                        "deterministic_bitwise_child", "-p", "no:cacheprovider"],
+                       env=env, capture_output=True, text=True, timeout=900,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "1 passed" in r.stdout, r.stdout[-2000:]
+
+
 def test_block_size_32_schedule(S):
     """bs = 32, the one accepted block size no other test runs: a multi-block hybrid schedule."""
     cfg = dataclasses.replace(synth.TINY, name="tiny-bs32", max_seq_len=256)

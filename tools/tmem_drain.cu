@@ -23,9 +23,12 @@ SARATHI_DEVICE void ld_x32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 
-template <int MODE>  // 0: x16 one in flight, 1: x16 pipelined, 2: x32 one in flight
-__global__ void __launch_bounds__(320, 1) drain(int chunks, unsigned long long* out, float* sink) {
+template <int MODE>  // 0: x16 one in flight, 1: x16 pipelined, 2: x32 one in flight, 3: 0 + bf16
+                     // transpose through smem + 16-B global stores (the GEMM's store epilogue), 4: 3 + sincos
+__global__ void __launch_bounds__(320, 1) drain(int chunks, unsigned long long* out, float* sink, __nv_bfloat16* gout,
+                                                 int ldo) {
   __shared__ uint32_t holder;
+  __shared__ __align__(16) uint16_t sbuf_all[8][16 * 32];
   const uint32_t warp = threadIdx.x >> 5;
   if (warp == 1) tmem_alloc(&holder, 512);
   tc_fence_before();
@@ -61,6 +64,34 @@ __global__ void __launch_bounds__(320, 1) drain(int chunks, unsigned long long* 
           for (int j = 0; j < 16; ++j) r[j] = n[j];
         }
       }
+    } else if (MODE >= 3) {
+      uint16_t* sb = sbuf_all[warp - 2];
+      const uint32_t lane = threadIdx.x & 31;
+      const int row0 = blockIdx.x * 128 + quarter * 32;
+      for (int ch = eh; ch < chunks; ch += 2) {
+        uint32_t r[16];
+        tmem_ld_32x32b_x16(trow + (ch % 32) * 16, r);
+        tmem_ld_wait_regs(r);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float x = __uint_as_float(r[j]);
+          if (MODE == 4) {
+            float sn, cs;
+            __sincosf(x * 0.001f + j, &sn, &cs);
+            x = x * cs + sn;
+          }
+          sb[j * 32 + lane] = __bfloat16_as_ushort(__float2bfloat16_rn(x));
+        }
+        __syncwarp();
+        const int g = static_cast<int>(lane & 3), m = row0 + g * 8;
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+          const int tok = ch * 16 + pass * 8 + static_cast<int>(lane >> 2);
+          *reinterpret_cast<uint4*>(gout + static_cast<size_t>(tok) * ldo + m) =
+              *reinterpret_cast<const uint4*>(sb + (pass * 8 + (lane >> 2)) * 32 + g * 8);
+        }
+        __syncwarp();
+      }
     } else {
       for (int ch = 2 * eh; ch < chunks; ch += 4) {
         uint32_t r[32];
@@ -87,16 +118,21 @@ template <int MODE>
 void run(int chunks, int sms) {
   unsigned long long* d;
   float* sink;
+  __nv_bfloat16* gout;
+  const int ldo = sms * 128;
   cudaMalloc(&d, sms * 8);
   cudaMalloc(&sink, 4096);
-  for (int it = 0; it < 3; ++it) drain<MODE><<<sms, 320>>>(chunks, d, sink);
+  cudaMalloc(&gout, static_cast<size_t>(chunks) * 16 * ldo * 2);
+  for (int it = 0; it < 3; ++it) drain<MODE><<<sms, 320>>>(chunks, d, sink, gout, ldo);
   cudaDeviceSynchronize();
   std::vector<unsigned long long> h(sms);
   cudaMemcpy(h.data(), d, sms * 8, cudaMemcpyDeviceToHost);
   std::sort(h.begin(), h.end());
-  printf("mode %d (%s) chunks %d: drain %.2f us (median over %d CTAs, max %.2f)  err=%s\n", MODE,
-         MODE == 0 ? "x16, 1 in flight" : MODE == 1 ? "x16, pipelined" : "x32, 1 in flight", chunks, h[sms / 2] * 1e-3,
-         sms, h[sms - 1] * 1e-3, cudaGetErrorString(cudaGetLastError()));
+  const char* names[] = {"x16, 1 in flight", "x16, pipelined", "x32, 1 in flight", "x16 + smem transpose + stores",
+                         "x16 + sincos + transpose + stores"};
+  printf("mode %d (%s) chunks %d: drain %.2f us (median over %d CTAs, max %.2f)  err=%s\n", MODE, names[MODE], chunks,
+         h[sms / 2] * 1e-3, sms, h[sms - 1] * 1e-3, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(gout);
   cudaFree(d);
   cudaFree(sink);
 }
@@ -107,6 +143,8 @@ int main() {
     run<0>(chunks, sms);
     run<1>(chunks, sms);
     run<2>(chunks, sms);
+    run<3>(chunks, sms);
+    run<4>(chunks, sms);
   }
   return 0;
 }

@@ -299,6 +299,19 @@ __global__ void __launch_bounds__(160)
       if (dd == 0) a.part_lse[(static_cast<size_t>(j) * nq + qh) * a.splits + z] = M + log2f(L);
     }
   }
+  if (a.head_flag) {  // publish this KV head's rows once all d requests' CTAs wrote them
+    __threadfence();
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // read by the O GEMM's TMA loads
+    named_bar_sync(1, 128);
+    if (tid == 0) {
+      const int old = atomicAdd(a.head_cnt + kvh, 1);
+      if (old == a.d - 1) {
+        a.head_cnt[kvh] = 0;  // re-arm for the next launch
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.head_flag + kvh), "r"(a.epoch) : "memory");
+      }
+    }
+  }
   // attention chain: the grid must not complete before the prefill grid; one CTA waiting is
   // enough (the others keep their SM slots free for the rest of the grid)
   if (a.wait_at_end && last_cta) griddep_wait();
@@ -753,6 +766,20 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, L::kTmemCols);
+  }
+  if (a.done_flag) {  // the grid's last CTA to finish publishes completion (O GEMM X dependency)
+    __threadfence();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int total = static_cast<int>(gridDim.x * gridDim.y * gridDim.z);
+      const int old = atomicAdd(a.done_cnt, 1);
+      if (old == total - 1) {
+        *a.done_cnt = 0;
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.done_flag), "r"(a.epoch) : "memory");
+      }
+    }
   }
   if (a.trace && threadIdx.x == 0 && blockIdx.x < 384) a.trace[257 + 2 * blockIdx.x] = globaltimer_ns();
   if (a.span_end && threadIdx.x == 0) atomicMax(a.span_end, globaltimer_ns());

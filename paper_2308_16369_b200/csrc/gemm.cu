@@ -58,6 +58,23 @@ struct KParams {
 };
 
 
+// X-flag wait (EpiParams::xflag): relaxed spin, one acquire fence, then order the async proxy (TMA)
+// after it; a lost flag traps instead of hanging the GPU
+SARATHI_DEVICE void xflag_wait(const unsigned* f, unsigned epoch) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  if (static_cast<int>(v - epoch) < 0) {
+    const unsigned long long t0 = globaltimer_ns();
+    do {
+      __nanosleep(64);
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+    } while (static_cast<int>(v - epoch) < 0);
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 SARATHI_DEVICE long long unit_begin(int c, const KParams& p) {
   return (static_cast<long long>(c) * p.units) / p.ctas;
 }
@@ -160,7 +177,9 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
   // uneven split (n0 = 256 + a 16..240-token tail n1, single accumulator): one full-width UMMA plus
   // a narrow one instead of two halves, for single-segment plans (no epilogue overlap to keep)
   const bool ring = p.n_mma == 2 && p.n0 == p.n1 && 3 * ni <= 512;
-  if (warp != 0) griddep_wait();  // the producer waits after prefetching its first W tiles
+  // the producer waits after prefetching its first W tiles; with X flags (ep.xflag) only the
+  // epilogue waits for the predecessor grid
+  if (warp >= 2 || (warp == 1 && !ep.xflag)) griddep_wait();
 
   if (warp == 0) {
     // ---------------- TMA producer (whole warp, warp-uniform; one elected lane issues) ----------------
@@ -191,7 +210,12 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
           }
         }
       }
-      griddep_wait();
+      if (!ep.xflag) {
+        griddep_wait();
+      } else if (ep.xflag2) {
+        xflag_wait(ep.xflag2, ep.xepoch);
+      }
+      int have_lo = 0, have = -1;  // X flags [have_lo, have] already acquired (ep.xflag)
       while (it.next(p, tile, kb0, kb1)) {
         const int pt = tile / p.n_tiles, nt = tile % p.n_tiles;
         int wrow = ((pt * 2 + static_cast<int>(rank)) * p.KB + kb0) * kWRowsPerTile;  // row in the 512-B view
@@ -204,6 +228,28 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
             if (rank == 0) mbar_arrive_expect_tx_warp(&full[s], tx);
             // W tile: the contiguous 16 KB pre-swizzled tile as 32 rows x 512 B (unswizzled map)
             if (!(DBG && (ep.dbg & 2))) tma_load_2d_pair_warp(a, &mapW, &full[s], 0, wrow, pol_w);
+          }
+          if (ep.xflag) {
+            const int need = (kb * kBK) / ep.xflag_cols;
+            if (need < have_lo || need > have) {
+              // warp-wide relaxed scan of the next 32 flags, block on the first unready one only
+              have_lo = need;
+              while (true) {
+                const int q = need + static_cast<int>(lane);
+                unsigned v = 0xFFFFFFFFu;
+                if (q < ep.xflag_n) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ep.xflag + q) : "memory");
+                const bool ok = q >= ep.xflag_n || static_cast<int>(v - ep.xepoch) >= 0;
+                const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+                const int nready = bad ? __ffs(bad) - 1 : 32;
+                if (nready > 0) {
+                  have = need + nready - 1;
+                  break;
+                }
+                xflag_wait(ep.xflag + need, ep.xepoch);
+              }
+              asm volatile("fence.acq_rel.gpu;" ::: "memory");
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
           }
           if (!(DBG && (ep.dbg & 1))) {
             tma_load_2d_pair_warp(b, &mapX, &full[s], kb * kBK, nt * p.bn + static_cast<int>(rank) * (p.n0 / 2), pol_x);

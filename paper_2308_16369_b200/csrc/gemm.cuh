@@ -40,6 +40,15 @@ struct EpiParams {
   unsigned long long* span_start = nullptr;  // profiling: atomicMin of CTA start times (globaltimer)
   unsigned long long* span_end = nullptr;    // profiling: atomicMax of CTA end times
   int dbg = 0;  // debug: bit0 skip X loads, bit1 skip W loads, bit2 skip whole-tile epilogue stores (timing experiments only; results invalid)
+  // X produced by the still-running predecessor grids (the O projection after the attention
+  // kernels): instead of the grid dependency, the TMA producer waits, per k-block kb, for
+  // xflag[(kb * 64) / xflag_cols] >= xepoch and once for *xflag2 >= xepoch (if set); the MMA warp
+  // does not wait at all and the epilogue keeps the grid dependency (it touches other buffers)
+  const unsigned* xflag = nullptr;
+  int xflag_cols = 0;
+  int xflag_n = 0;  // number of X flags
+  const unsigned* xflag2 = nullptr;
+  unsigned xepoch = 0;
 };
 
 struct GemmPlan {

@@ -39,6 +39,12 @@ struct DecodeAttnArgs {
   // profiling (sarathi_op_kernel_times): min CTA start / max CTA end, globaltimer ns, or null
   unsigned long long* span_start = nullptr;
   unsigned long long* span_end = nullptr;
+  // per-KV-head completion (splits == 1): the d-th CTA of KV head g to finish its output rows sets
+  // head_flag[g] = epoch (release), so the O projection can start on finished heads inside this
+  // grid's last wave (GEMM EpiParams::xflag); head_cnt zero between launches
+  unsigned* head_flag = nullptr;
+  int* head_cnt = nullptr;
+  unsigned epoch = 0;
 };
 
 struct PrefillAttnArgs {
@@ -66,6 +72,10 @@ struct PrefillAttnArgs {
   int* counters = nullptr;   // [pairs], zero between launches (the merging CTA re-zeroes)
   unsigned long long* span_start = nullptr;  // profiling, as DecodeAttnArgs (tcgen05 kernel)
   unsigned long long* span_end = nullptr;
+  // grid completion (tcgen05 kernel): the last CTA to finish sets done_flag = epoch (release)
+  unsigned* done_flag = nullptr;
+  int* done_cnt = nullptr;
+  unsigned epoch = 0;
 };
 
 size_t decode_smem_bytes(int head_dim, int block_size, int stages, int G);

@@ -389,6 +389,10 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   pp_pairs = ((Tmax + 127) / 128) * nq_l;
   SRET(dalloc(&pp_ctr, pp_pairs));
   SRET(check(cudaMemset(pp_ctr, 0, pp_pairs * sizeof(int)), "memset"));
+  SRET(dalloc(&aflags, static_cast<size_t>(nkv_l + 1)));
+  SRET(dalloc(&acnt, static_cast<size_t>(nkv_l + 1)));
+  SRET(check(cudaMemset(aflags, 0, (nkv_l + 1) * sizeof(unsigned)), "memset"));
+  SRET(check(cudaMemset(acnt, 0, (nkv_l + 1) * sizeof(int)), "memset"));
   // layer chain (world == 1; SARATHI_CHAIN=0 keeps one launch per GEMM + RMSNorm kernels)
   {
     const char* ce = getenv("SARATHI_CHAIN");
@@ -1084,6 +1088,14 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     op_end(SARATHI_OP_GEMM_QKV, ob);
     }
     const bool chain = attn_chain && p > 0 && d > 0 && !no_aux;
+    // SARATHI_O_EARLY=1: the O projection starts on finished KV heads inside the decode attention's
+    // last wave (per-head flags instead of the grid dependency).  Measured: no earlier O completion
+    // (the third split-K contributors need the last heads) and the decode slows by the overlap,
+    // 18.79 vs 18.66 ms (profiles/r02_ab_oearly.txt), so off by default
+    static const bool o_early = getenv("SARATHI_O_EARLY") && atoi(getenv("SARATHI_O_EARLY")) == 1;
+    const bool xflags_try = o_early && d > 0 && (p == 0 || chain);
+    bool xflags = false;
+    if (xflags_try) ++attn_epoch;
     if (p > 0) {
       PrefillAttnArgs pa;
       pa.q = q;
@@ -1134,6 +1146,11 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
         pa.part_o = pp_o;
         pa.part_ml = pp_ml;
         pa.counters = pp_ctr;
+      }
+      if (xflags_try) {
+        pa.done_flag = aflags + nkv_l;
+        pa.done_cnt = acnt + nkv_l;
+        pa.epoch = attn_epoch;
       }
       // with decodes in the batch, the chunk's attention overlaps the decode attention: by default
       // both run in the main stream as an "attention chain" (prefill, PDL-launched, waits for QKV
@@ -1239,6 +1256,12 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       da.part_lse = part_lse;
       da.out = o;
       da.out_ld = q_dim_l;
+      if (xflags_try && da.splits == 1) {
+        da.head_flag = aflags;
+        da.head_cnt = acnt;
+        da.epoch = attn_epoch;
+        xflags = true;
+      }
       ob = op_begin();
       SRET(take_span(SARATHI_OP_DECODE_ATTN, &da.span_start, &da.span_end));
       SRET(check(launch_decode_attention(da, kmap[l], vmap[l], stream), "decode attention"));
@@ -1262,6 +1285,13 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       eo.mode = EPI_STORE_BF16;
       eo.out = ar_target();
       eo.ldo = H;
+    }
+    if (xflags) {  // X = o: per KV head (G query heads x hd columns) + the chunk's rows
+      eo.xflag = aflags;
+      eo.xflag_cols = (nq_l / nkv_l) * hd;
+      eo.xflag_n = nkv_l;
+      eo.xflag2 = p > 0 ? aflags + nkv_l : nullptr;
+      eo.xepoch = attn_epoch;
     }
     ob = op_begin();
     SRET(gemm(w.m_o, H, q_dim_l, o, q_dim_l, T, eo, SARATHI_OP_GEMM_O));

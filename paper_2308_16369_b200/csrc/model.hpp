@@ -175,6 +175,11 @@ struct Model {
   Status chain_plan(int T, bool with_qkv, const ChainPlanDev** out);
   Status run_chain(int l, int T, bool with_qkv, const int* d_pos, const int* d_slot);
   Status xmap(const void* X, int N, int K, int ldx, int box_rows, const CUtensorMap** out);
+  // attention -> O projection handoff (EpiParams::xflag): per-KV-head completion flags of the decode
+  // attention + the prefill attention's grid-completion flag, epoch-valued; counters zero between launches
+  unsigned* aflags = nullptr;  // [n_kv_l] heads | [1] prefill done
+  int* acnt = nullptr;         // [n_kv_l + 1]
+  unsigned attn_epoch = 0;
   int64_t launches = 0;
   // I/O accounting and per-op timers
   int64_t last_h2d = 0, last_d2h = 0;

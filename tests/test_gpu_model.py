@@ -147,14 +147,17 @@ def test_prefill_attention_multitile(S, hd, n_kv, C, bs):
 @pytest.mark.parametrize("env,select,n", [({"SARATHI_PREFILL_BK": "64"}, "prefill_attention_multitile", 4),
                                           ({"SARATHI_PREFILL_PT": "0"}, "prefill_attention_multitile", 4),
                                           ({"SARATHI_ATTN_CHAIN": "0"}, "prefill_attention_multitile or config1", 5),
-                                          ({"SARATHI_PREFILL_KSPLIT": "3"}, "prefill_attention_multitile", 4)])
+                                          ({"SARATHI_PREFILL_KSPLIT": "3"}, "prefill_attention_multitile", 4),
+                                          ({"SARATHI_O_EARLY": "1"}, "prefill_attention_multitile or config1", 5)])
 def test_prefill_attention_variants(env, select, n):
     """The non-default attention paths, selected once per process by environment, rerun hybrid-batch
     cases in a child process: the 64-key prefill tile (SARATHI_PREFILL_BK=64: single-buffered V at
     hd 128, 2 CTAs per SM; bs 128 keeps the wide tile), the smem P image (SARATHI_PREFILL_PT=0),
     the side-stream + event-join overlap instead of the attention chain (SARATHI_ATTN_CHAIN=0) and
     the key split merged by the last CTA of each (q-tile, head) pair (SARATHI_PREFILL_KSPLIT=3,
-    capped by the first q-tile's key tiles, so the later chunks of the 700-token prompt split)."""
+    capped by the first q-tile's key tiles, so the later chunks of the 700-token prompt split) and
+    the O projection gated by the attention kernels' per-KV-head / grid-completion flags instead of
+    the grid dependency (SARATHI_O_EARLY=1)."""
     env = dict(os.environ, SARATHI_PREFILL_VARIANT_CHILD="1", **env)
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m", "gpu", "-k",
                         select, "-p", "no:cacheprovider"],

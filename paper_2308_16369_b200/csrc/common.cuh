@@ -381,6 +381,28 @@ SARATHI_DEVICE void umma_f16_ss_pair_warp(uint32_t d_tmem, uint64_t a_desc, uint
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Pair MMA with the A operand from TMEM (each CTA's 128 rows at the same TMEM address; lanes = rows,
+// 32-bit columns holding two consecutive bf16 K elements), B from shared memory.
+SARATHI_DEVICE void umma_f16_ts_pair_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// shared memory -> TMEM copy of a 128-row x 256-bit matrix (one k16 slice of a K-major bf16 operand)
+// in both CTAs of the pair (each from its own shared memory); executes in issue order with the MMAs
+SARATHI_DEVICE void tmem_cp_128x256b_pair_warp(uint32_t taddr, uint64_t s_desc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.cp.cta_group::2.128x256b [%0], %1;\n\t}\n" ::"r"(taddr),
+      "l"(s_desc)
+      : "memory");
+}
 SARATHI_DEVICE void umma_commit_pair_mc_warp(uint64_t* bar, uint16_t cta_mask) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

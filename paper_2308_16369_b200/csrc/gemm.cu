@@ -55,7 +55,10 @@ struct KParams {
   uint32_t tmem_cols;
   uint32_t ring_bytes;
   int n0, n1;             // tokens of UMMA 0 / 1 per k-step (n_mma == 2: equal halves, or 256 + tail)
+  int ts;                 // A (weights) staged in TMEM by tcgen05.cp at column kTsCol: the second UMMA of
+                          // a k-step does not re-read A from shared memory
 };
+constexpr int kTsCol = 480;  // 4 k16 slices x 8 columns of the A operand (one k-block)
 
 
 // X-flag wait (EpiParams::xflag): relaxed spin, one acquire fence, then order the async proxy (TMA)
@@ -306,13 +309,24 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
             // warp-uniform issue (operands stay in uniform registers), one elected lane issues
             const uint32_t a = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
             const uint32_t b = a + kABytes;
+            if (p.ts) {
+              const uint32_t at = tmem + kTsCol;
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) {
-              const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
-              umma_f16_ss_pair_warp(d0, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc, acc);
-              if (p.n_mma == 2)
-                umma_f16_ss_pair_warp(d1, make_desc_k_sw128(a + k * 32),
-                                      make_desc_k_sw128(b + (p.n0 / 2) * 128 + k * 32), idesc1, acc);
+              for (int k = 0; k < kBK / 16; ++k) {
+                const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
+                tmem_cp_128x256b_pair_warp(at + k * 8, make_desc_k_sw128(a + k * 32));
+                umma_f16_ts_pair_warp(d0, at + k * 8, make_desc_k_sw128(b + k * 32), idesc, acc);
+                umma_f16_ts_pair_warp(d1, at + k * 8, make_desc_k_sw128(b + (p.n0 / 2) * 128 + k * 32), idesc1, acc);
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < kBK / 16; ++k) {
+                const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
+                umma_f16_ss_pair_warp(d0, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc, acc);
+                if (p.n_mma == 2)
+                  umma_f16_ss_pair_warp(d1, make_desc_k_sw128(a + k * 32),
+                                        make_desc_k_sw128(b + (p.n0 / 2) * 128 + k * 32), idesc1, acc);
+              }
             }
             umma_commit_pair_mc_warp(&empty[s], 0x3);
             if (kb == kb1 - 1) umma_commit_pair_mc_warp(&tfull[tb_idx], 0x3);
@@ -882,6 +896,20 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   kp.red_partials = pl.red_partials;
   kp.atomic = pl.atomic;
   kp.tmem_cols = (pl.nbuf == 2 || (pl.n_mma == 2 && 3 * (pl.bn / 2) <= 512)) ? 512 : pow2_cols(pl.bn);
+  {
+    // A from TMEM for two-UMMA k-steps (T > 256) whose accumulators leave columns [kTsCol, 512)
+    // free (ring of 3 x <= 160, or one accumulator of <= 480 tokens): tcgen05.cp stages each k16
+    // slice of the weight tile once and both UMMAs read it from TMEM, instead of each UMMA
+    // re-reading it from shared memory (the second UMMA of a k-step cost ~0.13 us per k-block
+    // whatever its width: shared-memory operand bandwidth).  Measured at [13B-1]: per-k-block
+    // 0.48 -> 0.448 us (N = 320, tools/probe_ts.sh), layer GEMMs 240 -> 226 us, step 19.00 ->
+    // 18.51 ms (interleaved A/B, profiles/r02_ab_ts.txt).  SARATHI_GEMM_TS=0 disables.
+    static const bool ts_on = !(getenv("SARATHI_GEMM_TS") && atoi(getenv("SARATHI_GEMM_TS")) == 0);
+    const bool ring = pl.n_mma == 2 && pl.n0 == pl.n1 && 3 * pl.n0 <= 512;
+    const int used = pl.n_mma != 2 ? 512 : ring ? 3 * pl.n0 : pl.bn;
+    kp.ts = ts_on && pl.n_mma == 2 && used <= kTsCol;
+    if (kp.ts) kp.tmem_cols = 512;
+  }
   kp.ring_bytes = static_cast<uint32_t>(pl.stages * (kABytes + static_cast<size_t>(pl.bn / 2) * kBK * 2));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pl.ctas);

@@ -180,9 +180,103 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
   // uneven split (n0 = 256 + a 16..240-token tail n1, single accumulator): one full-width UMMA plus
   // a narrow one instead of two halves, for single-segment plans (no epilogue overlap to keep)
   const bool ring = p.n_mma == 2 && p.n0 == p.n1 && 3 * ni <= 512;
-  // the producer waits after prefetching its first W tiles; with X flags (ep.xflag) only the
-  // epilogue waits for the predecessor grid
-  if (warp >= 2 || (warp == 1 && !ep.xflag)) griddep_wait();
+  if (ep.norm_h) {
+    constexpr int kThr = 64 + 128 * NEH;  // threads per CTA
+    // fused RMSNorm prologue: the producer first issues its first ring of W tiles (they do not
+    // depend on the predecessor), then every thread waits for the grid dependency, normalises its
+    // CTA's rows, and the grid meets at a barrier before the first X load
+    if (warp == 0) {
+      SegIter it0;
+      it0.init(p, pair);
+      int tile, kb0, kb1;
+      if (it0.next(p, tile, kb0, kb1)) {
+        const uint32_t tx = 2 * stage_bytes;
+        const int npre0 = min(p.stages, kb1 - kb0);
+        const int pt = tile / p.n_tiles;
+        const int wrow0 = ((pt * 2 + static_cast<int>(rank)) * p.KB + kb0) * kWRowsPerTile;
+        for (int j = 0; j < npre0; ++j) {
+          if (rank == 0) mbar_arrive_expect_tx_warp(&full[j], tx);
+          tma_load_2d_pair_warp(smem + static_cast<size_t>(j) * stage_bytes, &mapW, &full[j], 0,
+                                wrow0 + j * kWRowsPerTile, policy_evict_first());
+        }
+      }
+    }
+    griddep_wait();
+    // this CTA's rows r = blockIdx.x + j * grid (j < kMaxRows) are normalised together: all their
+    // loads in flight at once, one reduction round for all of them
+    constexpr int kMaxRows = 4;
+    float* red = stage_buf;  // [kMaxRows][10] warp partial sums (the transpose buffers are idle here)
+    const int tid = threadIdx.x, H = ep.norm_H;
+    const __nv_bfloat16* g = static_cast<const __nv_bfloat16*>(ep.norm_g);
+    __nv_bfloat16* xo = static_cast<__nv_bfloat16*>(ep.norm_out);
+    for (int r0 = blockIdx.x; r0 < ep.norm_T; r0 += kMaxRows * gridDim.x) {
+      float4 v[kMaxRows][4];
+      float ss[kMaxRows];
+#pragma unroll
+      for (int j = 0; j < kMaxRows; ++j) {
+        const int r = r0 + j * gridDim.x;
+        ss[j] = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int i = (c * kThr + tid) * 4;
+          v[j][c] = (r < ep.norm_T && i < H) ? __ldcg(reinterpret_cast<const float4*>(ep.norm_h + static_cast<size_t>(r) * H + i))
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kMaxRows; ++j) {
+        const int r = r0 + j * gridDim.x;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ss[j] += v[j][c].x * v[j][c].x + v[j][c].y * v[j][c].y + v[j][c].z * v[j][c].z + v[j][c].w * v[j][c].w;
+        if (r < ep.norm_T)
+          for (int i = (4 * kThr + tid) * 4; i < H; i += kThr * 4) {  // H > 4 * 4 * threads
+            const float4 w = __ldcg(reinterpret_cast<const float4*>(ep.norm_h + static_cast<size_t>(r) * H + i));
+            ss[j] += w.x * w.x + w.y * w.y + w.z * w.z + w.w * w.w;
+          }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) ss[j] += __shfl_xor_sync(0xffffffffu, ss[j], off);
+        if (lane == 0) red[j * 16 + warp] = ss[j];
+      }
+      named_bar_sync(3, kThr);
+#pragma unroll
+      for (int j = 0; j < kMaxRows; ++j) {
+        const int r = r0 + j * gridDim.x;
+        if (r >= ep.norm_T) break;
+        float tot = 0.f;
+        for (int w = 0; w < kThr / 32; ++w) tot += red[j * 16 + w];  // warp order: deterministic
+        const float inv = rsqrtf(tot / static_cast<float>(H) + ep.norm_eps);
+        auto put = [&](int i, float4 w) {
+          const uint2 graw = *reinterpret_cast<const uint2*>(g + i);
+          const float2 g01 = unpack_bf16x2(graw.x), g23 = unpack_bf16x2(graw.y);
+          uint2 pk;
+          pk.x = pack_bf16x2(w.x * inv * g01.x, w.y * inv * g01.y);
+          pk.y = pack_bf16x2(w.z * inv * g23.x, w.w * inv * g23.y);
+          *reinterpret_cast<uint2*>(xo + static_cast<size_t>(r) * H + i) = pk;
+        };
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int i = (c * kThr + tid) * 4;
+          if (i < H) put(i, v[j][c]);
+        }
+        for (int i = (4 * kThr + tid) * 4; i < H; i += kThr * 4)
+          put(i, __ldcg(reinterpret_cast<const float4*>(ep.norm_h + static_cast<size_t>(r) * H + i)));
+      }
+      named_bar_sync(3, kThr);  // (red is rewritten by the next group of rows)
+    }
+    // grid barrier: every CTA's rows written (and visible to the async proxy) before any X load
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence();
+    named_bar_sync(3, kThr);
+    if (threadIdx.x == 0) {
+      atomicAdd(ep.norm_ctr, 1u);
+      xflag_wait(ep.norm_ctr, ep.norm_target);
+    }
+    named_bar_sync(3, kThr);
+  } else {
+    // the producer waits after prefetching its first W tiles; with X flags (ep.xflag) only the
+    // epilogue waits for the predecessor grid
+    if (warp >= 2 || (warp == 1 && !ep.xflag)) griddep_wait();
+  }
 
   if (warp == 0) {
     // ---------------- TMA producer (whole warp, warp-uniform; one elected lane issues) ----------------
@@ -200,7 +294,10 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
       // PDL: weights do not depend on the previous kernel, so the first ring's W tiles are fetched
       // before the grid-dependency wait (overlapping the predecessor's tail); X loads come after it
       int npre = 0;
-      {
+      if (ep.norm_h) {  // the prologue issued the first ring of W tiles already
+        SegIter it0 = it;
+        if (it0.next(p, tile, kb0, kb1)) npre = min(p.stages, kb1 - kb0);
+      } else {
         SegIter it0 = it;
         if (it0.next(p, tile, kb0, kb1)) {
           npre = min(p.stages, kb1 - kb0);
@@ -213,7 +310,9 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
           }
         }
       }
-      if (!ep.xflag) {
+      if (ep.norm_h) {
+        // grid dependency and X (this kernel's own prologue) already waited for
+      } else if (!ep.xflag) {
         griddep_wait();
       } else if (ep.xflag2) {
         xflag_wait(ep.xflag2, ep.xepoch);

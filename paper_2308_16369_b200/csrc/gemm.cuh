@@ -49,6 +49,17 @@ struct EpiParams {
   int xflag_n = 0;  // number of X flags
   const unsigned* xflag2 = nullptr;
   unsigned xepoch = 0;
+  // RMSNorm prologue (replaces the rmsnorm kernel before this GEMM): after the grid dependency,
+  // the CTAs normalise rows r = blockIdx, blockIdx + grid, ... of norm_h (fp32 [T][norm_H]) into
+  // the GEMM's own X (norm_out, bf16 [T][norm_H]: x * rsqrt(mean x^2 + eps) * g, reading O-8), then
+  // meet at a grid barrier (monotonic counter: wait for norm_target arrivals) before any X load
+  const float* norm_h = nullptr;
+  const void* norm_g = nullptr;
+  void* norm_out = nullptr;
+  int norm_T = 0, norm_H = 0;
+  float norm_eps = 0.f;
+  unsigned* norm_ctr = nullptr;
+  unsigned norm_target = 0;
 };
 
 struct GemmPlan {

@@ -389,6 +389,8 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   pp_pairs = ((Tmax + 127) / 128) * nq_l;
   SRET(dalloc(&pp_ctr, pp_pairs));
   SRET(check(cudaMemset(pp_ctr, 0, pp_pairs * sizeof(int)), "memset"));
+  SRET(dalloc(&norm_ctr, 1));
+  SRET(check(cudaMemset(norm_ctr, 0, sizeof(unsigned)), "memset"));
   SRET(dalloc(&aflags, static_cast<size_t>(nkv_l + 1)));
   SRET(dalloc(&acnt, static_cast<size_t>(nkv_l + 1)));
   SRET(check(cudaMemset(aflags, 0, (nkv_l + 1) * sizeof(unsigned)), "memset"));
@@ -795,6 +797,11 @@ Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, 
   SRET(xmap(X, N, K, ldx, pl.box_rows, &mx));
   SRET(xmap(X, N, K, ldx, pl.box_rows2, &mx2));
   EpiParams ep = ep_in;
+  if (ep.norm_h) {  // fused RMSNorm prologue: grid barrier target = all arrivals so far + this grid
+    norm_arrivals += 2u * static_cast<unsigned>(pl.ctas);
+    ep.norm_ctr = norm_ctr;
+    ep.norm_target = norm_arrivals;
+  }
   ep.ws = gemm_ws;
   ep.ws_red = gemm_ws + gemm_ws_floats / 2;
   ep.counters = gemm_counters;
@@ -1054,9 +1061,23 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   const int pairs_avail = num_sms / 2;
   const bool chain_fits = 4 * ((gu_rows + 255) / 256) >= 3 * pairs_avail && 4 * ((qkv_rows + 255) / 256) >= 3 * pairs_avail;
   const bool use_chain = chain_on && gemm_token_tiling(T).n_tiles == 1 && (chain_fits || chain_force);
+  // SARATHI_NORM_FUSED=1: RMSNorm fused into the next GEMM as a prologue + grid barrier (no
+  // RMSNorm launch; world 1: no pending TP partial to add).  Measured slower than the PDL-chained
+  // rmsnorm kernel (18.63 vs 18.51 ms, interleaved A/B, profiles/r02_ab_norm.txt): every CTA waits
+  // for the slowest one before its first X load, so off by default.
+  static const bool norm_fused_env = getenv("SARATHI_NORM_FUSED") && atoi(getenv("SARATHI_NORM_FUSED")) == 1;
+  const bool norm_fused = norm_fused_env && world == 1;
+  auto set_norm = [&](EpiParams& e, const __nv_bfloat16* g) {
+    e.norm_h = h;
+    e.norm_g = g;
+    e.norm_out = a;
+    e.norm_T = T;
+    e.norm_H = H;
+    e.norm_eps = cfg.rms_eps;
+  };
   for (int l = 0; l < nl; ++l) {  // this stage's layers (local index)
     LayerWeights& w = layers[l];
-    if (l == 0 || !use_chain) {
+    if ((l == 0 || !use_chain) && !norm_fused) {
     ob = op_begin();
     {
       unsigned long long *sp0, *sp1;
@@ -1071,6 +1092,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     if (l > 0) SRET(dump_h(l));  // h after layer l-1 (TP: once the all-reduce has been added)
     if (l == 0 || !use_chain) {
     EpiParams e;
+    if (norm_fused) set_norm(e, w.g1);
     e.mode = EPI_QKV_ROPE;
     e.out = q;
     e.ldo = q_dim_l;
@@ -1301,6 +1323,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       SRET(allreduce());
       op_end(SARATHI_OP_ALLREDUCE, ob);
     }
+    if (!norm_fused) {
     ob = op_begin();
     {
       unsigned long long *sp0, *sp1;
@@ -1310,8 +1333,10 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     if (world > 1) SRET(ar_end());
     op_end(SARATHI_OP_RMSNORM, ob);
     ++launches;
+    }
     // FFN
     EpiParams ef;
+    if (norm_fused) set_norm(ef, w.g2);
     ef.mode = cfg.ffn_kind == SARATHI_FFN_SWIGLU ? EPI_SILU_MUL : EPI_GELU;
     ef.out = f;
     ef.ldo = h2_l;

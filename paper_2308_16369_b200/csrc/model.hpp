@@ -180,6 +180,10 @@ struct Model {
   unsigned* aflags = nullptr;  // [n_kv_l] heads | [1] prefill done
   int* acnt = nullptr;         // [n_kv_l + 1]
   unsigned attn_epoch = 0;
+  // fused RMSNorm prologue of the QKV / gate||up GEMMs (EpiParams::norm_*): grid-barrier counter
+  // (monotonic) and the arrivals issued so far
+  unsigned* norm_ctr = nullptr;
+  unsigned norm_arrivals = 0;
   int64_t launches = 0;
   // I/O accounting and per-op timers
   int64_t last_h2d = 0, last_d2h = 0;

@@ -148,7 +148,8 @@ def test_prefill_attention_multitile(S, hd, n_kv, C, bs):
                                           ({"SARATHI_PREFILL_PT": "0"}, "prefill_attention_multitile", 4),
                                           ({"SARATHI_ATTN_CHAIN": "0"}, "prefill_attention_multitile or config1", 5),
                                           ({"SARATHI_PREFILL_KSPLIT": "3"}, "prefill_attention_multitile", 4),
-                                          ({"SARATHI_O_EARLY": "1"}, "prefill_attention_multitile or config1", 5)])
+                                          ({"SARATHI_O_EARLY": "1"}, "prefill_attention_multitile or config1", 5),
+                                          ({"SARATHI_NORM_FUSED": "1"}, "prefill_attention_multitile or config1", 5)])
 def test_prefill_attention_variants(env, select, n):
     """The non-default attention paths, selected once per process by environment, rerun hybrid-batch
     cases in a child process: the 64-key prefill tile (SARATHI_PREFILL_BK=64: single-buffered V at
@@ -157,7 +158,8 @@ def test_prefill_attention_variants(env, select, n):
     the key split merged by the last CTA of each (q-tile, head) pair (SARATHI_PREFILL_KSPLIT=3,
     capped by the first q-tile's key tiles, so the later chunks of the 700-token prompt split) and
     the O projection gated by the attention kernels' per-KV-head / grid-completion flags instead of
-    the grid dependency (SARATHI_O_EARLY=1)."""
+    the grid dependency (SARATHI_O_EARLY=1), and RMSNorm fused into the QKV / gate||up GEMMs as a
+    prologue + grid barrier (SARATHI_NORM_FUSED=1)."""
     env = dict(os.environ, SARATHI_PREFILL_VARIANT_CHILD="1", **env)
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m", "gpu", "-k",
                         select, "-p", "no:cacheprovider"],

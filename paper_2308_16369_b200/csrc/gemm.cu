@@ -762,7 +762,9 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
     // (GPT-3 TP-8 rank, K = 12288: QKV 52.6 -> 55.4, gate 53.6 -> 65.9 us with the split, so long
     // K keeps the full token tile: the mainloop dominates and narrow UMMAs cost more than the
     // epilogue saves)
-    const bool small = atomic_epilogue ? KB <= 32 : (2 * pm * tt.n_tiles < num_sms / 2 && KB <= 128);
+    // (residual adds: only up to 16 k-blocks; the GPT-3 TP-8 rank's O, K = 1536, measured 23.1 us
+    // split vs 19.4 unsplit, tools/shard_sweep.sh, profiles/r02_shard_sweep.txt)
+    const bool small = atomic_epilogue ? KB <= 16 : (2 * pm * tt.n_tiles < num_sms / 2 && KB <= 128);
     if (nt_small > tt.n_tiles && force_pairs == 0 && small) {
       pl.n_tiles = nt_small;
       const int per = (N + nt_small - 1) / nt_small;

@@ -18,6 +18,7 @@
 
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -890,7 +891,19 @@ Status Model::collect_op_times() {
   return Status::ok();
 }
 
+namespace {
+// NVTX ranges (SURVEY §5 tracing): one per hybrid batch and one per layer, visible to nsys / ncu
+// --nvtx; header-only nvtx3, a no-op when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
+
 Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* dec, float* logits, int32_t flags) {
+  NvtxRange nvtx_batch("sarathi_run_hybrid_batch");
   if (!kv_ready) return Status::err(SARATHI_ESTATE, "run_hybrid_batch: alloc_kv not called");
   // a pipeline stage before the last hands its residual stream on (sarathi_stage_output): no logits
   if (pp_stage != pp_stages - 1) flags = (flags | SARATHI_NO_LOGITS) & ~SARATHI_LOGITS_HOST;
@@ -1076,6 +1089,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     e.norm_eps = cfg.rms_eps;
   };
   for (int l = 0; l < nl; ++l) {  // this stage's layers (local index)
+    NvtxRange nvtx_layer("layer");
     LayerWeights& w = layers[l];
     if ((l == 0 || !use_chain) && !norm_fused) {
     ob = op_begin();

@@ -46,6 +46,7 @@ struct KParams {
   int sk_tiles;           // tiles processed stream-K (first), split across all pairs
   int dp_per_pair;        // whole tiles per pair processed after the stream-K part
   int dp_extra;           // pairs [0, dp_extra) take one more whole tile
+  int half_items;         // pairs [0, half_items) then take one token half of a remainder tile
   int tiles;              // total pair-tiles = pm_tiles * n_tiles
   int stages;
   int nbuf;               // TMEM accumulator buffers (2 if bn <= 256)
@@ -88,17 +89,24 @@ SARATHI_DEVICE int cta_of(long long u, const KParams& p) {
 
 // Work of one CTA pair: first its stream-K range of units over the split tiles [0, sk_tiles) (so
 // their reductions overlap later work), then dp_per_pair whole tiles (reduction-free epilogues).
+// Finally (p.half_items > 0) one token-half item: the tiles % P remainder tiles are not split over
+// K (partials + a reduction pass) but over their two UMMA token halves, one half per pair.
 struct SegIter {
   long long u, u_end;
   int dp_t, dp_end;
+  int hi;    // this pair's token-half item (-1: none or done)
+  int half;  // of the segment returned last: -1 whole tile / k-range, else the token half (UMMA 0 / 1)
   SARATHI_DEVICE void init(const KParams& p, int pair) {
     u = unit_begin(pair, p);
     u_end = unit_begin(pair + 1, p);
     dp_t = p.sk_tiles + pair * p.dp_per_pair + min(pair, p.dp_extra);
-    dp_end = min(p.tiles, dp_t + p.dp_per_pair + (pair < p.dp_extra ? 1 : 0));
+    dp_end = min(p.tiles - p.half_items / 2, dp_t + p.dp_per_pair + (pair < p.dp_extra ? 1 : 0));
+    hi = pair < p.half_items ? pair : -1;
+    half = -1;
   }
   // next segment: tile, k-block range [kb0, kb1); false when done
   SARATHI_DEVICE bool next(const KParams& p, int& tile, int& kb0, int& kb1) {
+    half = -1;
     if (u < u_end) {
       tile = static_cast<int>(u / p.KB);
       kb0 = static_cast<int>(u % p.KB);
@@ -108,6 +116,14 @@ struct SegIter {
     }
     if (dp_t < dp_end) {
       tile = dp_t++;
+      kb0 = 0;
+      kb1 = p.KB;
+      return true;
+    }
+    if (hi >= 0) {
+      tile = p.tiles - p.half_items / 2 + (hi >> 1);
+      half = hi & 1;
+      hi = -1;
       kb0 = 0;
       kb1 = p.KB;
       return true;
@@ -190,7 +206,7 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
       it0.init(p, pair);
       int tile, kb0, kb1;
       if (it0.next(p, tile, kb0, kb1)) {
-        const uint32_t tx = 2 * stage_bytes;
+        const uint32_t tx = 2 * stage_bytes - (it0.half >= 0 ? 2u * (p.n1 / 2) * kBK * 2 : 0u);
         const int npre0 = min(p.stages, kb1 - kb0);
         const int pt = tile / p.n_tiles;
         const int wrow0 = ((pt * 2 + static_cast<int>(rank)) * p.KB + kb0) * kWRowsPerTile;
@@ -285,6 +301,8 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
       const uint64_t pol_x = policy_evict_last();
       // incremental (k-block, stage, phase) counters inside a segment: no division in the hot loop
       const uint32_t tx = 2 * (stage_bytes - ((DBG && (ep.dbg & 1)) ? b_bytes : 0) - ((DBG && (ep.dbg & 2)) ? kABytes : 0));
+      // a token-half item loads only its UMMA's half of the tokens
+      const uint32_t txh = (DBG && (ep.dbg & 1)) ? tx : tx - 2u * (p.n1 / 2) * kBK * 2;
       int s = 0;
       uint32_t ph = 0;
       long long i = 0;
@@ -305,7 +323,7 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
           const int wrow0 = ((pt * 2 + static_cast<int>(rank)) * p.KB + kb0) * kWRowsPerTile;
           for (int j = 0; j < npre; ++j) {
             uint8_t* a = smem + static_cast<size_t>(j) * stage_bytes;
-            if (rank == 0) mbar_arrive_expect_tx_warp(&full[j], tx);
+            if (rank == 0) mbar_arrive_expect_tx_warp(&full[j], it0.half >= 0 ? txh : tx);
             if (!(DBG && (ep.dbg & 2))) tma_load_2d_pair_warp(a, &mapW, &full[j], 0, wrow0 + j * kWRowsPerTile, pol_w);
           }
         }
@@ -327,7 +345,7 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
           if (i >= npre) {
             mbar_wait(&empty[s], ph ^ 1);
             // both CTAs' bytes are counted on the leader's full[s] (pair TMA)
-            if (rank == 0) mbar_arrive_expect_tx_warp(&full[s], tx);
+            if (rank == 0) mbar_arrive_expect_tx_warp(&full[s], it.half >= 0 ? txh : tx);
             // W tile: the contiguous 16 KB pre-swizzled tile as 32 rows x 512 B (unswizzled map)
             if (!(DBG && (ep.dbg & 2))) tma_load_2d_pair_warp(a, &mapW, &full[s], 0, wrow, pol_w);
           }
@@ -353,7 +371,11 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
               asm volatile("fence.proxy.async.global;" ::: "memory");
             }
           }
-          if (!(DBG && (ep.dbg & 1))) {
+          if (DBG && (ep.dbg & 1)) {
+          } else if (it.half >= 0) {  // token-half item (n0 == n1): UMMA `half`'s tokens into the first B slot
+            tma_load_2d_pair_warp(b, &mapX, &full[s], kb * kBK, nt * p.bn + it.half * p.n0 + static_cast<int>(rank) * (p.n0 / 2),
+                                  pol_x);
+          } else {
             tma_load_2d_pair_warp(b, &mapX, &full[s], kb * kBK, nt * p.bn + static_cast<int>(rank) * (p.n0 / 2), pol_x);
             if (p.n_mma == 2)
               tma_load_2d_pair_warp(b + (p.n0 / 2) * kBK * 2, p.n0 == p.n1 ? &mapX : &mapX2, &full[s], kb * kBK,
@@ -379,14 +401,18 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
       it.init(p, pair);
       int tile, kb0, kb1;
       int uses[3] = {0, 0, 0};
+      int rs = 0;  // ring slots taken so far (a whole tile takes two, a token-half item one)
       while (it.next(p, tile, kb0, kb1)) {
         const int buf = seg % p.nbuf;
         const uint32_t use = seg / p.nbuf;
+        const bool hseg = it.half >= 0;
         uint32_t d0, d1;
         int tb_idx;  // tfull barrier of this segment
         if (ring) {
-          const int sa = (2 * seg) % 3, sb = (2 * seg + 1) % 3;
+          const int sa = rs % 3, sb = (rs + 1) % 3;
+          rs += hseg ? 1 : 2;
           for (int k : {sa, sb}) {  // both CTAs' epilogues drained the slot's previous use
+            if (hseg && k == sb) continue;
             if (uses[k]) mbar_wait_cluster(&tempty[k], (uses[k] - 1) & 1);
             ++uses[k];
           }
@@ -415,14 +441,15 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
                 const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
                 tmem_cp_128x256b_pair_warp(at + k * 8, make_desc_k_sw128(a + k * 32));
                 umma_f16_ts_pair_warp(d0, at + k * 8, make_desc_k_sw128(b + k * 32), idesc, acc);
-                umma_f16_ts_pair_warp(d1, at + k * 8, make_desc_k_sw128(b + (p.n0 / 2) * 128 + k * 32), idesc1, acc);
+                if (!hseg)
+                  umma_f16_ts_pair_warp(d1, at + k * 8, make_desc_k_sw128(b + (p.n0 / 2) * 128 + k * 32), idesc1, acc);
               }
             } else {
 #pragma unroll
               for (int k = 0; k < kBK / 16; ++k) {
                 const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
                 umma_f16_ss_pair_warp(d0, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc, acc);
-                if (p.n_mma == 2)
+                if (p.n_mma == 2 && !hseg)
                   umma_f16_ss_pair_warp(d1, make_desc_k_sw128(a + k * 32),
                                         make_desc_k_sw128(b + (p.n0 / 2) * 128 + k * 32), idesc1, acc);
               }
@@ -449,6 +476,7 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
     float* sbuf = stage_buf + ew * kStageFloats;            // this warp's transpose buffer
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
     int seg = 0;
+    int rs = 0;  // ring slots taken so far (as the MMA issuer counts them)
     const size_t tile_elems = static_cast<size_t>(p.bn) * kBM;
     constexpr bool rope_mode = MODE == EPI_QKV_ROPE;
     SegIter it;
@@ -467,9 +495,13 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
       const int nchunks = (tvalid + 15) / 16;
       // accumulator column of chunk ch and the TMEM releases this warp owes (see `ring`)
       const int nA = ring ? ni / 16 : (1 << 30);
-      const int sA = (2 * seg) % 3, sB = (2 * seg + 1) % 3;
+      const bool hseg = it.half >= 0;  // token-half item: chunks [c_lo, c_hi) in ONE ring slot
+      const int sA = rs % 3, sB = (rs + 1) % 3;
+      rs += hseg ? 1 : 2;
+      const int c_lo = hseg ? it.half * nA : 0, c_hi = hseg ? min(c_lo + nA, nchunks) : nchunks;
       auto tcol = [&](int ch) -> uint32_t {
         if (!ring) return static_cast<uint32_t>(buf * 256 + ch * 16);
+        if (hseg) return static_cast<uint32_t>(sA * ni + (ch - c_lo) * 16);
         return static_cast<uint32_t>(ch < nA ? sA * ni + ch * 16 : sB * ni + (ch - nA) * 16);
       };
       auto arrive_slot = [&](int k) {
@@ -477,23 +509,27 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_leader + k * 8);
       };
-      auto last_of = [&](int lim) {  // this warp's last chunk below lim (-1 if none)
-        if (lim <= eh) return -1;
-        return eh + ((lim - 1 - eh) / NEH) * NEH;
+      auto last_of = [&](int lim) {  // this warp's last chunk in [c_lo, lim) (-1 if none)
+        if (lim <= c_lo + eh) return -1;
+        return c_lo + eh + ((lim - 1 - c_lo - eh) / NEH) * NEH;
       };
-      const int lastA = last_of(min(nA, nchunks)), lastAll = last_of(nchunks);
+      const int lastA = hseg ? -1 : last_of(min(nA, nchunks)), lastAll = last_of(c_hi);
       auto release_tmem = [&]() {  // everything this warp owes for the segment
         if (ring) {
           arrive_slot(sA);
-          arrive_slot(sB);
+          if (!hseg) arrive_slot(sB);
         } else {
           arrive_slot(buf);
         }
       };
       auto after_load = [&](int c) {  // chunk c's accumulator is in registers
         if (ring) {
-          if (c == lastA) arrive_slot(sA);
-          if (c == lastAll) arrive_slot(sB);  // (with A when this warp has no half-B chunk)
+          if (hseg) {
+            if (c == lastAll) arrive_slot(sA);
+          } else {
+            if (c == lastA) arrive_slot(sA);
+            if (c == lastAll) arrive_slot(sB);  // (with A when this warp has no half-B chunk)
+          }
         } else if (c == lastAll) {
           arrive_slot(buf);
         }
@@ -567,10 +603,10 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
         // chunk's load in flight across the emit, for every epilogue mode (tools/tmem_drain.cu;
         // [13B-1] QKV 66.2 -> 64.8 us, gate||up 92.3 -> 89.8, O 30.8 -> 30.2; step 19.05 -> 18.85 ms,
         // interleaved A/B, profiles/r02_ab_drain.txt)
-        if (eh >= nchunks) {
+        if (c_lo + eh >= c_hi) {
           release_tmem();
         } else {
-          for (int ch = eh; ch < nchunks; ch += NEH) {
+          for (int ch = c_lo + eh; ch < c_hi; ch += NEH) {
             uint32_t raw[16];
             tmem_ld_32x32b_x16(trow + tcol(ch), raw);
             tmem_ld_wait_regs(raw);
@@ -819,7 +855,18 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
     pairs = P;
     dp_per = tiles / P;
     sk_tiles = tiles % P;
-    if (static_cast<long long>(sk_tiles) * KB < 4LL * P) {  // remainder too small to split: whole tiles
+    // Token-half remainder: with two equal UMMAs per k-step (ring accumulator), the tiles % P
+    // remainder tiles are split over their two token halves instead of over K, one half per pair
+    // after its whole tiles: no partials, no reduction pass, and the first whole tile's epilogue
+    // overlaps the half item's mainloop.  LLaMA-13B gate||up at T = 320 (108 tiles on 74 pairs):
+    // the stream-K remainder's partial drain stalled the next segment and its last contributors'
+    // reductions formed the kernel's tail (tools/probe_layer.sh).  SARATHI_GEMM_HALF=0 disables.
+    static const bool half_on = !(getenv("SARATHI_GEMM_HALF") && atoi(getenv("SARATHI_GEMM_HALF")) == 0);
+    const bool ring_shape = pl.n_tiles == 1 && pl.n_mma == 2 && 3 * (pl.bn / 2) <= 512 && N > pl.bn / 2;
+    if (half_on && !atomic_epilogue && ring_shape && sk_tiles > 0 && 2 * sk_tiles <= P) {
+      pl.half_items = 2 * sk_tiles;
+      sk_tiles = 0;
+    } else if (static_cast<long long>(sk_tiles) * KB < 4LL * P) {  // remainder too small to split: whole tiles
       dp_extra = sk_tiles;
       sk_tiles = 0;
     }
@@ -871,7 +918,7 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
     for (int c = 0; c < pl.ctas; ++c) {
       const long long u0 = static_cast<long long>(c) * pl.units / pl.ctas, u1 = static_cast<long long>(c + 1) * pl.units / pl.ctas;
       const int sk = u1 > u0 ? static_cast<int>((u1 - 1) / KB - u0 / KB + 1) : 0;
-      max_segs = std::max(max_segs, sk + pl.dp_per_pair + (c < pl.dp_extra ? 1 : 0));
+      max_segs = std::max(max_segs, sk + pl.dp_per_pair + (c < pl.dp_extra ? 1 : 0) + (c < pl.half_items ? 1 : 0));
     }
     const int per = (N + pl.n_tiles - 1) / pl.n_tiles;
     if (uneven_on && pl.n_mma == 2 && pl.n_tiles == 1 && max_segs <= 1 && per > 256 && per <= 512) {
@@ -988,6 +1035,7 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   kp.sk_tiles = pl.sk_tiles;
   kp.dp_per_pair = pl.dp_per_pair;
   kp.dp_extra = pl.dp_extra;
+  kp.half_items = pl.half_items;
   kp.tiles = pl.tiles;
   kp.stages = pl.stages;
   kp.nbuf = pl.nbuf;

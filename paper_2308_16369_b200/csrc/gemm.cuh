@@ -77,6 +77,8 @@ struct GemmPlan {
   int sk_tiles = 0;    // tiles split stream-K across all pairs (processed first)
   int dp_per_pair = 0; // whole tiles per pair processed after the stream-K part
   int dp_extra = 0;    // pairs [0, dp_extra) take one extra whole tile
+  int half_items = 0;  // token-half items after the whole tiles: pair q < half_items runs UMMA (q & 1)'s
+                       // tokens of tile tiles - half_items/2 + q/2 (no split-K, no reduction)
   int max_slots = 1;   // stream-K partial slots per tile
   int red_partials = 0;  // split tiles accumulate by red.add into ONE zeroed slot (ws_red)
   int atomic = 0;        // residual-add split tiles red.add every contributor's partial into the output

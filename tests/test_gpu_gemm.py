@@ -29,6 +29,10 @@ SHAPES = [
     (200, 37, 192, 0), (128, 600, 256, 0), (1280, 282, 8192, 0), (512, 257, 1024, 3), (640, 512, 640, 2),
     # 256 < N <= 512 with one segment per CTA pair: the uneven split (UMMA N = 256 + 16-multiple tail)
     (256, 257, 256, 0), (768, 300, 512, 0), (256, 497, 128, 0), (5120, 272, 1024, 0),
+    # more 256-row tiles than CTA pairs with two equal UMMAs per k-step: the remainder tiles run as
+    # token-half items (one UMMA's tokens per pair), incl. a ragged second half, a ragged last row
+    # tile and two whole tiles per pair before the half item
+    (27648, 320, 256, 0), (19000, 300, 128, 0), (40000, 288, 64, 0),
 ]
 
 
@@ -75,6 +79,37 @@ def test_gemm_silu_mul_interleaved(S):
     torch.cuda.synchronize()
     err = (out.double().cpu() - ref).abs().max() / ref.abs().max()
     assert err < 1e-2
+
+
+@pytest.mark.parametrize("half", ["1", "0"])
+def test_gemm_silu_mul_gate_up_shape(S, half):
+    """LLaMA-13B gate||up at T = 320 (108 row tiles on 74 CTA pairs): the remainder as token-half
+    items (default) and as the stream-K split (SARATHI_GEMM_HALF=0, in a child process: the switch is
+    read once per process)."""
+    import subprocess
+    import sys
+    code = (
+        "import torch, sys; sys.path.insert(0, '.');"
+        "from paper_2308_16369_b200 import sarathi as S;"
+        "M, N, K = 27648, 320, 1024;"
+        "g = torch.Generator().manual_seed(11);"
+        "W = (torch.randn(M, K, generator=g) / 32).to(torch.bfloat16);"
+        "X = torch.randn(N, K, generator=g).to(torch.bfloat16);"
+        "acc = (X.double() @ W.double().T).reshape(N, M // 32, 2, 16);"
+        "gate, up = acc[:, :, 0, :], acc[:, :, 1, :];"
+        "ref = (gate / (1 + torch.exp(-gate)) * up).reshape(N, M // 2);"
+        "out = torch.empty((N, M // 2), device='cuda', dtype=torch.bfloat16);"
+        "Wd, Xd = W.cuda(), X.cuda();"
+        "S.op_gemm(Wd.data_ptr(), Xd.data_ptr(), out.data_ptr(), M, N, K, S.EPI_SILU_MUL, 0, torch.cuda.current_stream().cuda_stream);"
+        "torch.cuda.synchronize();"
+        "err = ((out.double().cpu() - ref).abs().max() / ref.abs().max()).item();"
+        "print('err', err); assert err < 1e-2, err"
+    )
+    import os
+    env = dict(os.environ, SARATHI_GEMM_HALF=half)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
 
 
 def test_gemm_gelu(S):

@@ -18,7 +18,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--workload", default="llama13b-p256-s768-d64-ctx1024")
     ap.add_argument("--kind", default="hybrid", choices=["hybrid", "prefill", "decode"])
+    ap.add_argument("--spans", type=int, default=0,
+                    help="print the device-span timeline of the first N kernels of one profiled step "
+                         "(SARATHI_SPANS_ONLY: no per-op events, the PDL chain is intact)")
     args = ap.parse_args()
+    if args.spans:  # read once by the library (static), so before the first launch
+        os.environ["SARATHI_SPANS_ONLY"] = "1"
+        os.environ["SARATHI_SPAN_DUMP"] = str(args.spans)
     import torch
     import bench
     import synth
@@ -45,6 +51,14 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if args.spans:
+        m.set_profiling(True)
+        step()
+        torch.cuda.synchronize()
+        m.op_times(reset=True)
+        ks = m.op_kernel_times(reset=True)
+        print("kernel spans (ms per step):", {k: round(v[0], 4) if isinstance(v, tuple) else v for k, v in ks.items()})
+        m.set_profiling(False)
     torch.cuda.profiler.start()
     for _ in range(args.steps):
         step()

@@ -133,6 +133,73 @@ struct SegIter {
 };
 
 
+// RMSNorm (reading O-8, Table 1 "ln" rows) of rows r = blockIdx.x, blockIdx.x + grid, ...
+// of h (fp32 [T][H]) into out (bf16 [T][H]: x * rsqrt(mean x^2 + eps) * g) by the whole CTA (kThr
+// threads, named barrier 3); up to kMaxRows rows are normalised together (all their loads in flight,
+// one reduction round).  `red` = kMaxRows x 16 floats of scratch shared memory.  The per-row sum is
+// reduced in a fixed order (warp shuffles, then warps in index order): deterministic.
+template <int kThr>
+SARATHI_DEVICE void norm_rows(const float* h, const __nv_bfloat16* g, __nv_bfloat16* xo, int T, int H, float eps,
+                              float* red) {
+  constexpr int kMaxRows = 4;
+  const int tid = threadIdx.x;
+  const uint32_t warp = tid >> 5, lane = tid & 31;
+  for (int r0 = blockIdx.x; r0 < T; r0 += kMaxRows * gridDim.x) {
+    float4 v[kMaxRows][4];
+    float ss[kMaxRows];
+#pragma unroll
+    for (int j = 0; j < kMaxRows; ++j) {
+      const int r = r0 + j * gridDim.x;
+      ss[j] = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = (c * kThr + tid) * 4;
+        v[j][c] = (r < T && i < H) ? __ldcg(reinterpret_cast<const float4*>(h + static_cast<size_t>(r) * H + i))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxRows; ++j) {
+      const int r = r0 + j * gridDim.x;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) ss[j] += v[j][c].x * v[j][c].x + v[j][c].y * v[j][c].y + v[j][c].z * v[j][c].z + v[j][c].w * v[j][c].w;
+      if (r < T)
+        for (int i = (4 * kThr + tid) * 4; i < H; i += kThr * 4) {  // H > 4 * 4 * threads
+          const float4 w = __ldcg(reinterpret_cast<const float4*>(h + static_cast<size_t>(r) * H + i));
+          ss[j] += w.x * w.x + w.y * w.y + w.z * w.z + w.w * w.w;
+        }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) ss[j] += __shfl_xor_sync(0xffffffffu, ss[j], off);
+      if (lane == 0) red[j * 16 + warp] = ss[j];
+    }
+    named_bar_sync(3, kThr);
+#pragma unroll
+    for (int j = 0; j < kMaxRows; ++j) {
+      const int r = r0 + j * gridDim.x;
+      if (r >= T) break;
+      float tot = 0.f;
+      for (int w = 0; w < kThr / 32; ++w) tot += red[j * 16 + w];  // warp order: deterministic
+      const float inv = rsqrtf(tot / static_cast<float>(H) + eps);
+      auto put = [&](int i, float4 w) {
+        const uint2 graw = *reinterpret_cast<const uint2*>(g + i);
+        const float2 g01 = unpack_bf16x2(graw.x), g23 = unpack_bf16x2(graw.y);
+        uint2 pk;
+        pk.x = pack_bf16x2(w.x * inv * g01.x, w.y * inv * g01.y);
+        pk.y = pack_bf16x2(w.z * inv * g23.x, w.w * inv * g23.y);
+        *reinterpret_cast<uint2*>(xo + static_cast<size_t>(r) * H + i) = pk;
+      };
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = (c * kThr + tid) * 4;
+        if (i < H) put(i, v[j][c]);
+      }
+      for (int i = (4 * kThr + tid) * 4; i < H; i += kThr * 4)
+        put(i, __ldcg(reinterpret_cast<const float4*>(h + static_cast<size_t>(r) * H + i)));
+    }
+    named_bar_sync(3, kThr);  // (red is rewritten by the next group of rows)
+  }
+}
+
 template <int NEH, int MODE, bool DBG>
 __global__ void __launch_bounds__(threads_of<NEH>(), 1)
     gemm_bf16_pair(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX,
@@ -218,67 +285,8 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
       }
     }
     griddep_wait();
-    // this CTA's rows r = blockIdx.x + j * grid (j < kMaxRows) are normalised together: all their
-    // loads in flight at once, one reduction round for all of them
-    constexpr int kMaxRows = 4;
-    float* red = stage_buf;  // [kMaxRows][10] warp partial sums (the transpose buffers are idle here)
-    const int tid = threadIdx.x, H = ep.norm_H;
-    const __nv_bfloat16* g = static_cast<const __nv_bfloat16*>(ep.norm_g);
-    __nv_bfloat16* xo = static_cast<__nv_bfloat16*>(ep.norm_out);
-    for (int r0 = blockIdx.x; r0 < ep.norm_T; r0 += kMaxRows * gridDim.x) {
-      float4 v[kMaxRows][4];
-      float ss[kMaxRows];
-#pragma unroll
-      for (int j = 0; j < kMaxRows; ++j) {
-        const int r = r0 + j * gridDim.x;
-        ss[j] = 0.f;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int i = (c * kThr + tid) * 4;
-          v[j][c] = (r < ep.norm_T && i < H) ? __ldcg(reinterpret_cast<const float4*>(ep.norm_h + static_cast<size_t>(r) * H + i))
-                                             : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kMaxRows; ++j) {
-        const int r = r0 + j * gridDim.x;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) ss[j] += v[j][c].x * v[j][c].x + v[j][c].y * v[j][c].y + v[j][c].z * v[j][c].z + v[j][c].w * v[j][c].w;
-        if (r < ep.norm_T)
-          for (int i = (4 * kThr + tid) * 4; i < H; i += kThr * 4) {  // H > 4 * 4 * threads
-            const float4 w = __ldcg(reinterpret_cast<const float4*>(ep.norm_h + static_cast<size_t>(r) * H + i));
-            ss[j] += w.x * w.x + w.y * w.y + w.z * w.z + w.w * w.w;
-          }
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) ss[j] += __shfl_xor_sync(0xffffffffu, ss[j], off);
-        if (lane == 0) red[j * 16 + warp] = ss[j];
-      }
-      named_bar_sync(3, kThr);
-#pragma unroll
-      for (int j = 0; j < kMaxRows; ++j) {
-        const int r = r0 + j * gridDim.x;
-        if (r >= ep.norm_T) break;
-        float tot = 0.f;
-        for (int w = 0; w < kThr / 32; ++w) tot += red[j * 16 + w];  // warp order: deterministic
-        const float inv = rsqrtf(tot / static_cast<float>(H) + ep.norm_eps);
-        auto put = [&](int i, float4 w) {
-          const uint2 graw = *reinterpret_cast<const uint2*>(g + i);
-          const float2 g01 = unpack_bf16x2(graw.x), g23 = unpack_bf16x2(graw.y);
-          uint2 pk;
-          pk.x = pack_bf16x2(w.x * inv * g01.x, w.y * inv * g01.y);
-          pk.y = pack_bf16x2(w.z * inv * g23.x, w.w * inv * g23.y);
-          *reinterpret_cast<uint2*>(xo + static_cast<size_t>(r) * H + i) = pk;
-        };
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int i = (c * kThr + tid) * 4;
-          if (i < H) put(i, v[j][c]);
-        }
-        for (int i = (4 * kThr + tid) * 4; i < H; i += kThr * 4)
-          put(i, __ldcg(reinterpret_cast<const float4*>(ep.norm_h + static_cast<size_t>(r) * H + i)));
-      }
-      named_bar_sync(3, kThr);  // (red is rewritten by the next group of rows)
-    }
+    norm_rows<64 + 128 * NEH>(ep.norm_h, static_cast<const __nv_bfloat16*>(ep.norm_g),
+                              static_cast<__nv_bfloat16*>(ep.norm_out), ep.norm_T, ep.norm_H, ep.norm_eps, stage_buf);
     // grid barrier: every CTA's rows written (and visible to the async proxy) before any X load
     asm volatile("fence.proxy.async.global;" ::: "memory");
     __threadfence();
@@ -714,6 +722,21 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
     }
   }
 
+  if (MODE == EPI_ADD_F32 && ep.pnorm_out) {
+    // RMSNorm of the updated residual stream (the next GEMM's input) by this grid: every CTA's
+    // residual adds land (fence + grid barrier on the monotonic counter; all CTAs of the persistent
+    // grid are resident), then the CTAs normalise rows blockIdx.x, blockIdx.x + grid, ...  Replaces
+    // the rmsnorm launch and its grid-completion gap.
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicAdd(ep.norm_ctr, 1u);
+      xflag_wait(ep.norm_ctr, ep.norm_target);
+    }
+    __syncthreads();
+    norm_rows<64 + 128 * NEH>(static_cast<const float*>(ep.out), static_cast<const __nv_bfloat16*>(ep.pnorm_g),
+                              static_cast<__nv_bfloat16*>(ep.pnorm_out), ep.norm_T, ep.norm_H, ep.norm_eps, stage_buf);
+  }
   tc_fence_before();
   __syncthreads();
   if (ep.span_end && threadIdx.x == 0) atomicMax(ep.span_end, globaltimer_ns());

@@ -60,6 +60,11 @@ struct EpiParams {
   float norm_eps = 0.f;
   unsigned* norm_ctr = nullptr;
   unsigned norm_target = 0;
+  // RMSNorm epilogue (EPI_ADD_F32 only; replaces the rmsnorm kernel AFTER this GEMM): once every
+  // CTA's residual adds landed (grid barrier on norm_ctr / norm_target), the CTAs normalise rows of
+  // out (fp32 [norm_T][norm_H]) into pnorm_out (bf16) with gains pnorm_g and eps norm_eps
+  const void* pnorm_g = nullptr;
+  void* pnorm_out = nullptr;
 };
 
 struct GemmPlan {

@@ -798,7 +798,7 @@ Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, 
   SRET(xmap(X, N, K, ldx, pl.box_rows, &mx));
   SRET(xmap(X, N, K, ldx, pl.box_rows2, &mx2));
   EpiParams ep = ep_in;
-  if (ep.norm_h) {  // fused RMSNorm prologue: grid barrier target = all arrivals so far + this grid
+  if (ep.norm_h || ep.pnorm_out) {  // fused RMSNorm prologue / epilogue: grid barrier target = all arrivals so far + this grid
     norm_arrivals += 2u * static_cast<unsigned>(pl.ctas);
     ep.norm_ctr = norm_ctr;
     ep.norm_target = norm_arrivals;
@@ -1080,6 +1080,21 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   // for the slowest one before its first X load, so off by default.
   static const bool norm_fused_env = getenv("SARATHI_NORM_FUSED") && atoi(getenv("SARATHI_NORM_FUSED")) == 1;
   const bool norm_fused = norm_fused_env && world == 1;
+  // SARATHI_POST_NORM=1: RMSNorm as the residual-add GEMM's epilogue (O -> norm2, down -> the next
+  // layer's norm1; grid barrier + every CTA normalising rows): no rmsnorm launch and no
+  // grid-completion gap before it (world 1, standalone GEMMs).  Parity-tested; measured slower than
+  // the PDL-chained rmsnorm kernel (18.90 vs 18.80 ms interleaved A/B: O + norm 41-44 us vs 33 us,
+  // the barrier waits for the slowest CTA's red.adds; profiles/r02_ab_pnorm.txt), so off by default.
+  static const bool post_norm_env = getenv("SARATHI_POST_NORM") && atoi(getenv("SARATHI_POST_NORM")) == 1;
+  const bool post_norm = post_norm_env && world == 1 && !norm_fused && !use_chain;
+  bool normed_next = false;  // the previous layer's down GEMM already wrote this layer's norm1 into `a`
+  auto set_pnorm = [&](EpiParams& e, const __nv_bfloat16* g) {
+    e.pnorm_g = g;
+    e.pnorm_out = a;
+    e.norm_T = T;
+    e.norm_H = H;
+    e.norm_eps = cfg.rms_eps;
+  };
   auto set_norm = [&](EpiParams& e, const __nv_bfloat16* g) {
     e.norm_h = h;
     e.norm_g = g;
@@ -1091,7 +1106,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   for (int l = 0; l < nl; ++l) {  // this stage's layers (local index)
     NvtxRange nvtx_layer("layer");
     LayerWeights& w = layers[l];
-    if ((l == 0 || !use_chain) && !norm_fused) {
+    if ((l == 0 || !use_chain) && !norm_fused && !normed_next) {
     ob = op_begin();
     {
       unsigned long long *sp0, *sp1;
@@ -1329,6 +1344,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       eo.xflag2 = p > 0 ? aflags + nkv_l : nullptr;
       eo.xepoch = attn_epoch;
     }
+    if (post_norm) set_pnorm(eo, w.g2);
     ob = op_begin();
     SRET(gemm(w.m_o, H, q_dim_l, o, q_dim_l, T, eo, SARATHI_OP_GEMM_O));
     op_end(SARATHI_OP_GEMM_O, ob);
@@ -1337,7 +1353,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       SRET(allreduce());
       op_end(SARATHI_OP_ALLREDUCE, ob);
     }
-    if (!norm_fused) {
+    if (!norm_fused && !post_norm) {
     ob = op_begin();
     {
       unsigned long long *sp0, *sp1;
@@ -1367,6 +1383,8 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       ed.out = ar_target();
       ed.ldo = H;
     }
+    normed_next = post_norm && l + 1 < nl;
+    if (normed_next) set_pnorm(ed, layers[l + 1].g1);
     ob = op_begin();
     SRET(gemm(w.m_down, H, h2_l, f, h2_l, T, ed, SARATHI_OP_GEMM_DOWN));
     op_end(SARATHI_OP_GEMM_DOWN, ob);

@@ -393,6 +393,64 @@ SARATHI_DEVICE void umma_f16_ts_pair_warp(uint32_t d_tmem, uint32_t a_tmem, uint
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// One 64-deep k-block of pair MMAs (4 k16 steps; per step UMMA 0 into d0 and, if `two`, UMMA 1 into
+// d1 over the second B slice) issued by ONE elected lane in ONE asm block.  The k16 slices advance
+// the SW128 K-major descriptors by 32 B (+2 in the 16-B address field) and the TMEM A operand by 8
+// columns.  Issuing each UMMA through its own asm statement cost ~20 SASS instructions per UMMA
+// (ELECT, R2UR.BROADCAST x5, VOTEU, BRA.DIV): at <= 256 tokens the issue, not the tensor core,
+// paced the k-block (tools/probe_narrow2.sh: 0.34 us per k-block at N = 144 with no loads at all).
+// acc0: accumulate into d for the first k16 step (the later steps always accumulate).
+SARATHI_DEVICE void umma_kblock_ss_pair(uint32_t d0, uint32_t d1, uint64_t a_desc, uint64_t b_desc0, uint64_t b_desc1,
+                                        uint32_t idesc0, uint32_t idesc1, uint32_t acc0, uint32_t two) {
+  asm volatile(
+      "{\n\t.reg .pred e, t, p, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3, c1, c2, c3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %7, 0;\n\t"
+      "setp.eq.b32 q, %7, %7;\n\t"
+      "setp.ne.and.b32 t, %8, 0, e;\n\t"
+      "add.s64 a1, %2, 2;\n\tadd.s64 a2, %2, 4;\n\tadd.s64 a3, %2, 6;\n\t"
+      "add.s64 b1, %3, 2;\n\tadd.s64 b2, %3, 4;\n\tadd.s64 b3, %3, 6;\n\t"
+      "add.s64 c1, %4, 2;\n\tadd.s64 c2, %4, 4;\n\tadd.s64 c3, %4, 6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, p;\n\t"
+      "@t tcgen05.mma.cta_group::2.kind::f16 [%1], %2, %4, %6, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %5, q;\n\t"
+      "@t tcgen05.mma.cta_group::2.kind::f16 [%1], a1, c1, %6, q;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %5, q;\n\t"
+      "@t tcgen05.mma.cta_group::2.kind::f16 [%1], a2, c2, %6, q;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %5, q;\n\t"
+      "@t tcgen05.mma.cta_group::2.kind::f16 [%1], a3, c3, %6, q;\n\t}\n" ::"r"(d0),
+      "r"(d1), "l"(a_desc), "l"(b_desc0), "l"(b_desc1), "r"(idesc0), "r"(idesc1), "r"(acc0), "r"(two)
+      : "memory");
+}
+// The same with the A operand staged into TMEM first (tcgen05.cp of each k16 slice to a_tmem + 8k;
+// cp and mma execute in issue order), both UMMAs reading A from TMEM.
+SARATHI_DEVICE void umma_kblock_ts_pair(uint32_t d0, uint32_t d1, uint32_t a_tmem, uint64_t a_sdesc, uint64_t b_desc0,
+                                        uint64_t b_desc1, uint32_t idesc0, uint32_t idesc1, uint32_t acc0, uint32_t two) {
+  asm volatile(
+      "{\n\t.reg .pred e, t, p, q;\n\t.reg .b64 s1, s2, s3, b1, b2, b3, c1, c2, c3;\n\t.reg .b32 t1, t2, t3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %8, 0;\n\t"
+      "setp.eq.b32 q, %8, %8;\n\t"
+      "setp.ne.and.b32 t, %9, 0, e;\n\t"
+      "add.s64 s1, %3, 2;\n\tadd.s64 s2, %3, 4;\n\tadd.s64 s3, %3, 6;\n\t"
+      "add.s64 b1, %4, 2;\n\tadd.s64 b2, %4, 4;\n\tadd.s64 b3, %4, 6;\n\t"
+      "add.s64 c1, %5, 2;\n\tadd.s64 c2, %5, 4;\n\tadd.s64 c3, %5, 6;\n\t"
+      "add.u32 t1, %2, 8;\n\tadd.u32 t2, %2, 16;\n\tadd.u32 t3, %2, 24;\n\t"
+      "@e tcgen05.cp.cta_group::2.128x256b [%2], %3;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%2], %4, %6, p;\n\t"
+      "@t tcgen05.mma.cta_group::2.kind::f16 [%1], [%2], %5, %7, p;\n\t"
+      "@e tcgen05.cp.cta_group::2.128x256b [t1], s1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t1], b1, %6, q;\n\t"
+      "@t tcgen05.mma.cta_group::2.kind::f16 [%1], [t1], c1, %7, q;\n\t"
+      "@e tcgen05.cp.cta_group::2.128x256b [t2], s2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t2], b2, %6, q;\n\t"
+      "@t tcgen05.mma.cta_group::2.kind::f16 [%1], [t2], c2, %7, q;\n\t"
+      "@e tcgen05.cp.cta_group::2.128x256b [t3], s3;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [t3], b3, %6, q;\n\t"
+      "@t tcgen05.mma.cta_group::2.kind::f16 [%1], [t3], c3, %7, q;\n\t}\n" ::"r"(d0),
+      "r"(d1), "r"(a_tmem), "l"(a_sdesc), "l"(b_desc0), "l"(b_desc1), "r"(idesc0), "r"(idesc1), "r"(acc0), "r"(two)
+      : "memory");
+}
 // shared memory -> TMEM copy of a 128-row x 256-bit matrix (one k16 slice of a K-major bf16 operand)
 // in both CTAs of the pair (each from its own shared memory); executes in issue order with the MMAs
 SARATHI_DEVICE void tmem_cp_128x256b_pair_warp(uint32_t taddr, uint64_t s_desc) {

@@ -401,6 +401,8 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader, lane 0) / stage relay (peer) ----------------
     if (rank == 0) {
+      // SARATHI_GEMM_KBASM=0: one asm statement per UMMA (the earlier issue path)
+      const bool kblock_asm = ep.kbasm;
       const uint32_t idesc = make_idesc_bf16_f32(2 * kBM, p.n0);
       const uint32_t idesc1 = make_idesc_bf16_f32(2 * kBM, p.n1);
       int i = 0, seg = 0, s = 0;
@@ -442,7 +444,17 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
             // warp-uniform issue (operands stay in uniform registers), one elected lane issues
             const uint32_t a = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
             const uint32_t b = a + kABytes;
-            if (p.ts) {
+            if (kblock_asm) {
+              // the whole k-block in one asm block (one elect, descriptors advanced in registers)
+              const uint32_t acc0 = kb != kb0 ? 1u : 0u;
+              const uint32_t two = (p.n_mma == 2 && !hseg) ? 1u : 0u;
+              if (p.ts)
+                umma_kblock_ts_pair(d0, d1, tmem + kTsCol, make_desc_k_sw128(a), make_desc_k_sw128(b),
+                                    make_desc_k_sw128(b + (p.n0 / 2) * 128), idesc, idesc1, acc0, two);
+              else
+                umma_kblock_ss_pair(d0, d1, make_desc_k_sw128(a), make_desc_k_sw128(b),
+                                    make_desc_k_sw128(b + (p.n0 / 2) * 128), idesc, idesc1, acc0, two);
+            } else if (p.ts) {
               const uint32_t at = tmem + kTsCol;
 #pragma unroll
               for (int k = 0; k < kBK / 16; ++k) {
@@ -1045,6 +1057,9 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   }
   if (ep.mode < 0 || ep.mode > 5) return cudaErrorInvalidValue;
   const KFn fn = table[(ep.dbg || ep.trace) ? 1 : 0][ep.mode];
+  static const bool kbasm_on = !(getenv("SARATHI_GEMM_KBASM") && atoi(getenv("SARATHI_GEMM_KBASM")) == 0);
+  EpiParams epk = ep;
+  epk.kbasm = kbasm_on ? 1 : 0;
   KParams kp;
   kp.M = pl.M;
   kp.N = pl.N;
@@ -1097,7 +1112,7 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, fn, mapW, mapX, mapX2, kp, ep);
+  return cudaLaunchKernelEx(&cfg, fn, mapW, mapX, mapX2, kp, epk);
 }
 
 }  // namespace sarathi

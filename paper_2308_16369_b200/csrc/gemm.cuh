@@ -65,6 +65,7 @@ struct EpiParams {
   // out (fp32 [norm_T][norm_H]) into pnorm_out (bf16) with gains pnorm_g and eps norm_eps
   const void* pnorm_g = nullptr;
   void* pnorm_out = nullptr;
+  int kbasm = 1;  // MMA issue: a k-block's UMMAs in one asm block (set by launch_gemm)
 };
 
 struct GemmPlan {

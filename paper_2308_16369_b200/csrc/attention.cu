@@ -479,11 +479,15 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
     mbar_wait(&k_full[buf], (g >> 1) & 1);
     tc_fence_after();
     const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + buf * L::kKV);
+    if (HD == 128 && a.mma8) {  // the 8 k16 steps in one asm block (one elect; GEMM finding)
+      umma8_ss_halves(tS(sb), make_desc_k_sw128(qa), (kPBQ * 128) >> 4, make_desc_k_sw128(kb), (BK * 128) >> 4, idesc_s, 0u);
+    } else {
 #pragma unroll
-    for (int k = 0; k < HD / 16; ++k) {
-      const uint32_t off = (k >> 2) * (kPBQ * 128) + (k & 3) * 32;  // hd half, 32 B step in the row
-      umma_f16_ss_warp(tS(sb), make_desc_k_sw128(qa + off), make_desc_k_sw128(kb + (k >> 2) * (BK * 128) + (k & 3) * 32),
-                       idesc_s, k > 0 ? 1u : 0u);
+      for (int k = 0; k < HD / 16; ++k) {
+        const uint32_t off = (k >> 2) * (kPBQ * 128) + (k & 3) * 32;  // hd half, 32 B step in the row
+        umma_f16_ss_warp(tS(sb), make_desc_k_sw128(qa + off), make_desc_k_sw128(kb + (k >> 2) * (BK * 128) + (k & 3) * 32),
+                         idesc_s, k > 0 ? 1u : 0u);
+      }
     }
     umma_commit_warp(&s_done[sb]);
   };
@@ -636,6 +640,9 @@ __global__ void __launch_bounds__(256, BK == 128 ? 1 : 2)
       else mbar_wait(&v_full[0], g & 1);
       tc_fence_after();
       const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + (L::kVdb ? buf : 0) * L::kKV);
+      if (PT && BK == 128 && a.mma8) {  // 8 k16 steps in one asm block; V descriptor + 2048 B per step
+        umma8_ts(tO, tS(sb), make_desc_mn_sw128(vb, BK * 128, 1024), 2048 >> 4, idesc_o, t > 0 ? 1u : 0u);
+      } else
 #pragma unroll
       for (int k = 0; k < BK / 16; ++k) {
         const uint64_t bdesc = make_desc_mn_sw128(vb + k * 2048, BK * 128, 1024);
@@ -842,10 +849,13 @@ cudaError_t launch_prefill_tc(const PrefillAttnArgs& a, const CUtensorMap& mq, c
   const int items = (a.p + kPBQ - 1) / kPBQ * a.n_q_local * std::max(1, a.ksplit);
   static const int cap = getenv("SARATHI_PREFILL_CTAS") ? atoi(getenv("SARATHI_PREFILL_CTAS")) : 0;  // experiment
   const int ctas = cap > 0 ? std::min(cap, items) : items;
+  static const bool mma8 = !(getenv("SARATHI_ATTN_MMA8") && atoi(getenv("SARATHI_ATTN_MMA8")) == 0);
+  PrefillAttnArgs a8 = a;
+  a8.mma8 = mma8 ? 1 : 0;
   if (a.pdl)
-    launch_pdl(prefill_attn_tc<HD, BK, PT>, dim3(ctas), dim3(256), L::kTotal, st, mq, mk, mv, a);
+    launch_pdl(prefill_attn_tc<HD, BK, PT>, dim3(ctas), dim3(256), L::kTotal, st, mq, mk, mv, a8);
   else
-    prefill_attn_tc<HD, BK, PT><<<ctas, 256, L::kTotal, st>>>(mq, mk, mv, a);
+    prefill_attn_tc<HD, BK, PT><<<ctas, 256, L::kTotal, st>>>(mq, mk, mv, a8);
   return cudaGetLastError();
 }
 

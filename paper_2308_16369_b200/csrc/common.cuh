@@ -216,6 +216,54 @@ SARATHI_DEVICE void umma_f16_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t 
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Eight k16 UMMAs (cta_group::1) in ONE asm block with one elect (see umma_kblock_ss_pair for why):
+// both operands in shared memory, the descriptor of step k = desc0 + (k / 4) * half + (k % 4) * 2
+// (a 128-deep K split in two 64-element SW128 halves, 32 B per k16 step).  acc0: accumulate at k = 0.
+SARATHI_DEVICE void umma8_ss_halves(uint32_t d, uint64_t a0, uint64_t ah, uint64_t b0, uint64_t bh, uint32_t idesc,
+                                    uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a<8>, b<8>;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 q, %6, %6;\n\t"
+      "mov.b64 a0, %1;\n\tadd.s64 a1, a0, 2;\n\tadd.s64 a2, a0, 4;\n\tadd.s64 a3, a0, 6;\n\t"
+      "add.s64 a4, a0, %2;\n\tadd.s64 a5, a4, 2;\n\tadd.s64 a6, a4, 4;\n\tadd.s64 a7, a4, 6;\n\t"
+      "mov.b64 b0, %3;\n\tadd.s64 b1, b0, 2;\n\tadd.s64 b2, b0, 4;\n\tadd.s64 b3, b0, 6;\n\t"
+      "add.s64 b4, b0, %4;\n\tadd.s64 b5, b4, 2;\n\tadd.s64 b6, b4, 4;\n\tadd.s64 b7, b4, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %5, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %5, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %5, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %5, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %5, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %5, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %5, q;\n\t}\n" ::"r"(d),
+      "l"(a0), "l"(ah), "l"(b0), "l"(bh), "r"(idesc), "r"(acc0)
+      : "memory");
+}
+// Eight k16 UMMAs (cta_group::1) in one asm block, A from TMEM at t0 + (k / 4) * 64 + (k % 4) * 8
+// (packed bf16 pairs, two 64-column halves), B descriptor(k) = b0 + k * bstep.
+SARATHI_DEVICE void umma8_ts(uint32_t d, uint32_t t0, uint64_t b0, uint64_t bstep, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, q;\n\t.reg .b64 b<8>;\n\t.reg .b32 t<8>;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "setp.eq.b32 q, %5, %5;\n\t"
+      "mov.b32 t0, %1;\n\tadd.u32 t1, t0, 8;\n\tadd.u32 t2, t0, 16;\n\tadd.u32 t3, t0, 24;\n\t"
+      "add.u32 t4, t0, 64;\n\tadd.u32 t5, t0, 72;\n\tadd.u32 t6, t0, 80;\n\tadd.u32 t7, t0, 88;\n\t"
+      "mov.b64 b0, %2;\n\tadd.s64 b1, b0, %3;\n\tadd.s64 b2, b1, %3;\n\tadd.s64 b3, b2, %3;\n\t"
+      "add.s64 b4, b3, %3;\n\tadd.s64 b5, b4, %3;\n\tadd.s64 b6, b5, %3;\n\tadd.s64 b7, b6, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t0], b0, %4, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t1], b1, %4, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t2], b2, %4, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t3], b3, %4, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t4], b4, %4, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t5], b5, %4, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t6], b6, %4, q;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [t7], b7, %4, q;\n\t}\n" ::"r"(d),
+      "r"(t0), "l"(b0), "l"(bstep), "r"(idesc), "r"(acc0)
+      : "memory");
+}
 SARATHI_DEVICE void umma_commit_warp(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

@@ -76,6 +76,7 @@ struct PrefillAttnArgs {
   unsigned* done_flag = nullptr;
   int* done_cnt = nullptr;
   unsigned epoch = 0;
+  int mma8 = 1;  // issue S = QK^T / O += PV as 8 UMMAs in one asm block (SARATHI_ATTN_MMA8=0: one asm per UMMA)
 };
 
 size_t decode_smem_bytes(int head_dim, int block_size, int stages, int G);

@@ -401,8 +401,11 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader, lane 0) / stage relay (peer) ----------------
     if (rank == 0) {
-      // SARATHI_GEMM_KBASM=0: one asm statement per UMMA (the earlier issue path)
-      const bool kblock_asm = ep.kbasm;
+      // k-block issue from one asm block for two UMMAs per k-step and for narrow single UMMAs (issue-
+      // paced); single wide UMMAs (N >= 192) keep the per-UMMA statements, measured 1-3 % faster at
+      // T = 256 (QKV 46.4 vs 47.9 us, down 39.5 vs 40.9; profiles/r02_t256_kbasm.txt).
+      // SARATHI_GEMM_KBASM=0: the per-UMMA path everywhere.
+      const bool kblock_asm = ep.kbasm && (p.n_mma == 2 || p.n0 < 192);
       const uint32_t idesc = make_idesc_bf16_f32(2 * kBM, p.n0);
       const uint32_t idesc1 = make_idesc_bf16_f32(2 * kBM, p.n1);
       int i = 0, seg = 0, s = 0;

@@ -351,6 +351,13 @@ SARATHI_DEVICE uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 SARATHI_DEVICE void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
 }
+// Relaxed remote arrive for TMEM-slot releases: the waiter (the MMA issuer) needs only the
+// arriving warp's completed tcgen05.ld (ordered by tcgen05.wait::ld + tcgen05.fence::before_thread_sync),
+// not its generic global stores; .release.cluster compiles to MEMBAR.ALL.GPU, which waits for every
+// store / red.add the epilogue warp has in flight before the slot is handed back.
+SARATHI_DEVICE void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
 
 // Pair TMA load: data lands in this CTA's smem, transaction bytes are counted on the LEADER's
 // (rank 0) mbarrier (peer bit of the barrier address cleared).

@@ -498,6 +498,7 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
     const int r = static_cast<int>(quarter * 32 + lane);    // accumulator row within this CTA's half
     float* sbuf = stage_buf + ew * kStageFloats;            // this warp's transpose buffer
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+    const bool relaxed_rel = ep.relaxed_rel;  // SARATHI_GEMM_RELAXED=0: release.cluster arrives
     int seg = 0;
     int rs = 0;  // ring slots taken so far (as the MMA issuer counts them)
     const size_t tile_elems = static_cast<size_t>(p.bn) * kBM;
@@ -530,7 +531,12 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
       auto arrive_slot = [&](int k) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(tempty_leader + k * 8);
+        if (lane == 0) {
+          if (relaxed_rel)
+            mbar_arrive_cluster_relaxed(tempty_leader + k * 8);
+          else
+            mbar_arrive_cluster(tempty_leader + k * 8);
+        }
       };
       auto last_of = [&](int lim) {  // this warp's last chunk in [c_lo, lim) (-1 if none)
         if (lim <= c_lo + eh) return -1;
@@ -1063,6 +1069,8 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
   static const bool kbasm_on = !(getenv("SARATHI_GEMM_KBASM") && atoi(getenv("SARATHI_GEMM_KBASM")) == 0);
   EpiParams epk = ep;
   epk.kbasm = kbasm_on ? 1 : 0;
+  static const bool relaxed_on = !(getenv("SARATHI_GEMM_RELAXED") && atoi(getenv("SARATHI_GEMM_RELAXED")) == 0);
+  epk.relaxed_rel = relaxed_on ? 1 : 0;
   KParams kp;
   kp.M = pl.M;
   kp.N = pl.N;

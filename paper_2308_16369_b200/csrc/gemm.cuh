@@ -66,6 +66,7 @@ struct EpiParams {
   const void* pnorm_g = nullptr;
   void* pnorm_out = nullptr;
   int kbasm = 1;  // MMA issue: a k-block's UMMAs in one asm block (set by launch_gemm)
+  int relaxed_rel = 1;  // TMEM-slot releases by relaxed (not release) cluster arrives (set by launch_gemm)
 };
 
 struct GemmPlan {

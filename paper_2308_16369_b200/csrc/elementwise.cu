@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h
                                                            const __nv_bfloat16* __restrict__ g,
                                                            __nv_bfloat16* __restrict__ out, const int* __restrict__ rows,
                                                            int H, float eps, unsigned long long* span_start,
-                                                           unsigned long long* span_end) {
+                                                           unsigned long long* span_end, const NormFlags fl) {
   __shared__ float sred[kThreads / 32];
   griddep_launch_dependents();
   // g is a weight: fetched before the grid dependency resolves (overlaps the predecessor's tail)
@@ -116,7 +116,22 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h
     const int i = (c * kThreads + threadIdx.x) * 4;
     if (i < H) gv[c] = *reinterpret_cast<const uint2*>(g + i);
   }
-  griddep_wait();  // h / add come from the preceding GEMM (PDL)
+  if (fl.wait_ctr) {  // flag chaining: the producing GEMM's CTAs finished their residual adds
+    if (threadIdx.x == 0) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl.wait_ctr) : "memory");
+      const unsigned long long t0 = globaltimer_ns();
+      while (static_cast<int>(v - fl.wait_target) < 0) {
+        __nanosleep(32);
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl.wait_ctr) : "memory");
+        if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+      }
+    }
+    __syncthreads();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  } else {
+    griddep_wait();  // h / add come from the preceding GEMM (PDL)
+  }
   peer_wait(add);  // fused all-reduce: every rank's partial published
   if (span_start && threadIdx.x == 0) atomicMin(span_start, globaltimer_ns());
   const int r = blockIdx.x;
@@ -151,6 +166,11 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_kernel(float* __restrict__ h
       pk.y = pack_bf16x2(v[c].z * inv * g1.x, v[c].w * inv * g1.y);
       *reinterpret_cast<uint2*>(o + i) = pk;
     }
+  }
+  if (fl.done_ctr) {  // count this CTA in after its stores (the consumer GEMM's producer waits on it)
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(fl.done_ctr, 1u);
   }
   if (span_end && threadIdx.x == 0) atomicMax(span_end, globaltimer_ns());
 }
@@ -241,17 +261,17 @@ cudaError_t launch_embedding(const int* tok, const __nv_bfloat16* E, float* h, i
 
 cudaError_t launch_rmsnorm(float* h, const PeerSum& add, const __nv_bfloat16* g, __nv_bfloat16* out,
                            const int* rows, int R, int H, float eps, cudaStream_t st, unsigned long long* span_start,
-                           unsigned long long* span_end) {
+                           unsigned long long* span_end, const NormFlags& fl) {
   if (R == 0) return cudaSuccess;
   if (H % 4) return cudaErrorInvalidValue;
   // one CTA per row, sized so that every row of a batch (T <= 512) is resident in ONE wave
   // (a second partial wave doubles the latency of this latency-bound kernel)
   if (H <= 256 * 4 * 2) {
-    launch_pdl(rmsnorm_kernel<256, 2>, dim3(R), dim3(256), 0, st, h, add, g, out, rows, H, eps, span_start, span_end);
+    launch_pdl(rmsnorm_kernel<256, 2>, dim3(R), dim3(256), 0, st, h, add, g, out, rows, H, eps, span_start, span_end, fl);
   } else if (H <= 256 * 4 * 5) {
-    launch_pdl(rmsnorm_kernel<256, 5>, dim3(R), dim3(256), 0, st, h, add, g, out, rows, H, eps, span_start, span_end);
+    launch_pdl(rmsnorm_kernel<256, 5>, dim3(R), dim3(256), 0, st, h, add, g, out, rows, H, eps, span_start, span_end, fl);
   } else if (H <= 512 * 4 * 8) {
-    launch_pdl(rmsnorm_kernel<512, 8>, dim3(R), dim3(512), 0, st, h, add, g, out, rows, H, eps, span_start, span_end);
+    launch_pdl(rmsnorm_kernel<512, 8>, dim3(R), dim3(512), 0, st, h, add, g, out, rows, H, eps, span_start, span_end, fl);
   } else {
     return cudaErrorInvalidValue;
   }

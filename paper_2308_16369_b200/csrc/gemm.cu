@@ -758,8 +758,10 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
     norm_rows<64 + 128 * NEH>(static_cast<const float*>(ep.out), static_cast<const __nv_bfloat16*>(ep.pnorm_g),
                               static_cast<__nv_bfloat16*>(ep.pnorm_out), ep.norm_T, ep.norm_H, ep.norm_eps, stage_buf);
   }
+  if (ep.done_ctr) __threadfence();  // this thread's stores / red.adds before the CTA's count
   tc_fence_before();
   __syncthreads();
+  if (ep.done_ctr && threadIdx.x == 0) atomicAdd(ep.done_ctr, 1u);
   if (ep.span_end && threadIdx.x == 0) atomicMax(ep.span_end, globaltimer_ns());
   if ((DBG ? ep.trace : nullptr) && threadIdx.x == 0) {
     (DBG ? ep.trace : nullptr)[2048 + blockIdx.x] = globaltimer_ns();  // per-CTA end (debug)

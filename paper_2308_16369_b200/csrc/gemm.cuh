@@ -65,6 +65,9 @@ struct EpiParams {
   // out (fp32 [norm_T][norm_H]) into pnorm_out (bf16) with gains pnorm_g and eps norm_eps
   const void* pnorm_g = nullptr;
   void* pnorm_out = nullptr;
+  // flag chaining (world 1): every CTA counts itself into *done_ctr after its epilogue's stores /
+  // residual adds (the next kernel waits on the count instead of this grid's completion)
+  unsigned* done_ctr = nullptr;
   int kbasm = 1;  // MMA issue: a k-block's UMMAs in one asm block (set by launch_gemm)
   int relaxed_rel = 1;  // TMEM-slot releases by relaxed (not release) cluster arrives (set by launch_gemm)
 };

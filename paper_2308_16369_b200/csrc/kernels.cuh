@@ -108,11 +108,22 @@ struct PeerSum {
 // h[t][:] = float(E[tok[t]][:])
 cudaError_t launch_embedding(const int* tok, const __nv_bfloat16* E, float* h, int T, int H, cudaStream_t st);
 
+// Flag chaining of the rmsnorm kernel (world 1): instead of the grid dependency on the preceding
+// residual-add GEMM it waits until *wait_ctr >= wait_target (that GEMM's CTAs count themselves in
+// after their residual adds), and every CTA counts itself into *done_ctr after its stores (the next
+// GEMM's TMA producer waits on that instead of this grid's completion).  Monotonic counters.
+struct NormFlags {
+  const unsigned* wait_ctr = nullptr;
+  unsigned wait_target = 0;
+  unsigned* done_ctr = nullptr;
+};
+
 // out[r][:] = bf16(RMSNorm(h[row(r)]) * g); row(r) = rows ? rows[r] : r.
 // With TP partials (PeerSum world >= 1): h[row] += sum of the partials' row first and h is updated.
 cudaError_t launch_rmsnorm(float* h, const PeerSum& add, const __nv_bfloat16* g, __nv_bfloat16* out,
                            const int* rows, int R, int H, float eps, cudaStream_t st,
-                           unsigned long long* span_start = nullptr, unsigned long long* span_end = nullptr);
+                           unsigned long long* span_start = nullptr, unsigned long long* span_end = nullptr,
+                           const NormFlags& flags = NormFlags());
 inline cudaError_t launch_rmsnorm(float* h, const __nv_bfloat16* add, const __nv_bfloat16* g, __nv_bfloat16* out,
                                   const int* rows, int R, int H, float eps, cudaStream_t st,
                                   unsigned long long* span_start = nullptr, unsigned long long* span_end = nullptr) {

@@ -392,6 +392,10 @@ Status Model::init(const sarathi_model_config& c, const sarathi_dist& d, uint64_
   SRET(check(cudaMemset(pp_ctr, 0, pp_pairs * sizeof(int)), "memset"));
   SRET(dalloc(&norm_ctr, 1));
   SRET(check(cudaMemset(norm_ctr, 0, sizeof(unsigned)), "memset"));
+  SRET(dalloc(&gemm_done, 1));
+  SRET(check(cudaMemset(gemm_done, 0, sizeof(unsigned)), "memset"));
+  SRET(dalloc(&norm_done, 1));
+  SRET(check(cudaMemset(norm_done, 0, sizeof(unsigned)), "memset"));
   SRET(dalloc(&aflags, static_cast<size_t>(nkv_l + 1)));
   SRET(dalloc(&acnt, static_cast<size_t>(nkv_l + 1)));
   SRET(check(cudaMemset(aflags, 0, (nkv_l + 1) * sizeof(unsigned)), "memset"));
@@ -798,6 +802,7 @@ Status Model::gemm(const CUtensorMap& mw, int M, int K, const void* X, int ldx, 
   SRET(xmap(X, N, K, ldx, pl.box_rows, &mx));
   SRET(xmap(X, N, K, ldx, pl.box_rows2, &mx2));
   EpiParams ep = ep_in;
+  if (ep.done_ctr) gemm_done_arrivals += 2u * static_cast<unsigned>(pl.ctas);  // flag-chained RMSNorm
   if (ep.norm_h || ep.pnorm_out) {  // fused RMSNorm prologue / epilogue: grid barrier target = all arrivals so far + this grid
     norm_arrivals += 2u * static_cast<unsigned>(pl.ctas);
     ep.norm_ctr = norm_ctr;
@@ -1088,6 +1093,29 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   static const bool post_norm_env = getenv("SARATHI_POST_NORM") && atoi(getenv("SARATHI_POST_NORM")) == 1;
   const bool post_norm = post_norm_env && world == 1 && !norm_fused && !use_chain;
   bool normed_next = false;  // the previous layer's down GEMM already wrote this layer's norm1 into `a`
+  // Flag-chained RMSNorm (world 1, standalone GEMMs): the residual-add GEMM's CTAs count themselves
+  // in after their red.adds, the rmsnorm kernel waits on that count instead of the GEMM grid's
+  // completion, and the next GEMM's TMA producer waits on the rmsnorm CTAs' count instead of the
+  // rmsnorm grid's completion: the two grid-completion + launch gaps around every RMSNorm go.
+  // Opt-in (SARATHI_NORM_FLAGS=1): parity-tested, measured slower (18.52 vs 18.06 ms interleaved
+  // A/B: the early-resident rmsnorm CTAs stretch the norm to 5.9 us and gate||up by 11 us;
+  // profiles/r02_ab_nflags.txt).
+  static const bool norm_flags_env = getenv("SARATHI_NORM_FLAGS") && atoi(getenv("SARATHI_NORM_FLAGS")) == 1;
+  const bool norm_flags = norm_flags_env && world == 1 && !norm_fused && !post_norm && !use_chain;
+  bool flag_next = false;  // the previous layer's down GEMM counts into gemm_done (this layer's norm1 waits)
+  auto flag_norm = [&](NormFlags& nf) {  // rmsnorm after a counting GEMM; returns via nf
+    nf.wait_ctr = gemm_done;
+    nf.wait_target = gemm_done_arrivals;
+    nf.done_ctr = norm_done;
+    norm_done_arrivals += static_cast<unsigned>(T);  // one CTA per row
+  };
+  auto flag_x = [&](EpiParams& e) {  // the GEMM after a flagged rmsnorm: X ready when all its CTAs counted in
+    e.xflag = norm_done;
+    e.xflag_cols = H;
+    e.xflag_n = 1;
+    e.xflag2 = nullptr;
+    e.xepoch = norm_done_arrivals;
+  };
   auto set_pnorm = [&](EpiParams& e, const __nv_bfloat16* g) {
     e.pnorm_g = g;
     e.pnorm_out = a;
@@ -1106,12 +1134,17 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
   for (int l = 0; l < nl; ++l) {  // this stage's layers (local index)
     NvtxRange nvtx_layer("layer");
     LayerWeights& w = layers[l];
+    const bool flag1 = flag_next;
+    flag_next = false;
     if ((l == 0 || !use_chain) && !norm_fused && !normed_next) {
     ob = op_begin();
     {
       unsigned long long *sp0, *sp1;
       SRET(take_span(SARATHI_OP_RMSNORM, &sp0, &sp1));
-      SRET(check(launch_rmsnorm(h, pending_ar ? pend : no_add, w.g1, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1), "rmsnorm1"));
+      NormFlags nf;
+      if (flag1) flag_norm(nf);
+      SRET(check(launch_rmsnorm(h, pending_ar ? pend : no_add, w.g1, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1, nf),
+                 "rmsnorm1"));
     }
     if (pending_ar) SRET(ar_end());
     op_end(SARATHI_OP_RMSNORM, ob);
@@ -1122,6 +1155,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     if (l == 0 || !use_chain) {
     EpiParams e;
     if (norm_fused) set_norm(e, w.g1);
+    if (flag1) flag_x(e);
     e.mode = EPI_QKV_ROPE;
     e.out = q;
     e.ldo = q_dim_l;
@@ -1345,6 +1379,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
       eo.xepoch = attn_epoch;
     }
     if (post_norm) set_pnorm(eo, w.g2);
+    if (norm_flags) eo.done_ctr = gemm_done;
     ob = op_begin();
     SRET(gemm(w.m_o, H, q_dim_l, o, q_dim_l, T, eo, SARATHI_OP_GEMM_O));
     op_end(SARATHI_OP_GEMM_O, ob);
@@ -1358,7 +1393,10 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     {
       unsigned long long *sp0, *sp1;
       SRET(take_span(SARATHI_OP_RMSNORM, &sp0, &sp1));
-      SRET(check(launch_rmsnorm(h, world > 1 ? pend : no_add, w.g2, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1), "rmsnorm2"));
+      NormFlags nf;
+      if (norm_flags) flag_norm(nf);
+      SRET(check(launch_rmsnorm(h, world > 1 ? pend : no_add, w.g2, a, nullptr, T, H, cfg.rms_eps, stream, sp0, sp1, nf),
+                 "rmsnorm2"));
     }
     if (world > 1) SRET(ar_end());
     op_end(SARATHI_OP_RMSNORM, ob);
@@ -1367,6 +1405,7 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     // FFN
     EpiParams ef;
     if (norm_fused) set_norm(ef, w.g2);
+    if (norm_flags) flag_x(ef);
     ef.mode = cfg.ffn_kind == SARATHI_FFN_SWIGLU ? EPI_SILU_MUL : EPI_GELU;
     ef.out = f;
     ef.ldo = h2_l;
@@ -1385,6 +1424,8 @@ Status Model::run(const sarathi_prefill_chunk* pre, const sarathi_decode_set* de
     }
     normed_next = post_norm && l + 1 < nl;
     if (normed_next) set_pnorm(ed, layers[l + 1].g1);
+    flag_next = norm_flags && l + 1 < nl;
+    if (flag_next) ed.done_ctr = gemm_done;
     ob = op_begin();
     SRET(gemm(w.m_down, H, h2_l, f, h2_l, T, ed, SARATHI_OP_GEMM_DOWN));
     op_end(SARATHI_OP_GEMM_DOWN, ob);

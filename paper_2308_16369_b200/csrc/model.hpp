@@ -184,6 +184,12 @@ struct Model {
   // (monotonic) and the arrivals issued so far
   unsigned* norm_ctr = nullptr;
   unsigned norm_arrivals = 0;
+  // flag-chained RMSNorm (SARATHI_NORM_FLAGS): residual-add GEMM CTAs -> gemm_done, rmsnorm CTAs ->
+  // norm_done (monotonic; targets = all arrivals so far)
+  unsigned* gemm_done = nullptr;
+  unsigned gemm_done_arrivals = 0;
+  unsigned* norm_done = nullptr;
+  unsigned norm_done_arrivals = 0;
   int64_t launches = 0;
   // I/O accounting and per-op timers
   int64_t last_h2d = 0, last_d2h = 0;

@@ -150,7 +150,8 @@ def test_prefill_attention_multitile(S, hd, n_kv, C, bs):
                                           ({"SARATHI_PREFILL_KSPLIT": "3"}, "prefill_attention_multitile", 4),
                                           ({"SARATHI_O_EARLY": "1"}, "prefill_attention_multitile or config1", 5),
                                           ({"SARATHI_NORM_FUSED": "1"}, "prefill_attention_multitile or config1", 5),
-                                          ({"SARATHI_POST_NORM": "1"}, "prefill_attention_multitile or config1", 5)])
+                                          ({"SARATHI_POST_NORM": "1"}, "prefill_attention_multitile or config1", 5),
+                                          ({"SARATHI_NORM_FLAGS": "1"}, "prefill_attention_multitile or config1", 5)])
 def test_prefill_attention_variants(env, select, n):
     """The non-default attention paths, selected once per process by environment, rerun hybrid-batch
     cases in a child process: the 64-key prefill tile (SARATHI_PREFILL_BK=64: single-buffered V at
@@ -161,7 +162,7 @@ def test_prefill_attention_variants(env, select, n):
     the O projection gated by the attention kernels' per-KV-head / grid-completion flags instead of
     the grid dependency (SARATHI_O_EARLY=1), and RMSNorm fused into the QKV / gate||up GEMMs as a
     prologue + grid barrier (SARATHI_NORM_FUSED=1), and RMSNorm as the O / down GEMMs' epilogue
-    after a grid barrier (SARATHI_POST_NORM=1)."""
+    after a grid barrier (SARATHI_POST_NORM=1), and the flag-chained RMSNorm (SARATHI_NORM_FLAGS=1)."""
     env = dict(os.environ, SARATHI_PREFILL_VARIANT_CHILD="1", **env)
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m", "gpu", "-k",
                         select, "-p", "no:cacheprovider"],

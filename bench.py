@@ -366,7 +366,30 @@ def ours(args):
                                   "dependency -> last CTA end"}
         roofline, roofline_secondary = roofline_chain, roofline
     else:
-        roofline_secondary = None
+        # gemm_bf16_pair over the four layer GEMMs (QKV, O, gate||up, down): the kernel function
+        # with the largest share of the step in the ncu launch list (~58 % vs the decode attention's
+        # ~32 %); per-layer figures (four launches), tensor-bound against the sustained bf16 peak
+        lay = gemm.get("all_layer_gemms")
+        if lay and lay.get("us"):
+            sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+            lay_fl = lay["frac_tensor"] * sus * 1e12 * lay["us"] * 1e-6
+            gtraffic = ncu_traffic("gemm_layer", args.workload)
+            roofline_gemm = {"kernel": "gemm_bf16_pair (QKV + O + gate_up + down of one layer)", "bound": "tensor",
+                             "achieved": round(lay_fl / (lay["us"] * 1e-6) / 1e12, 1), "peak": sus,
+                             "unit": "TFLOP/s", "frac": lay["frac_tensor"],
+                             "traffic": gtraffic["dram_bytes_per_launch"] if gtraffic else None,
+                             "traffic_source": gtraffic["source"] if gtraffic else None,
+                             "traffic_unit": "bytes per layer (4 launches)",
+                             "algorithmic_flops_per_layer": round(lay_fl),
+                             "algorithmic_weight_bytes_per_layer": round(sum(
+                                 v["weight_gbs"] * 1e9 * v["us"] * 1e-6 for k, v in gemm.items() if k.startswith("gemm_"))),
+                             "us_per_layer": lay["us"], "frac_span": lay.get("frac_tensor_kernel"),
+                             "peak_source": peaks["source"] + " (sustained bf16: the GEMMs run at the power-capped clock)",
+                             "note": "per-op CUDA events of the profiled pass (they break the PDL chain: launch gaps "
+                                     "included); frac_span = the kernels' own device spans"}
+            roofline, roofline_secondary = roofline_gemm, roofline
+        else:
+            roofline_secondary = None
 
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,

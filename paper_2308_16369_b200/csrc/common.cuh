@@ -453,7 +453,7 @@ SARATHI_DEVICE void umma_f16_ts_pair_warp(uint32_t d_tmem, uint32_t a_tmem, uint
 // the SW128 K-major descriptors by 32 B (+2 in the 16-B address field) and the TMEM A operand by 8
 // columns.  Issuing each UMMA through its own asm statement cost ~20 SASS instructions per UMMA
 // (ELECT, R2UR.BROADCAST x5, VOTEU, BRA.DIV): at <= 256 tokens the issue, not the tensor core,
-// paced the k-block (tools/probe_narrow2.sh: 0.34 us per k-block at N = 144 with no loads at all).
+// paced the k-block (tools/experiments.sh narrow2: 0.34 us per k-block at N = 144 with no loads at all).
 // acc0: accumulate into d for the first k16 step (the later steps always accumulate).
 SARATHI_DEVICE void umma_kblock_ss_pair(uint32_t d0, uint32_t d1, uint64_t a_desc, uint64_t b_desc0, uint64_t b_desc1,
                                         uint32_t idesc0, uint32_t idesc1, uint32_t acc0, uint32_t two) {

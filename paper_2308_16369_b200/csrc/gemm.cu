@@ -906,7 +906,7 @@ GemmPlan plan_gemm(int M, int N, int K, int num_sms, size_t ws_cap_floats, int f
     // after its whole tiles: no partials, no reduction pass, and the first whole tile's epilogue
     // overlaps the half item's mainloop.  LLaMA-13B gate||up at T = 320 (108 tiles on 74 pairs):
     // the stream-K remainder's partial drain stalled the next segment and its last contributors'
-    // reductions formed the kernel's tail (tools/probe_layer.sh).  SARATHI_GEMM_HALF=0 disables.
+    // reductions formed the kernel's tail (tools/experiments.sh layer).  SARATHI_GEMM_HALF=0 disables.
     static const bool half_on = !(getenv("SARATHI_GEMM_HALF") && atoi(getenv("SARATHI_GEMM_HALF")) == 0);
     const bool ring_shape = pl.n_tiles == 1 && pl.n_mma == 2 && 3 * (pl.bn / 2) <= 512 && N > pl.bn / 2;
     if (half_on && !atomic_epilogue && ring_shape && sk_tiles > 0 && 2 * sk_tiles <= P) {
@@ -1102,7 +1102,7 @@ cudaError_t launch_gemm(const CUtensorMap& mapW, const CUtensorMap& mapX, const 
     // slice of the weight tile once and both UMMAs read it from TMEM, instead of each UMMA
     // re-reading it from shared memory (the second UMMA of a k-step cost ~0.13 us per k-block
     // whatever its width: shared-memory operand bandwidth).  Measured at [13B-1]: per-k-block
-    // 0.48 -> 0.448 us (N = 320, tools/probe_ts.sh), layer GEMMs 240 -> 226 us, step 19.00 ->
+    // 0.48 -> 0.448 us (N = 320, tools/experiments.sh ts), layer GEMMs 240 -> 226 us, step 19.00 ->
     // 18.51 ms (interleaved A/B, profiles/r02_ab_ts.txt).  SARATHI_GEMM_TS=0 disables.
     static const bool ts_on = !(getenv("SARATHI_GEMM_TS") && atoi(getenv("SARATHI_GEMM_TS")) == 0);
     const bool ring = pl.n_mma == 2 && pl.n0 == pl.n1 && 3 * pl.n0 <= 512;

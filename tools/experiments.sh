@@ -151,6 +151,20 @@ ts)
   mkdir -p gpurun_out/ab4
   for r in 1 2; do for t in 1 0; do SARATHI_GEMM_TS=$t timeout 300 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/ab4/ts${t}_r$r.json 2>/dev/null; done; done
   ;;
+ntsmall)
+  # TP-rank shapes with / without the small-M token split (SARATHI_GEMM_NT_SMALLM=0), after the MMA-issue fix
+  build
+  for r in 1 2; do for v in 2 0; do
+    echo "== r$r nt_smallm=$v" >> gpurun_out/ntsmall.txt
+    SARATHI_GEMM_NT_SMALLM=$v timeout 600 python tools/shard_step.py >> gpurun_out/ntsmall.txt 2>/dev/null
+  done; done
+  ;;
+sweep)
+  # chunk / tile sweep (NEXT-2) and the zipf request workload on the session-3 kernels
+  build
+  timeout 1500 python tools/chunk_sweep.py --reps 2 > gpurun_out/chunk_sweep.txt 2> gpurun_out/chunk_sweep.err
+  timeout 900 python bench.py --workload zipf-p10-llama13b --no-cpu-baseline > gpurun_out/bench_zipf.json 2> gpurun_out/bench_zipf.err
+  ;;
 *) echo "unknown experiment $exp" >&2; exit 2 ;;
 esac
 done

@@ -76,12 +76,12 @@ def gemm_token_capacity(T: int) -> int:
 
 def b200_chunk(C: int, d: int, remaining: int) -> int:
     """The paper's tile-quantization chunk rule (trim the chunk so chunk + decodes lands
-    on the tile boundary) restated for the B200 GEMM's quanta: if T = C + d overshoots a cost step
-    b in {256, 512} by at most C/8, trim to b - d; otherwise fill the padded tile to
-    gemm_token_capacity(T) - d.  Clamped to [1, remaining]."""
+    on the tile boundary) restated for the B200 GEMM's quanta (reading O-23): if
+    T = C + d overshoots the cost step b = 512 (a second token tile) by at most C/8, trim to b - d;
+    otherwise fill the padded tile to gemm_token_capacity(T) - d.  Clamped to [1, remaining]."""
     T = C + d
     p = gemm_token_capacity(T) - d
-    for b in (256, 512):
+    for b in (512,):
         if b < T <= b + C // 8 and b - d >= 1:
             p = b - d
             break

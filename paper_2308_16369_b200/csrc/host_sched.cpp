@@ -27,7 +27,7 @@ TokenTiling gemm_token_tiling(int T) {
 int b200_chunk(int C, int d, int remaining) {
   const int T = C + d;
   int p = gemm_token_tiling(T).capacity() - d;
-  for (int b : {256, 512})
+  for (int b : {512})  // (the T = 256 step, one -> two UMMAs per k-step, is gone since the k-block issue fix)
     if (T > b && T - b <= C / 8 && b - d >= 1) {
       p = b - d;
       break;

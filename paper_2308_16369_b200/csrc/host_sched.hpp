@@ -23,10 +23,11 @@ TokenTiling gemm_token_tiling(int T);
 // B200 analogue of the paper's tile-quantization chunk rule (§4.4: the chunk is
 // trimmed to C - (B-1) so chunk + decodes fills 256 tokens exactly, because crossing a 128-token
 // tile boundary costs a whole extra tile).  Here the token quantum is the UMMA N granularity (16/32)
-// and the cost steps are at T = 256 (one -> two UMMAs per k-step, TMEM double buffer -> ring) and
-// T = 512 (a second token tile).  Given the configured chunk C, the batch's decode count d and the
-// request's remaining prompt tokens:
-//   * T = C + d just past a step b in {256, 512} (T - b <= C / 8): trim, p = b - d;
+// and the cost step is at T = 512 (a second token tile re-streams the weights); the step at T = 256
+// (one -> two UMMAs per k-step) disappeared with the one-asm k-block issue (reading O-23,
+// profiles/r02_chunk_sweep_13b_s3.txt).  Given the configured chunk C, the batch's decode count d and
+// the request's remaining prompt tokens:
+//   * T = C + d just past the step b = 512 (T - b <= C / 8): trim, p = b - d;
 //   * otherwise fill the padded tile: p = capacity(C + d) - d (>= C; those columns are computed anyway);
 //   p = min(p, remaining), at least 1.
 int b200_chunk(int C, int d, int remaining);

@@ -140,3 +140,20 @@ def test_gemm_llama13b_shapes_random(S, M, K):
     torch.cuda.synchronize()
     err = ((out.double() - ref).abs().max() / ref.abs().max()).item()
     assert err < 5e-5, err   # fp32 accumulation over K <= 13824 terms
+
+
+@pytest.mark.skipif(__import__("os").environ.get("SARATHI_GEMM_VARIANT_CHILD") == "1", reason="child process")
+@pytest.mark.parametrize("env", [{"SARATHI_GEMM_KBASM": "0"}, {"SARATHI_GEMM_RELAXED": "0"}])
+def test_gemm_issue_variants(env):
+    """The per-UMMA issue path (SARATHI_GEMM_KBASM=0) and release-semantics TMEM-slot arrives
+    (SARATHI_GEMM_RELAXED=0), read once per process, rerun the exact-integer shapes in a child."""
+    import os
+    import subprocess
+    import sys
+    e = dict(os.environ, SARATHI_GEMM_VARIANT_CHILD="1", **env)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m", "gpu", "-k",
+                        "exact_integers", "-p", "no:cacheprovider"], env=e, capture_output=True, text=True,
+                       timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert f"{len(SHAPES)} passed" in r.stdout

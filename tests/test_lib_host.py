@@ -180,9 +180,9 @@ def test_b200_chunk_advisor_hand_cases_and_cpp_twin(S):
         [16, 16, 32, 256, 256, 288, 288, 320, 320, 512, 576, 1024]
     ch = osch.b200_chunk
     assert ch(256, 0, 10**6) == 256          # exactly on the quantum
-    assert ch(256, 1, 10**6) == 255          # 257 tokens: trim to 256 (the paper's 256 - (B-1))
-    assert ch(256, 32, 10**6) == 224         # overshoot 32 = C/8: still trimmed
-    assert ch(256, 33, 10**6) == 287         # overshoot 33 > C/8: fill the 320-token tile... bn 320
+    assert ch(256, 1, 10**6) == 287          # 257 tokens: no step at 256 any more, fill the 288-token tile
+    assert ch(256, 32, 10**6) == 256         # T = 288 = capacity
+    assert ch(256, 33, 10**6) == 287         # T = 289: fill the 320-token tile
     assert ch(256, 64, 10**6) == 256         # T = 320 = capacity
     assert ch(128, 5, 10**6) == 139          # T = 133 -> 144-token tile: fill
     assert ch(128, 5, 50) == 50              # the last chunk of a prompt

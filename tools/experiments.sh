@@ -165,6 +165,16 @@ sweep)
   timeout 1500 python tools/chunk_sweep.py --reps 2 > gpurun_out/chunk_sweep.txt 2> gpurun_out/chunk_sweep.err
   timeout 900 python bench.py --workload zipf-p10-llama13b --no-cpu-baseline > gpurun_out/bench_zipf.json 2> gpurun_out/bench_zipf.err
   ;;
+epi)
+  # in-model QKV epilogue components (pair 0 trace): full, TMEM loads only (dbg 4), no RoPE (32),
+  # no global stores (8); plus the issue-variant GEMM tests
+  build
+  for dbg in 0 4 32 8; do
+    echo "== dbg $dbg" >> gpurun_out/epi_model.txt
+    SARATHI_GEMM_DBG=$dbg SARATHI_MODEL_TRACE=5:320 timeout 300 python tools/profile_step.py --steps 1 2>&1 | grep -E "CTA end|seg|chunk" >> gpurun_out/epi_model.txt
+  done
+  timeout 900 python -m pytest tests/test_gpu_gemm.py -x -q -k "variants" > gpurun_out/pytest_gemm_var.log 2>&1; echo rc=$? >> gpurun_out/pytest_gemm_var.log
+  ;;
 *) echo "unknown experiment $exp" >&2; exit 2 ;;
 esac
 done

@@ -175,6 +175,18 @@ epi)
   done
   timeout 900 python -m pytest tests/test_gpu_gemm.py -x -q -k "variants" > gpurun_out/pytest_gemm_var.log 2>&1; echo rc=$? >> gpurun_out/pytest_gemm_var.log
   ;;
+ropetab)
+  # per-batch RoPE (cos, sin) table read by the QKV epilogue (SARATHI_ROPE_TABLE, default on)
+  build
+  timeout 900 python -m pytest tests/test_gpu_model.py tests/test_gpu_fullsize.py tests/test_gpu_tp_local.py -x -q > gpurun_out/pytest_model.log 2>&1; echo rc=$? >> gpurun_out/pytest_model.log
+  for v in 1 0; do
+    echo "== rope_table=$v" >> gpurun_out/ropetab.txt
+    SARATHI_ROPE_TABLE=$v SARATHI_MODEL_TRACE=5:320 timeout 300 python tools/profile_step.py --steps 1 2>&1 | grep -E "CTA end|seg|chunk (0|2|10|16|18) " >> gpurun_out/ropetab.txt
+  done
+  timeout 600 python tools/shard_step.py > gpurun_out/shard_step.txt 2> gpurun_out/shard_step.err
+  rm -rf gpurun_out/ab
+  bash tools/ab.sh "SARATHI_ROPE_TABLE=1" "SARATHI_ROPE_TABLE=0"
+  ;;
 *) echo "unknown experiment $exp" >&2; exit 2 ;;
 esac
 done

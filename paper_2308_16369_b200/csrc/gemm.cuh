@@ -178,6 +178,8 @@ struct ChainLaunch {
   // debug timeline (SARATHI_CHAIN_TRACE): [pairs][kChainTraceSegs][8] globaltimer stamps of the
   // leader CTA: mma start / first stage / last commit, epilogue wake / published, producer dep-wait ns
   unsigned long long* trace = nullptr;
+  int kbasm = 1;     // a k-block's UMMAs from one asm block (set by launch_chain; SARATHI_GEMM_KBASM=0: per UMMA)
+  int relaxed = 1;   // relaxed cluster arrives for TMEM-slot releases (SARATHI_GEMM_RELAXED=0: release)
 };
 constexpr int kChainTraceSegs = 16;
 struct ChainMaps {

@@ -260,13 +260,18 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
           if (tr && kb == sg.kb0) tr[1] = globaltimer_ns();
           const uint32_t a = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
           const uint32_t b = a + kABytes;
+          if (p.kbasm) {  // the whole k-block from one asm block (gemm.cu: per-UMMA issue paced the mainloop)
+            umma_kblock_ss_pair(d0, d1, make_desc_k_sw128(a), make_desc_k_sw128(b), make_desc_k_sw128(b + (ni / 2) * 128),
+                                idesc, idesc, kb != sg.kb0 ? 1u : 0u, p.n_mma == 2 ? 1u : 0u);
+          } else {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint32_t acc = (kb != sg.kb0 || k != 0) ? 1u : 0u;
-            umma_f16_ss_pair_warp(d0, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc, acc);
-            if (p.n_mma == 2)
-              umma_f16_ss_pair_warp(d1, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + (ni / 2) * 128 + k * 32),
-                                    idesc, acc);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint32_t acc = (kb != sg.kb0 || k != 0) ? 1u : 0u;
+              umma_f16_ss_pair_warp(d0, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + k * 32), idesc, acc);
+              if (p.n_mma == 2)
+                umma_f16_ss_pair_warp(d1, make_desc_k_sw128(a + k * 32), make_desc_k_sw128(b + (ni / 2) * 128 + k * 32),
+                                      idesc, acc);
+            }
           }
           umma_commit_pair_mc_warp(&empty[s], 0x3);
           if (kb == sg.kb1 - 1) umma_commit_pair_mc_warp(&tfull[tb_idx], 0x3);
@@ -317,7 +322,12 @@ __global__ void __launch_bounds__(threads_of<kNEHc>(), 1)
       auto arrive_slot = [&](int k) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(tempty_leader + k * 8);
+        if (lane == 0) {
+          if (p.relaxed)
+            mbar_arrive_cluster_relaxed(tempty_leader + k * 8);
+          else
+            mbar_arrive_cluster(tempty_leader + k * 8);
+        }
       };
       auto last_of = [&](int lim) {
         if (lim <= eh) return -1;
@@ -659,7 +669,12 @@ cudaError_t launch_chain(const ChainMaps& maps, const ChainLaunch& cl, int ffn_m
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, fn, maps, cl);
+  static const bool kbasm_on = !(getenv("SARATHI_GEMM_KBASM") && atoi(getenv("SARATHI_GEMM_KBASM")) == 0);
+  static const bool relaxed_on = !(getenv("SARATHI_GEMM_RELAXED") && atoi(getenv("SARATHI_GEMM_RELAXED")) == 0);
+  ChainLaunch c2 = cl;
+  c2.kbasm = kbasm_on ? 1 : 0;
+  c2.relaxed = relaxed_on ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, fn, maps, c2);
 }
 
 }  // namespace sarathi

@@ -187,6 +187,14 @@ ropetab)
   rm -rf gpurun_out/ab
   bash tools/ab.sh "SARATHI_ROPE_TABLE=1" "SARATHI_ROPE_TABLE=0"
   ;;
+chainkb)
+  # the layer chain with the one-asm k-block issue + relaxed slot releases vs the standalone GEMMs
+  build
+  timeout 1500 python -m pytest tests/test_gpu_model.py -x -q -k "chain" > gpurun_out/pytest_chain.log 2>&1; echo rc=$? >> gpurun_out/pytest_chain.log
+  rm -rf gpurun_out/ab
+  bash tools/ab.sh "SARATHI_CHAIN=1" "SARATHI_CHAIN=0"
+  SARATHI_CHAIN=1 timeout 600 python tools/shard_step.py > gpurun_out/shard_step_chain.txt 2>/dev/null
+  ;;
 *) echo "unknown experiment $exp" >&2; exit 2 ;;
 esac
 done

@@ -495,7 +495,6 @@ __global__ void __launch_bounds__(threads_of<NEH>(), 1)
     const int ew = static_cast<int>(warp) - 2;              // 0..7
     const int eh = ew >> 2;
     const uint32_t quarter = warp & 3;                      // TMEM lane quarter of this warp
-    const int r = static_cast<int>(quarter * 32 + lane);    // accumulator row within this CTA's half
     float* sbuf = stage_buf + ew * kStageFloats;            // this warp's transpose buffer
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
     const bool relaxed_rel = ep.relaxed_rel;  // SARATHI_GEMM_RELAXED=0: release.cluster arrives

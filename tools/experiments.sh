@@ -195,6 +195,11 @@ chainkb)
   bash tools/ab.sh "SARATHI_CHAIN=1" "SARATHI_CHAIN=0"
   SARATHI_CHAIN=1 timeout 600 python tools/shard_step.py > gpurun_out/shard_step_chain.txt 2>/dev/null
   ;;
+ppb)
+  # pipeline bubbles (paper §5.3, NEXT-4) with stage costs measured on the session-3 kernels
+  build
+  timeout 1200 python tools/pp_bubbles.py > gpurun_out/pp_bubbles.txt 2> gpurun_out/pp_bubbles.err
+  ;;
 *) echo "unknown experiment $exp" >&2; exit 2 ;;
 esac
 done

@@ -200,6 +200,18 @@ ppb)
   build
   timeout 1200 python tools/pp_bubbles.py > gpurun_out/pp_bubbles.txt 2> gpurun_out/pp_bubbles.err
   ;;
+pairbar)
+  # prefill attention: row-half max exchange through per-quarter 2-warp barriers (SARATHI_PREFILL_PAIRBAR)
+  build
+  timeout 900 python -m pytest tests/test_gpu_model.py tests/test_gpu_fullsize.py -x -q > gpurun_out/pytest_model.log 2>&1; echo rc=$? >> gpurun_out/pytest_model.log
+  for v in 1 0; do
+    echo "== pairbar=$v" >> gpurun_out/pairbar.txt
+    SARATHI_PREFILL_PAIRBAR=$v timeout 600 python tools/shard_step.py >> gpurun_out/pairbar.txt 2>/dev/null
+    SARATHI_PREFILL_PAIRBAR=$v timeout 300 python tools/cliff.py --cases 256:0 >> gpurun_out/pairbar.txt 2>/dev/null
+  done
+  rm -rf gpurun_out/ab
+  bash tools/ab.sh "SARATHI_PREFILL_PAIRBAR=1" "SARATHI_PREFILL_PAIRBAR=0"
+  ;;
 *) echo "unknown experiment $exp" >&2; exit 2 ;;
 esac
 done

@@ -92,6 +92,8 @@ def main():
     ap.add_argument("--n-factor", type=float, default=2.0)
     ap.add_argument("--chunk", type=int, default=256)
     ap.add_argument("--policies", nargs="*", default=["sarathi", "request_level", "orca_best"])
+    ap.add_argument("--pd-optimal", action="store_true",
+                    help="per length, P:D = C / (B - 1) (the paper's balanced ratio, P:L62 / P:L100) instead of --pd")
     args = ap.parse_args()
     import torch
     import synth
@@ -102,7 +104,10 @@ def main():
     stream = torch.cuda.Stream()
     bs = 64
     pol = {"sarathi": S.POLICY_SARATHI, "request_level": S.POLICY_REQUEST_LEVEL, "orca_best": S.POLICY_ORCA_BEST,
-           "sarathi_b200": (S.POLICY_SARATHI, 2)}  # chunk per iteration by the B200 advisor
+           "sarathi_b200": (S.POLICY_SARATHI, 2),  # chunk per iteration by the B200 advisor
+           # Orca worst case: all requests begin and end together, no prefill/decode overlap,
+           # "similar to our earlier baseline" -- the request-level cohort schedule
+           "orca_worst": S.POLICY_REQUEST_LEVEL}
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     rows = []
     for L in args.lengths:
@@ -112,7 +117,7 @@ def main():
         num_blocks = B * per_req_blocks + 8
         m.alloc_kv(num_blocks, bs)
         N = max(B, int(args.n_factor * B))
-        for r in args.pd:
+        for r in ([args.chunk / max(1, B - 1)] if args.pd_optimal else args.pd):
             P, D = synth.split_pd(L, r)
             res = {}
             for name in args.policies:

@@ -212,6 +212,17 @@ pairbar)
   rm -rf gpurun_out/ab
   bash tools/ab.sh "SARATHI_PREFILL_PAIRBAR=1" "SARATHI_PREFILL_PAIRBAR=0"
   ;;
+pdsweep)
+  # paper §5.2 Fig. orca: (b) P:D sweep at 1K (chunks 256 / 512 vs Orca best / request-level);
+  # (a) the balanced P:D = C/(B-1) at 1K / 2K / 3K (LLaMA-13B)
+  build
+  timeout 1800 python tools/e2e_policies.py --model llama-13b --lengths 1024 --pd 1 2 5 10 15 20 30 50 \
+    --policies sarathi request_level orca_best > gpurun_out/e2e_pd_c256.txt 2> gpurun_out/e2e_pd_c256.err
+  timeout 1200 python tools/e2e_policies.py --model llama-13b --lengths 1024 --pd 1 2 5 10 15 20 30 50 --chunk 512 \
+    --policies sarathi request_level > gpurun_out/e2e_pd_c512.txt 2> gpurun_out/e2e_pd_c512.err
+  timeout 1500 python tools/e2e_policies.py --model llama-13b --lengths 1024 2048 3072 --pd-optimal \
+    --policies sarathi request_level orca_best > gpurun_out/e2e_opt.txt 2> gpurun_out/e2e_opt.err
+  ;;
 *) echo "unknown experiment $exp" >&2; exit 2 ;;
 esac
 done

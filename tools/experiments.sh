@@ -223,6 +223,18 @@ pdsweep)
   timeout 1500 python tools/e2e_policies.py --model llama-13b --lengths 1024 2048 3072 --pd-optimal \
     --policies sarathi request_level orca_best > gpurun_out/e2e_opt.txt 2> gpurun_out/e2e_opt.err
   ;;
+kbcommit)
+  # the k-block's empty-barrier commit inside the k-block asm block (SARATHI_GEMM_KBCOMMIT)
+  build
+  timeout 600 python -m pytest tests/test_gpu_gemm.py -x -q > gpurun_out/pytest_gemm.log 2>&1; echo rc=$? >> gpurun_out/pytest_gemm.log
+  timeout 900 python -m pytest tests/test_gpu_model.py -x -q -k "not variants" > gpurun_out/pytest_model.log 2>&1; echo rc=$? >> gpurun_out/pytest_model.log
+  for v in 1 0; do
+    echo "== kbcommit=$v" >> gpurun_out/kbcommit.txt
+    SARATHI_GEMM_KBCOMMIT=$v timeout 600 python tools/shard_step.py >> gpurun_out/kbcommit.txt 2>/dev/null
+  done
+  rm -rf gpurun_out/ab
+  bash tools/ab.sh "SARATHI_GEMM_KBCOMMIT=1" "SARATHI_GEMM_KBCOMMIT=0"
+  ;;
 *) echo "unknown experiment $exp" >&2; exit 2 ;;
 esac
 done

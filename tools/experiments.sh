@@ -235,6 +235,15 @@ kbcommit)
   rm -rf gpurun_out/ab
   bash tools/ab.sh "SARATHI_GEMM_KBCOMMIT=1" "SARATHI_GEMM_KBCOMMIT=0"
   ;;
+ksplit)
+  # prefill key split on the TP-8 rank shapes after the session-3 GEMM changes (cost model vs forced)
+  build
+  for r in 1 2; do for k in 0 2 4 6 8; do
+    echo "== r$r ksplit=$k" >> gpurun_out/ksplit.txt
+    if [ $k = 0 ]; then timeout 600 python tools/shard_step.py --which llama70b-tp8 gpt3-tp8 >> gpurun_out/ksplit.txt 2>/dev/null
+    else SARATHI_PREFILL_KSPLIT=$k timeout 600 python tools/shard_step.py --which llama70b-tp8 gpt3-tp8 >> gpurun_out/ksplit.txt 2>/dev/null; fi
+  done; done
+  ;;
 *) echo "unknown experiment $exp" >&2; exit 2 ;;
 esac
 done
